@@ -1,0 +1,307 @@
+// ORACLE / TEST INFRASTRUCTURE ONLY -- never linked into the product path.
+//
+// extern "C" shim over the UNMODIFIED reference library (the sources under
+// /root/reference/proj/src are compiled as-is by oracle/Makefile into
+// oracle/_ref/liboscar_ref.so).  Only tests/, __graft_entry__.smoke() and
+// bench.py's cpu_baseline / --impl reference legs load it.
+//
+// Every entry point drives the reference's own public API:
+//   apply_method        -> fht_tensor + omni_token_scale   (pipeline.cpp:224-236)
+//   KvCache             -> buffer_quant_k / buffer_quant_v (kv_cache.cpp:194-292)
+//   materialize_k/v     -> kv_cache.cpp:327-381
+//   attention           -> pipeline.cpp:184-198
+//   dump                -> KVC1 debug format               (kv_cache.cpp:469-507)
+// GQA is expressed without head repetition: a GQA group of g query heads per
+// KV head is passed to attention() as g query "tokens" x Hkv heads, which the
+// reference evaluates as g independent non-causal rows per KV head
+// (pipeline.cpp:184-198).
+#include <chrono>
+#include <cstdint>
+#include <cstring>
+#include <exception>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#ifdef _OPENMP
+#include <omp.h>
+#endif
+
+#include "oscar/hadamard.hpp"
+#include "oscar/kv_cache.hpp"
+#include "oscar/pipeline.hpp"
+#include "oscar/quant.hpp"
+
+using namespace oscar;
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(const std::exception &e) {
+    g_err = e.what();
+    if (dynamic_cast<const std::invalid_argument *>(&e)) return 1;
+    if (dynamic_cast<const std::logic_error *>(&e)) return 2;
+    return 3;
+}
+
+struct RefCache {
+    PipelineConfig cfg;
+    KvCache cache;
+    bool rotate_v = false;  // explicit-V mode: fht_tensor(v) before buffer_quant_v
+};
+
+PipelineConfig make_cfg(int method, int bits, int64_t G, int64_t R, int scaling, int64_t d,
+                        int64_t H) {
+    PipelineConfig c;
+    c.method = static_cast<Method>(method);
+    c.bits = bits;
+    c.group_size = G;
+    c.residual_len = R;
+    c.scaling = static_cast<Scaling>(scaling);
+    c.head_dim = d;
+    c.heads = H;
+    c.validate();
+    return c;
+}
+
+Tensor3 to_tensor(const double *x, int64_t s, int64_t h, int64_t d) {
+    if (s == 0) return Tensor3(0, h, d);
+    return Tensor3(s, h, d, std::vector<double>(x, x + s * h * d));
+}
+
+// apply_method's key half (pipeline.cpp:224-236): rotate then scale.
+void transform_k(const PipelineConfig &cfg, const Tensor3 &xk, Tensor3 &k_out,
+                 std::vector<double> &norms) {
+    if (cfg.scales()) {
+        ScaledTokens st = omni_token_scale(cfg.rotates() ? fht_tensor(xk) : xk, cfg.scaling);
+        k_out = std::move(st.scaled);
+        norms = std::move(st.norms);
+    } else {
+        k_out = cfg.rotates() ? fht_tensor(xk) : xk;
+        norms.assign(static_cast<size_t>(xk.tokens * xk.heads), 1.0);
+    }
+}
+
+}  // namespace
+
+extern "C" {
+
+const char *ref_last_error() { return g_err.c_str(); }
+
+int ref_cache_create(int method, int bits, int64_t G, int64_t R, int scaling, int64_t d,
+                     int64_t H, int rotate_v, void **out) {
+    try {
+        auto *c = new RefCache();
+        c->cfg = make_cfg(method, bits, G, R, scaling, d, H);
+        c->cache = KvCache(c->cfg);
+        c->rotate_v = rotate_v != 0;
+        *out = c;
+        return 0;
+    } catch (const std::exception &e) {
+        return fail(e);
+    }
+}
+
+void ref_cache_destroy(void *h) { delete static_cast<RefCache *>(h); }
+
+// Raw (untransformed) keys xk[S,H,d] and values xv[S,H,d] go through the
+// reference transform and into buffer_quant_k / buffer_quant_v. The first
+// call on a cache is the prefill branch (kv_cache.cpp:204-218).
+int ref_cache_append(void *h, const double *xk, const double *xv, int64_t S) {
+    try {
+        auto *c = static_cast<RefCache *>(h);
+        const int64_t H = c->cfg.heads, d = c->cfg.head_dim;
+        Tensor3 k_t;
+        std::vector<double> norms;
+        transform_k(c->cfg, to_tensor(xk, S, H, d), k_t, norms);
+        if (S == 0) k_t = Tensor3(0, H, d);
+        c->cache.buffer_quant_k(k_t, norms);
+        Tensor3 v = to_tensor(xv, S, H, d);
+        c->cache.buffer_quant_v(c->rotate_v && S > 0 ? fht_tensor(v) : v);
+        return 0;
+    } catch (const std::exception &e) {
+        return fail(e);
+    }
+}
+
+int ref_cache_stats(void *h, int64_t *out4) {
+    auto *c = static_cast<RefCache *>(h);
+    out4[0] = c->cache.packed_tokens();
+    out4[1] = c->cache.residual_tokens();
+    out4[2] = c->cache.total_tokens();
+    out4[3] = c->cache.flush_count();
+    return 0;
+}
+
+int ref_cache_memory_report(void *h, int64_t *out8, double *eff_bits) {
+    auto *c = static_cast<RefCache *>(h);
+    const MemoryReport r = c->cache.memory_report();
+    out8[0] = r.packed_tokens;
+    out8[1] = r.residual_tokens;
+    out8[2] = r.packed_k_payload_bits;
+    out8[3] = r.packed_v_payload_bits;
+    out8[4] = r.residual_k_payload_bits;
+    out8[5] = r.residual_v_payload_bits;
+    out8[6] = r.k_norm_bits;
+    out8[7] = r.param_bits;
+    *eff_bits = r.effective_bits_per_value();
+    return 0;
+}
+
+int ref_cache_dump(void *h, const char *path) {
+    try {
+        static_cast<RefCache *>(h)->cache.dump(path);
+        return 0;
+    } catch (const std::exception &e) {
+        return fail(e);
+    }
+}
+
+int ref_cache_load(const char *path, void **out) {
+    try {
+        auto *c = new RefCache();
+        c->cache = KvCache::load(path);
+        c->cfg = c->cache.config();
+        *out = c;
+        return 0;
+    } catch (const std::exception &e) {
+        return fail(e);
+    }
+}
+
+// materialize_k / materialize_v into caller buffers of total_tokens*H*d.
+int ref_cache_materialize(void *h, double *k_out, double *v_out) {
+    try {
+        auto *c = static_cast<RefCache *>(h);
+        const Tensor3 k = c->cache.materialize_k();
+        const Tensor3 v = c->cache.materialize_v();
+        if (k_out) std::memcpy(k_out, k.data.data(), sizeof(double) * k.data.size());
+        if (v_out) std::memcpy(v_out, v.data.data(), sizeof(double) * v.data.size());
+        return 0;
+    } catch (const std::exception &e) {
+        return fail(e);
+    }
+}
+
+// decode_step body without projections (pipeline.cpp:292-323) for GQA:
+// q_raw[Hq,d], k_raw[H,d], v[H,d] for the current token, Hq = g*H with q head
+// (h*g + j) served by KV head h. Attention sees history (materialized) plus
+// the current token at full precision; the append happens afterwards.
+// out[Hq,d] is in the cache's value space (rotated V when V is folded).
+int ref_decode_step(void *h, const double *q_raw, const double *k_raw, const double *v_raw,
+                    int64_t g, double *out, int do_append) {
+    try {
+        auto *c = static_cast<RefCache *>(h);
+        const PipelineConfig &cfg = c->cfg;
+        const int64_t H = cfg.heads, d = cfg.head_dim;
+        // apply_method on the current token (pipeline.cpp:292)
+        Tensor3 xk = to_tensor(k_raw, 1, H, d);
+        Tensor3 k_t;
+        std::vector<double> norms;
+        transform_k(cfg, xk, k_t, norms);
+        Tensor3 xv = to_tensor(v_raw, 1, H, d);
+        if (c->rotate_v) xv = fht_tensor(xv);
+        // q as [g tokens, H heads, d]: row (j, h) = q head h*g + j
+        Tensor3 q(g, H, d);
+        for (int64_t hh = 0; hh < H; ++hh)
+            for (int64_t j = 0; j < g; ++j)
+                std::memcpy(q.row(j, hh), q_raw + (hh * g + j) * d, sizeof(double) * d);
+        const Tensor3 qt = cfg.rotates() ? fht_tensor(q) : q;
+        // history + current (pipeline.cpp:294-310)
+        const Tensor3 k_hist = c->cache.materialize_k();
+        const Tensor3 v_hist = c->cache.materialize_v();
+        const int64_t total = k_hist.tokens + 1;
+        Tensor3 k_all(total, H, d), v_all(total, H, d);
+        std::memcpy(k_all.data.data(), k_hist.data.data(), sizeof(double) * k_hist.data.size());
+        std::memcpy(v_all.data.data(), v_hist.data.data(), sizeof(double) * v_hist.data.size());
+        for (int64_t hh = 0; hh < H; ++hh) {
+            const double s = norms[static_cast<size_t>(hh)];
+            const double *src = k_t.row(0, hh);
+            double *dst = k_all.row(total - 1, hh);
+            for (int64_t cc = 0; cc < d; ++cc) dst[cc] = src[cc] * s;
+            std::memcpy(v_all.row(total - 1, hh), xv.row(0, hh), sizeof(double) * d);
+        }
+        const Tensor3 o = attention(qt, k_all, v_all);
+        for (int64_t hh = 0; hh < H; ++hh)
+            for (int64_t j = 0; j < g; ++j)
+                std::memcpy(out + (hh * g + j) * d, o.row(j, hh), sizeof(double) * d);
+        if (do_append) {
+            c->cache.buffer_quant_k(k_t, norms);
+            c->cache.buffer_quant_v(xv);
+        }
+        return 0;
+    } catch (const std::exception &e) {
+        return fail(e);
+    }
+}
+
+// Free functions used by the pinning tests.
+int ref_fht(double *v, int64_t d) {
+    try {
+        fht_inplace(v, d);
+        return 0;
+    } catch (const std::exception &e) {
+        return fail(e);
+    }
+}
+
+int ref_token_scale(const double *x, int64_t S, int64_t H, int64_t d, int scaling,
+                    double *scaled, double *norms, int64_t *degenerate) {
+    try {
+        const ScaledTokens st =
+            omni_token_scale(to_tensor(x, S, H, d), static_cast<Scaling>(scaling));
+        std::memcpy(scaled, st.scaled.data.data(), sizeof(double) * st.scaled.data.size());
+        std::memcpy(norms, st.norms.data(), sizeof(double) * st.norms.size());
+        *degenerate = st.degenerate_count;
+        return 0;
+    } catch (const std::exception &e) {
+        return fail(e);
+    }
+}
+
+int ref_quant_params(const double *x, int64_t n, int bits, double *delta, int64_t *zp,
+                     double *constant) {
+    try {
+        const QuantParams p = quant_params(x, n, bits);
+        *delta = p.delta;
+        *zp = p.zero_point;
+        *constant = p.constant;
+        return 0;
+    } catch (const std::exception &e) {
+        return fail(e);
+    }
+}
+
+int ref_pack_2bit(const uint16_t *codes, int64_t n, uint16_t *words) {
+    try {
+        const PackedWords w = pack_2bit(std::vector<uint16_t>(codes, codes + n));
+        std::memcpy(words, w.words.data(), sizeof(uint16_t) * w.words.size());
+        return 0;
+    } catch (const std::exception &e) {
+        return fail(e);
+    }
+}
+
+int ref_attention(const double *q, int64_t Tq, const double *k, const double *v, int64_t S,
+                  int64_t H, int64_t d, double *out) {
+    try {
+        const Tensor3 o = attention(to_tensor(q, Tq, H, d), to_tensor(k, S, H, d),
+                                    to_tensor(v, S, H, d));
+        std::memcpy(out, o.data.data(), sizeof(double) * o.data.size());
+        return 0;
+    } catch (const std::exception &e) {
+        return fail(e);
+    }
+}
+
+int ref_num_threads() {
+#ifdef _OPENMP
+    return omp_get_max_threads();
+#else
+    return 1;
+#endif
+}
+
+}  // extern "C"

@@ -1,0 +1,144 @@
+/* oscar_kv.h -- C-ABI of the B200-native OScaR KV-cache path.
+ *
+ * Drop-in boundary for the reference's C++ cache API
+ * (/root/reference/proj/include/oscar/kv_cache.hpp, pipeline.hpp).  Plain
+ * pointers and sizes only; device pointers are CUDA device addresses, streams
+ * are cudaStream_t passed as void*.  Every entry point returns 0 on success,
+ * 1 invalid argument (reference std::invalid_argument), 2 logic/state error
+ * (std::logic_error, e.g. residual overflow kv_cache.cpp:225-227), 3 CUDA /
+ * runtime error; oscar_last_error() holds the thread-local message.
+ *
+ * One handle = one writer (kv_cache.hpp:58-60 single-writer contract) holding
+ * `batch` sequences of identical length, each with `heads` KV heads.  All
+ * work is enqueued on the caller's stream; no internal host synchronisation
+ * except the *_host and export entry points, which synchronise their stream.
+ */
+#ifndef OSCAR_KV_H
+#define OSCAR_KV_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Method / Scaling enums, same values as the reference (kv_cache.hpp:11-12). */
+enum oscar_method { OSCAR_FP = 0, OSCAR_KIVI = 1, OSCAR_ROTATE_ONLY = 2, OSCAR_SCALE_ONLY = 3, OSCAR_OSCAR = 4 };
+enum oscar_scaling { OSCAR_L2 = 0, OSCAR_RSQRT = 1, OSCAR_MAX = 2, OSCAR_MEAN_ABS = 3 };
+
+/* PipelineConfig (kv_cache.hpp:19-32) plus the value-rotation mode.
+ * rotate_v = 0: V arrives already rotated (W_V folded by preprocess,
+ *               pipeline.cpp:38-78) and attention outputs stay in that space;
+ * rotate_v = 1: the append kernel applies the Hadamard rotation to V and the
+ *               attention output is rotated back (explicit mode). */
+typedef struct oscar_kv_config {
+    int32_t method;
+    int32_t bits;          /* 0 (exact bf16 cache), 2, 4 on device */
+    int64_t group_size;    /* G; device kernels: 32 */
+    int64_t residual_len;  /* R; device kernels: 128 */
+    int32_t scaling;
+    int32_t rotate_v;
+    int64_t head_dim;      /* d_h; device kernels: 128 */
+    int64_t heads;         /* H = KV heads */
+} oscar_kv_config;
+
+/* MemoryReport (kv_cache.hpp:45-56): the reference's accounting (fp64 params
+ * and norms) plus the device's actual resident bytes. */
+typedef struct oscar_kv_memory_report {
+    int64_t packed_tokens, residual_tokens;
+    int64_t packed_k_payload_bits, packed_v_payload_bits;
+    int64_t residual_k_payload_bits, residual_v_payload_bits;
+    int64_t k_norm_bits, param_bits;
+    double effective_bits_per_value;
+    int64_t device_hot_bytes;    /* bytes the decode kernel streams per sequence */
+    int64_t device_total_bytes;  /* all device allocations of the handle */
+} oscar_kv_memory_report_t;
+
+typedef struct oscar_kv_handle oscar_kv_handle;
+
+const char *oscar_last_error(void);
+
+/* PipelineConfig::validate (kv_cache.cpp:51-67) + device shape limits. */
+int oscar_kv_config_validate(const oscar_kv_config *cfg);
+
+/* KvCache(const PipelineConfig&) (kv_cache.cpp:80-85).  q_heads = GQA query
+ * heads (q_heads % heads == 0, q_heads/heads <= 8); max_tokens = capacity per
+ * sequence; keep_exact = keep fp64 (lo, hi) per group and fp64 norms on
+ * device so oscar_kv_export can return bit-exact reference params. */
+int oscar_kv_create(const oscar_kv_config *cfg, int64_t batch, int64_t q_heads, int64_t max_tokens,
+                    int device, int keep_exact, oscar_kv_handle **out);
+int oscar_kv_destroy(oscar_kv_handle *h);
+
+/* buffer_quant_k + buffer_quant_v fused (kv_cache.cpp:194-292), taking RAW
+ * keys: the kernel applies apply_method's key transform (fht_tensor +
+ * omni_token_scale, pipeline.cpp:224-236) in fp64 first.
+ * k, v: bf16 [batch, n_tokens, heads, head_dim] device pointers.  The first
+ * call is the prefill branch (S - S mod R packed, the rest residual); later
+ * calls append token by token and flush at exactly R. */
+int oscar_kv_append(oscar_kv_handle *h, const void *k, const void *v, int64_t n_tokens, void *stream);
+
+/* decode_step body (pipeline.cpp:292-323) without projections:
+ * attention of q over (cache history + the current token at full precision),
+ * then the current token is appended (a flush, if the window fills, runs
+ * after the attention kernel -- the reference's ordering contract).
+ * q: bf16 [batch, q_heads, d]; k, v: bf16 [batch, heads, d] (current token);
+ * out: fp32 [batch, q_heads, d]; lse: optional fp32 [batch, q_heads] (natural
+ * log of the softmax denominator of logits q.k/sqrt(d)). */
+int oscar_kv_decode_step(oscar_kv_handle *h, const void *q, const void *k, const void *v, float *out,
+                         float *lse, void *stream);
+
+/* Attention over the cache contents only (no current token, no append).
+ * Used for sequence sharding: each rank attends its R-aligned shard and the
+ * (out, lse) partials are merged with oscar_lse_merge. */
+int oscar_kv_attend(oscar_kv_handle *h, const void *q, float *out, float *lse, void *stream);
+
+/* decode_step with HOST buffers (pinned or pageable): copies q/k/v in and
+ * out/lse back inside the call; synchronises the stream. */
+int oscar_kv_decode_step_host(oscar_kv_handle *h, const void *q_host, const void *k_host,
+                              const void *v_host, float *out_host, float *lse_host, void *stream);
+
+/* packed_tokens / residual_tokens / flush_count (kv_cache.hpp:67-71). */
+int oscar_kv_stats(const oscar_kv_handle *h, int64_t *packed, int64_t *residual, int64_t *flushes);
+int oscar_kv_memory_report(const oscar_kv_handle *h, oscar_kv_memory_report_t *out);
+
+/* Export sequence b in the reference's own layout (PackedBlock,
+ * kv_cache.hpp:38-43 / KvCache members 104-122).  Counts per head:
+ *   nblk = packed/R; K params per block d*(R/G) at [j*(R/G)+g];
+ *   V params per block R*(d/G) at [t*(d/G)+g];
+ *   bits==2 payload: R*d/8 uint16 words per block (pack_2bit, quant.cpp:162-175)
+ *   bits==4 payload: R*d uint16 codes per block; bits==0: raw fp64 rows.
+ * Any pointer may be NULL to skip that section.  Requires keep_exact for
+ * the params and norms.  Synchronises the handle's last stream. */
+typedef struct oscar_kv_export_t {
+    uint16_t *k_payload, *v_payload;  /* [H][nblk][...] */
+    double *k_delta, *k_constant, *v_delta, *v_constant;
+    int64_t *k_zp, *v_zp;
+    double *k_raw, *v_raw;           /* bits==0: [H][nblk][R*d] */
+    double *k_norms;                 /* [H][packed] */
+    double *k_residual;              /* [r][H][d] transformed K_u rows */
+    double *k_norms_residual;        /* [r*H] */
+    double *v_residual;              /* [r][H][d] */
+} oscar_kv_export_t;
+int oscar_kv_export(oscar_kv_handle *h, int64_t b, oscar_kv_export_t *out);
+
+/* KvCache::dump (kv_cache.cpp:469-507): KVC1 file for sequence b, readable by
+ * the reference's KvCache::load. */
+int oscar_kv_dump(oscar_kv_handle *h, int64_t b, const char *path);
+
+/* materialize_k / materialize_v (kv_cache.cpp:327-381) of sequence b into
+ * host fp64 [total, H, d] buffers (a debug/parity path, not the hot path). */
+int oscar_kv_materialize(oscar_kv_handle *h, int64_t b, double *k_out, double *v_out);
+
+/* Log-sum-exp merge of P partial attention results (sequence sharding):
+ * outs: fp32 [P, rows, d], lses: fp32 [P, rows] -> out fp32 [rows, d],
+ * lse_out optional.  Device pointers. */
+int oscar_lse_merge(const float *outs, const float *lses, int64_t parts, int64_t rows, int64_t d,
+                    float *out, float *lse_out, void *stream);
+
+/* Number of kernels the last decode/attend call launched (instrumentation). */
+int oscar_kv_last_launch_count(const oscar_kv_handle *h);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

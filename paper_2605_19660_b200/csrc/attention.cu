@@ -1,0 +1,796 @@
+// attention.cu -- fused-dequant split-KV decode attention over the packed
+// OScaR cache (replaces materialize_k + materialize_v + the attend_one loop,
+// pipeline.cpp:294-319 / kv_cache.cpp:327-381).
+//
+// Persistent, stream-K style: one CTA per SM gets an equal contiguous range
+// of the global (sequence*KV-head, R-block) space, so every SM streams the
+// same number of bytes.  Warp roles:
+//   warp NCW      producer: one elected lane streams whole R-block records
+//                 (12.8 KB INT2 / 21 KB INT4, see layout.h) HBM -> shared
+//                 memory with cp.async.bulk (TMA engine) into an NST-stage
+//                 mbarrier ring, L2 evict-first;
+//   warps 0..NCW-1 consumers: block p of the range goes to warp p % NCW.
+// Per block a consumer runs QK^T and P.V on the tensor cores
+// (mma.sync m16n8k16, fp16 in / fp32 accumulate) straight from the packed
+// codes: every loaded 32-bit word ANDed with a field mask IS an A register
+// holding fp16 subnormals code*2^(f*BITS-24); the per-group step a is folded
+// into the B operand (Q*aK for keys, P*aV for values), the per-group offset b
+// into one extra MMA per block, the per-token key norm into the fp32
+// epilogue.  Online softmax in log2 units; partials are merged per CTA in
+// shared memory and across CTAs by the last-arriving CTA of each (b, kv-head)
+// (atomic ticket), which also writes the current token into the residual
+// ring.  The residual window (< R full-precision tokens) plus the current
+// token are attended with fp32 CUDA-core math by the CTA that owns the last
+// packed block of the sequence.
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+#include <math_constants.h>
+
+#include "device_common.cuh"
+#include "kernels.h"
+#include "layout.h"
+
+namespace osk {
+
+namespace {
+
+constexpr int NCW = 8;                 // consumer warps
+constexpr int NTHREADS = (NCW + 1) * 32;
+constexpr int MERGE_FLOATS = 8 * D + 16;  // per-warp partial: O[8][128], m[8], l[8]
+constexpr float LOG2E = 1.4426950408889634f;
+constexpr float LN2 = 0.6931471805599453f;
+
+template <int BITS>
+struct AttnCfg {
+    static constexpr int BYTES = (BITS == 0) ? BF16_BLOCK_BYTES : Block<BITS == 0 ? 2 : BITS>::BYTES;
+    static constexpr int NST = (BITS == 2) ? 13 : (BITS == 4 ? 8 : 2);
+    static constexpr int RING = NST * BYTES;
+    static constexpr int MERGE_OFF = RING;
+    static constexpr int QS_OFF = MERGE_OFF + NCW * MERGE_FLOATS * 4;
+    static constexpr int QR_OFF = QS_OFF + 8 * D * 4;
+    static constexpr int BAR_OFF = QR_OFF + 8 * D * 4;
+    static constexpr int MISC_OFF = BAR_OFF + 2 * NST * 8;
+    static constexpr int SMEM = MISC_OFF + 16;
+};
+
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+// normalized FHT of a 128-vector held 4 per lane (channel lane*4+e), fp32
+__device__ __forceinline__ void fht128_warp(float (&x)[4], int lane) {
+    // half = 1, 2 inside the lane
+    {
+        float a = x[0], b = x[1];
+        x[0] = a + b;
+        x[1] = a - b;
+        a = x[2];
+        b = x[3];
+        x[2] = a + b;
+        x[3] = a - b;
+        a = x[0];
+        b = x[2];
+        x[0] = a + b;
+        x[2] = a - b;
+        a = x[1];
+        b = x[3];
+        x[1] = a + b;
+        x[3] = a - b;
+    }
+#pragma unroll
+    for (int xm = 1; xm < 32; xm <<= 1) {
+        const bool upper = (lane & xm) != 0;
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            const float o = __shfl_xor_sync(0xffffffffu, x[e], xm);
+            x[e] = upper ? (o - x[e]) : (x[e] + o);
+        }
+    }
+    const float sc = 0.08838834764831845f;  // 1/sqrt(128)
+#pragma unroll
+    for (int e = 0; e < 4; ++e) x[e] *= sc;
+}
+
+__device__ __forceinline__ void load_bf16x4(const __nv_bfloat16 *p, float (&x)[4]) {
+    const uint2 u = *reinterpret_cast<const uint2 *>(p);
+    x[0] = __uint_as_float(u.x << 16);
+    x[1] = __uint_as_float(u.x & 0xffff0000u);
+    x[2] = __uint_as_float(u.y << 16);
+    x[3] = __uint_as_float(u.y & 0xffff0000u);
+}
+
+__device__ __forceinline__ int64_t cta_of(int64_t x, int64_t total, int ncta) {
+    return ((x + 1) * ncta - 1) / total;
+}
+
+// ----------------------------------------------------------------------------
+// per-warp accumulator state (fragment layouts, see layout.h)
+struct WarpState {
+    float o[8][4];   // P.V accumulators: m-tile mm, (row gq|gq+8) x (head 2tq|2tq+1)
+    float ob[4];     // V-offset accumulator: row gq = channel group
+    float m[2], l[2];
+};
+
+template <int BITS>
+__device__ __forceinline__ void process_block(const uint8_t *__restrict__ sb, WarpState &st,
+                                              const uint32_t (&qf)[8][2], int lane, float c0) {
+    using Blk = Block<BITS>;
+    constexpr int TPW = 16 / BITS;   // m-tiles per half-word
+    constexpr int WPF = 8 / TPW;     // words per fragment family per k-step
+    constexpr int HALFT = TPW / 2;   // fields reachable without a shift
+    constexpr uint32_t FMASK = (BITS == 2) ? 0x00030003u : 0x000F000Fu;
+    const int gq = lane >> 2, tq = lane & 3;
+
+    // ---- key offsets: bias[grp][head] = sum_c bK[c,grp] * Qrot[head,c] -------------
+    float kbias[4] = {0.f, 0.f, 0.f, 0.f};
+    {
+        uint32_t bk[16];
+        if (gq < 4) {
+            const uint4 *p = reinterpret_cast<const uint4 *>(sb + Blk::KB_OFF + (gq * 4 + tq) * 64);
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const uint4 u = p[i];
+                bk[4 * i] = u.x;
+                bk[4 * i + 1] = u.y;
+                bk[4 * i + 2] = u.z;
+                bk[4 * i + 3] = u.w;
+            }
+        } else {
+#pragma unroll
+            for (int i = 0; i < 16; ++i) bk[i] = 0u;
+        }
+#pragma unroll
+        for (int s = 0; s < 8; ++s) mma16816(kbias, bk[2 * s], 0u, bk[2 * s + 1], 0u, qf[s][0], qf[s][1]);
+    }
+
+    // ---- QK^T --------------------------------------------------------------------
+    float sacc[8][4];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) sacc[i][0] = sacc[i][1] = sacc[i][2] = sacc[i][3] = 0.f;
+#pragma unroll
+    for (int s = 0; s < 8; ++s) {
+        uint32_t kw[4 * WPF], kwh[4 * WPF];
+        {
+            const uint4 *p = reinterpret_cast<const uint4 *>(sb + Blk::K_OFF + (s * 32 + lane) * 16 * WPF);
+#pragma unroll
+            for (int v = 0; v < WPF; ++v) {
+                const uint4 u = p[v];
+                kw[4 * v] = u.x;
+                kw[4 * v + 1] = u.y;
+                kw[4 * v + 2] = u.z;
+                kw[4 * v + 3] = u.w;
+            }
+#pragma unroll
+            for (int v = 0; v < 4 * WPF; ++v) kwh[v] = kw[v] >> 8;
+        }
+        uint32_t bq[4][2];
+        {
+            const uint4 *p = reinterpret_cast<const uint4 *>(sb + Blk::KA_OFF + (s * 4 + tq) * 32);
+            const uint4 a01 = p[0], a23 = p[1];
+            bq[0][0] = hmul2_u32(qf[s][0], a01.x);
+            bq[0][1] = hmul2_u32(qf[s][1], a01.y);
+            bq[1][0] = hmul2_u32(qf[s][0], a01.z);
+            bq[1][1] = hmul2_u32(qf[s][1], a01.w);
+            bq[2][0] = hmul2_u32(qf[s][0], a23.x);
+            bq[2][1] = hmul2_u32(qf[s][1], a23.y);
+            bq[3][0] = hmul2_u32(qf[s][0], a23.z);
+            bq[3][1] = hmul2_u32(qf[s][1], a23.w);
+        }
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            const int half = i / TPW, f = i % TPW;
+            const int fs = f % HALFT;
+            const uint32_t mask = FMASK << (BITS * fs);
+            const uint32_t *src = (f < HALFT) ? kw : kwh;
+            // word of family fam, half `half`: index fam*WPF + half
+            mma16816(sacc[i], src[0 * WPF + half] & mask, src[1 * WPF + half] & mask,
+                     src[2 * WPF + half] & mask, src[3 * WPF + half] & mask, bq[i >> 1][0], bq[i >> 1][1]);
+        }
+    }
+
+    // ---- logits (log2 units) ------------------------------------------------------------
+    float nrm[16];
+    {
+        const uint4 *p = reinterpret_cast<const uint4 *>(sb + Blk::NORM_OFF + gq * 64);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const uint4 u = p[i];
+            nrm[4 * i] = __uint_as_float(u.x) * c0;
+            nrm[4 * i + 1] = __uint_as_float(u.y) * c0;
+            nrm[4 * i + 2] = __uint_as_float(u.z) * c0;
+            nrm[4 * i + 3] = __uint_as_float(u.w) * c0;
+        }
+    }
+    float kb0[4], kb1[4];
+#pragma unroll
+    for (int grp = 0; grp < 4; ++grp) {
+        kb0[grp] = __shfl_sync(0xffffffffu, kbias[0], grp * 4 + tq);
+        kb1[grp] = __shfl_sync(0xffffffffu, kbias[1], grp * 4 + tq);
+    }
+    float bm0 = -CUDART_INF_F, bm1 = -CUDART_INF_F;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        const int fs = (i % TPW) % HALFT;
+        const float sc = __int_as_float((127 + 24 - BITS * fs) << 23);  // 2^(24 - BITS*fs)
+        const int grp = i >> 1;
+        sacc[i][0] = fmaf(sacc[i][0], sc, kb0[grp]) * nrm[2 * i];
+        sacc[i][1] = fmaf(sacc[i][1], sc, kb1[grp]) * nrm[2 * i];
+        sacc[i][2] = fmaf(sacc[i][2], sc, kb0[grp]) * nrm[2 * i + 1];
+        sacc[i][3] = fmaf(sacc[i][3], sc, kb1[grp]) * nrm[2 * i + 1];
+        bm0 = fmaxf(bm0, fmaxf(sacc[i][0], sacc[i][2]));
+        bm1 = fmaxf(bm1, fmaxf(sacc[i][1], sacc[i][3]));
+    }
+#pragma unroll
+    for (int o = 4; o < 32; o <<= 1) {
+        bm0 = fmaxf(bm0, __shfl_xor_sync(0xffffffffu, bm0, o));
+        bm1 = fmaxf(bm1, __shfl_xor_sync(0xffffffffu, bm1, o));
+    }
+    const float mn0 = fmaxf(st.m[0], bm0), mn1 = fmaxf(st.m[1], bm1);
+    const float al0 = fast_exp2(st.m[0] - mn0), al1 = fast_exp2(st.m[1] - mn1);
+    st.m[0] = mn0;
+    st.m[1] = mn1;
+    float ls0 = 0.f, ls1 = 0.f;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        sacc[i][0] = fast_exp2(sacc[i][0] - mn0);
+        sacc[i][1] = fast_exp2(sacc[i][1] - mn1);
+        sacc[i][2] = fast_exp2(sacc[i][2] - mn0);
+        sacc[i][3] = fast_exp2(sacc[i][3] - mn1);
+        ls0 += sacc[i][0] + sacc[i][2];
+        ls1 += sacc[i][1] + sacc[i][3];
+    }
+    st.l[0] = st.l[0] * al0 + ls0;
+    st.l[1] = st.l[1] * al1 + ls1;
+#pragma unroll
+    for (int mm = 0; mm < 8; ++mm) {
+        st.o[mm][0] *= al0;
+        st.o[mm][1] *= al1;
+        st.o[mm][2] *= al0;
+        st.o[mm][3] *= al1;
+    }
+    st.ob[0] *= al0;
+    st.ob[1] *= al1;
+
+    // ---- P.V ---------------------------------------------------------------------------
+    uint32_t vbA[16];  // value offsets as A: row gq = channel group, k = tokens
+    if (gq < 4) {
+        const uint4 *p = reinterpret_cast<const uint4 *>(sb + Blk::VB_OFF + (gq * 4 + tq) * 64);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const uint4 u = p[i];
+            vbA[4 * i] = u.x;
+            vbA[4 * i + 1] = u.y;
+            vbA[4 * i + 2] = u.z;
+            vbA[4 * i + 3] = u.w;
+        }
+    } else {
+#pragma unroll
+        for (int i = 0; i < 16; ++i) vbA[i] = 0u;
+    }
+    const int srcA = 4 * tq + (gq >> 1), srcB = 4 * (tq + 4) + (gq >> 1);
+    const bool odd = (gq & 1) != 0;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+        const uint32_t H0 = pack_half2(sacc[j][0], sacc[j][2]);
+        const uint32_t H1 = pack_half2(sacc[j][1], sacc[j][3]);
+        const uint32_t x0 = __shfl_sync(0xffffffffu, H0, srcA);
+        const uint32_t x1 = __shfl_sync(0xffffffffu, H1, srcA);
+        const uint32_t y0 = __shfl_sync(0xffffffffu, H0, srcB);
+        const uint32_t y1 = __shfl_sync(0xffffffffu, H1, srcB);
+        const uint32_t bp0 = odd ? x1 : x0, bp1 = odd ? y1 : y0;
+        uint32_t bv[4][2];
+        {
+            const uint4 *p = reinterpret_cast<const uint4 *>(sb + Blk::VA_OFF + (j * 4 + tq) * 32);
+            const uint4 a01 = p[0], a23 = p[1];
+            bv[0][0] = hmul2_u32(bp0, a01.x);
+            bv[0][1] = hmul2_u32(bp1, a01.y);
+            bv[1][0] = hmul2_u32(bp0, a01.z);
+            bv[1][1] = hmul2_u32(bp1, a01.w);
+            bv[2][0] = hmul2_u32(bp0, a23.x);
+            bv[2][1] = hmul2_u32(bp1, a23.y);
+            bv[3][0] = hmul2_u32(bp0, a23.z);
+            bv[3][1] = hmul2_u32(bp1, a23.w);
+        }
+        uint32_t vw[4 * WPF], vwh[4 * WPF];
+        {
+            const uint4 *p = reinterpret_cast<const uint4 *>(sb + Blk::V_OFF + (j * 32 + lane) * 16 * WPF);
+#pragma unroll
+            for (int v = 0; v < WPF; ++v) {
+                const uint4 u = p[v];
+                vw[4 * v] = u.x;
+                vw[4 * v + 1] = u.y;
+                vw[4 * v + 2] = u.z;
+                vw[4 * v + 3] = u.w;
+            }
+#pragma unroll
+            for (int v = 0; v < 4 * WPF; ++v) vwh[v] = vw[v] >> 8;
+        }
+#pragma unroll
+        for (int mm = 0; mm < 8; ++mm) {
+            const int half = mm / TPW, f = mm % TPW;
+            const int fs = f % HALFT;
+            const uint32_t mask = FMASK << (BITS * fs);
+            const uint32_t *src = (f < HALFT) ? vw : vwh;
+            mma16816(st.o[mm], src[0 * WPF + half] & mask, src[1 * WPF + half] & mask,
+                     src[2 * WPF + half] & mask, src[3 * WPF + half] & mask, bv[mm >> 1][0], bv[mm >> 1][1]);
+        }
+        mma16816(st.ob, vbA[2 * j], 0u, vbA[2 * j + 1], 0u, bp0, bp1);
+    }
+}
+
+// bf16 baseline block: raw K/V [token][channel] bf16 (no dequant); same
+// fragment orders, A operands built from shared memory with plain loads.
+__device__ __forceinline__ void process_block_bf16(const uint8_t *__restrict__ sb, WarpState &st,
+                                                   const uint32_t (&qf)[8][2], int lane, float c0) {
+    const int gq = lane >> 2, tq = lane & 3;
+    const uint16_t *K = reinterpret_cast<const uint16_t *>(sb);
+    const uint16_t *V = K + R * D;
+    // K rows: swizzle-free layout with row stride 256 B: 4B loads of channel pairs
+    float sacc[8][4];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) sacc[i][0] = sacc[i][1] = sacc[i][2] = sacc[i][3] = 0.f;
+#pragma unroll
+    for (int s = 0; s < 8; ++s) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            const int t0 = 16 * i + gq, t1 = t0 + 8;
+            const int c = 16 * s + 2 * tq;
+            const uint32_t a0 = *reinterpret_cast<const uint32_t *>(K + t0 * D + c);
+            const uint32_t a1 = *reinterpret_cast<const uint32_t *>(K + t1 * D + c);
+            const uint32_t a2 = *reinterpret_cast<const uint32_t *>(K + t0 * D + c + 8);
+            const uint32_t a3 = *reinterpret_cast<const uint32_t *>(K + t1 * D + c + 8);
+            mma16816_bf16(sacc[i], a0, a1, a2, a3, qf[s][0], qf[s][1]);
+        }
+    }
+    float bm0 = -CUDART_INF_F, bm1 = -CUDART_INF_F;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+#pragma unroll
+        for (int e = 0; e < 4; ++e) sacc[i][e] *= c0;
+        bm0 = fmaxf(bm0, fmaxf(sacc[i][0], sacc[i][2]));
+        bm1 = fmaxf(bm1, fmaxf(sacc[i][1], sacc[i][3]));
+    }
+#pragma unroll
+    for (int o = 4; o < 32; o <<= 1) {
+        bm0 = fmaxf(bm0, __shfl_xor_sync(0xffffffffu, bm0, o));
+        bm1 = fmaxf(bm1, __shfl_xor_sync(0xffffffffu, bm1, o));
+    }
+    const float mn0 = fmaxf(st.m[0], bm0), mn1 = fmaxf(st.m[1], bm1);
+    const float al0 = fast_exp2(st.m[0] - mn0), al1 = fast_exp2(st.m[1] - mn1);
+    st.m[0] = mn0;
+    st.m[1] = mn1;
+    float ls0 = 0.f, ls1 = 0.f;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        sacc[i][0] = fast_exp2(sacc[i][0] - mn0);
+        sacc[i][1] = fast_exp2(sacc[i][1] - mn1);
+        sacc[i][2] = fast_exp2(sacc[i][2] - mn0);
+        sacc[i][3] = fast_exp2(sacc[i][3] - mn1);
+        ls0 += sacc[i][0] + sacc[i][2];
+        ls1 += sacc[i][1] + sacc[i][3];
+    }
+    st.l[0] = st.l[0] * al0 + ls0;
+    st.l[1] = st.l[1] * al1 + ls1;
+#pragma unroll
+    for (int mm = 0; mm < 8; ++mm) {
+        st.o[mm][0] *= al0;
+        st.o[mm][1] *= al1;
+        st.o[mm][2] *= al0;
+        st.o[mm][3] *= al1;
+    }
+    const int srcA = 4 * tq + (gq >> 1), srcB = 4 * (tq + 4) + (gq >> 1);
+    const bool odd = (gq & 1) != 0;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+        const uint32_t H0 = pack_bf162(sacc[j][0], sacc[j][2]);
+        const uint32_t H1 = pack_bf162(sacc[j][1], sacc[j][3]);
+        const uint32_t x0 = __shfl_sync(0xffffffffu, H0, srcA);
+        const uint32_t x1 = __shfl_sync(0xffffffffu, H1, srcA);
+        const uint32_t y0 = __shfl_sync(0xffffffffu, H0, srcB);
+        const uint32_t y1 = __shfl_sync(0xffffffffu, H1, srcB);
+        const uint32_t bp0 = odd ? x1 : x0, bp1 = odd ? y1 : y0;
+        const int t1 = 16 * j + tq, t2 = t1 + 8, t3 = t1 + 4, t4 = t1 + 12;
+#pragma unroll
+        for (int mm = 0; mm < 8; ++mm) {
+            const int c0r = 16 * mm + gq, c1r = c0r + 8;
+            const uint32_t a0 = (uint32_t)V[t1 * D + c0r] | ((uint32_t)V[t2 * D + c0r] << 16);
+            const uint32_t a1 = (uint32_t)V[t1 * D + c1r] | ((uint32_t)V[t2 * D + c1r] << 16);
+            const uint32_t a2 = (uint32_t)V[t3 * D + c0r] | ((uint32_t)V[t4 * D + c0r] << 16);
+            const uint32_t a3 = (uint32_t)V[t3 * D + c1r] | ((uint32_t)V[t4 * D + c1r] << 16);
+            mma16816_bf16(st.o[mm], a0, a1, a2, a3, bp0, bp1);
+        }
+    }
+}
+
+template <int BITS>
+__global__ void __launch_bounds__(NTHREADS, 1) decode_attn_kernel(const AttnArgs a) {
+    using C = AttnCfg<BITS>;
+    extern __shared__ __align__(1024) uint8_t smem[];
+    float *merge = reinterpret_cast<float *>(smem + C::MERGE_OFF);
+    float *qs = reinterpret_cast<float *>(smem + C::QS_OFF);  // rotated q [8][D]
+    float *qr = reinterpret_cast<float *>(smem + C::QR_OFF);  // raw q [8][D]
+    uint64_t *full = reinterpret_cast<uint64_t *>(smem + C::BAR_OFF);
+    uint64_t *empty = full + C::NST;
+    int *misc = reinterpret_cast<int *>(smem + C::MISC_OFF);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int cta = blockIdx.x;
+    const int64_t nb = a.nb;
+    const int64_t total = (int64_t)a.BH * nb;
+    int64_t start, end;
+    if (total > 0) {
+        start = (cta * total) / a.ncta;
+        end = ((cta + 1) * total) / a.ncta;
+    } else {
+        start = end = 0;
+    }
+
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < C::NST; ++i) {
+            mbar_init(&full[i], 1);
+            mbar_init(&empty[i], 1);
+        }
+        fence_mbar_init();
+    }
+    __syncthreads();
+
+    if (warp == NCW) {
+        // ================= producer =================
+        if (lane == 0 && end > start) {
+            const uint64_t pol = l2_evict_first_policy();
+            for (int64_t p = 0; p < end - start; ++p) {
+                const int64_t gidx = start + p;
+                const int64_t bh = gidx / nb, blk = gidx % nb;
+                const int stg = (int)(p % C::NST);
+                if (p >= C::NST) mbar_wait(&empty[stg], (uint32_t)(((p / C::NST) - 1) & 1));
+                mbar_arrive_expect_tx(&full[stg], C::BYTES);
+                bulk_g2s(smem + stg * C::BYTES, a.blocks + (bh * a.max_blocks + blk) * (int64_t)C::BYTES, C::BYTES,
+                         &full[stg], pol);
+            }
+        }
+        return;
+    }
+
+    // ================= consumers =================
+    const float c0 = LOG2E * 0.08838834764831845f;  // log2(e)/sqrt(128)
+    const int gq = lane >> 2, tq = lane & 3;
+    const int g = a.g;
+
+    // segments: residual-only mode (nb == 0): CTA c <-> bh c
+    int64_t seg_bh_first, seg_bh_last;
+    if (total > 0) {
+        if (end <= start) return;
+        seg_bh_first = start / nb;
+        seg_bh_last = (end - 1) / nb;
+    } else {
+        if (cta >= a.BH) return;
+        seg_bh_first = seg_bh_last = cta;
+    }
+
+    for (int64_t bh = seg_bh_first; bh <= seg_bh_last; ++bh) {
+        const int b = (int)(bh / a.Hkv), kvh = (int)(bh % a.Hkv);
+        const int64_t lo = total > 0 ? (bh * nb > start ? bh * nb : start) : 0;
+        const int64_t hi = total > 0 ? ((bh + 1) * nb < end ? (bh + 1) * nb : end) : 0;
+        const bool owns_tail = total == 0 || hi == (bh + 1) * nb;
+
+        // ---- q for this (b, kv head): raw and rotated, fp32 in smem ----
+        for (int j = warp; j < 8; j += NCW) {
+            float x[4] = {0.f, 0.f, 0.f, 0.f};
+            if (j < g) {
+                load_bf16x4(reinterpret_cast<const __nv_bfloat16 *>(a.q) + ((int64_t)b * a.Hq + kvh * g + j) * D +
+                                lane * 4,
+                            x);
+            }
+#pragma unroll
+            for (int e = 0; e < 4; ++e) qr[j * D + lane * 4 + e] = x[e];
+            if (a.rotates) fht128_warp(x, lane);
+#pragma unroll
+            for (int e = 0; e < 4; ++e) qs[j * D + lane * 4 + e] = x[e];
+        }
+        named_bar(1, NCW * 32);
+        uint32_t qf[8][2];
+#pragma unroll
+        for (int s = 0; s < 8; ++s) {
+            const float *qrow = qs + gq * D + 16 * s + 2 * tq;
+            if (BITS == 0) {
+                // bf16 baseline attends raw K: use the raw q
+                const float *rrow = qr + gq * D + 16 * s + 2 * tq;
+                qf[s][0] = pack_bf162(rrow[0], rrow[1]);
+                qf[s][1] = pack_bf162(rrow[8], rrow[9]);
+            } else {
+                qf[s][0] = pack_half2(qrow[0], qrow[1]);
+                qf[s][1] = pack_half2(qrow[8], qrow[9]);
+            }
+        }
+
+        WarpState st;
+#pragma unroll
+        for (int mm = 0; mm < 8; ++mm) st.o[mm][0] = st.o[mm][1] = st.o[mm][2] = st.o[mm][3] = 0.f;
+        st.ob[0] = st.ob[1] = st.ob[2] = st.ob[3] = 0.f;
+        st.m[0] = st.m[1] = -CUDART_INF_F;
+        st.l[0] = st.l[1] = 0.f;
+
+        // ---- packed blocks of this segment: positions p = gidx - start, p % NCW == warp ----
+        if (total > 0) {
+            int64_t p0 = lo - start;
+            int64_t first = p0 + ((warp - (int)(p0 % NCW)) + NCW) % NCW;
+            for (int64_t p = first; p < hi - start; p += NCW) {
+                const int stg = (int)(p % C::NST);
+                mbar_wait(&full[stg], (uint32_t)((p / C::NST) & 1));
+                const uint8_t *sb = smem + stg * C::BYTES;
+                if constexpr (BITS == 0) {
+                    process_block_bf16(sb, st, qf, lane, c0);
+                } else {
+                    process_block<BITS>(sb, st, qf, lane, c0);
+                }
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&empty[stg]);
+            }
+        }
+
+        // ---- warp partial -> merge slot (unnormalized O[h][c], m[h], l[h]) ----
+        float *slot = merge + warp * MERGE_FLOATS;
+        {
+            float l0 = st.l[0], l1 = st.l[1];
+#pragma unroll
+            for (int o = 4; o < 32; o <<= 1) {
+                l0 += __shfl_xor_sync(0xffffffffu, l0, o);
+                l1 += __shfl_xor_sync(0xffffffffu, l1, o);
+            }
+            float vb0[4], vb1[4];
+#pragma unroll
+            for (int gc = 0; gc < 4; ++gc) {
+                vb0[gc] = __shfl_sync(0xffffffffu, st.ob[0], gc * 4 + tq);
+                vb1[gc] = __shfl_sync(0xffffffffu, st.ob[1], gc * 4 + tq);
+            }
+            constexpr int TPW = BITS == 0 ? 8 : 16 / (BITS == 0 ? 2 : BITS);
+            constexpr int HALFT = TPW / 2;
+#pragma unroll
+            for (int mm = 0; mm < 8; ++mm) {
+                const int fs = (mm % TPW) % HALFT;
+                const float sc = (BITS == 0) ? 1.f : __int_as_float((127 + 24 - (BITS == 0 ? 0 : BITS) * fs) << 23);
+                const int cA = 16 * mm + gq, cB = cA + 8;
+                const int h0 = 2 * tq, h1 = 2 * tq + 1;
+                const float bb0 = BITS == 0 ? 0.f : vb0[mm >> 1], bb1 = BITS == 0 ? 0.f : vb1[mm >> 1];
+                slot[h0 * D + cA] = st.o[mm][0] * sc + bb0;
+                slot[h1 * D + cA] = st.o[mm][1] * sc + bb1;
+                slot[h0 * D + cB] = st.o[mm][2] * sc + bb0;
+                slot[h1 * D + cB] = st.o[mm][3] * sc + bb1;
+            }
+            if (gq == 0) {
+                slot[8 * D + 2 * tq] = st.m[0];
+                slot[8 * D + 2 * tq + 1] = st.m[1];
+                slot[8 * D + 8 + 2 * tq] = l0;
+                slot[8 * D + 8 + 2 * tq + 1] = l1;
+            }
+            __syncwarp();
+        }
+
+        // ---- residual window + current token (fp32 CUDA cores), merged into the slot ----
+        if (owns_tail) {
+            const int ntok = a.r + (a.kcur ? 1 : 0);
+            if (warp < ntok) {
+                float qv[8][4];
+#pragma unroll
+                for (int j = 0; j < 8; ++j)
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) qv[j][e] = qr[j * D + lane * 4 + e];
+                float mr[8], lr[8], orr[8][4];
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                    mr[j] = -CUDART_INF_F;
+                    lr[j] = 0.f;
+                    orr[j][0] = orr[j][1] = orr[j][2] = orr[j][3] = 0.f;
+                }
+                for (int t = warp; t < ntok; t += NCW) {
+                    const __nv_bfloat16 *kp, *vp;
+                    if (t < a.r) {
+                        kp = reinterpret_cast<const __nv_bfloat16 *>(a.ring_k) + (bh * R + t) * D;
+                        vp = reinterpret_cast<const __nv_bfloat16 *>(a.ring_v) + (bh * R + t) * D;
+                    } else {
+                        kp = reinterpret_cast<const __nv_bfloat16 *>(a.kcur) + ((int64_t)b * a.Hkv + kvh) * D;
+                        vp = reinterpret_cast<const __nv_bfloat16 *>(a.vcur) + ((int64_t)b * a.Hkv + kvh) * D;
+                    }
+                    float k4[4], v4[4];
+                    load_bf16x4(kp + lane * 4, k4);
+                    load_bf16x4(vp + lane * 4, v4);
+                    if (a.rotate_v) fht128_warp(v4, lane);
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) {
+                        if (j < g) {
+                            float d = qv[j][0] * k4[0] + qv[j][1] * k4[1] + qv[j][2] * k4[2] + qv[j][3] * k4[3];
+                            d = warp_sum(d) * c0;
+                            const float mn = fmaxf(mr[j], d);
+                            const float al = fast_exp2(mr[j] - mn), pp = fast_exp2(d - mn);
+                            lr[j] = lr[j] * al + pp;
+#pragma unroll
+                            for (int e = 0; e < 4; ++e) orr[j][e] = orr[j][e] * al + pp * v4[e];
+                            mr[j] = mn;
+                        }
+                    }
+                }
+                // merge with the packed-block partial in this warp's slot
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                    if (j < g) {
+                        const float ms = slot[8 * D + j], ls = slot[8 * D + 8 + j];
+                        const float M = fmaxf(ms, mr[j]);
+                        const float fs = (ms == -CUDART_INF_F) ? 0.f : fast_exp2(ms - M);
+                        const float fr = (mr[j] == -CUDART_INF_F) ? 0.f : fast_exp2(mr[j] - M);
+#pragma unroll
+                        for (int e = 0; e < 4; ++e) {
+                            float *op = slot + j * D + lane * 4 + e;
+                            *op = *op * fs + orr[j][e] * fr;
+                        }
+                        __syncwarp();
+                        if (lane == 0) {
+                            slot[8 * D + j] = M;
+                            slot[8 * D + 8 + j] = ls * fs + lr[j] * fr;
+                        }
+                    }
+                }
+                __syncwarp();
+            }
+        }
+        named_bar(1, NCW * 32);
+
+        // ---- CTA merge of the NCW warp partials -> global partial slot ----
+        int64_t first_cta = 0, last_cta = 0;
+        if (total > 0) {
+            first_cta = cta_of(bh * nb, total, a.ncta);
+            last_cta = cta_of((bh + 1) * nb - 1, total, a.ncta);
+        }
+        const int expected = (int)(last_cta - first_cta + 1);
+        const int pslot = (int)(total > 0 ? cta - first_cta : 0);
+        float *po = a.part_o + ((int64_t)bh * a.maxp + pslot) * 8 * D;
+        float *pml = a.part_ml + ((int64_t)bh * a.maxp + pslot) * 16;
+        for (int idx = threadIdx.x; idx < g * D; idx += NCW * 32) {
+            const int h = idx / D;
+            float M = -CUDART_INF_F;
+#pragma unroll
+            for (int w = 0; w < NCW; ++w) M = fmaxf(M, merge[w * MERGE_FLOATS + 8 * D + h]);
+            float O = 0.f, L = 0.f;
+#pragma unroll
+            for (int w = 0; w < NCW; ++w) {
+                const float mw = merge[w * MERGE_FLOATS + 8 * D + h];
+                const float f = (mw == -CUDART_INF_F) ? 0.f : fast_exp2(mw - M);
+                O += merge[w * MERGE_FLOATS + idx] * f;
+                L += merge[w * MERGE_FLOATS + 8 * D + 8 + h] * f;
+            }
+            po[idx] = O;
+            if ((idx % D) == 0) {
+                pml[2 * h] = M;
+                pml[2 * h + 1] = L;
+            }
+        }
+        __threadfence();
+        named_bar(1, NCW * 32);
+        if (threadIdx.x == 0) {
+            const int prev = atomicAdd(&a.counters[bh], 1);
+            misc[0] = (prev == expected - 1) ? 1 : 0;
+        }
+        named_bar(1, NCW * 32);
+        const bool last = misc[0] != 0;
+        if (last) {
+            __threadfence();
+            // final merge across the CTA partials of this (b, kv head)
+            float *ob = merge;  // reuse: normalized O [8][D]
+            for (int idx = threadIdx.x; idx < g * D; idx += NCW * 32) {
+                const int h = idx / D;
+                const float *pmb = a.part_ml + (int64_t)bh * a.maxp * 16;
+                const float *pob = a.part_o + (int64_t)bh * a.maxp * 8 * D;
+                float M = -CUDART_INF_F;
+                for (int s = 0; s < expected; ++s) M = fmaxf(M, __ldcg(pmb + s * 16 + 2 * h));
+                float O = 0.f, L = 0.f;
+                for (int s = 0; s < expected; ++s) {
+                    const float ms = __ldcg(pmb + s * 16 + 2 * h);
+                    const float f = (ms == -CUDART_INF_F) ? 0.f : fast_exp2(ms - M);
+                    O += __ldcg(pob + s * 8 * D + idx) * f;
+                    L += __ldcg(pmb + s * 16 + 2 * h + 1) * f;
+                }
+                const float v = (L > 0.f) ? O / L : 0.f;
+                if (a.rotate_v) {
+                    ob[idx] = v;
+                } else {
+                    a.out[((int64_t)b * a.Hq + kvh * g + h) * D + (idx % D)] = v;
+                }
+                if (a.lse && (idx % D) == 0)
+                    a.lse[(int64_t)b * a.Hq + kvh * g + h] = (L > 0.f) ? (M + __log2f(L)) * LN2 : -CUDART_INF_F;
+            }
+            if (a.rotate_v) {
+                named_bar(1, NCW * 32);
+                for (int j = warp; j < g; j += NCW) {
+                    float x[4];
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) x[e] = ob[j * D + lane * 4 + e];
+                    fht128_warp(x, lane);
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) a.out[((int64_t)b * a.Hq + kvh * g + j) * D + lane * 4 + e] = x[e];
+                }
+            }
+            if (threadIdx.x == 0) a.counters[bh] = 0;
+        }
+        // current token -> residual ring (after everyone read the ring)
+        if (owns_tail && a.write_ring && a.kcur) {
+            if (warp == 0) {
+                const uint2 *ks = reinterpret_cast<const uint2 *>(reinterpret_cast<const __nv_bfloat16 *>(a.kcur) +
+                                                                   ((int64_t)b * a.Hkv + kvh) * D);
+                const uint2 *vs = reinterpret_cast<const uint2 *>(reinterpret_cast<const __nv_bfloat16 *>(a.vcur) +
+                                                                   ((int64_t)b * a.Hkv + kvh) * D);
+                reinterpret_cast<uint2 *>(reinterpret_cast<__nv_bfloat16 *>(a.ring_k) + (bh * R + a.r) * D)[lane] =
+                    ks[lane];
+                reinterpret_cast<uint2 *>(reinterpret_cast<__nv_bfloat16 *>(a.ring_v) + (bh * R + a.r) * D)[lane] =
+                    vs[lane];
+            }
+        }
+        named_bar(1, NCW * 32);
+    }
+}
+
+__global__ void lse_merge_kernel(const float *outs, const float *lses, int64_t parts, int64_t rows, int64_t d,
+                                 float *out, float *lse_out) {
+    const int64_t row = blockIdx.x;
+    float M = -CUDART_INF_F;
+    for (int64_t p = 0; p < parts; ++p) M = fmaxf(M, lses[p * rows + row]);
+    for (int64_t c = threadIdx.x; c < d; c += blockDim.x) {
+        float O = 0.f, L = 0.f;
+        for (int64_t p = 0; p < parts; ++p) {
+            const float l = lses[p * rows + row];
+            const float w = (l == -CUDART_INF_F) ? 0.f : __expf(l - M);
+            O += outs[(p * rows + row) * d + c] * w;
+            L += w;
+        }
+        out[row * d + c] = L > 0.f ? O / L : 0.f;
+        if (lse_out && c == 0) lse_out[row] = L > 0.f ? M + __logf(L) : -CUDART_INF_F;
+    }
+}
+
+template <int BITS>
+cudaError_t launch_t(const AttnArgs &a, cudaStream_t st) {
+    using C = AttnCfg<BITS>;
+    static bool init = false;
+    if (!init) {
+        cudaError_t e = cudaFuncSetAttribute(decode_attn_kernel<BITS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             C::SMEM);
+        if (e != cudaSuccess) return e;
+        init = true;
+    }
+    decode_attn_kernel<BITS><<<a.ncta, NTHREADS, C::SMEM, st>>>(a);
+    return cudaGetLastError();
+}
+
+}  // namespace
+
+int attention_grid(int bits, int num_sms, int64_t nb, int BH) {
+    (void)bits;
+    const int64_t total = nb * BH;
+    if (total == 0) return BH;
+    return (int)(total < num_sms ? total : num_sms);
+}
+
+int attention_max_partials(int64_t nb, int BH, int ncta) {
+    const int64_t total = nb * BH;
+    if (total == 0) return 1;
+    const int64_t per = total / ncta;  // >= 1
+    return (int)(nb / (per > 0 ? per : 1) + 2);
+}
+
+cudaError_t launch_attention(int bits, const AttnArgs &a, cudaStream_t st) {
+    switch (bits) {
+        case 2: return launch_t<2>(a, st);
+        case 4: return launch_t<4>(a, st);
+        case 0: return launch_t<0>(a, st);
+        default: return cudaErrorInvalidValue;
+    }
+}
+
+cudaError_t launch_lse_merge(const float *outs, const float *lses, int64_t parts, int64_t rows, int64_t d, float *out,
+                             float *lse_out, cudaStream_t st) {
+    if (rows == 0) return cudaSuccess;
+    lse_merge_kernel<<<(unsigned)rows, 128, 0, st>>>(outs, lses, parts, rows, d, out, lse_out);
+    return cudaGetLastError();
+}
+
+}  // namespace osk

@@ -1,0 +1,757 @@
+// capi.cpp -- host runtime behind include/oscar_kv.h.
+//
+// Mirrors the reference KvCache state machine (kv_cache.cpp:194-292) on the
+// host (token counters only -- every sequence of a handle advances together)
+// and drives the device kernels:
+//   prefill      -> quantize kernel over the S - S mod R full blocks + ring copy
+//   append       -> ring copy, flush (quantize kernel from the ring) at exactly R
+//   decode_step  -> ONE attention kernel (attends cache + current token, writes
+//                   the current token into the ring) [+ flush kernel when the
+//                   window fills, after the attention -- pipeline.cpp:294-323]
+// and converts the device cache back into the reference's layout (export,
+// KVC1 dump, materialize).  Compiled with -ffp-contract=off.
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <fstream>
+#include <memory>
+#include <sstream>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/oscar_kv.h"
+#include "host_ref.h"
+#include "kernels.h"
+#include "layout.h"
+
+using namespace osk;
+
+namespace {
+
+thread_local std::string g_err;
+
+struct InvalidArg : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+struct LogicErr : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+struct CudaErr : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+
+#define CK(x)                                                                                       \
+    do {                                                                                            \
+        cudaError_t e_ = (x);                                                                       \
+        if (e_ != cudaSuccess) throw CudaErr(std::string(#x) + ": " + cudaGetErrorString(e_));    \
+    } while (0)
+
+template <typename F>
+int guard(F &&f) {
+    try {
+        f();
+        return 0;
+    } catch (const InvalidArg &e) {
+        g_err = e.what();
+        return 1;
+    } catch (const LogicErr &e) {
+        g_err = e.what();
+        return 2;
+    } catch (const std::exception &e) {
+        g_err = e.what();
+        return 3;
+    }
+}
+
+bool rotates(const oscar_kv_config &c) { return c.method == OSCAR_ROTATE_ONLY || c.method == OSCAR_OSCAR; }
+bool scales(const oscar_kv_config &c) { return c.method == OSCAR_SCALE_ONLY || c.method == OSCAR_OSCAR; }
+bool quantizes(const oscar_kv_config &c) { return c.method != OSCAR_FP && c.bits != 0; }
+
+void validate(const oscar_kv_config &c) {
+    // PipelineConfig::validate (kv_cache.cpp:51-67)
+    if (c.heads <= 0 || c.head_dim <= 0) throw InvalidArg("config: heads and head_dim must be positive");
+    if (c.bits != 0 && c.bits != 2 && c.bits != 3 && c.bits != 4 && c.bits != 8 && c.bits != 16)
+        throw InvalidArg("config: bits must be one of 0,2,3,4,8,16");
+    if (c.residual_len <= 0 || c.group_size <= 0 || c.residual_len % c.group_size != 0)
+        throw InvalidArg("config: residual_len must be a positive multiple of group_size");
+    if (quantizes(c) && c.head_dim % c.group_size != 0)
+        throw InvalidArg("config: head_dim must be divisible by group_size for the value path");
+    if (rotates(c) && (c.head_dim & (c.head_dim - 1)) != 0)
+        throw InvalidArg("config: head_dim must be a power of two when rotating");
+    if (c.method < 0 || c.method > 4) throw InvalidArg("config: unknown method");
+    if (c.scaling < 0 || c.scaling > 3) throw InvalidArg("config: unknown scaling strategy");
+    // device kernel limits
+    if (c.head_dim != D) throw InvalidArg("device: head_dim must be 128");
+    if (c.residual_len != R) throw InvalidArg("device: residual_len must be 128");
+    if (quantizes(c) && c.group_size != G) throw InvalidArg("device: group_size must be 32");
+    if (quantizes(c) && c.bits != 2 && c.bits != 4) throw InvalidArg("device: bits must be 0, 2 or 4");
+}
+
+}  // namespace
+
+struct oscar_kv_handle {
+    oscar_kv_config cfg{};
+    int dbits = 0;  // 0, 2, 4 (effective device format)
+    int64_t B = 0, Hq = 0, g = 0, BH = 0, max_tokens = 0, max_blocks = 0;
+    int device = 0, num_sms = 148;
+    bool keep_exact = true;
+    int64_t block_bytes = 0;
+    // state (kv_cache.hpp:104-122), uniform over the batch
+    bool prefilled = false;
+    int64_t packed = 0, residual = 0, flushes = 0;
+    // device memory
+    uint8_t *blocks = nullptr;
+    double *shadow = nullptr;
+    void *ring_k = nullptr, *ring_v = nullptr;
+    float *part_o = nullptr, *part_ml = nullptr;
+    int *counters = nullptr;
+    int maxp_alloc = 0;
+    void *stage = nullptr;  // host-API staging: q, k, v, out, lse
+    int64_t device_bytes = 0;
+    int last_launches = 0;
+    cudaStream_t last_stream = nullptr;
+
+    TransformCfg tc() const {
+        TransformCfg t;
+        t.bits = dbits;
+        t.rotates = rotates(cfg);
+        t.scales = scales(cfg);
+        t.scaling = cfg.scaling;
+        t.rotate_v = cfg.rotate_v;
+        return t;
+    }
+
+    void *dalloc(size_t bytes) {
+        void *p = nullptr;
+        CK(cudaMalloc(&p, bytes));
+        device_bytes += (int64_t)bytes;
+        return p;
+    }
+
+    ~oscar_kv_handle() {
+        cudaSetDevice(device);
+        cudaFree(blocks);
+        cudaFree(shadow);
+        cudaFree(ring_k);
+        cudaFree(ring_v);
+        cudaFree(part_o);
+        cudaFree(part_ml);
+        cudaFree(counters);
+        cudaFree(stage);
+    }
+
+    // ---- kernels --------------------------------------------------------------
+    void quantize_from(const void *k, const void *v, int64_t sb, int64_t st, int64_t sh, int64_t tok0,
+                       int64_t nblk, int64_t blk0, cudaStream_t s) {
+        QuantizeArgs a{};
+        a.k = k;
+        a.v = v;
+        a.sb = sb;
+        a.st = st;
+        a.sh = sh;
+        a.tok0 = tok0;
+        a.B = (int)B;
+        a.H = (int)cfg.heads;
+        a.n_blocks = nblk;
+        a.blocks = blocks;
+        a.max_blocks = max_blocks;
+        a.blk0 = blk0;
+        a.shadow = shadow;
+        a.tc = tc();
+        CK(launch_quantize(a, s));
+        ++last_launches;
+    }
+    void ring_copy(const void *k, const void *v, int64_t sb, int64_t st, int64_t sh, int64_t tok0, int64_t n,
+                   int64_t slot0, cudaStream_t s) {
+        RingCopyArgs a{};
+        a.k = k;
+        a.v = v;
+        a.sb = sb;
+        a.st = st;
+        a.sh = sh;
+        a.tok0 = tok0;
+        a.B = (int)B;
+        a.H = (int)cfg.heads;
+        a.n = n;
+        a.ring_k = ring_k;
+        a.ring_v = ring_v;
+        a.slot0 = slot0;
+        CK(launch_ring_copy(a, s));
+        ++last_launches;
+    }
+    void flush(cudaStream_t s) {
+        // the ring [bh][R][D] is the source of one block per (b, h)
+        const int64_t H = cfg.heads;
+        quantize_from(ring_k, ring_v, H * R * D, D, (int64_t)R * D, 0, 1, packed / R, s);
+        packed += R;
+        residual = 0;
+    }
+
+    void append(const void *k, const void *v, int64_t n, cudaStream_t s) {
+        const int64_t H = cfg.heads;
+        if (n < 0) throw InvalidArg("append: negative token count");
+        if (packed + residual + n > max_tokens) throw InvalidArg("append: cache capacity exceeded");
+        last_launches = 0;
+        const int64_t sb = n * H * D, st = H * D, sh = D;
+        if (!prefilled) {
+            // prefill branch (kv_cache.cpp:204-218)
+            prefilled = true;
+            const int64_t r = n % R;
+            const int64_t nfull = (n - r) / R;
+            if (nfull > 0) quantize_from(k, v, sb, st, sh, 0, nfull, 0, s);
+            packed += n - r;
+            if (r > 0) ring_copy(k, v, sb, st, sh, n - r, r, 0, s);
+            residual = r;
+            return;
+        }
+        // decode branch (kv_cache.cpp:219-249): token by token, flush at exactly R
+        int64_t pos = 0;
+        while (pos < n) {
+            const int64_t m = std::min(n - pos, R - residual);
+            ring_copy(k, v, sb, st, sh, pos, m, residual, s);
+            residual += m;
+            pos += m;
+            if (residual == R) {
+                flush(s);
+                ++flushes;
+            }
+        }
+    }
+
+    AttnArgs attn_args(const void *q, const void *kc, const void *vc, float *out, float *lse) {
+        AttnArgs a{};
+        a.blocks = blocks;
+        a.max_blocks = max_blocks;
+        a.nb = packed / R;
+        a.BH = (int)BH;
+        a.Hkv = (int)cfg.heads;
+        a.g = (int)g;
+        a.Hq = (int)Hq;
+        a.q = q;
+        a.kcur = kc;
+        a.vcur = vc;
+        a.ring_k = ring_k;
+        a.ring_v = ring_v;
+        a.r = (int)residual;
+        a.write_ring = kc != nullptr;
+        a.rotates = dbits != 0 && rotates(cfg);
+        a.scales = scales(cfg);
+        a.rotate_v = dbits != 0 && cfg.rotate_v;
+        a.out = out;
+        a.lse = lse;
+        a.part_o = part_o;
+        a.part_ml = part_ml;
+        a.counters = counters;
+        a.ncta = attention_grid(dbits, num_sms, a.nb, a.BH);
+        a.maxp = maxp_alloc;
+        // exact partial-slot requirement
+        if (a.nb > 0) {
+            const int64_t total = a.nb * a.BH;
+            auto cta_of = [&](int64_t x) { return ((x + 1) * a.ncta - 1) / total; };
+            int64_t need = 0;
+            for (int64_t bh = 0; bh < a.BH; ++bh)
+                need = std::max(need, cta_of((bh + 1) * a.nb - 1) - cta_of(bh * a.nb) + 1);
+            if (need > maxp_alloc) throw LogicErr("internal: partial buffer too small");
+        }
+        return a;
+    }
+
+    void decode_step(const void *q, const void *k, const void *v, float *out, float *lse, cudaStream_t s) {
+        if (packed + residual + 1 > max_tokens) throw InvalidArg("decode_step: cache capacity exceeded");
+        last_launches = 0;
+        AttnArgs a = attn_args(q, k, v, out, lse);
+        CK(launch_attention(dbits, a, s));
+        ++last_launches;
+        // buffer_quant_k/v of the current token (written into the ring by the kernel)
+        prefilled = true;
+        residual += 1;
+        if (residual == R) {
+            flush(s);
+            ++flushes;
+        }
+    }
+
+    void attend(const void *q, float *out, float *lse, cudaStream_t s) {
+        last_launches = 0;
+        if (packed + residual == 0) throw LogicErr("attend: empty cache");
+        AttnArgs a = attn_args(q, nullptr, nullptr, out, lse);
+        CK(launch_attention(dbits, a, s));
+        ++last_launches;
+    }
+};
+
+namespace {
+
+// ---------------------------------------------------------------------------
+// export: device layout -> reference layout for one sequence
+struct HostCache {
+    int bits = 2;
+    int64_t H = 0, nblk = 0, packed = 0, r = 0;
+    // per head, per block
+    std::vector<std::vector<std::vector<uint16_t>>> k_codes, v_codes;  // reference order
+    std::vector<std::vector<std::vector<double>>> k_delta, k_const, v_delta, v_const;
+    std::vector<std::vector<std::vector<int64_t>>> k_zp, v_zp;
+    std::vector<std::vector<std::vector<double>>> k_raw, v_raw;  // bits 0
+    std::vector<std::vector<double>> k_norms;                    // per head [packed]
+    std::vector<double> k_res, k_norms_res, v_res;                // [r][H][d], [r*H]
+};
+
+HostCache build_host_cache(oscar_kv_handle *h, int64_t b) {
+    if (b < 0 || b >= h->B) throw InvalidArg("export: sequence index out of range");
+    if (h->last_stream) CK(cudaStreamSynchronize(h->last_stream));
+    CK(cudaDeviceSynchronize());
+    HostCache hc;
+    const oscar_kv_config &cfg = h->cfg;
+    const int64_t H = cfg.heads;
+    hc.bits = h->dbits;
+    hc.H = H;
+    hc.packed = h->packed;
+    hc.nblk = h->packed / R;
+    hc.r = h->residual;
+    const bool quant = h->dbits != 0;
+    if (quant && !h->keep_exact) throw InvalidArg("export: handle created without keep_exact");
+    const TransformCfg tc = h->tc();
+    auto resize3 = [&](auto &v, size_t inner) {
+        v.assign(H, {});
+        for (auto &x : v) x.assign(hc.nblk, std::vector<typename std::decay_t<decltype(v[0][0])>::value_type>(inner));
+    };
+    if (quant) {
+        resize3(hc.k_codes, R * D);
+        resize3(hc.v_codes, R * D);
+        resize3(hc.k_delta, D * (R / G));
+        resize3(hc.k_const, D * (R / G));
+        resize3(hc.k_zp, D * (R / G));
+        resize3(hc.v_delta, R * (D / G));
+        resize3(hc.v_const, R * (D / G));
+        resize3(hc.v_zp, R * (D / G));
+    } else {
+        resize3(hc.k_raw, R * D);
+        resize3(hc.v_raw, R * D);
+    }
+    hc.k_norms.assign(H, std::vector<double>(hc.packed));
+    std::vector<uint8_t> blk(h->block_bytes);
+    std::vector<double> sh(SHADOW_DOUBLES);
+    for (int64_t hh = 0; hh < H; ++hh) {
+        const int64_t bh = b * H + hh;
+        for (int64_t k = 0; k < hc.nblk; ++k) {
+            const int64_t rec = bh * h->max_blocks + k;
+            CK(cudaMemcpy(blk.data(), h->blocks + rec * h->block_bytes, h->block_bytes, cudaMemcpyDeviceToHost));
+            if (quant) {
+                CK(cudaMemcpy(sh.data(), h->shadow + rec * SHADOW_DOUBLES, sizeof(double) * SHADOW_DOUBLES,
+                              cudaMemcpyDeviceToHost));
+                const int bits = h->dbits;
+                const int tpw = 16 / bits;
+                const int64_t code_bytes = (int64_t)R * D * bits / 8;
+                const uint32_t *kw = reinterpret_cast<const uint32_t *>(blk.data());
+                const uint32_t *vw = reinterpret_cast<const uint32_t *>(blk.data() + code_bytes);
+                const int nwords = (int)(code_bytes / 4);
+                const uint32_t fmask = (1u << bits) - 1;
+                auto &kc = hc.k_codes[hh][k];
+                auto &vc = hc.v_codes[hh][k];
+                for (int w = 0; w < nwords; ++w)
+                    for (int hi = 0; hi < 2; ++hi)
+                        for (int f = 0; f < tpw; ++f) {
+                            int t, c;
+                            const int sh_ = hi * 16 + f * bits;
+                            k_word_coords(bits, w, f, hi, t, c);
+                            kc[(size_t)c * R + t] = (uint16_t)((kw[w] >> sh_) & fmask);  // j*R + t
+                            v_word_coords(bits, w, f, hi, t, c);
+                            vc[(size_t)t * D + c] = (uint16_t)((vw[w] >> sh_) & fmask);  // t*d + c
+                        }
+                for (int c = 0; c < D; ++c)
+                    for (int grp = 0; grp < R / G; ++grp) {
+                        const int p = c * (R / G) + grp;  // kv_cache.cpp:114
+                        host::params_from_lohi(sh[(c * NGRP + grp) * 2], sh[(c * NGRP + grp) * 2 + 1], bits,
+                                               hc.k_delta[hh][k][p], hc.k_zp[hh][k][p], hc.k_const[hh][k][p]);
+                    }
+                for (int t = 0; t < R; ++t)
+                    for (int gc = 0; gc < D / G; ++gc) {
+                        const int p = t * (D / G) + gc;  // kv_cache.cpp:144
+                        host::params_from_lohi(sh[SHADOW_K_DOUBLES + (t * NGC + gc) * 2],
+                                               sh[SHADOW_K_DOUBLES + (t * NGC + gc) * 2 + 1], bits,
+                                               hc.v_delta[hh][k][p], hc.v_zp[hh][k][p], hc.v_const[hh][k][p]);
+                    }
+                for (int t = 0; t < R; ++t)
+                    hc.k_norms[hh][k * R + t] = sh[SHADOW_K_DOUBLES + SHADOW_V_DOUBLES + t];
+            } else {
+                // raw bf16 block: K rows -> apply_method transform in fp64 (exact replay)
+                const uint16_t *kr = reinterpret_cast<const uint16_t *>(blk.data());
+                const uint16_t *vr = kr + R * D;
+                for (int t = 0; t < R; ++t) {
+                    double row[D];
+                    for (int c = 0; c < D; ++c) row[c] = host::bf16_to_double(kr[t * D + c]);
+                    double s = 1.0;
+                    if (tc.rotates) host::fht(row, D);
+                    if (tc.scales) s = host::token_scale(row, D, cfg.scaling);
+                    for (int c = 0; c < D; ++c) hc.k_raw[hh][k][t * D + c] = row[c];
+                    hc.k_norms[hh][k * R + t] = s;
+                    for (int c = 0; c < D; ++c) row[c] = host::bf16_to_double(vr[t * D + c]);
+                    if (cfg.rotate_v) host::fht(row, D);
+                    for (int c = 0; c < D; ++c) hc.v_raw[hh][k][t * D + c] = row[c];
+                }
+            }
+        }
+    }
+    // residual window: raw bf16 ring -> K_u rows and norms (kv_cache.cpp:219-224)
+    hc.k_res.assign(hc.r * H * D, 0.0);
+    hc.k_norms_res.assign(hc.r * H, 0.0);
+    hc.v_res.assign(hc.r * H * D, 0.0);
+    std::vector<uint16_t> rk(R * D), rv(R * D);
+    for (int64_t hh = 0; hh < H; ++hh) {
+        const int64_t bh = b * H + hh;
+        if (hc.r == 0) break;
+        CK(cudaMemcpy(rk.data(), reinterpret_cast<uint16_t *>(h->ring_k) + bh * R * D, sizeof(uint16_t) * R * D,
+                      cudaMemcpyDeviceToHost));
+        CK(cudaMemcpy(rv.data(), reinterpret_cast<uint16_t *>(h->ring_v) + bh * R * D, sizeof(uint16_t) * R * D,
+                      cudaMemcpyDeviceToHost));
+        for (int64_t t = 0; t < hc.r; ++t) {
+            double row[D];
+            for (int c = 0; c < D; ++c) row[c] = host::bf16_to_double(rk[t * D + c]);
+            double s = 1.0;
+            if (tc.rotates) host::fht(row, D);
+            if (tc.scales) s = host::token_scale(row, D, cfg.scaling);
+            for (int c = 0; c < D; ++c) hc.k_res[(t * H + hh) * D + c] = row[c];
+            hc.k_norms_res[t * H + hh] = s;
+            for (int c = 0; c < D; ++c) row[c] = host::bf16_to_double(rv[t * D + c]);
+            if (cfg.rotate_v) host::fht(row, D);
+            for (int c = 0; c < D; ++c) hc.v_res[(t * H + hh) * D + c] = row[c];
+        }
+    }
+    return hc;
+}
+
+// pack_2bit (quant.cpp:162-175)
+std::vector<uint16_t> pack2(const std::vector<uint16_t> &codes) {
+    std::vector<uint16_t> w((codes.size() + 7) / 8, 0);
+    for (size_t i = 0; i < codes.size(); ++i) w[i / 8] = (uint16_t)(w[i / 8] | (codes[i] << (2 * (i % 8))));
+    return w;
+}
+
+const char *method_name(int m) {
+    static const char *n[] = {"fp", "kivi", "rotate-only", "scale-only", "oscar"};
+    return n[m];
+}
+const char *scaling_name(int s) {
+    static const char *n[] = {"l2", "rsqrt", "max", "mean-abs"};
+    return n[s];
+}
+
+}  // namespace
+
+// ===========================================================================
+extern "C" {
+
+const char *oscar_last_error(void) { return g_err.c_str(); }
+
+int oscar_kv_config_validate(const oscar_kv_config *cfg) {
+    return guard([&] {
+        if (!cfg) throw InvalidArg("null config");
+        validate(*cfg);
+    });
+}
+
+int oscar_kv_create(const oscar_kv_config *cfg, int64_t batch, int64_t q_heads, int64_t max_tokens, int device,
+                    int keep_exact, oscar_kv_handle **out) {
+    return guard([&] {
+        if (!cfg || !out) throw InvalidArg("null argument");
+        validate(*cfg);
+        if (batch <= 0) throw InvalidArg("create: batch must be positive");
+        if (q_heads <= 0 || q_heads % cfg->heads != 0 || q_heads / cfg->heads > 8)
+            throw InvalidArg("create: q_heads must be a multiple of heads with at most 8 per KV head");
+        if (max_tokens < 0) throw InvalidArg("create: max_tokens must be non-negative");
+        auto h = std::make_unique<oscar_kv_handle>();
+        h->cfg = *cfg;
+        h->dbits = quantizes(*cfg) ? cfg->bits : 0;
+        h->B = batch;
+        h->Hq = q_heads;
+        h->g = q_heads / cfg->heads;
+        h->BH = batch * cfg->heads;
+        h->max_tokens = max_tokens;
+        h->max_blocks = max_tokens / R + 1;
+        h->device = device;
+        h->keep_exact = keep_exact != 0;
+        CK(cudaSetDevice(device));
+        CK(cudaDeviceGetAttribute(&h->num_sms, cudaDevAttrMultiProcessorCount, device));
+        h->block_bytes = h->dbits == 2 ? Block<2>::BYTES : h->dbits == 4 ? Block<4>::BYTES : BF16_BLOCK_BYTES;
+        h->blocks = (uint8_t *)h->dalloc((size_t)(h->BH * h->max_blocks * h->block_bytes));
+        if (h->dbits != 0 && h->keep_exact)
+            h->shadow = (double *)h->dalloc(sizeof(double) * (size_t)(h->BH * h->max_blocks * SHADOW_DOUBLES));
+        h->ring_k = h->dalloc((size_t)(h->BH * R * D * 2));
+        h->ring_v = h->dalloc((size_t)(h->BH * R * D * 2));
+        h->maxp_alloc = (int)(2 * h->num_sms / h->BH + 3);
+        h->part_o = (float *)h->dalloc(sizeof(float) * (size_t)(h->BH * h->maxp_alloc * 8 * D));
+        h->part_ml = (float *)h->dalloc(sizeof(float) * (size_t)(h->BH * h->maxp_alloc * 16));
+        h->counters = (int *)h->dalloc(sizeof(int) * (size_t)h->BH);
+        CK(cudaMemset(h->counters, 0, sizeof(int) * (size_t)h->BH));
+        const size_t stage_bytes = (size_t)(h->B * h->Hq * D * 2 + 2 * h->BH * D * 2 + h->B * h->Hq * D * 4 +
+                                            h->B * h->Hq * 4 + 256);
+        h->stage = h->dalloc(stage_bytes);
+        *out = h.release();
+    });
+}
+
+int oscar_kv_destroy(oscar_kv_handle *h) {
+    return guard([&] { delete h; });
+}
+
+int oscar_kv_append(oscar_kv_handle *h, const void *k, const void *v, int64_t n_tokens, void *stream) {
+    return guard([&] {
+        if (!h) throw InvalidArg("null handle");
+        if (n_tokens > 0 && (!k || !v)) throw InvalidArg("append: null tensor");
+        CK(cudaSetDevice(h->device));
+        h->last_stream = (cudaStream_t)stream;
+        h->append(k, v, n_tokens, (cudaStream_t)stream);
+    });
+}
+
+int oscar_kv_decode_step(oscar_kv_handle *h, const void *q, const void *k, const void *v, float *out, float *lse,
+                         void *stream) {
+    return guard([&] {
+        if (!h || !q || !k || !v || !out) throw InvalidArg("decode_step: null argument");
+        CK(cudaSetDevice(h->device));
+        h->last_stream = (cudaStream_t)stream;
+        h->decode_step(q, k, v, out, lse, (cudaStream_t)stream);
+    });
+}
+
+int oscar_kv_attend(oscar_kv_handle *h, const void *q, float *out, float *lse, void *stream) {
+    return guard([&] {
+        if (!h || !q || !out) throw InvalidArg("attend: null argument");
+        CK(cudaSetDevice(h->device));
+        h->last_stream = (cudaStream_t)stream;
+        h->attend(q, out, lse, (cudaStream_t)stream);
+    });
+}
+
+int oscar_kv_decode_step_host(oscar_kv_handle *h, const void *q_host, const void *k_host, const void *v_host,
+                              float *out_host, float *lse_host, void *stream) {
+    return guard([&] {
+        if (!h || !q_host || !k_host || !v_host || !out_host) throw InvalidArg("decode_step_host: null argument");
+        CK(cudaSetDevice(h->device));
+        cudaStream_t s = (cudaStream_t)stream;
+        h->last_stream = s;
+        uint8_t *p = (uint8_t *)h->stage;
+        const size_t qb = (size_t)(h->B * h->Hq * D * 2), kb = (size_t)(h->BH * D * 2);
+        const size_t ob = (size_t)(h->B * h->Hq * D * 4), lb = (size_t)(h->B * h->Hq * 4);
+        void *dq = p, *dk = p + qb, *dv = p + qb + kb;
+        float *dout = (float *)(p + qb + 2 * kb);
+        float *dlse = (float *)(p + qb + 2 * kb + ob);
+        CK(cudaMemcpyAsync(dq, q_host, qb, cudaMemcpyHostToDevice, s));
+        CK(cudaMemcpyAsync(dk, k_host, kb, cudaMemcpyHostToDevice, s));
+        CK(cudaMemcpyAsync(dv, v_host, kb, cudaMemcpyHostToDevice, s));
+        h->decode_step(dq, dk, dv, dout, lse_host ? dlse : nullptr, s);
+        CK(cudaMemcpyAsync(out_host, dout, ob, cudaMemcpyDeviceToHost, s));
+        if (lse_host) CK(cudaMemcpyAsync(lse_host, dlse, lb, cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+    });
+}
+
+int oscar_kv_stats(const oscar_kv_handle *h, int64_t *packed, int64_t *residual, int64_t *flushes) {
+    return guard([&] {
+        if (!h) throw InvalidArg("null handle");
+        if (packed) *packed = h->packed;
+        if (residual) *residual = h->residual;
+        if (flushes) *flushes = h->flushes;
+    });
+}
+
+int oscar_kv_memory_report(const oscar_kv_handle *h, oscar_kv_memory_report_t *r) {
+    return guard([&] {
+        if (!h || !r) throw InvalidArg("null argument");
+        // KvCache::memory_report (kv_cache.cpp:383-402), per sequence
+        const int64_t d = D, H = h->cfg.heads;
+        const bool q = quantizes(h->cfg);
+        const int payload_bits = q ? h->cfg.bits : 64;
+        *r = oscar_kv_memory_report_t{};
+        r->packed_tokens = h->packed;
+        r->residual_tokens = h->residual;
+        r->packed_k_payload_bits = h->packed * H * d * payload_bits;
+        r->packed_v_payload_bits = h->packed * H * d * payload_bits;
+        r->residual_k_payload_bits = h->residual * H * d * 64;
+        r->residual_v_payload_bits = h->residual * H * d * 64;
+        r->k_norm_bits = (h->packed + h->residual) * H * 64;
+        if (q) {
+            const int64_t kg = h->packed / h->cfg.group_size * d * H;
+            const int64_t vg = h->packed * (d / h->cfg.group_size) * H;
+            r->param_bits = (kg + vg) * 2 * 64;
+        }
+        const int64_t total = r->packed_k_payload_bits + r->packed_v_payload_bits + r->residual_k_payload_bits +
+                              r->residual_v_payload_bits + r->k_norm_bits + r->param_bits;
+        const int64_t values = 2 * (h->packed + h->residual);
+        r->effective_bits_per_value = values ? (double)total / (double)values : 0.0;
+        r->device_hot_bytes = (h->packed / R) * H * h->block_bytes + h->residual * H * d * 2 * 2;
+        r->device_total_bytes = h->device_bytes;
+    });
+}
+
+int oscar_kv_export(oscar_kv_handle *h, int64_t b, oscar_kv_export_t *o) {
+    return guard([&] {
+        if (!h || !o) throw InvalidArg("null argument");
+        HostCache hc = build_host_cache(h, b);
+        const int64_t H = hc.H, nb = hc.nblk;
+        const int64_t kp = D * (R / G), vp = R * (D / G);
+        for (int64_t hh = 0; hh < H; ++hh)
+            for (int64_t k = 0; k < nb; ++k) {
+                const int64_t blk = hh * nb + k;
+                if (hc.bits == 2) {
+                    if (o->k_payload) {
+                        auto w = pack2(hc.k_codes[hh][k]);
+                        std::memcpy(o->k_payload + blk * (R * D / 8), w.data(), w.size() * 2);
+                    }
+                    if (o->v_payload) {
+                        auto w = pack2(hc.v_codes[hh][k]);
+                        std::memcpy(o->v_payload + blk * (R * D / 8), w.data(), w.size() * 2);
+                    }
+                } else if (hc.bits == 4) {
+                    if (o->k_payload) std::memcpy(o->k_payload + blk * R * D, hc.k_codes[hh][k].data(), R * D * 2);
+                    if (o->v_payload) std::memcpy(o->v_payload + blk * R * D, hc.v_codes[hh][k].data(), R * D * 2);
+                }
+                if (hc.bits != 0) {
+                    if (o->k_delta) std::memcpy(o->k_delta + blk * kp, hc.k_delta[hh][k].data(), kp * 8);
+                    if (o->k_zp) std::memcpy(o->k_zp + blk * kp, hc.k_zp[hh][k].data(), kp * 8);
+                    if (o->k_constant) std::memcpy(o->k_constant + blk * kp, hc.k_const[hh][k].data(), kp * 8);
+                    if (o->v_delta) std::memcpy(o->v_delta + blk * vp, hc.v_delta[hh][k].data(), vp * 8);
+                    if (o->v_zp) std::memcpy(o->v_zp + blk * vp, hc.v_zp[hh][k].data(), vp * 8);
+                    if (o->v_constant) std::memcpy(o->v_constant + blk * vp, hc.v_const[hh][k].data(), vp * 8);
+                } else {
+                    if (o->k_raw) std::memcpy(o->k_raw + blk * R * D, hc.k_raw[hh][k].data(), R * D * 8);
+                    if (o->v_raw) std::memcpy(o->v_raw + blk * R * D, hc.v_raw[hh][k].data(), R * D * 8);
+                }
+            }
+        if (o->k_norms)
+            for (int64_t hh = 0; hh < H; ++hh)
+                std::memcpy(o->k_norms + hh * hc.packed, hc.k_norms[hh].data(), hc.packed * 8);
+        if (o->k_residual) std::memcpy(o->k_residual, hc.k_res.data(), hc.k_res.size() * 8);
+        if (o->k_norms_residual) std::memcpy(o->k_norms_residual, hc.k_norms_res.data(), hc.k_norms_res.size() * 8);
+        if (o->v_residual) std::memcpy(o->v_residual, hc.v_res.data(), hc.v_res.size() * 8);
+    });
+}
+
+int oscar_kv_dump(oscar_kv_handle *h, int64_t b, const char *path) {
+    return guard([&] {
+        if (!h || !path) throw InvalidArg("null argument");
+        HostCache hc = build_host_cache(h, b);
+        std::ofstream f(path, std::ios::binary);
+        if (!f) throw std::runtime_error(std::string("cache dump: cannot open ") + path);
+        const oscar_kv_config &c = h->cfg;
+        const int64_t H = hc.H, nb = hc.nblk;
+        // manifest: nlohmann::json object (std::map => sorted keys), compact dump
+        auto sizes = [&](bool is_v) {
+            std::ostringstream s;
+            s << "[";
+            for (int64_t hh = 0; hh < H; ++hh) {
+                s << (hh ? ",[" : "[");
+                for (int64_t k = 0; k < nb; ++k) {
+                    const int64_t params = hc.bits ? (is_v ? R * (D / G) : D * (R / G)) : 0;
+                    const int64_t words = hc.bits == 2 ? R * D / 8 : 0;
+                    const int64_t pc = hc.bits == 2 ? R * D : 0;
+                    const int64_t codes = hc.bits == 4 ? R * D : 0;
+                    const int64_t raw = hc.bits == 0 ? R * D : 0;
+                    s << (k ? "," : "") << "{\"codes\":" << codes << ",\"packed_count\":" << pc
+                      << ",\"params\":" << params << ",\"raw\":" << raw << ",\"words\":" << words << "}";
+                }
+                s << "]";
+            }
+            s << "]";
+            return s.str();
+        };
+        const bool pre = h->prefilled;
+        std::ostringstream m;
+        m << "{\"G\":" << c.group_size << ",\"H\":" << H << ",\"R\":" << c.residual_len << ",\"S_packed\":" << hc.packed
+          << ",\"S_packed_v\":" << hc.packed << ",\"b\":" << c.bits << ",\"d_h\":" << c.head_dim
+          << ",\"flush_count\":" << h->flushes << ",\"k_blocks\":" << sizes(false)
+          << ",\"k_prefilled\":" << (pre ? "true" : "false") << ",\"magic\":\"KVC1\",\"method\":\""
+          << method_name(c.method) << "\",\"residual_tokens\":" << hc.r << ",\"scaling\":\""
+          << scaling_name(c.scaling) << "\",\"v_blocks\":" << sizes(true)
+          << ",\"v_prefilled\":" << (pre ? "true" : "false") << ",\"v_residual_tokens\":" << hc.r << "}";
+        f << m.str() << "\n";
+        auto write_blocks = [&](bool is_v, int64_t hh) {
+            for (int64_t k = 0; k < nb; ++k) {
+                if (hc.bits) {
+                    const auto &dl = is_v ? hc.v_delta[hh][k] : hc.k_delta[hh][k];
+                    const auto &zp = is_v ? hc.v_zp[hh][k] : hc.k_zp[hh][k];
+                    const auto &cs = is_v ? hc.v_const[hh][k] : hc.k_const[hh][k];
+                    for (size_t i = 0; i < dl.size(); ++i) {
+                        f.write(reinterpret_cast<const char *>(&dl[i]), 8);
+                        f.write(reinterpret_cast<const char *>(&zp[i]), 8);
+                        f.write(reinterpret_cast<const char *>(&cs[i]), 8);
+                    }
+                    const auto &codes = is_v ? hc.v_codes[hh][k] : hc.k_codes[hh][k];
+                    if (hc.bits == 2) {
+                        auto w = pack2(codes);
+                        f.write(reinterpret_cast<const char *>(w.data()), (std::streamsize)(w.size() * 2));
+                    } else {
+                        f.write(reinterpret_cast<const char *>(codes.data()), (std::streamsize)(codes.size() * 2));
+                    }
+                } else {
+                    const auto &raw = is_v ? hc.v_raw[hh][k] : hc.k_raw[hh][k];
+                    f.write(reinterpret_cast<const char *>(raw.data()), (std::streamsize)(raw.size() * 8));
+                }
+            }
+        };
+        for (int64_t hh = 0; hh < H; ++hh) {
+            write_blocks(false, hh);
+            f.write(reinterpret_cast<const char *>(hc.k_norms[hh].data()), (std::streamsize)(hc.packed * 8));
+        }
+        f.write(reinterpret_cast<const char *>(hc.k_res.data()), (std::streamsize)(hc.k_res.size() * 8));
+        f.write(reinterpret_cast<const char *>(hc.k_norms_res.data()), (std::streamsize)(hc.k_norms_res.size() * 8));
+        for (int64_t hh = 0; hh < H; ++hh) write_blocks(true, hh);
+        f.write(reinterpret_cast<const char *>(hc.v_res.data()), (std::streamsize)(hc.v_res.size() * 8));
+        if (!f) throw std::runtime_error("cache dump: write failed");
+    });
+}
+
+int oscar_kv_materialize(oscar_kv_handle *h, int64_t b, double *k_out, double *v_out) {
+    return guard([&] {
+        if (!h) throw InvalidArg("null handle");
+        HostCache hc = build_host_cache(h, b);
+        const int64_t H = hc.H, nb = hc.nblk;
+        // kv_cache.cpp:327-381 (unpack_block + dequantize_one x norm)
+        for (int64_t hh = 0; hh < H; ++hh)
+            for (int64_t k = 0; k < nb; ++k)
+                for (int t = 0; t < R; ++t) {
+                    const int64_t tok = k * R + t;
+                    const double s = hc.k_norms[hh][tok];
+                    for (int c = 0; c < D; ++c) {
+                        double xk, xv;
+                        if (hc.bits) {
+                            const int pk = c * (R / G) + t / G, pv = t * (D / G) + c / G;
+                            const double dk = hc.k_delta[hh][k][pk], dv = hc.v_delta[hh][k][pv];
+                            xk = dk == 0.0 ? hc.k_const[hh][k][pk]
+                                           : dk * ((double)hc.k_codes[hh][k][c * R + t] - (double)hc.k_zp[hh][k][pk]);
+                            xv = dv == 0.0 ? hc.v_const[hh][k][pv]
+                                           : dv * ((double)hc.v_codes[hh][k][t * D + c] - (double)hc.v_zp[hh][k][pv]);
+                        } else {
+                            xk = hc.k_raw[hh][k][t * D + c];
+                            xv = hc.v_raw[hh][k][t * D + c];
+                        }
+                        if (k_out) k_out[(tok * H + hh) * D + c] = xk * s;
+                        if (v_out) v_out[(tok * H + hh) * D + c] = xv;
+                    }
+                }
+        for (int64_t t = 0; t < hc.r; ++t)
+            for (int64_t hh = 0; hh < H; ++hh) {
+                const double s = hc.k_norms_res[t * H + hh];
+                for (int c = 0; c < D; ++c) {
+                    if (k_out) k_out[((hc.packed + t) * H + hh) * D + c] = hc.k_res[(t * H + hh) * D + c] * s;
+                    if (v_out) v_out[((hc.packed + t) * H + hh) * D + c] = hc.v_res[(t * H + hh) * D + c];
+                }
+            }
+    });
+}
+
+int oscar_lse_merge(const float *outs, const float *lses, int64_t parts, int64_t rows, int64_t d, float *out,
+                    float *lse_out, void *stream) {
+    return guard([&] {
+        if (!outs || !lses || !out) throw InvalidArg("lse_merge: null argument");
+        if (parts <= 0 || rows < 0 || d <= 0) throw InvalidArg("lse_merge: bad sizes");
+        CK(launch_lse_merge(outs, lses, parts, rows, d, out, lse_out, (cudaStream_t)stream));
+    });
+}
+
+int oscar_kv_last_launch_count(const oscar_kv_handle *h) { return h ? h->last_launches : 0; }
+
+}  // extern "C"

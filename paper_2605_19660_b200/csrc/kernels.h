@@ -1,0 +1,73 @@
+// kernels.h -- host-side launchers of the device kernels (internal to the
+// library; the public boundary is include/oscar_kv.h).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace osk {
+
+struct TransformCfg {
+    int bits;       // 0, 2, 4 (0 => raw bf16 block, no transform)
+    int rotates;    // K (and Q) Hadamard rotation
+    int scales;     // Omni-Token Scaling of K
+    int scaling;    // 0 l2, 1 rsqrt, 2 max, 3 mean-abs
+    int rotate_v;   // explicit V rotation
+};
+
+// Quantise n_blocks R-blocks per (sequence, head) from a bf16 source.
+// Source element (b, h, token t, channel c) lives at
+//   src + b*sb + (tok0 + t)*st + h*sh + c
+// Block k of (b,h) is written to blocks[((b*H+h)*max_blocks + blk0 + k)*bytes].
+struct QuantizeArgs {
+    const void *k, *v;
+    int64_t sb, st, sh, tok0;
+    int B, H;
+    int64_t n_blocks;
+    uint8_t *blocks;
+    int64_t max_blocks, blk0;
+    double *shadow;  // nullable: [bh][max_blocks][SHADOW_DOUBLES]
+    TransformCfg tc;
+};
+cudaError_t launch_quantize(const QuantizeArgs &a, cudaStream_t st);
+
+// Copy n tokens of raw bf16 K/V into the residual ring at slot0.
+struct RingCopyArgs {
+    const void *k, *v;
+    int64_t sb, st, sh, tok0;
+    int B, H;
+    int64_t n;
+    void *ring_k, *ring_v;  // [bh][R][D]
+    int64_t slot0;
+};
+cudaError_t launch_ring_copy(const RingCopyArgs &a, cudaStream_t st);
+
+struct AttnArgs {
+    const uint8_t *blocks;
+    int64_t max_blocks;
+    int64_t nb;        // packed blocks per (b,h)
+    int BH, Hkv, g, Hq;
+    const void *q;     // bf16 [B][Hq][D]
+    const void *kcur, *vcur;  // bf16 [B][Hkv][D] or null
+    void *ring_k, *ring_v;    // [bh][R][D]
+    int r;             // residual rows in ring
+    int write_ring;    // store kcur/vcur at ring slot r
+    int rotates;       // rotate q for the packed part
+    int scales;        // unused on device (norms are stored), kept for clarity
+    int rotate_v;      // un-rotate output
+    float *out;        // fp32 [B][Hq][D]
+    float *lse;        // fp32 [B][Hq] or null
+    float *part_o;     // [BH][maxp][8][D]
+    float *part_ml;    // [BH][maxp][8][2]
+    int *counters;     // [BH], zero between launches
+    int maxp;
+    int ncta;
+};
+// bits: 2, 4 or 0 (bf16 baseline)
+cudaError_t launch_attention(int bits, const AttnArgs &a, cudaStream_t st);
+int attention_max_partials(int64_t nb, int BH, int ncta);
+int attention_grid(int bits, int num_sms, int64_t nb, int BH);
+
+cudaError_t launch_lse_merge(const float *outs, const float *lses, int64_t parts, int64_t rows, int64_t d,
+                             float *out, float *lse_out, cudaStream_t st);
+
+}  // namespace osk

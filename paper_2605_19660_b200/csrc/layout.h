@@ -1,0 +1,169 @@
+// layout.h -- the device cache layout (shared by the quantize kernel, the
+// decode-attention kernel and the host-side export).
+//
+// One R-block (R = 128 tokens) of one (sequence, KV head) is ONE contiguous
+// record in HBM, fetched by a single cp.async.bulk into shared memory:
+//
+//   INT2 record (12800 B)                       INT4 record (20992 B)
+//   [K codes  4096 B]  mma A-fragment order      [K codes  8192 B]
+//   [V codes  4096 B]  mma A-fragment order      [V codes  8192 B]
+//   [K a      1024 B]  fp16 step  per (ch,grp)   ... same params/norms ...
+//   [K b      1024 B]  fp16 offset per (ch,grp)
+//   [V a      1024 B]  fp16 step  per (tok,gc)
+//   [V b      1024 B]  fp16 offset per (tok,gc)
+//   [norms     512 B]  fp32 per token
+//
+// Dequantisation is affine per group: x = a*code + b with a = delta and
+// b = -delta*zp (a = 0, b = constant for a constant group), i.e. exactly the
+// reference's dequantize_one (quant.cpp:65-68) narrowed to fp16.
+//
+// The codes are the reference's codes (bit-identical values) permuted inside
+// the block so that every 32-bit word a lane loads IS an mma.m16n8k16 A
+// register after one AND: the low half-word carries 8 codes of one (row, k)
+// element pair for 8 different m-tiles, the high half the partner k element.
+// Masking a 2-bit field at position 2i leaves the fp16 SUBNORMAL code*2^(2i-24)
+// (exact; tensor cores keep fp16 subnormals -- measured, scratch/mma_probe.cu),
+// whose power-of-two scale is removed per m-tile in the fp32 epilogue.
+//
+// QK^T:  D[token, head] = sum_c codeK[token, c] * (Qrot[head, c] * aK[c, grp])
+//   m-tile i (0..7) = tokens 16i..16i+15 (one quantisation group: grp = i/2),
+//   row r -> token 16i + r; k-step s (0..7) = channels 16s..16s+15, k-col kc
+//   -> channel 16s + kc.
+// P.V:   D[channel, head] = sum_t codeV[t, channel] * (P[head, t] * aV[t, gc])
+//   m-tile m (0..7) = channels 16m..16m+15 (gc = m/2), row r -> channel 16m+r;
+//   k-step j (0..7) = tokens of QK m-tile j with k-col -> token
+//   16j + {tq, tq+8, tq+4, tq+12} for k = {2tq, 2tq+1, 2tq+8, 2tq+9} -- the
+//   order that turns the QK accumulator into the PV B operand with two
+//   shuffles per register.
+//
+// export (oscar_kv_export) inverts the permutation back to the reference's
+// channel-major K / token-major V code order (kv_cache.cpp:116, 146) and
+// pack_2bit words (quant.cpp:162-175).
+#pragma once
+#include <stdint.h>
+
+#ifdef __CUDACC__
+#define OSK_HD __host__ __device__ __forceinline__
+#else
+#define OSK_HD inline
+#endif
+
+namespace osk {
+
+constexpr int D = 128;        // head_dim
+constexpr int R = 128;        // residual_len (block)
+constexpr int G = 32;         // group_size
+constexpr int NGRP = R / G;   // K groups per channel per block (4)
+constexpr int NGC = D / G;    // V groups per token (4)
+
+template <int BITS>
+struct Block {
+    static constexpr int CODE_BYTES = R * D * BITS / 8;      // per K or V
+    static constexpr int K_OFF = 0;
+    static constexpr int V_OFF = CODE_BYTES;
+    static constexpr int KA_OFF = 2 * CODE_BYTES;
+    static constexpr int KB_OFF = KA_OFF + D * NGRP * 2;
+    static constexpr int VA_OFF = KB_OFF + D * NGRP * 2;
+    static constexpr int VB_OFF = VA_OFF + R * NGC * 2;
+    static constexpr int NORM_OFF = VB_OFF + R * NGC * 2;
+    static constexpr int BYTES = NORM_OFF + R * 4;
+    // words per lane per k-step (each word = 8/BITS*... m-tiles)
+    static constexpr int TILES_PER_WORD = 16 / BITS;          // 8 (int2) / 4 (int4)
+    static constexpr int WORDS_PER_LANE_STEP = 4 * 8 / TILES_PER_WORD;  // 4 / 8
+};
+static_assert(Block<2>::BYTES == 12800, "int2 block size");
+static_assert(Block<4>::BYTES == 20992, "int4 block size");
+constexpr int BF16_BLOCK_BYTES = 2 * R * D * 2;  // raw bf16 K then V, [token][channel]
+
+// ---- K code words --------------------------------------------------------
+// word index w = ((s*32 + lane)*4 + fam)*WPF + half, WPF = 8/TILES_PER_WORD
+//   fam: 0 (pair0,row g) 1 (pair0,row g+8) 2 (pair1,row g) 3 (pair1,row g+8)
+//   pair0 = channels (16s+2tq, 16s+2tq+1), pair1 = (16s+2tq+8, 16s+2tq+9)
+// field f (0..TILES_PER_WORD-1) of the low/high half -> m-tile i = half*TPW+f
+OSK_HD void k_word_coords(int BITS, int w, int f, int hi, int &token, int &channel) {
+    const int tpw = 16 / BITS, wpf = 8 / tpw;
+    const int half = w % wpf;
+    const int fam = (w / wpf) % 4;
+    const int lane = (w / wpf / 4) % 32;
+    const int s = w / wpf / 4 / 32;
+    const int g = lane >> 2, tq = lane & 3;
+    const int i = half * tpw + f;
+    const int row = g + ((fam & 1) ? 8 : 0);
+    token = 16 * i + row;
+    channel = 16 * s + 2 * tq + ((fam & 2) ? 8 : 0) + hi;
+}
+
+// ---- V code words ----------------------------------------------------------
+// word index w = ((j*32 + lane)*4 + fam)*WPF + half
+//   fam: 0 (row g; t1,t2) 1 (row g+8; t1,t2) 2 (row g; t3,t4) 3 (row g+8; t3,t4)
+//   t1 = 16j+tq, t2 = 16j+tq+8, t3 = 16j+tq+4, t4 = 16j+tq+12
+//   low half -> first token of the pair, high half -> second
+// field f -> PV m-tile m = half*TPW + f -> channel 16m + row
+OSK_HD void v_word_coords(int BITS, int w, int f, int hi, int &token, int &channel) {
+    const int tpw = 16 / BITS, wpf = 8 / tpw;
+    const int half = w % wpf;
+    const int fam = (w / wpf) % 4;
+    const int lane = (w / wpf / 4) % 32;
+    const int j = w / wpf / 4 / 32;
+    const int g = lane >> 2, tq = lane & 3;
+    const int m = half * tpw + f;
+    const int row = g + ((fam & 1) ? 8 : 0);
+    channel = 16 * m + row;
+    const int base = 16 * j + tq + ((fam & 2) ? 4 : 0);
+    token = base + (hi ? 8 : 0);
+}
+
+// ---- params ----------------------------------------------------------------
+// channel c = 16s + kc; slot of kc within the lane's 4 B-fragment channels
+OSK_HD void k_chan_split(int c, int &s, int &tq, int &slot) {
+    s = c >> 4;
+    const int kc = c & 15;
+    tq = (kc & 7) >> 1;
+    slot = (kc & 1) + ((kc >> 3) << 1);
+}
+// K a-params: [s][tq][grp][slot]  (lane reads 32 B per k-step: all 4 groups)
+OSK_HD int ka_index(int c, int grp) {
+    int s, tq, slot;
+    k_chan_split(c, s, tq, slot);
+    return ((s * 4 + tq) * 4 + grp) * 4 + slot;
+}
+// K b-params: [grp][tq][s][slot]  (lane g<4 reads 64 B: its group, all k-steps)
+OSK_HD int kb_index(int c, int grp) {
+    int s, tq, slot;
+    k_chan_split(c, s, tq, slot);
+    return ((grp * 4 + tq) * 8 + s) * 4 + slot;
+}
+// token t = 16j + r; the B-fragment slot order is (tq, tq+8, tq+4, tq+12)
+OSK_HD void v_tok_split(int t, int &j, int &tq, int &slot) {
+    j = t >> 4;
+    const int r = t & 15;
+    tq = r & 3;
+    const int q = r >> 2;  // 0..3 <-> offsets 0,4,8,12
+    slot = (q == 0) ? 0 : (q == 2) ? 1 : (q == 1) ? 2 : 3;
+}
+// V a-params: [j][tq][gc][slot]
+OSK_HD int va_index(int t, int gc) {
+    int j, tq, slot;
+    v_tok_split(t, j, tq, slot);
+    return ((j * 4 + tq) * 4 + gc) * 4 + slot;
+}
+// V b-params: [gc][tq][j][slot]
+OSK_HD int vb_index(int t, int gc) {
+    int j, tq, slot;
+    v_tok_split(t, j, tq, slot);
+    return ((gc * 4 + tq) * 8 + j) * 4 + slot;
+}
+// norms: [g][i][2] -> token 16i + g (+8 for slot 1)
+OSK_HD int norm_index(int t) {
+    const int i = t >> 4, r = t & 15;
+    return ((r & 7) * 8 + i) * 2 + (r >> 3);
+}
+
+// exact shadow (keep_exact): per block K lohi [ch][grp][2], V lohi [tok][gc][2],
+// norms fp64 [tok]
+constexpr int SHADOW_K_DOUBLES = D * NGRP * 2;
+constexpr int SHADOW_V_DOUBLES = R * NGC * 2;
+constexpr int SHADOW_N_DOUBLES = R;
+constexpr int SHADOW_DOUBLES = SHADOW_K_DOUBLES + SHADOW_V_DOUBLES + SHADOW_N_DOUBLES;
+
+}  // namespace osk

@@ -1,0 +1,360 @@
+// quantize.cu -- the quantize/append kernel: Canalized Rotation + Omni-Token
+// Scaling + KIVI-style group quantisation + bit packing, in fp64 with the
+// reference's exact operation order (compiled with -fmad=false; every
+// arithmetic op is an explicit IEEE round-to-nearest intrinsic on top).
+//
+// Reference semantics reproduced bit-for-bit:
+//   fht_inplace        hadamard.cpp:10-26   butterfly stages half=1..64, then *1/sqrt(d)
+//   omni_token_scale   pipeline.cpp:90-148  zero test, sequential FMA-free sum of squares
+//   fast_rsqrt         pipeline.cpp:80-88
+//   quant_params       quant.cpp:21-47      lo/hi in index order, delta, llround zp (unclamped)
+//   quantize_one       quant.cpp:53-57
+//   flush_k_block      kv_cache.cpp:101-129 per-channel groups of G tokens
+//   flush_v_block      kv_cache.cpp:131-157 per-token groups of G channels
+//
+// One CTA = one R-block of one (sequence, head): 128 threads, processed one
+// 32-token group at a time.  Thread (token tl, quarter q) owns 32 channels
+// of one token; the Hadamard butterfly runs 5 stages in registers and the
+// last 2 across the 4-lane quad with shuffles; the l2 sum of squares is a
+// sequential chain handed across the quad so the addition order is the
+// reference's c = 0..127.
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+
+#include "device_common.cuh"
+#include "kernels.h"
+#include "layout.h"
+
+namespace osk {
+
+namespace {
+
+constexpr int QT = 128;  // threads per CTA
+
+__device__ __forceinline__ double dadd(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ double dsub(double a, double b) { return __dsub_rn(a, b); }
+__device__ __forceinline__ double dmul(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ double ddiv(double a, double b) { return __ddiv_rn(a, b); }
+
+// 32 bf16 -> fp64 (exact)
+__device__ __forceinline__ void load32(const __nv_bfloat16 *p, double (&x)[32]) {
+    const uint4 *p4 = reinterpret_cast<const uint4 *>(p);
+#pragma unroll
+    for (int v = 0; v < 4; ++v) {
+        uint4 u = p4[v];
+        uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            x[v * 8 + 2 * e] = (double)__uint_as_float(w[e] << 16);
+            x[v * 8 + 2 * e + 1] = (double)__uint_as_float(w[e] & 0xffff0000u);
+        }
+    }
+}
+
+// hadamard.cpp:10-26 on a 128-vector spread over a 4-lane quad (32 per lane)
+__device__ __forceinline__ void fht128_quad(double (&x)[32], int q) {
+#pragma unroll
+    for (int half = 1; half < 32; half <<= 1) {
+#pragma unroll
+        for (int base = 0; base < 32; base += 2 * half) {
+#pragma unroll
+            for (int i = base; i < base + half; ++i) {
+                const double a = x[i], b = x[i + half];
+                x[i] = dadd(a, b);
+                x[i + half] = dsub(a, b);
+            }
+        }
+    }
+    // half = 32: partner quarter q^1; half = 64: partner quarter q^2
+#pragma unroll
+    for (int xm = 1; xm <= 2; xm <<= 1) {
+        const bool upper = (q & xm) != 0;
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+            const double o = __shfl_xor_sync(0xffffffffu, x[i], xm);
+            x[i] = upper ? dsub(o, x[i]) : dadd(x[i], o);
+        }
+    }
+    const double scale = ddiv(1.0, __dsqrt_rn(128.0));
+#pragma unroll
+    for (int i = 0; i < 32; ++i) x[i] = dmul(x[i], scale);
+}
+
+// pipeline.cpp:80-88
+__device__ __forceinline__ double fast_rsqrt_ref(double x) {
+    const float xf = __double2float_rn(x);
+    if (xf <= 0.0f || !isfinite(xf)) return ddiv(1.0, __dsqrt_rn(x));
+    double y = (double)__fdiv_rn(1.0f, __fsqrt_rn(xf));
+    // y * (1.5 - 0.5 * x * y * y), left to right
+    const double t = dmul(dmul(dmul(0.5, x), y), y);
+    return dmul(y, dsub(1.5, t));
+}
+
+// sequential chain over the quad: acc_{c+1} = acc_c (+) f(x_c), c = 0..127
+template <typename F>
+__device__ __forceinline__ double quad_chain(const double (&x)[32], int q, int lane, F f) {
+    double acc = 0.0;
+#pragma unroll
+    for (int step = 0; step < 4; ++step) {
+        if (q == step) {
+#pragma unroll
+            for (int i = 0; i < 32; ++i) acc = dadd(acc, f(x[i]));
+        }
+        acc = __shfl_sync(0xffffffffu, acc, (lane & ~3) | step);
+    }
+    return acc;
+}
+
+// quant.cpp:21-47 on 32 values in index order; returns delta, zp, lo, hi
+struct GroupQ {
+    double lo, hi, delta;
+    long long zp;
+};
+template <typename Get>
+__device__ __forceinline__ GroupQ group_params(Get get, int bits) {
+    GroupQ p;
+    double lo = get(0), hi = lo;
+#pragma unroll
+    for (int i = 0; i < 32; ++i) {
+        const double x = get(i);
+        lo = (x < lo) ? x : lo;  // std::min(lo, x)
+        hi = (hi < x) ? x : hi;  // std::max(hi, x)
+    }
+    p.lo = lo;
+    p.hi = hi;
+    if (hi == lo) {
+        p.delta = 0.0;
+        p.zp = 0;
+    } else {
+        p.delta = ddiv(dsub(hi, lo), (double)((1 << bits) - 1));
+        p.zp = llround(ddiv(-lo, p.delta));
+    }
+    return p;
+}
+
+// quant.cpp:53-57
+__device__ __forceinline__ uint8_t quantize_one(double x, const GroupQ &p, int bits) {
+    if (p.delta == 0.0) return 0;
+    long long q = llround(ddiv(x, p.delta)) + p.zp;
+    const long long mx = (1 << bits) - 1;
+    q = q < 0 ? 0 : (q > mx ? mx : q);
+    return (uint8_t)q;
+}
+
+// affine fp16 form used by the attention kernel: x = a*code + b
+__device__ __forceinline__ void affine16(const GroupQ &p, __half &a, __half &b) {
+    if (p.delta == 0.0) {
+        a = __double2half(0.0);
+        b = __double2half(p.lo);
+    } else {
+        a = __double2half(p.delta);
+        b = __double2half(dmul(p.delta, -(double)p.zp));
+    }
+}
+
+template <int BITS>
+__global__ void __launch_bounds__(QT) quantize_kernel(const QuantizeArgs a) {
+    using Blk = Block<BITS>;
+    extern __shared__ __align__(16) uint8_t smem[];
+    double *ku = reinterpret_cast<double *>(smem);               // [32][129]
+    uint8_t *ck = smem + 32 * 129 * 8;                            // [128][128] K codes
+    uint8_t *cv = ck + R * D;                                     // [128][128] V codes
+    uint8_t *prm = cv + R * D;                                    // params + norms (BYTES - KA_OFF)
+    __half *ka = reinterpret_cast<__half *>(prm);
+    __half *kb = ka + D * NGRP;
+    __half *va = kb + D * NGRP;
+    __half *vb = va + R * NGC;
+    float *nrm = reinterpret_cast<float *>(vb + R * NGC);
+
+    const int tid = threadIdx.x, lane = tid & 31, q = tid & 3, tl = tid >> 2;
+    const int bh = blockIdx.y, b = bh / a.H, h = bh % a.H;
+    const int64_t blk = blockIdx.x;
+    const __nv_bfloat16 *kin = reinterpret_cast<const __nv_bfloat16 *>(a.k) + b * a.sb + h * a.sh;
+    const __nv_bfloat16 *vin = reinterpret_cast<const __nv_bfloat16 *>(a.v) + b * a.sb + h * a.sh;
+    const int64_t tok_base = a.tok0 + blk * R;
+    const int64_t out_blk = (int64_t)bh * a.max_blocks + a.blk0 + blk;
+    double *shadow = a.shadow ? a.shadow + out_blk * SHADOW_DOUBLES : nullptr;
+    const TransformCfg tc = a.tc;
+
+    for (int gi = 0; gi < NGRP; ++gi) {
+        const int t = gi * G + tl;  // token within the block
+        // ---------------- K: rotate, scale (apply_method) ----------------
+        double x[32];
+        load32(kin + (tok_base + t) * a.st + q * 32, x);
+        if (tc.rotates) fht128_quad(x, q);
+        double s = 1.0, inv = 1.0;
+        if (tc.scales) {
+            bool nz = false;
+#pragma unroll
+            for (int i = 0; i < 32; ++i) nz |= (x[i] != 0.0);
+            // zero test over all 128 channels (pipeline.cpp:99-102; -0.0 counts as zero)
+            const unsigned ballot = __ballot_sync(0xffffffffu, nz);
+            const bool quad_zero = ((ballot >> (lane & ~3)) & 0xFu) == 0;
+            if (quad_zero) {
+                s = 1e-12;
+                inv = ddiv(1.0, 1e-12);
+            } else if (tc.scaling == 0 || tc.scaling == 1) {
+                const double ss = quad_chain(x, q, lane, [](double v) { return dmul(v, v); });
+                if (tc.scaling == 0) {
+                    s = __dsqrt_rn(ss);
+                    inv = ddiv(1.0, s);
+                } else {
+                    inv = fast_rsqrt_ref(ss);
+                    s = ddiv(1.0, inv);
+                }
+            } else if (tc.scaling == 2) {
+                double m = 0.0;
+#pragma unroll
+                for (int i = 0; i < 32; ++i) {
+                    const double av = fabs(x[i]);
+                    m = (m < av) ? av : m;
+                }
+                m = fmax(m, __shfl_xor_sync(0xffffffffu, m, 1));
+                m = fmax(m, __shfl_xor_sync(0xffffffffu, m, 2));
+                s = m;
+                inv = ddiv(1.0, s);
+            } else {
+                const double sa = quad_chain(x, q, lane, [](double v) { return fabs(v); });
+                s = ddiv(sa, 128.0);
+                inv = ddiv(1.0, s);
+            }
+#pragma unroll
+            for (int i = 0; i < 32; ++i) x[i] = dmul(x[i], inv);
+        }
+        if (q == 0) {
+            nrm[norm_index(t)] = __double2float_rn(s);
+            if (shadow) shadow[SHADOW_K_DOUBLES + SHADOW_V_DOUBLES + t] = s;
+        }
+#pragma unroll
+        for (int i = 0; i < 32; ++i) ku[tl * 129 + q * 32 + i] = x[i];
+
+        // ---------------- V: optional rotation, per-token groups ----------------
+        {
+            double y[32];
+            load32(vin + (tok_base + t) * a.st + q * 32, y);
+            if (tc.rotate_v) fht128_quad(y, q);
+            const GroupQ p = group_params([&](int i) { return y[i]; }, BITS);
+#pragma unroll
+            for (int i = 0; i < 32; ++i) cv[t * D + q * 32 + i] = quantize_one(y[i], p, BITS);
+            __half ha, hb;
+            affine16(p, ha, hb);
+            va[va_index(t, q)] = ha;
+            vb[vb_index(t, q)] = hb;
+            if (shadow) {
+                shadow[SHADOW_K_DOUBLES + (t * NGC + q) * 2] = p.lo;
+                shadow[SHADOW_K_DOUBLES + (t * NGC + q) * 2 + 1] = p.hi;
+            }
+        }
+        __syncthreads();
+        // ---------------- K: per-channel group of G tokens ----------------
+        {
+            const int c = tid;  // channel
+            const GroupQ p = group_params([&](int i) { return ku[i * 129 + c]; }, BITS);
+            for (int i = 0; i < G; ++i) ck[(gi * G + i) * D + c] = quantize_one(ku[i * 129 + c], p, BITS);
+            __half ha, hb;
+            affine16(p, ha, hb);
+            ka[ka_index(c, gi)] = ha;
+            kb[kb_index(c, gi)] = hb;
+            if (shadow) {
+                shadow[(c * NGRP + gi) * 2] = p.lo;
+                shadow[(c * NGRP + gi) * 2 + 1] = p.hi;
+            }
+        }
+        __syncthreads();
+    }
+
+    // ---------------- assemble the permuted code words ----------------
+    uint8_t *out = a.blocks + out_blk * (int64_t)Blk::BYTES;
+    constexpr int NWORDS = R * D * BITS / 32;
+    constexpr int TPW = 16 / BITS;
+    for (int w = tid; w < NWORDS; w += QT) {
+        uint32_t wk = 0, wv = 0;
+#pragma unroll
+        for (int hi = 0; hi < 2; ++hi) {
+#pragma unroll
+            for (int f = 0; f < TPW; ++f) {
+                int t, c;
+                k_word_coords(BITS, w, f, hi, t, c);
+                wk |= (uint32_t)ck[t * D + c] << (hi * 16 + f * BITS);
+                v_word_coords(BITS, w, f, hi, t, c);
+                wv |= (uint32_t)cv[t * D + c] << (hi * 16 + f * BITS);
+            }
+        }
+        reinterpret_cast<uint32_t *>(out + Blk::K_OFF)[w] = wk;
+        reinterpret_cast<uint32_t *>(out + Blk::V_OFF)[w] = wv;
+    }
+    // params + norms: contiguous tail of the record
+    constexpr int TAIL = Blk::BYTES - Blk::KA_OFF;
+    for (int i = tid; i < TAIL / 16; i += QT)
+        reinterpret_cast<uint4 *>(out + Blk::KA_OFF)[i] = reinterpret_cast<const uint4 *>(prm)[i];
+}
+
+// bits == 0 / method fp: the block is the raw bf16 K then V, [token][channel]
+__global__ void __launch_bounds__(QT) raw_block_kernel(const QuantizeArgs a) {
+    const int bh = blockIdx.y, b = bh / a.H, h = bh % a.H;
+    const int64_t blk = blockIdx.x;
+    const int64_t out_blk = (int64_t)bh * a.max_blocks + a.blk0 + blk;
+    uint8_t *out = a.blocks + out_blk * (int64_t)BF16_BLOCK_BYTES;
+    const uint16_t *kin = reinterpret_cast<const uint16_t *>(a.k) + b * a.sb + h * a.sh;
+    const uint16_t *vin = reinterpret_cast<const uint16_t *>(a.v) + b * a.sb + h * a.sh;
+    const int64_t tok_base = a.tok0 + blk * R;
+    // 128 tokens x 256 B per tensor; 16 B per thread-iteration
+    for (int i = threadIdx.x; i < R * 16; i += QT) {
+        const int t = i >> 4, part = i & 15;
+        const uint4 kv = *reinterpret_cast<const uint4 *>(kin + (tok_base + t) * a.st + part * 8);
+        const uint4 vv = *reinterpret_cast<const uint4 *>(vin + (tok_base + t) * a.st + part * 8);
+        reinterpret_cast<uint4 *>(out)[i] = kv;
+        reinterpret_cast<uint4 *>(out + R * D * 2)[i] = vv;
+    }
+}
+
+__global__ void ring_copy_kernel(const RingCopyArgs a) {
+    const int bh = blockIdx.y, b = bh / a.H, h = bh % a.H;
+    const int64_t t = blockIdx.x;
+    const uint16_t *kin = reinterpret_cast<const uint16_t *>(a.k) + b * a.sb + h * a.sh + (a.tok0 + t) * a.st;
+    const uint16_t *vin = reinterpret_cast<const uint16_t *>(a.v) + b * a.sb + h * a.sh + (a.tok0 + t) * a.st;
+    uint16_t *rk = reinterpret_cast<uint16_t *>(a.ring_k) + ((int64_t)bh * R + a.slot0 + t) * D;
+    uint16_t *rv = reinterpret_cast<uint16_t *>(a.ring_v) + ((int64_t)bh * R + a.slot0 + t) * D;
+    const int i = threadIdx.x;  // 32 threads x 8 bf16... use 16 threads each for k and v
+    if (i < 16) reinterpret_cast<uint4 *>(rk)[i] = reinterpret_cast<const uint4 *>(kin)[i];
+    else reinterpret_cast<uint4 *>(rv)[i - 16] = reinterpret_cast<const uint4 *>(vin)[i - 16];
+}
+
+}  // namespace
+
+cudaError_t launch_quantize(const QuantizeArgs &a, cudaStream_t st) {
+    if (a.n_blocks <= 0) return cudaSuccess;
+    dim3 grid((unsigned)a.n_blocks, (unsigned)(a.B * a.H));
+    if (a.tc.bits == 0) {
+        raw_block_kernel<<<grid, QT, 0, st>>>(a);
+        return cudaGetLastError();
+    }
+    const int smem_common = 32 * 129 * 8 + 2 * R * D;
+    if (a.tc.bits == 2) {
+        const int smem = smem_common + Block<2>::BYTES - Block<2>::KA_OFF;
+        static bool init = false;
+        if (!init) {
+            cudaFuncSetAttribute(quantize_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+            init = true;
+        }
+        quantize_kernel<2><<<grid, QT, smem, st>>>(a);
+    } else {
+        const int smem = smem_common + Block<4>::BYTES - Block<4>::KA_OFF;
+        static bool init = false;
+        if (!init) {
+            cudaFuncSetAttribute(quantize_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+            init = true;
+        }
+        quantize_kernel<4><<<grid, QT, smem, st>>>(a);
+    }
+    return cudaGetLastError();
+}
+
+cudaError_t launch_ring_copy(const RingCopyArgs &a, cudaStream_t st) {
+    if (a.n <= 0) return cudaSuccess;
+    dim3 grid((unsigned)a.n, (unsigned)(a.B * a.H));
+    ring_copy_kernel<<<grid, 32, 0, st>>>(a);
+    return cudaGetLastError();
+}
+
+}  // namespace osk

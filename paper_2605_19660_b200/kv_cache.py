@@ -1,0 +1,294 @@
+"""Host-side mirror of the reference KvCache API over the C-ABI library.
+
+Reference interface (C++): oscar::KvCache (kv_cache.hpp:61-123),
+oscar::PipelineConfig (kv_cache.hpp:19-32), decode_step / attention
+(pipeline.hpp:43-68).  This module binds include/oscar_kv.h with ctypes; it
+holds no compute of its own.  Device tensors are passed as raw pointers
+(torch is used only to own device memory).  If the CUDA library
+(liboscar_b200.so) is missing, importing this module raises -- there is no CPU
+fallback.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "liboscar_b200.so")
+
+METHODS = {"fp": 0, "kivi": 1, "rotate-only": 2, "scale-only": 3, "oscar": 4}
+SCALINGS = {"l2": 0, "rsqrt": 1, "max": 2, "mean-abs": 3}
+R, D, G = 128, 128, 32
+
+
+class _Config(ctypes.Structure):
+    _fields_ = [
+        ("method", ctypes.c_int32),
+        ("bits", ctypes.c_int32),
+        ("group_size", ctypes.c_int64),
+        ("residual_len", ctypes.c_int64),
+        ("scaling", ctypes.c_int32),
+        ("rotate_v", ctypes.c_int32),
+        ("head_dim", ctypes.c_int64),
+        ("heads", ctypes.c_int64),
+    ]
+
+
+class _MemReport(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_int64) for n in (
+        "packed_tokens", "residual_tokens", "packed_k_payload_bits", "packed_v_payload_bits",
+        "residual_k_payload_bits", "residual_v_payload_bits", "k_norm_bits", "param_bits")] + [
+        ("effective_bits_per_value", ctypes.c_double),
+        ("device_hot_bytes", ctypes.c_int64),
+        ("device_total_bytes", ctypes.c_int64),
+    ]
+
+
+_P = ctypes.c_void_p
+
+
+class _Export(ctypes.Structure):
+    _fields_ = [(n, _P) for n in (
+        "k_payload", "v_payload", "k_delta", "k_constant", "v_delta", "v_constant", "k_zp", "v_zp",
+        "k_raw", "v_raw", "k_norms", "k_residual", "k_norms_residual", "v_residual")]
+
+
+_lib = None
+
+
+def lib():
+    """Load liboscar_b200.so (fails loudly: the product has no CPU path)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise RuntimeError(f"CUDA library missing: {LIB_PATH} (run __graft_entry__.build())")
+        L = ctypes.CDLL(LIB_PATH)
+        L.oscar_last_error.restype = ctypes.c_char_p
+        L.oscar_kv_config_validate.argtypes = [ctypes.POINTER(_Config)]
+        L.oscar_kv_create.argtypes = [ctypes.POINTER(_Config), ctypes.c_int64, ctypes.c_int64, ctypes.c_int64,
+                                      ctypes.c_int, ctypes.c_int, ctypes.POINTER(_P)]
+        L.oscar_kv_destroy.argtypes = [_P]
+        L.oscar_kv_append.argtypes = [_P, _P, _P, ctypes.c_int64, _P]
+        L.oscar_kv_decode_step.argtypes = [_P, _P, _P, _P, _P, _P, _P]
+        L.oscar_kv_attend.argtypes = [_P, _P, _P, _P, _P]
+        L.oscar_kv_decode_step_host.argtypes = [_P, _P, _P, _P, _P, _P, _P]
+        L.oscar_kv_stats.argtypes = [_P, ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(ctypes.c_int64),
+                                     ctypes.POINTER(ctypes.c_int64)]
+        L.oscar_kv_memory_report.argtypes = [_P, ctypes.POINTER(_MemReport)]
+        L.oscar_kv_export.argtypes = [_P, ctypes.c_int64, ctypes.POINTER(_Export)]
+        L.oscar_kv_dump.argtypes = [_P, ctypes.c_int64, ctypes.c_char_p]
+        L.oscar_kv_materialize.argtypes = [_P, ctypes.c_int64, _P, _P]
+        L.oscar_lse_merge.argtypes = [_P, _P, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64, _P, _P, _P]
+        L.oscar_kv_last_launch_count.argtypes = [_P]
+        _lib = L
+    return _lib
+
+
+# every entry point declared in include/oscar_kv.h
+C_ABI_SYMBOLS = [
+    "oscar_last_error", "oscar_kv_config_validate", "oscar_kv_create", "oscar_kv_destroy", "oscar_kv_append",
+    "oscar_kv_decode_step", "oscar_kv_attend", "oscar_kv_decode_step_host", "oscar_kv_stats",
+    "oscar_kv_memory_report", "oscar_kv_export", "oscar_kv_dump", "oscar_kv_materialize", "oscar_lse_merge",
+    "oscar_kv_last_launch_count",
+]
+
+
+def _check(rc: int):
+    if rc != 0:
+        msg = lib().oscar_last_error().decode()
+        # reference exception types: invalid_argument / logic_error / runtime_error
+        raise {1: ValueError, 2: RuntimeError}.get(rc, OSError)(msg)
+
+
+@dataclass
+class PipelineConfig:
+    """oscar::PipelineConfig (kv_cache.hpp:19-32) + the value-rotation mode."""
+
+    method: str = "oscar"
+    bits: int = 2
+    group_size: int = 32
+    residual_len: int = 128
+    scaling: str = "l2"
+    head_dim: int = 128
+    heads: int = 1
+    rotate_v: bool = False
+
+    def _c(self) -> _Config:
+        return _Config(METHODS[self.method], self.bits, self.group_size, self.residual_len, SCALINGS[self.scaling],
+                       int(self.rotate_v), self.head_dim, self.heads)
+
+    def rotates(self):
+        return self.method in ("rotate-only", "oscar")
+
+    def scales(self):
+        return self.method in ("scale-only", "oscar")
+
+    def quantizes(self):
+        return self.method != "fp" and self.bits != 0
+
+    def validate(self):
+        c = self._c()
+        _check(lib().oscar_kv_config_validate(ctypes.byref(c)))
+
+
+def _ptr(t) -> int:
+    if t is None:
+        return None
+    return t.data_ptr()
+
+
+def _stream(stream):
+    if stream is None:
+        import torch
+
+        return torch.cuda.current_stream().cuda_stream
+    return stream
+
+
+class KvCache:
+    """Device KV cache for `batch` sequences x cfg.heads KV heads (one writer)."""
+
+    def __init__(self, cfg: PipelineConfig, batch: int, q_heads: int, max_tokens: int, device: int = 0,
+                 keep_exact: bool = True):
+        self.cfg = cfg
+        self.B, self.Hq, self.H, self.max_tokens, self.device = batch, q_heads, cfg.heads, max_tokens, device
+        self._c = cfg._c()
+        h = _P()
+        _check(lib().oscar_kv_create(ctypes.byref(self._c), batch, q_heads, max_tokens, device, int(keep_exact),
+                                     ctypes.byref(h)))
+        self._h = h
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().oscar_kv_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # ---- buffer_quant_k + buffer_quant_v (kv_cache.cpp:194-292), raw inputs ----
+    def buffer_quant(self, k, v, stream=None):
+        """k, v: bf16 CUDA tensors [B, S, H, d] (raw keys; values pre-rotated
+        unless cfg.rotate_v)."""
+        n = 0 if k is None else k.shape[1]
+        _check(lib().oscar_kv_append(self._h, _ptr(k), _ptr(v), n, _stream(stream)))
+
+    append = buffer_quant
+
+    # ---- decode_step body (pipeline.cpp:292-323) --------------------------------
+    def decode_step(self, q, k, v, out=None, lse=None, stream=None):
+        import torch
+
+        if out is None:
+            out = torch.empty((self.B, self.Hq, D), dtype=torch.float32, device=q.device)
+        _check(lib().oscar_kv_decode_step(self._h, _ptr(q), _ptr(k), _ptr(v), _ptr(out), _ptr(lse),
+                                          _stream(stream)))
+        return out
+
+    def attend(self, q, out=None, lse=None, stream=None):
+        import torch
+
+        if out is None:
+            out = torch.empty((self.B, self.Hq, D), dtype=torch.float32, device=q.device)
+        if lse is None:
+            lse = torch.empty((self.B, self.Hq), dtype=torch.float32, device=q.device)
+        _check(lib().oscar_kv_attend(self._h, _ptr(q), _ptr(out), _ptr(lse), _stream(stream)))
+        return out, lse
+
+    def decode_step_host(self, q: np.ndarray, k: np.ndarray, v: np.ndarray, out: np.ndarray, lse=None,
+                         stream=None):
+        """HOST buffers (uint16 bf16 bit patterns for q/k/v, fp32 out)."""
+        _check(lib().oscar_kv_decode_step_host(
+            self._h, q.ctypes.data, k.ctypes.data, v.ctypes.data, out.ctypes.data,
+            None if lse is None else lse.ctypes.data, _stream(stream)))
+        return out
+
+    # ---- counters (kv_cache.hpp:67-71) ---------------------------------------------
+    def _stats(self):
+        p, r, f = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
+        _check(lib().oscar_kv_stats(self._h, ctypes.byref(p), ctypes.byref(r), ctypes.byref(f)))
+        return p.value, r.value, f.value
+
+    @property
+    def packed_tokens(self):
+        return self._stats()[0]
+
+    @property
+    def residual_tokens(self):
+        return self._stats()[1]
+
+    @property
+    def total_tokens(self):
+        p, r, _ = self._stats()
+        return p + r
+
+    @property
+    def flush_count(self):
+        return self._stats()[2]
+
+    def last_launch_count(self) -> int:
+        return lib().oscar_kv_last_launch_count(self._h)
+
+    def memory_report(self) -> dict:
+        m = _MemReport()
+        _check(lib().oscar_kv_memory_report(self._h, ctypes.byref(m)))
+        return {n: getattr(m, n) for n, _ in _MemReport._fields_}
+
+    # ---- reference-layout views (parity / checkpoint) -----------------------------
+    def export(self, b: int = 0) -> dict:
+        """Sequence b in the reference's own layout (see oscar_kv_export)."""
+        packed, r, flushes = self._stats()
+        H, nb, bits = self.H, packed // R, (self.cfg.bits if self.cfg.quantizes() else 0)
+        kp, vp = D * (R // G), R * (D // G)
+        arr = {}
+        if bits == 2:
+            arr["k_payload"] = np.zeros((H, nb, R * D // 8), np.uint16)
+            arr["v_payload"] = np.zeros((H, nb, R * D // 8), np.uint16)
+        elif bits == 4:
+            arr["k_payload"] = np.zeros((H, nb, R * D), np.uint16)
+            arr["v_payload"] = np.zeros((H, nb, R * D), np.uint16)
+        if bits:
+            for kind, n in (("k", kp), ("v", vp)):
+                arr[f"{kind}_delta"] = np.zeros((H, nb, n))
+                arr[f"{kind}_constant"] = np.zeros((H, nb, n))
+                arr[f"{kind}_zp"] = np.zeros((H, nb, n), np.int64)
+        else:
+            arr["k_raw"] = np.zeros((H, nb, R * D))
+            arr["v_raw"] = np.zeros((H, nb, R * D))
+        arr["k_norms"] = np.zeros((H, packed))
+        arr["k_residual"] = np.zeros((r, H, D))
+        arr["k_norms_residual"] = np.zeros(r * H)
+        arr["v_residual"] = np.zeros((r, H, D))
+        ex = _Export(**{n: (a.ctypes.data if a.size else None) for n, a in arr.items()})
+        _check(lib().oscar_kv_export(self._h, b, ctypes.byref(ex)))
+        arr.update(packed=packed, residual=r, flushes=flushes, bits=bits)
+        return arr
+
+    def dump(self, b: int, path: str):
+        """KvCache::dump (kv_cache.cpp:469-507) for sequence b."""
+        _check(lib().oscar_kv_dump(self._h, b, path.encode()))
+
+    def materialize(self, b: int = 0):
+        """materialize_k / materialize_v (kv_cache.cpp:327-381) of sequence b."""
+        n = self.total_tokens
+        k = np.zeros((n, self.H, D))
+        v = np.zeros((n, self.H, D))
+        _check(lib().oscar_kv_materialize(self._h, b, k.ctypes.data, v.ctypes.data))
+        return k, v
+
+
+def lse_merge(outs, lses, out=None, lse_out=None, stream=None):
+    """Merge P partial attentions: outs [P, rows, d], lses [P, rows] (device)."""
+    import torch
+
+    P, rows, d = outs.shape
+    if out is None:
+        out = torch.empty((rows, d), dtype=torch.float32, device=outs.device)
+    _check(lib().oscar_lse_merge(_ptr(outs), _ptr(lses), P, rows, d, _ptr(out), _ptr(lse_out), _stream(stream)))
+    return out

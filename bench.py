@@ -1,0 +1,483 @@
+#!/usr/bin/env python
+"""Decode-step benchmark of the B200 OScaR KV-cache path (BASELINE.json metric).
+
+Workload (BASELINE.json configs[1], "C2"): one Llama-3-8B attention layer
+(32 query / 8 KV heads, head_dim 128), batch 16 per GPU, 32K context, INT2
+keys per-channel + values per-token (G=32, R=128), synthetic bf16 inputs.
+A "step" is one decode step of the whole batch through the public C-ABI
+(oscar_kv_decode_step): attention over the packed cache + residual window +
+current token, then the append (one flush every R=128 steps lands inside the
+timed region).  N GPUs = N independent batches (batch-sharded, no collective).
+
+Prints ONE JSON line on rank 0.  `--impl reference` times the reference's own
+CPU implementation (oracle/_ref, compiled from /root/reference) instead.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "INT2-KV decode tokens/s and µs/step at 32K ctx; achieved HBM GB/s vs peak"
+R, D = 128, 128
+BLOCK_BYTES = {2: 12800, 4: 20992, 0: 65536}
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=128)
+    p.add_argument("--warmup", type=int, default=8)
+    p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--batch", type=int, default=16)
+    p.add_argument("--ctx", type=int, default=32768)
+    p.add_argument("--q-heads", type=int, default=32)
+    p.add_argument("--kv-heads", type=int, default=8)
+    p.add_argument("--bits", type=int, default=2)
+    p.add_argument("--no-compare", action="store_true", help="skip the INT4 / bf16 comparison legs")
+    p.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    return p.parse_args()
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            m = json.load(f)
+        return float(m["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy bandwidth)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+# ----------------------------------------------------------------------------- clocks
+class ClockSampler:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.15)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except Exception:
+            self.proc.kill()
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [x.strip() for x in ln.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                smax.append(float(parts[2]))
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(smax) if smax else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ----------------------------------------------------------------------------- data
+def synth_kv(B, S, H, seed, device):
+    """TNI keys (oscar_cli.cpp:364-384 recipe) and N(0,1) values, bf16 [B,S,H,D]."""
+    import torch
+
+    g = torch.Generator(device=device)
+    g.manual_seed(seed)
+    k = torch.randn((B, S, H, D), generator=g, device=device, dtype=torch.float32)
+    signs = torch.where(torch.rand((B, 1, H, 4), generator=g, device=device) < 0.5, -1.0, 1.0)
+    k[..., 0:4] = signs * 18.0 + 0.3 * k[..., 0:4]
+    k[..., 4:12] *= 8.0
+    sinks = torch.randint(0, S, (B, 8), generator=g, device=device)
+    for b in range(B):
+        k[b, sinks[b]] = 0.01 * 44.0 * torch.randn((8, H, D), generator=g, device=device) / 11.3
+    v = torch.randn((B, S, H, D), generator=g, device=device, dtype=torch.float32)
+    return k.to(torch.bfloat16), v.to(torch.bfloat16)
+
+
+def step_inputs(n, B, Hq, Hkv, seed, device):
+    import torch
+
+    g = torch.Generator(device=device)
+    g.manual_seed(seed + 1)
+    q = torch.randn((n, B, Hq, D), generator=g, device=device).to(torch.bfloat16)
+    k, v = synth_kv(B, n, Hkv, seed + 2, device)
+    return q, k.transpose(0, 1).contiguous(), v.transpose(0, 1).contiguous()
+
+
+def algorithmic_bytes(bits, B, Hq, Hkv, packed, r, with_current=True):
+    """Bytes one decode-attention launch must move."""
+    per_bh = (packed // R) * BLOCK_BYTES[bits] + r * 2 * D * 2
+    if with_current:
+        per_bh += 2 * D * 2 * 2  # read current k,v + write them into the residual ring
+    return B * Hkv * per_bh + B * Hq * D * 2 + B * Hq * D * 4  # + q read + fp32 out write
+
+
+# ----------------------------------------------------------------------------- our arm
+def run_ours(args, rank, world, local_rank):
+    import numpy as np
+    import torch
+
+    from paper_2605_19660_b200 import KvCache, PipelineConfig
+
+    dev = torch.device("cuda", local_rank)
+    torch.cuda.set_device(dev)
+    B, S, Hq, Hkv, K, W = args.batch, args.ctx, args.q_heads, args.kv_heads, args.steps, args.warmup
+    stream = torch.cuda.current_stream()
+    dist = world > 1
+    if dist:
+        import torch.distributed as td
+
+    def barrier():
+        if dist:
+            td.barrier()
+        torch.cuda.synchronize()
+
+    def build(bits, seed):
+        cfg = PipelineConfig(method="oscar", bits=bits, heads=Hkv)
+        cache = KvCache(cfg, batch=B, q_heads=Hq, max_tokens=S + W + 2 * K + 2 * R, device=local_rank,
+                        keep_exact=(bits != 0))
+        k, v = synth_kv(B, S, Hkv, seed, dev)
+        cache.buffer_quant(k, v)
+        torch.cuda.synchronize()
+        del k, v
+        return cache
+
+    def timed_decode(cache, bits, nsteps, nwarm, seed, per_step_events=True):
+        q, kn, vn = step_inputs(nwarm + nsteps, B, Hq, Hkv, seed, dev)
+        out = torch.empty((B, Hq, D), dtype=torch.float32, device=dev)
+        for i in range(nwarm):
+            cache.decode_step(q[i], kn[i], vn[i], out=out)
+        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(nsteps)]
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        launches, flush_steps, resid = 0, [], []
+        barrier()
+        e0.record(stream)
+        for i in range(nsteps):
+            r_before = cache.residual_tokens if per_step_events else 0
+            f_before = cache.flush_count
+            if per_step_events:
+                evs[i][0].record(stream)
+            cache.decode_step(q[nwarm + i], kn[nwarm + i], vn[nwarm + i], out=out)
+            if per_step_events:
+                evs[i][1].record(stream)
+            launches += cache.last_launch_count()
+            if cache.flush_count != f_before:
+                flush_steps.append(i)
+            resid.append(r_before)
+        e1.record(stream)
+        barrier()
+        total_ms = e0.elapsed_time(e1)
+        per = [evs[i][0].elapsed_time(evs[i][1]) for i in range(nsteps)] if per_step_events else []
+        return total_ms, per, launches, flush_steps, resid, out
+
+    peak, peak_src = peaks()
+    clocks = ClockSampler(local_rank)
+
+    # ---- headline: INT2 -------------------------------------------------------------
+    cache = build(args.bits, 1234 + rank)
+    packed0 = cache.packed_tokens
+    clocks.start()
+    total_ms, per, launches, flush_steps, resid, _ = timed_decode(cache, args.bits, K, W, 99 + rank)
+    t = torch.tensor([total_ms], device=dev)
+    if dist:
+        td.all_reduce(t, op=td.ReduceOp.MAX)
+    total_ms = float(t.item())
+    # dominant kernel = decode attention: steps without a flush launch exactly that kernel
+    attn_ms = [per[i] for i in range(K) if i not in flush_steps]
+    attn_avg_ms = sum(attn_ms) / len(attn_ms)
+    attn_bytes = [algorithmic_bytes(args.bits, B, Hq, Hkv, packed0 if i not in flush_steps else packed0, resid[i])
+                  for i in range(K) if i not in flush_steps]
+    achieved = (sum(attn_bytes) / len(attn_bytes)) / (attn_avg_ms * 1e-3) / 1e9
+
+    # ---- e2e through the host-buffer C-ABI entry (pinned host memory) -------------
+    qh, kh, vh = step_inputs(K, B, Hq, Hkv, 777 + rank, dev)
+    q_host = qh.cpu().pin_memory().view(torch.int16).numpy().view(np.uint16)
+    k_host = kh.cpu().pin_memory().view(torch.int16).numpy().view(np.uint16)
+    v_host = vh.cpu().pin_memory().view(torch.int16).numpy().view(np.uint16)
+    out_host = torch.empty((B, Hq, D), dtype=torch.float32).pin_memory().numpy()
+    barrier()
+    t0 = time.perf_counter()
+    for i in range(K):
+        cache.decode_step_host(q_host[i], k_host[i], v_host[i], out_host)
+    barrier()
+    e2e_s = time.perf_counter() - t0
+    te = torch.tensor([e2e_s], device=dev)
+    if dist:
+        td.all_reduce(te, op=td.ReduceOp.MAX)
+    e2e_s = float(te.item())
+    clk = clocks.stop()
+    h2d = q_host[0].nbytes + k_host[0].nbytes + v_host[0].nbytes
+    d2h = out_host.nbytes
+
+    result = {
+        "metric": METRIC,
+        "value": world * B * K / (total_ms * 1e-3),
+        "unit": "tokens/s",
+        "n_gpus": world,
+        "steps": K,
+        "warmup": W,
+        "ms_per_step": total_ms / K,
+        "us_per_step": 1e3 * total_ms / K,
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "int2" if args.bits == 2 else ("int4" if args.bits == 4 else "bf16"),
+        "compute": "2-bit codes as fp16-subnormal mma.sync A operands, fp16 B, fp32 accumulate/softmax",
+        "data": "synthetic (TNI-recipe keys, N(0,1) values/queries), bf16 inputs",
+        "config": {
+            "workload": f"C2: Llama-3-8B attention layer ({Hq} q / {Hkv} kv heads, d=128), batch {B}/GPU, "
+                        f"{S} ctx, INT{args.bits} K per-channel + V per-token, G=32, R=128",
+            "batch_per_gpu": B, "context": S, "q_heads": Hq, "kv_heads": Hkv, "bits": args.bits,
+            "parallelism": f"batch-sharded x{world} (no collective)",
+            "l2": "inputs larger than L2 (packed cache %.0f MB/GPU > 126 MB)" % (
+                B * Hkv * (S // R) * BLOCK_BYTES[args.bits] / 1e6),
+            "flushes_in_timed_region": len(flush_steps),
+        },
+        "gpu_launches": launches,
+        "roofline": {
+            "bound": "hbm",
+            "kernel": "decode_attn_kernel<%d>" % args.bits,
+            "achieved": achieved,
+            "peak": peak,
+            "peak_source": peak_src,
+            "unit": "GB/s",
+            "frac": achieved / peak,
+            "traffic": traffic_from_profile(args.bits),
+            "algorithmic_bytes_per_launch": sum(attn_bytes) / len(attn_bytes),
+            "avg_launch_us": attn_avg_ms * 1e3,
+        },
+        "e2e": {"value": world * B * K / e2e_s, "unit": "tokens/s", "h2d_bytes_per_step": int(h2d),
+                "d2h_bytes_per_step": int(d2h), "us_per_step": 1e6 * e2e_s / K,
+                "entry": "oscar_kv_decode_step_host (pinned host q/k/v in, fp32 out back)"},
+        "clocks": clk,
+    }
+    cache.close()
+    del cache
+    torch.cuda.empty_cache()
+
+    # ---- comparison legs (same GPU, same workload) -----------------------------------
+    if not args.no_compare:
+        cmp = {}
+        for bits in (4, 0):
+            c2 = build(bits, 4321 + rank)
+            p0 = c2.packed_tokens
+            ms, per2, _, fl2, res2, _ = timed_decode(c2, bits, 32, 4, 55 + rank)
+            a_ms = [per2[i] for i in range(32) if i not in fl2]
+            avg = sum(a_ms) / len(a_ms)
+            byt = algorithmic_bytes(bits, B, Hq, Hkv, p0, res2[0])
+            cmp["int4" if bits == 4 else "bf16_exact_cache"] = {
+                "us_per_step": 1e3 * ms / 32, "tokens_per_s": B * 32 / (ms * 1e-3),
+                "attn_kernel_us": avg * 1e3, "achieved_gbs": byt / (avg * 1e-3) / 1e9,
+                "frac": byt / (avg * 1e-3) / 1e9 / peak}
+            c2.close()
+            del c2
+            torch.cuda.empty_cache()
+        cmp["bf16_torch_sdpa"] = torch_sdpa_baseline(B, S, Hq, Hkv, dev)
+        bf = cmp["bf16_exact_cache"]["attn_kernel_us"]
+        cmp["speedup_int2_vs_bf16_kernel"] = bf / result["roofline"]["avg_launch_us"]
+        if cmp["bf16_torch_sdpa"].get("us"):
+            cmp["speedup_int2_vs_torch_sdpa"] = cmp["bf16_torch_sdpa"]["us"] / result["roofline"]["avg_launch_us"]
+        result["comparisons"] = cmp
+
+    if not args.no_cpu and rank == 0:
+        result["cpu_baseline"] = cpu_baseline(S, Hq, Hkv, n_steps=3)
+    return result
+
+
+def traffic_from_profile(bits):
+    """dram bytes per launch of the attention kernel from the committed ncu capture."""
+    p = os.path.join(ROOT, "profiles", "attention_traffic.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        return d.get(str(bits))
+    except Exception:
+        return None
+
+
+def torch_sdpa_baseline(B, S, Hq, Hkv, dev):
+    """bf16 decode attention through torch SDPA (library kernel), same shapes."""
+    import torch
+    import torch.nn.functional as F
+
+    try:
+        q = torch.randn((B, Hq, 1, D), device=dev, dtype=torch.bfloat16)
+        k = torch.randn((B, Hkv, S, D), device=dev, dtype=torch.bfloat16)
+        v = torch.randn((B, Hkv, S, D), device=dev, dtype=torch.bfloat16)
+        for _ in range(3):
+            F.scaled_dot_product_attention(q, k, v, enable_gqa=True)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        n = 20
+        e0.record()
+        for _ in range(n):
+            F.scaled_dot_product_attention(q, k, v, enable_gqa=True)
+        e1.record()
+        torch.cuda.synchronize()
+        us = 1e3 * e0.elapsed_time(e1) / n
+        byt = 2 * B * Hkv * S * D * 2
+        return {"us": us, "achieved_gbs": byt / (us * 1e-6) / 1e9}
+    except Exception as e:  # noqa: BLE001
+        return {"us": None, "error": str(e)[:200]}
+
+
+# ----------------------------------------------------------------------------- CPU legs
+def cpu_threads():
+    return os.cpu_count() or 1
+
+
+def cpu_baseline(S, Hq, Hkv, n_steps=3, heads_sample=None):
+    """The reference's own CPU path (oracle/_ref): KvCache + apply_method +
+    materialize + attention for one sequence at full context (pipeline.cpp:292-323
+    body, GQA via query rows).  Returns tokens/s of that sample."""
+    os.environ.setdefault("OMP_NUM_THREADS", str(cpu_threads()))
+    import numpy as np
+
+    from oracle import bindings as ob
+
+    kind = "reference" if ob.ref_available() else "port"
+    H = heads_sample or Hkv
+    g = Hq // Hkv
+    rng = np.random.default_rng(5)
+    from paper_2605_19660_b200.synthetic import make_inputs, make_queries
+
+    k, v = make_inputs(5, S + n_steps + 1, H)
+    q = make_queries(5, n_steps + 1, H * g)
+    if kind == "reference":
+        cache = ob.RefCache(H=H)
+    else:
+        cache = ob.PortCache(H=H)
+    t0 = time.perf_counter()
+    cache.append(k[:S], v[:S])
+    prefill_s = time.perf_counter() - t0
+    cache.decode_step(q[0], k[S], v[S], g)  # warm-up
+    t0 = time.perf_counter()
+    for i in range(1, n_steps + 1):
+        cache.decode_step(q[i], k[S + i], v[S + i], g)
+    dt = time.perf_counter() - t0
+    frac = H / Hkv
+    del rng
+    return {"value": frac * n_steps / dt, "unit": "tokens/s", "cores": cpu_threads(), "kind": kind,
+            "sample": f"1 sequence x {H}/{Hkv} KV heads ({H * g} q heads) at {S} ctx, {n_steps} decode steps "
+                      f"(apply_method + materialize_k/v + attention + buffer_quant; prefill {prefill_s:.1f}s untimed)",
+            "s_per_step": dt / n_steps}
+
+
+def run_reference(args):
+    """--impl reference: the reference CPU implementation on the same config."""
+    os.environ.setdefault("OMP_NUM_THREADS", str(cpu_threads()))
+    import numpy as np
+
+    from oracle import bindings as ob
+    from paper_2605_19660_b200.synthetic import make_inputs, make_queries
+
+    S, Hq, Hkv, K, W = args.ctx, args.q_heads, args.kv_heads, args.steps, args.warmup
+    g = Hq // Hkv
+    kind = "reference" if ob.ref_available() else "port"
+    mk = ob.RefCache if kind == "reference" else ob.PortCache
+    # bounded sample: one sequence, as many KV heads as fit ~150 s for W+K steps
+    probe_k, probe_v = make_inputs(3, S + 2, 1)
+    c = mk(H=1)
+    c.append(probe_k[:S], probe_v[:S])
+    qp = make_queries(3, 1, g)[0]
+    t0 = time.perf_counter()
+    c.decode_step(qp, probe_k[S], probe_v[S], g)
+    t_head = time.perf_counter() - t0
+    del c
+    H = int(max(1, min(Hkv, 150.0 / max(K + W, 1) / max(t_head, 1e-6))))
+    k, v = make_inputs(4, S + K + W, H)
+    q = make_queries(4, K + W, H * g)
+    cache = mk(H=H)
+    cache.append(k[:S], v[:S])
+    for i in range(W):
+        cache.decode_step(q[i], k[S + i], v[S + i], g)
+    t0 = time.perf_counter()
+    for i in range(W, W + K):
+        cache.decode_step(q[i], k[S + i], v[S + i], g)
+    dt = time.perf_counter() - t0
+    value = (H / Hkv) * K / dt
+    sample = (f"per step: 1 sequence x {H}/{Hkv} KV heads ({H * g}/{Hq} q heads) at {S} ctx: apply_method + "
+              f"materialize_k/v + attention + buffer_quant (reference decode_step body, pipeline.cpp:292-323); "
+              f"value scaled to whole-layer sequence-tokens")
+    del np
+    return {
+        "impl": "reference",
+        "metric": METRIC,
+        "value": value,
+        "unit": "tokens/s",
+        "n_gpus": args.gpus,
+        "steps": K,
+        "warmup": W,
+        "ms_per_step": 1e3 * dt / K,
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "f64",
+        "data": "synthetic (TNI-recipe keys, N(0,1) values/queries), bf16-representable",
+        "config": {"workload": f"C2 layer shape ({Hq} q / {Hkv} kv heads, d=128), {S} ctx, INT2, G=32, R=128 "
+                               f"(CPU sample of one sequence)", "context": S, "bits": 2},
+        "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": cpu_threads(), "kind": kind,
+                         "sample": sample},
+        "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+
+
+def main():
+    args = parse()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        print(json.dumps(run_reference(args)), flush=True)
+        return
+    if world > 1:
+        import torch
+        import torch.distributed as td
+
+        torch.cuda.set_device(local_rank)
+        td.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    res = run_ours(args, rank, world, local_rank)
+    if rank == 0:
+        print(json.dumps(res), flush=True)
+    if world > 1:
+        import torch.distributed as td
+
+        td.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -4,12 +4,12 @@
 //
 // Persistent, stream-K style: one CTA per SM gets an equal contiguous range
 // of the global (sequence*KV-head, R-block) space, so every SM streams the
-// same number of bytes.  Warp roles:
-//   warp NCW      producer: one elected lane streams whole R-block records
-//                 (12.8 KB INT2 / 21 KB INT4, see layout.h) HBM -> shared
-//                 memory with cp.async.bulk (TMA engine) into an NST-stage
-//                 mbarrier ring, L2 evict-first;
-//   warps 0..NCW-1 consumers: block p of the range goes to warp p % NCW.
+// same number of bytes.  All 8 warps consume: unit p of the range (one
+// R-block record of 12.8 KB INT2 / 21 KB INT4, or a 16 KB quarter of a bf16
+// record, see layout.h) is streamed HBM -> shared memory by ONE cp.async.bulk
+// (TMA engine, L2 evict-first) into stage p % NST of an mbarrier ring and
+// processed by warp p % 8, which then refills that same stage with unit
+// p + NST -- no producer warp, no empty barriers, 255 registers per thread.
 // Per block a consumer runs QK^T and P.V on the tensor cores
 // (mma.sync m16n8k16, fp16 in / fp32 accumulate) straight from the packed
 // codes: every loaded 32-bit word ANDed with a field mask IS an A register
@@ -34,23 +34,27 @@ namespace osk {
 
 namespace {
 
-constexpr int NCW = 8;                 // consumer warps
-constexpr int NTHREADS = (NCW + 1) * 32;
+constexpr int NCW = 8;                 // warps per CTA (all consume; each refills its own stage)
+constexpr int NTHREADS = NCW * 32;
 constexpr int MERGE_FLOATS = 8 * D + 16;  // per-warp partial: O[8][128], m[8], l[8]
 constexpr float LOG2E = 1.4426950408889634f;
 constexpr float LN2 = 0.6931471805599453f;
 
 template <int BITS>
 struct AttnCfg {
+    // one pipeline stage: a whole INT2/INT4 record, or a 32-token quarter of a bf16 record
     static constexpr int BYTES = (BITS == 0) ? BF16_BLOCK_BYTES : Block<BITS == 0 ? 2 : BITS>::BYTES;
-    static constexpr int NST = (BITS == 2) ? 13 : (BITS == 4 ? 8 : 2);
-    static constexpr int RING = NST * BYTES;
+    static constexpr int SUB = (BITS == 0) ? 4 : 1;
+    static constexpr int STAGE = BYTES / SUB;
+    static constexpr int NST = (BITS == 2) ? 13 : (BITS == 4 ? 8 : 11);
+    static constexpr int RING = NST * STAGE;
     static constexpr int MERGE_OFF = RING;
     static constexpr int QS_OFF = MERGE_OFF + NCW * MERGE_FLOATS * 4;
     static constexpr int QR_OFF = QS_OFF + 8 * D * 4;
     static constexpr int BAR_OFF = QR_OFF + 8 * D * 4;
-    static constexpr int MISC_OFF = BAR_OFF + 2 * NST * 8;
+    static constexpr int MISC_OFF = BAR_OFF + NST * 8;
     static constexpr int SMEM = MISC_OFF + 16;
+    static_assert(SMEM <= 232448, "shared memory budget");
 };
 
 __device__ __forceinline__ float warp_sum(float v) {
@@ -123,27 +127,15 @@ __device__ __forceinline__ void process_block(const uint8_t *__restrict__ sb, Wa
     constexpr uint32_t FMASK = (BITS == 2) ? 0x00030003u : 0x000F000Fu;
     const int gq = lane >> 2, tq = lane & 3;
 
-    // ---- key offsets: bias[grp][head] = sum_c bK[c,grp] * Qrot[head,c] -------------
-    float kbias[4] = {0.f, 0.f, 0.f, 0.f};
-    {
-        uint32_t bk[16];
-        if (gq < 4) {
-            const uint4 *p = reinterpret_cast<const uint4 *>(sb + Blk::KB_OFF + (gq * 4 + tq) * 64);
+    // ---- key zero points as A (row gq = group): bias[grp][head] =
+    //      sum_c nz[c,grp] * B[grp][c][head], B = Qrot*step -- the SAME fp16 B as the
+    //      code MMA, so dot = sum_c B*(code - zp) is consistent
+    // lane gq < 4 holds row gq (= group); rows 4..15 are zero
+    const uint2 *bkp = reinterpret_cast<const uint2 *>(sb + Blk::KB_OFF + ((gq & 3) * 4 + tq) * 64);
+    const uint32_t bkmask = gq < 4 ? 0xffffffffu : 0u;
+    float kbias[4][4];
 #pragma unroll
-            for (int i = 0; i < 4; ++i) {
-                const uint4 u = p[i];
-                bk[4 * i] = u.x;
-                bk[4 * i + 1] = u.y;
-                bk[4 * i + 2] = u.z;
-                bk[4 * i + 3] = u.w;
-            }
-        } else {
-#pragma unroll
-            for (int i = 0; i < 16; ++i) bk[i] = 0u;
-        }
-#pragma unroll
-        for (int s = 0; s < 8; ++s) mma16816(kbias, bk[2 * s], 0u, bk[2 * s + 1], 0u, qf[s][0], qf[s][1]);
-    }
+    for (int grp = 0; grp < 4; ++grp) kbias[grp][0] = kbias[grp][1] = kbias[grp][2] = kbias[grp][3] = 0.f;
 
     // ---- QK^T --------------------------------------------------------------------
     float sacc[8][4];
@@ -178,6 +170,12 @@ __device__ __forceinline__ void process_block(const uint8_t *__restrict__ sb, Wa
             bq[3][0] = hmul2_u32(qf[s][0], a23.z);
             bq[3][1] = hmul2_u32(qf[s][1], a23.w);
         }
+        {
+            const uint2 z = bkp[s];
+            const uint32_t z0 = z.x & bkmask, z1 = z.y & bkmask;
+#pragma unroll
+            for (int grp = 0; grp < 4; ++grp) mma16816(kbias[grp], z0, 0u, z1, 0u, bq[grp][0], bq[grp][1]);
+        }
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
             const int half = i / TPW, f = i % TPW;
@@ -206,8 +204,8 @@ __device__ __forceinline__ void process_block(const uint8_t *__restrict__ sb, Wa
     float kb0[4], kb1[4];
 #pragma unroll
     for (int grp = 0; grp < 4; ++grp) {
-        kb0[grp] = __shfl_sync(0xffffffffu, kbias[0], grp * 4 + tq);
-        kb1[grp] = __shfl_sync(0xffffffffu, kbias[1], grp * 4 + tq);
+        kb0[grp] = __shfl_sync(0xffffffffu, kbias[grp][0], grp * 4 + tq);
+        kb1[grp] = __shfl_sync(0xffffffffu, kbias[grp][1], grp * 4 + tq);
     }
     float bm0 = -CUDART_INF_F, bm1 = -CUDART_INF_F;
 #pragma unroll
@@ -254,21 +252,8 @@ __device__ __forceinline__ void process_block(const uint8_t *__restrict__ sb, Wa
     st.ob[1] *= al1;
 
     // ---- P.V ---------------------------------------------------------------------------
-    uint32_t vbA[16];  // value offsets as A: row gq = channel group, k = tokens
-    if (gq < 4) {
-        const uint4 *p = reinterpret_cast<const uint4 *>(sb + Blk::VB_OFF + (gq * 4 + tq) * 64);
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-            const uint4 u = p[i];
-            vbA[4 * i] = u.x;
-            vbA[4 * i + 1] = u.y;
-            vbA[4 * i + 2] = u.z;
-            vbA[4 * i + 3] = u.w;
-        }
-    } else {
-#pragma unroll
-        for (int i = 0; i < 16; ++i) vbA[i] = 0u;
-    }
+    // value offsets as A: row gq (< 4) = channel group, k = tokens
+    const uint2 *vbp = reinterpret_cast<const uint2 *>(sb + Blk::VB_OFF + ((gq & 3) * 4 + tq) * 64);
     const int srcA = 4 * tq + (gq >> 1), srcB = 4 * (tq + 4) + (gq >> 1);
     const bool odd = (gq & 1) != 0;
 #pragma unroll
@@ -316,37 +301,34 @@ __device__ __forceinline__ void process_block(const uint8_t *__restrict__ sb, Wa
             mma16816(st.o[mm], src[0 * WPF + half] & mask, src[1 * WPF + half] & mask,
                      src[2 * WPF + half] & mask, src[3 * WPF + half] & mask, bv[mm >> 1][0], bv[mm >> 1][1]);
         }
-        mma16816(st.ob, vbA[2 * j], 0u, vbA[2 * j + 1], 0u, bp0, bp1);
+        {
+            const uint2 z = vbp[j];
+            mma16816(st.ob, z.x & bkmask, 0u, z.y & bkmask, 0u, bp0, bp1);
+        }
     }
 }
 
-// bf16 baseline block: raw K/V [token][channel] bf16 (no dequant); same
-// fragment orders, A operands built from shared memory with plain loads.
-__device__ __forceinline__ void process_block_bf16(const uint8_t *__restrict__ sb, WarpState &st,
-                                                   const uint32_t (&qf)[8][2], int lane, float c0) {
+// bf16 baseline: one 32-token quarter of a raw bf16 record, [K 8 KB][V 8 KB]
+// already in A-fragment order (layout.h) -> one LDS.128 per MMA, no dequant.
+__device__ __forceinline__ void process_quarter_bf16(const uint8_t *__restrict__ sb, WarpState &st,
+                                                     const uint32_t (&qf)[8][2], int lane, float c0) {
     const int gq = lane >> 2, tq = lane & 3;
-    const uint16_t *K = reinterpret_cast<const uint16_t *>(sb);
-    const uint16_t *V = K + R * D;
-    // K rows: swizzle-free layout with row stride 256 B: 4B loads of channel pairs
-    float sacc[8][4];
+    const uint4 *K = reinterpret_cast<const uint4 *>(sb);
+    const uint4 *V = reinterpret_cast<const uint4 *>(sb + BF16_QUARTER_BYTES / 2);
+    float sacc[2][4];
 #pragma unroll
-    for (int i = 0; i < 8; ++i) sacc[i][0] = sacc[i][1] = sacc[i][2] = sacc[i][3] = 0.f;
+    for (int i = 0; i < 2; ++i) sacc[i][0] = sacc[i][1] = sacc[i][2] = sacc[i][3] = 0.f;
 #pragma unroll
     for (int s = 0; s < 8; ++s) {
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {
-            const int t0 = 16 * i + gq, t1 = t0 + 8;
-            const int c = 16 * s + 2 * tq;
-            const uint32_t a0 = *reinterpret_cast<const uint32_t *>(K + t0 * D + c);
-            const uint32_t a1 = *reinterpret_cast<const uint32_t *>(K + t1 * D + c);
-            const uint32_t a2 = *reinterpret_cast<const uint32_t *>(K + t0 * D + c + 8);
-            const uint32_t a3 = *reinterpret_cast<const uint32_t *>(K + t1 * D + c + 8);
-            mma16816_bf16(sacc[i], a0, a1, a2, a3, qf[s][0], qf[s][1]);
+        for (int i = 0; i < 2; ++i) {
+            const uint4 a = K[(i * 8 + s) * 32 + lane];
+            mma16816_bf16(sacc[i], a.x, a.y, a.z, a.w, qf[s][0], qf[s][1]);
         }
     }
     float bm0 = -CUDART_INF_F, bm1 = -CUDART_INF_F;
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
+    for (int i = 0; i < 2; ++i) {
 #pragma unroll
         for (int e = 0; e < 4; ++e) sacc[i][e] *= c0;
         bm0 = fmaxf(bm0, fmaxf(sacc[i][0], sacc[i][2]));
@@ -363,7 +345,7 @@ __device__ __forceinline__ void process_block_bf16(const uint8_t *__restrict__ s
     st.m[1] = mn1;
     float ls0 = 0.f, ls1 = 0.f;
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
+    for (int i = 0; i < 2; ++i) {
         sacc[i][0] = fast_exp2(sacc[i][0] - mn0);
         sacc[i][1] = fast_exp2(sacc[i][1] - mn1);
         sacc[i][2] = fast_exp2(sacc[i][2] - mn0);
@@ -383,7 +365,7 @@ __device__ __forceinline__ void process_block_bf16(const uint8_t *__restrict__ s
     const int srcA = 4 * tq + (gq >> 1), srcB = 4 * (tq + 4) + (gq >> 1);
     const bool odd = (gq & 1) != 0;
 #pragma unroll
-    for (int j = 0; j < 8; ++j) {
+    for (int j = 0; j < 2; ++j) {
         const uint32_t H0 = pack_bf162(sacc[j][0], sacc[j][2]);
         const uint32_t H1 = pack_bf162(sacc[j][1], sacc[j][3]);
         const uint32_t x0 = __shfl_sync(0xffffffffu, H0, srcA);
@@ -391,15 +373,10 @@ __device__ __forceinline__ void process_block_bf16(const uint8_t *__restrict__ s
         const uint32_t y0 = __shfl_sync(0xffffffffu, H0, srcB);
         const uint32_t y1 = __shfl_sync(0xffffffffu, H1, srcB);
         const uint32_t bp0 = odd ? x1 : x0, bp1 = odd ? y1 : y0;
-        const int t1 = 16 * j + tq, t2 = t1 + 8, t3 = t1 + 4, t4 = t1 + 12;
 #pragma unroll
         for (int mm = 0; mm < 8; ++mm) {
-            const int c0r = 16 * mm + gq, c1r = c0r + 8;
-            const uint32_t a0 = (uint32_t)V[t1 * D + c0r] | ((uint32_t)V[t2 * D + c0r] << 16);
-            const uint32_t a1 = (uint32_t)V[t1 * D + c1r] | ((uint32_t)V[t2 * D + c1r] << 16);
-            const uint32_t a2 = (uint32_t)V[t3 * D + c0r] | ((uint32_t)V[t4 * D + c0r] << 16);
-            const uint32_t a3 = (uint32_t)V[t3 * D + c1r] | ((uint32_t)V[t4 * D + c1r] << 16);
-            mma16816_bf16(st.o[mm], a0, a1, a2, a3, bp0, bp1);
+            const uint4 a = V[(j * 8 + mm) * 32 + lane];
+            mma16816_bf16(st.o[mm], a.x, a.y, a.z, a.w, bp0, bp1);
         }
     }
 }
@@ -412,12 +389,12 @@ __global__ void __launch_bounds__(NTHREADS, 1) decode_attn_kernel(const AttnArgs
     float *qs = reinterpret_cast<float *>(smem + C::QS_OFF);  // rotated q [8][D]
     float *qr = reinterpret_cast<float *>(smem + C::QR_OFF);  // raw q [8][D]
     uint64_t *full = reinterpret_cast<uint64_t *>(smem + C::BAR_OFF);
-    uint64_t *empty = full + C::NST;
     int *misc = reinterpret_cast<int *>(smem + C::MISC_OFF);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int cta = blockIdx.x;
-    const int64_t nb = a.nb;
+    constexpr int SUB = C::SUB;
+    const int64_t nb = a.nb * SUB;  // pipeline units per (b, kv head)
     const int64_t total = (int64_t)a.BH * nb;
     int64_t start, end;
     if (total > 0) {
@@ -426,32 +403,25 @@ __global__ void __launch_bounds__(NTHREADS, 1) decode_attn_kernel(const AttnArgs
     } else {
         start = end = 0;
     }
+    const int64_t nunits = end - start;
+    const uint64_t pol = l2_evict_first_policy();
+    // unit p of this CTA's range -> stage p % NST (TMA bulk copy, complete_tx on full[stage])
+    auto issue = [&](int64_t p) {
+        const int64_t gidx = start + p;
+        const int64_t bh = gidx / nb, unit = gidx % nb;
+        const int64_t blk = unit / SUB, sub = unit % SUB;
+        const int stg = (int)(p % C::NST);
+        mbar_arrive_expect_tx(&full[stg], C::STAGE);
+        bulk_g2s(smem + stg * C::STAGE, a.blocks + (bh * a.max_blocks + blk) * (int64_t)C::BYTES + sub * C::STAGE,
+                 C::STAGE, &full[stg], pol);
+    };
 
     if (threadIdx.x == 0) {
-        for (int i = 0; i < C::NST; ++i) {
-            mbar_init(&full[i], 1);
-            mbar_init(&empty[i], 1);
-        }
+        for (int i = 0; i < C::NST; ++i) mbar_init(&full[i], 1);
         fence_mbar_init();
+        for (int64_t p = 0; p < nunits && p < C::NST; ++p) issue(p);
     }
     __syncthreads();
-
-    if (warp == NCW) {
-        // ================= producer =================
-        if (lane == 0 && end > start) {
-            const uint64_t pol = l2_evict_first_policy();
-            for (int64_t p = 0; p < end - start; ++p) {
-                const int64_t gidx = start + p;
-                const int64_t bh = gidx / nb, blk = gidx % nb;
-                const int stg = (int)(p % C::NST);
-                if (p >= C::NST) mbar_wait(&empty[stg], (uint32_t)(((p / C::NST) - 1) & 1));
-                mbar_arrive_expect_tx(&full[stg], C::BYTES);
-                bulk_g2s(smem + stg * C::BYTES, a.blocks + (bh * a.max_blocks + blk) * (int64_t)C::BYTES, C::BYTES,
-                         &full[stg], pol);
-            }
-        }
-        return;
-    }
 
     // ================= consumers =================
     const float c0 = LOG2E * 0.08838834764831845f;  // log2(e)/sqrt(128)
@@ -489,7 +459,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) decode_attn_kernel(const AttnArgs
 #pragma unroll
             for (int e = 0; e < 4; ++e) qs[j * D + lane * 4 + e] = x[e];
         }
-        named_bar(1, NCW * 32);
+        __syncthreads();
         uint32_t qf[8][2];
 #pragma unroll
         for (int s = 0; s < 8; ++s) {
@@ -519,14 +489,18 @@ __global__ void __launch_bounds__(NTHREADS, 1) decode_attn_kernel(const AttnArgs
             for (int64_t p = first; p < hi - start; p += NCW) {
                 const int stg = (int)(p % C::NST);
                 mbar_wait(&full[stg], (uint32_t)((p / C::NST) & 1));
-                const uint8_t *sb = smem + stg * C::BYTES;
+                const uint8_t *sb = smem + stg * C::STAGE;
                 if constexpr (BITS == 0) {
-                    process_block_bf16(sb, st, qf, lane, c0);
+                    process_quarter_bf16(sb, st, qf, lane, c0);
                 } else {
                     process_block<BITS>(sb, st, qf, lane, c0);
                 }
+                // this warp owns the stage now: refill it with unit p + NST
                 __syncwarp();
-                if (lane == 0) mbar_arrive(&empty[stg]);
+                if (lane == 0 && p + C::NST < nunits) {
+                    fence_proxy_async_smem();
+                    issue(p + C::NST);
+                }
             }
         }
 
@@ -634,7 +608,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) decode_attn_kernel(const AttnArgs
                 __syncwarp();
             }
         }
-        named_bar(1, NCW * 32);
+        __syncthreads();
 
         // ---- CTA merge of the NCW warp partials -> global partial slot ----
         int64_t first_cta = 0, last_cta = 0;
@@ -666,12 +640,12 @@ __global__ void __launch_bounds__(NTHREADS, 1) decode_attn_kernel(const AttnArgs
             }
         }
         __threadfence();
-        named_bar(1, NCW * 32);
+        __syncthreads();
         if (threadIdx.x == 0) {
             const int prev = atomicAdd(&a.counters[bh], 1);
             misc[0] = (prev == expected - 1) ? 1 : 0;
         }
-        named_bar(1, NCW * 32);
+        __syncthreads();
         const bool last = misc[0] != 0;
         if (last) {
             __threadfence();
@@ -700,7 +674,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) decode_attn_kernel(const AttnArgs
                     a.lse[(int64_t)b * a.Hq + kvh * g + h] = (L > 0.f) ? (M + __log2f(L)) * LN2 : -CUDART_INF_F;
             }
             if (a.rotate_v) {
-                named_bar(1, NCW * 32);
+                __syncthreads();
                 for (int j = warp; j < g; j += NCW) {
                     float x[4];
 #pragma unroll
@@ -725,7 +699,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) decode_attn_kernel(const AttnArgs
                     vs[lane];
             }
         }
-        named_bar(1, NCW * 32);
+        __syncthreads();
     }
 }
 

@@ -377,9 +377,23 @@ HostCache build_host_cache(oscar_kv_handle *h, int64_t b) {
                 for (int t = 0; t < R; ++t)
                     hc.k_norms[hh][k * R + t] = sh[SHADOW_K_DOUBLES + SHADOW_V_DOUBLES + t];
             } else {
-                // raw bf16 block: K rows -> apply_method transform in fp64 (exact replay)
-                const uint16_t *kr = reinterpret_cast<const uint16_t *>(blk.data());
-                const uint16_t *vr = kr + R * D;
+                // raw bf16 block: undo the fragment order, then K rows -> apply_method
+                // transform in fp64 (exact replay of what the reference stores)
+                std::vector<uint16_t> kraw(R * D), vraw(R * D);
+                constexpr int QW = BF16_QUARTER_BYTES / 8;
+                for (int qu = 0; qu < 4; ++qu) {
+                    const uint32_t *qw = reinterpret_cast<const uint32_t *>(blk.data() + qu * BF16_QUARTER_BYTES);
+                    for (int w = 0; w < QW; ++w)
+                        for (int hi = 0; hi < 2; ++hi) {
+                            int t, c;
+                            bf16_k_coords(w, hi, t, c);
+                            kraw[(qu * 32 + t) * D + c] = (uint16_t)(qw[w] >> (16 * hi));
+                            bf16_v_coords(w, hi, t, c);
+                            vraw[(qu * 32 + t) * D + c] = (uint16_t)(qw[QW + w] >> (16 * hi));
+                        }
+                }
+                const uint16_t *kr = kraw.data();
+                const uint16_t *vr = vraw.data();
                 for (int t = 0; t < R; ++t) {
                     double row[D];
                     for (int c = 0; c < D; ++c) row[c] = host::bf16_to_double(kr[t * D + c]);

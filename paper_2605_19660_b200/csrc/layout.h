@@ -8,14 +8,16 @@
 //   [K codes  4096 B]  mma A-fragment order      [K codes  8192 B]
 //   [V codes  4096 B]  mma A-fragment order      [V codes  8192 B]
 //   [K a      1024 B]  fp16 step  per (ch,grp)   ... same params/norms ...
-//   [K b      1024 B]  fp16 offset per (ch,grp)
+//   [K z      1024 B]  fp16 -zero point per (ch,grp)
 //   [V a      1024 B]  fp16 step  per (tok,gc)
 //   [V b      1024 B]  fp16 offset per (tok,gc)
 //   [norms     512 B]  fp32 per token
 //
-// Dequantisation is affine per group: x = a*code + b with a = delta and
-// b = -delta*zp (a = 0, b = constant for a constant group), i.e. exactly the
-// reference's dequantize_one (quant.cpp:65-68) narrowed to fp16.
+// Keys dequantise as x = a*(code + z) with a = delta, z = -zp (a constant
+// group stores a = constant, z = 1: its codes are 0), values as x = a*code + b
+// with b = -delta*zp (a = 0, b = constant) -- the reference's dequantize_one
+// (quant.cpp:65-68) with the step narrowed to fp16; the key form keeps the
+// zero point exact so the kernel's dot product stays sum_c B_c*(code - zp).
 //
 // The codes are the reference's codes (bit-identical values) permuted inside
 // the block so that every 32-bit word a lane loads IS an mma.m16n8k16 A
@@ -73,7 +75,29 @@ struct Block {
 };
 static_assert(Block<2>::BYTES == 12800, "int2 block size");
 static_assert(Block<4>::BYTES == 20992, "int4 block size");
-constexpr int BF16_BLOCK_BYTES = 2 * R * D * 2;  // raw bf16 K then V, [token][channel]
+// bits == 0 (exact bf16 cache, the unquantized baseline): an R-block is four
+// 32-token quarters, each [K 8 KB][V 8 KB] of raw bf16 in A-fragment order so
+// a lane's four A registers are one 16-byte load.
+constexpr int BF16_BLOCK_BYTES = 2 * R * D * 2;
+constexpr int BF16_QUARTER_BYTES = BF16_BLOCK_BYTES / 4;
+// K word w (32-bit = 2 bf16) of a quarter: w = ((i*8 + s)*32 + lane)*4 + reg,
+//   reg 0:(row g, k 2tq) 1:(row g+8, k 2tq) 2:(row g, k 2tq+8) 3:(row g+8, k 2tq+8)
+//   row -> token 16i + row (within the quarter), k -> channel 16s + k (+0/+1 halves)
+OSK_HD void bf16_k_coords(int w, int hi, int &token, int &channel) {
+    const int reg = w & 3, lane = (w >> 2) & 31, s = (w >> 7) & 7, i = w >> 10;
+    const int g = lane >> 2, tq = lane & 3;
+    token = 16 * i + g + ((reg & 1) ? 8 : 0);
+    channel = 16 * s + 2 * tq + ((reg & 2) ? 8 : 0) + hi;
+}
+// V word w of a quarter: w = ((j*8 + m)*32 + lane)*4 + reg,
+//   reg 0:(row g; t1,t2) 1:(row g+8; t1,t2) 2:(row g; t3,t4) 3:(row g+8; t3,t4)
+//   row -> channel 16m + row; t1 = 16j+tq, t2 = t1+8, t3 = t1+4, t4 = t1+12 (hi = 2nd)
+OSK_HD void bf16_v_coords(int w, int hi, int &token, int &channel) {
+    const int reg = w & 3, lane = (w >> 2) & 31, m = (w >> 7) & 7, j = w >> 10;
+    const int g = lane >> 2, tq = lane & 3;
+    channel = 16 * m + g + ((reg & 1) ? 8 : 0);
+    token = 16 * j + tq + ((reg & 2) ? 4 : 0) + (hi ? 8 : 0);
+}
 
 // ---- K code words --------------------------------------------------------
 // word index w = ((s*32 + lane)*4 + fam)*WPF + half, WPF = 8/TILES_PER_WORD

@@ -251,10 +251,10 @@ __global__ void __launch_bounds__(QT) quantize_kernel(const QuantizeArgs a) {
             const int c = tid;  // channel
             const GroupQ p = group_params([&](int i) { return ku[i * 129 + c]; }, BITS);
             for (int i = 0; i < G; ++i) ck[(gi * G + i) * D + c] = quantize_one(ku[i * 129 + c], p, BITS);
-            __half ha, hb;
-            affine16(p, ha, hb);
-            ka[ka_index(c, gi)] = ha;
-            kb[kb_index(c, gi)] = hb;
+            // keys: step and NEGATED zero point, x = step*(code + nz); a constant
+            // group is (lo, +1) since its codes are 0 (quant.cpp:37-42, 65-68)
+            ka[ka_index(c, gi)] = __double2half(p.delta == 0.0 ? p.lo : p.delta);
+            kb[kb_index(c, gi)] = __double2half(p.delta == 0.0 ? 1.0 : -(double)p.zp);
             if (shadow) {
                 shadow[(c * NGRP + gi) * 2] = p.lo;
                 shadow[(c * NGRP + gi) * 2 + 1] = p.hi;
@@ -289,8 +289,12 @@ __global__ void __launch_bounds__(QT) quantize_kernel(const QuantizeArgs a) {
         reinterpret_cast<uint4 *>(out + Blk::KA_OFF)[i] = reinterpret_cast<const uint4 *>(prm)[i];
 }
 
-// bits == 0 / method fp: the block is the raw bf16 K then V, [token][channel]
-__global__ void __launch_bounds__(QT) raw_block_kernel(const QuantizeArgs a) {
+// bits == 0 / method fp: the record is raw bf16, four 32-token quarters of
+// [K 8 KB][V 8 KB] in A-fragment order (layout.h, bf16_k_coords / bf16_v_coords)
+__global__ void __launch_bounds__(QT) raw_block_kernel_dyn(const QuantizeArgs a) {
+    extern __shared__ __align__(16) uint8_t smem[];
+    uint16_t *sk = reinterpret_cast<uint16_t *>(smem);
+    uint16_t *sv = sk + R * D;
     const int bh = blockIdx.y, b = bh / a.H, h = bh % a.H;
     const int64_t blk = blockIdx.x;
     const int64_t out_blk = (int64_t)bh * a.max_blocks + a.blk0 + blk;
@@ -298,13 +302,25 @@ __global__ void __launch_bounds__(QT) raw_block_kernel(const QuantizeArgs a) {
     const uint16_t *kin = reinterpret_cast<const uint16_t *>(a.k) + b * a.sb + h * a.sh;
     const uint16_t *vin = reinterpret_cast<const uint16_t *>(a.v) + b * a.sb + h * a.sh;
     const int64_t tok_base = a.tok0 + blk * R;
-    // 128 tokens x 256 B per tensor; 16 B per thread-iteration
     for (int i = threadIdx.x; i < R * 16; i += QT) {
         const int t = i >> 4, part = i & 15;
-        const uint4 kv = *reinterpret_cast<const uint4 *>(kin + (tok_base + t) * a.st + part * 8);
-        const uint4 vv = *reinterpret_cast<const uint4 *>(vin + (tok_base + t) * a.st + part * 8);
-        reinterpret_cast<uint4 *>(out)[i] = kv;
-        reinterpret_cast<uint4 *>(out + R * D * 2)[i] = vv;
+        reinterpret_cast<uint4 *>(sk)[i] = *reinterpret_cast<const uint4 *>(kin + (tok_base + t) * a.st + part * 8);
+        reinterpret_cast<uint4 *>(sv)[i] = *reinterpret_cast<const uint4 *>(vin + (tok_base + t) * a.st + part * 8);
+    }
+    __syncthreads();
+    constexpr int QW = BF16_QUARTER_BYTES / 2 / 4;  // 32-bit words per tensor per quarter (2048)
+    for (int i = threadIdx.x; i < 4 * QW; i += QT) {
+        const int qu = i / QW, w = i % QW;
+        int t0, c0, t1, c1;
+        bf16_k_coords(w, 0, t0, c0);
+        bf16_k_coords(w, 1, t1, c1);
+        const uint32_t kw = (uint32_t)sk[(qu * 32 + t0) * D + c0] | ((uint32_t)sk[(qu * 32 + t1) * D + c1] << 16);
+        bf16_v_coords(w, 0, t0, c0);
+        bf16_v_coords(w, 1, t1, c1);
+        const uint32_t vw = (uint32_t)sv[(qu * 32 + t0) * D + c0] | ((uint32_t)sv[(qu * 32 + t1) * D + c1] << 16);
+        uint32_t *qo = reinterpret_cast<uint32_t *>(out + qu * BF16_QUARTER_BYTES);
+        qo[w] = kw;
+        qo[QW + w] = vw;
     }
 }
 
@@ -326,7 +342,12 @@ cudaError_t launch_quantize(const QuantizeArgs &a, cudaStream_t st) {
     if (a.n_blocks <= 0) return cudaSuccess;
     dim3 grid((unsigned)a.n_blocks, (unsigned)(a.B * a.H));
     if (a.tc.bits == 0) {
-        raw_block_kernel<<<grid, QT, 0, st>>>(a);
+        static bool init0 = false;
+        if (!init0) {
+            cudaFuncSetAttribute(raw_block_kernel_dyn, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * R * D * 2);
+            init0 = true;
+        }
+        raw_block_kernel_dyn<<<grid, QT, 2 * R * D * 2, st>>>(a);
         return cudaGetLastError();
     }
     const int smem_common = 32 * 129 * 8 + 2 * R * D;

@@ -34,8 +34,6 @@ namespace osk {
 
 namespace {
 
-constexpr int NCW = 8;                 // warps per CTA (all consume; each refills its own stage)
-constexpr int NTHREADS = NCW * 32;
 constexpr int MERGE_FLOATS = 8 * D + 16;  // per-warp partial: O[8][128], m[8], l[8]
 constexpr float LOG2E = 1.4426950408889634f;
 constexpr float LN2 = 0.6931471805599453f;
@@ -46,7 +44,12 @@ struct AttnCfg {
     static constexpr int BYTES = (BITS == 0) ? BF16_BLOCK_BYTES : Block<BITS == 0 ? 2 : BITS>::BYTES;
     static constexpr int SUB = (BITS == 0) ? 4 : 1;
     static constexpr int STAGE = BYTES / SUB;
-    static constexpr int NST = (BITS == 2) ? 13 : (BITS == 4 ? 8 : 11);
+    // warps per CTA; every warp owns NST/NCW private stages (units p with
+    // p % NCW == warp use stage p % NST), so each mbarrier has ONE waiter that
+    // is also the thread refilling it -- no phase aliasing between warps.
+    static constexpr int NCW = (BITS == 2) ? 12 : 8;
+    static constexpr int NTHREADS = NCW * 32;
+    static constexpr int NST = NCW;
     static constexpr int RING = NST * STAGE;
     static constexpr int MERGE_OFF = RING;
     static constexpr int QS_OFF = MERGE_OFF + NCW * MERGE_FLOATS * 4;
@@ -55,6 +58,7 @@ struct AttnCfg {
     static constexpr int MISC_OFF = BAR_OFF + NST * 8;
     static constexpr int SMEM = MISC_OFF + 16;
     static_assert(SMEM <= 232448, "shared memory budget");
+    static_assert(NST % NCW == 0, "stages must be private to warps");
 };
 
 __device__ __forceinline__ float warp_sum(float v) {
@@ -382,8 +386,9 @@ __device__ __forceinline__ void process_quarter_bf16(const uint8_t *__restrict__
 }
 
 template <int BITS>
-__global__ void __launch_bounds__(NTHREADS, 1) decode_attn_kernel(const AttnArgs a) {
+__global__ void __launch_bounds__(AttnCfg<BITS>::NTHREADS, 1) decode_attn_kernel(const AttnArgs a) {
     using C = AttnCfg<BITS>;
+    constexpr int NCW = C::NCW;
     extern __shared__ __align__(1024) uint8_t smem[];
     float *merge = reinterpret_cast<float *>(smem + C::MERGE_OFF);
     float *qs = reinterpret_cast<float *>(smem + C::QS_OFF);  // rotated q [8][D]
@@ -731,7 +736,7 @@ cudaError_t launch_t(const AttnArgs &a, cudaStream_t st) {
         if (e != cudaSuccess) return e;
         init = true;
     }
-    decode_attn_kernel<BITS><<<a.ncta, NTHREADS, C::SMEM, st>>>(a);
+    decode_attn_kernel<BITS><<<a.ncta, C::NTHREADS, C::SMEM, st>>>(a);
     return cudaGetLastError();
 }
 

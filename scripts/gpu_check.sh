@@ -8,7 +8,7 @@ tail -30 gpurun_out/pytest_gpu.txt
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.txt 2>&1; tail -3 gpurun_out/smoke.txt
 timeout 900 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err; tail -3 gpurun_out/bench.err; cat gpurun_out/bench.json
 if [ "${NCU:-1}" = "1" ]; then
-timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 40 --csv --log-file gpurun_out/launches.csv \
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"decode_attn|quantize_kernel|raw_block|ring_copy|lse_merge" -c 40 --csv --log-file gpurun_out/launches.csv \
   python bench.py --steps 16 --warmup 2 --no-compare --no-cpu > gpurun_out/ncu_bench.log 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:decode_attn -s 3 -c 1 \
   -o gpurun_out/prof_attn_int2 -f python bench.py --steps 8 --warmup 2 --no-compare --no-cpu > gpurun_out/ncu_full.log 2>&1

@@ -1,0 +1,63 @@
+"""Parity at bench-like sizes (the stage ring wraps many times per CTA).
+
+B=4 sequences x 8 KV heads x 16K tokens (128 packed blocks per sequence-head,
+4096 pipeline units over ~148 persistent CTAs); sequences 0 and 3 are checked
+against the CPU oracle: bit-exact export (codes, steps, zero points, norms)
+and the decode-step output within the stated tolerance.
+"""
+import numpy as np
+import pytest
+
+from oracle import bindings as ob
+
+from gpu_util import export_to_oracle, rel_err
+
+pytestmark = pytest.mark.gpu
+
+ATOL_REL = {2: 3e-3, 4: 3e-3, 0: 1e-2}
+
+
+def _torch_inputs(B, S, H, seed):
+    import torch
+
+    g = torch.Generator(device="cuda")
+    g.manual_seed(seed)
+    k = torch.randn((B, S, H, 128), generator=g, device="cuda")
+    k[..., 0:4] = 18.0 * torch.sign(torch.randn((B, 1, H, 4), generator=g, device="cuda")) + 0.3 * k[..., 0:4]
+    k[..., 4:12] *= 8.0
+    v = torch.randn((B, S, H, 128), generator=g, device="cuda")
+    return k.to(torch.bfloat16), v.to(torch.bfloat16)
+
+
+def _np(t):
+    return t.float().cpu().numpy().astype(np.float64)
+
+
+@pytest.mark.parametrize("bits", [2, 4, 0])
+def test_large_cache_parity(bits):
+    import torch
+
+    from paper_2605_19660_b200 import KvCache, PipelineConfig
+
+    B, S, H, g = 4, 16384, 8, 4
+    k, v = _torch_inputs(B, S + 1, H, 17 + bits)
+    q = torch.randn((B, H * g, 128), device="cuda").to(torch.bfloat16)
+    cache = KvCache(PipelineConfig(heads=H, bits=bits), batch=B, q_heads=H * g, max_tokens=S + 8)
+    cache.buffer_quant(k[:, :S].contiguous(), v[:, :S].contiguous())
+    out = cache.decode_step(q, k[:, S].contiguous(), v[:, S].contiguous()).cpu().numpy()
+    for b in (0, B - 1):
+        o = ob.PortCache(H=H, bits=bits)
+        kb, vb = _np(k[b]), _np(v[b])
+        o.append(kb[:S], vb[:S])
+        ref = o.decode_step(_np(q[b]), kb[S], vb[S], g, append=False)
+        err = rel_err(out[b].astype(np.float64), ref)
+        assert err <= ATOL_REL[bits], (b, err)
+        if bits:
+            mine = export_to_oracle(cache.export(b), H)
+            mine.residual_tokens = 0
+            theirs = o.export()
+            # compare the packed part (the device cache already holds the current token)
+            mine.k_residual = theirs.k_residual
+            mine.k_norms_residual = theirs.k_norms_residual
+            mine.v_residual = theirs.v_residual
+            assert ob.caches_equal(mine, theirs) == []

@@ -58,6 +58,8 @@ def peaks():
 
 # ----------------------------------------------------------------------------- clocks
 class ClockSampler:
+    """nvidia-smi sampled every 20 ms; stats over the samples inside [t0, t1]."""
+
     FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
               "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
               "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
@@ -71,41 +73,48 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
-                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+                 "-lms", "20"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.thread = threading.Thread(target=self._read, daemon=True)
             self.thread.start()
+            t0 = time.time()
+            while not self.lines and time.time() - t0 < 5.0:
+                time.sleep(0.01)
         except Exception:
             self.proc = None
 
     def _read(self):
         for line in self.proc.stdout:
-            self.lines.append(line.strip())
+            self.lines.append((time.time(), line.strip()))
 
-    def stop(self):
+    def stop(self, t0=None, t1=None):
         if self.proc is None:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        time.sleep(0.15)
+        time.sleep(0.05)
         self.proc.terminate()
         try:
             self.proc.wait(timeout=2)
         except Exception:
             self.proc.kill()
-        sm, smax, reasons = [], [], set()
+        sel = [ln for ts, ln in self.lines if t0 is None or (t0 - 0.03 <= ts <= t1 + 0.03)]
+        if len(sel) < 3:
+            sel = [ln for _, ln in self.lines][-8:]
+        sm, smax, power, reasons = [], [], [], set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
+        for ln in sel:
             parts = [x.strip() for x in ln.split(",")]
             if len(parts) < 9:
                 continue
             try:
                 sm.append(float(parts[1]))
                 smax.append(float(parts[2]))
+                power.append(float(parts[3]))
             except ValueError:
                 continue
             for n, v in zip(names, parts[5:9]):
                 if v.lower().startswith("active"):
                     reasons.add(n)
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(smax) if smax else None,
-                "reasons": sorted(reasons), "samples": len(sm)}
+                "power_w_max": max(power) if power else None, "reasons": sorted(reasons), "samples": len(sm)}
 
 
 # ----------------------------------------------------------------------------- data
@@ -174,15 +183,23 @@ def run_ours(args, rank, world, local_rank):
         del k, v
         return cache
 
-    def timed_decode(cache, bits, nsteps, nwarm, seed, per_step_events=True):
+    def timed_decode(cache, bits, nsteps, nwarm, seed, per_step_events=True, soak_s=0.0):
         q, kn, vn = step_inputs(nwarm + nsteps, B, Hq, Hkv, seed, dev)
         out = torch.empty((B, Hq, D), dtype=torch.float32, device=dev)
         for i in range(nwarm):
             cache.decode_step(q[i], kn[i], vn[i], out=out)
+        if soak_s > 0:  # untimed attend-only soak (cache unchanged) so clocks settle under load
+            lse = torch.empty((B, Hq), dtype=torch.float32, device=dev)
+            t_end = time.time() + soak_s
+            while time.time() < t_end:
+                for _ in range(20):
+                    cache.attend(q[0], out=out, lse=lse)
+                torch.cuda.synchronize()
         evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(nsteps)]
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         launches, flush_steps, resid = 0, [], []
         barrier()
+        windows.append(time.time())
         e0.record(stream)
         for i in range(nsteps):
             r_before = cache.residual_tokens if per_step_events else 0
@@ -198,18 +215,21 @@ def run_ours(args, rank, world, local_rank):
             resid.append(r_before)
         e1.record(stream)
         barrier()
+        windows.append(time.time())
         total_ms = e0.elapsed_time(e1)
         per = [evs[i][0].elapsed_time(evs[i][1]) for i in range(nsteps)] if per_step_events else []
         return total_ms, per, launches, flush_steps, resid, out
 
     peak, peak_src = peaks()
     clocks = ClockSampler(local_rank)
+    windows = []
 
     # ---- headline: INT2 -------------------------------------------------------------
     cache = build(args.bits, 1234 + rank)
     packed0 = cache.packed_tokens
     clocks.start()
-    total_ms, per, launches, flush_steps, resid, _ = timed_decode(cache, args.bits, K, W, 99 + rank)
+    total_ms, per, launches, flush_steps, resid, _ = timed_decode(cache, args.bits, K, W, 99 + rank, soak_s=0.4)
+    t_dev0, t_dev1 = windows[-2], windows[-1]
     t = torch.tensor([total_ms], device=dev)
     if dist:
         td.all_reduce(t, op=td.ReduceOp.MAX)
@@ -237,7 +257,8 @@ def run_ours(args, rank, world, local_rank):
     if dist:
         td.all_reduce(te, op=td.ReduceOp.MAX)
     e2e_s = float(te.item())
-    clk = clocks.stop()
+    clk = clocks.stop(t_dev0 - 0.4, t_dev1)
+    clk["window"] = "0.4 s attend-only soak + the timed device region (20 ms sampling)"
     h2d = q_host[0].nbytes + k_host[0].nbytes + v_host[0].nbytes
     d2h = out_host.nbytes
 

@@ -44,21 +44,19 @@ struct AttnCfg {
     static constexpr int BYTES = (BITS == 0) ? BF16_BLOCK_BYTES : Block<BITS == 0 ? 2 : BITS>::BYTES;
     static constexpr int SUB = (BITS == 0) ? 4 : 1;
     static constexpr int STAGE = BYTES / SUB;
-    // warps per CTA; every warp owns NST/NCW private stages (units p with
-    // p % NCW == warp use stage p % NST), so each mbarrier has ONE waiter that
-    // is also the thread refilling it -- no phase aliasing between warps.
-    static constexpr int NCW = (BITS == 2) ? 12 : 8;
+    static constexpr int NCW = (BITS == 4) ? 8 : 12;  // warps per CTA, all consumers
     static constexpr int NTHREADS = NCW * 32;
-    static constexpr int NST = NCW;
-    static constexpr int RING = NST * STAGE;
-    static constexpr int MERGE_OFF = RING;
-    static constexpr int QS_OFF = MERGE_OFF + NCW * MERGE_FLOATS * 4;
-    static constexpr int QR_OFF = QS_OFF + 8 * D * 4;
-    static constexpr int BAR_OFF = QR_OFF + 8 * D * 4;
-    static constexpr int MISC_OFF = BAR_OFF + NST * 8;
-    static constexpr int SMEM = MISC_OFF + 16;
+    static constexpr int QS_OFF = 0;                  // rotated q [8][D] fp32
+    static constexpr int QR_OFF = QS_OFF + 8 * D * 4;  // raw q [8][D] fp32
+    static constexpr int MISC_OFF = QR_OFF + 8 * D * 4;
+    static constexpr int BAR_OFF = MISC_OFF + 16;
+    // shared ring of NST stages: as many whole stages as fit in 227 KB
+    static constexpr int NST = (232448 - BAR_OFF - 1024) / STAGE;
+    static constexpr int CNT_OFF = BAR_OFF + NST * 8;       // consumed-round counter per stage
+    static constexpr int RING_OFF = ((CNT_OFF + NST * 4 + 127) / 128) * 128;
+    static constexpr int SMEM = RING_OFF + NST * STAGE;
     static_assert(SMEM <= 232448, "shared memory budget");
-    static_assert(NST % NCW == 0, "stages must be private to warps");
+    static_assert(NST >= NCW, "ring shallower than the warp count");
 };
 
 __device__ __forceinline__ float warp_sum(float v) {
@@ -390,11 +388,14 @@ __global__ void __launch_bounds__(AttnCfg<BITS>::NTHREADS, 1) decode_attn_kernel
     using C = AttnCfg<BITS>;
     constexpr int NCW = C::NCW;
     extern __shared__ __align__(1024) uint8_t smem[];
-    float *merge = reinterpret_cast<float *>(smem + C::MERGE_OFF);
     float *qs = reinterpret_cast<float *>(smem + C::QS_OFF);  // rotated q [8][D]
     float *qr = reinterpret_cast<float *>(smem + C::QR_OFF);  // raw q [8][D]
     uint64_t *full = reinterpret_cast<uint64_t *>(smem + C::BAR_OFF);
+    volatile int *consumed = reinterpret_cast<volatile int *>(smem + C::CNT_OFF);
+    uint8_t *ring = smem + C::RING_OFF;
     int *misc = reinterpret_cast<int *>(smem + C::MISC_OFF);
+    // per-warp partials live in (L2-resident) global scratch, not shared memory
+    float *merge = a.warp_part + (int64_t)blockIdx.x * NCW * MERGE_FLOATS;
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int cta = blockIdx.x;
@@ -410,19 +411,27 @@ __global__ void __launch_bounds__(AttnCfg<BITS>::NTHREADS, 1) decode_attn_kernel
     }
     const int64_t nunits = end - start;
     const uint64_t pol = l2_evict_first_policy();
-    // unit p of this CTA's range -> stage p % NST (TMA bulk copy, complete_tx on full[stage])
+    // Shared ring, any number of warps: unit p of this CTA's range lives in
+    // stage p % NST, round p / NST.  Its consumer (warp p % NCW) first waits
+    // until the stage's previous round is consumed (software counter), which
+    // also means the TMA for unit p was issued -- so the full-barrier wait
+    // below is on the right phase.  After consuming, the warp refills the
+    // stage with unit p + NST and bumps the counter.
     auto issue = [&](int64_t p) {
         const int64_t gidx = start + p;
         const int64_t bh = gidx / nb, unit = gidx % nb;
         const int64_t blk = unit / SUB, sub = unit % SUB;
         const int stg = (int)(p % C::NST);
         mbar_arrive_expect_tx(&full[stg], C::STAGE);
-        bulk_g2s(smem + stg * C::STAGE, a.blocks + (bh * a.max_blocks + blk) * (int64_t)C::BYTES + sub * C::STAGE,
+        bulk_g2s(ring + stg * C::STAGE, a.blocks + (bh * a.max_blocks + blk) * (int64_t)C::BYTES + sub * C::STAGE,
                  C::STAGE, &full[stg], pol);
     };
 
     if (threadIdx.x == 0) {
-        for (int i = 0; i < C::NST; ++i) mbar_init(&full[i], 1);
+        for (int i = 0; i < C::NST; ++i) {
+            mbar_init(&full[i], 1);
+            consumed[i] = 0;
+        }
         fence_mbar_init();
         for (int64_t p = 0; p < nunits && p < C::NST; ++p) issue(p);
     }
@@ -493,18 +502,27 @@ __global__ void __launch_bounds__(AttnCfg<BITS>::NTHREADS, 1) decode_attn_kernel
             int64_t first = p0 + ((warp - (int)(p0 % NCW)) + NCW) % NCW;
             for (int64_t p = first; p < hi - start; p += NCW) {
                 const int stg = (int)(p % C::NST);
-                mbar_wait(&full[stg], (uint32_t)((p / C::NST) & 1));
-                const uint8_t *sb = smem + stg * C::STAGE;
+                const int round = (int)(p / C::NST);
+                if (lane == 0)
+                    while (consumed[stg] < round) {
+                    }
+                __syncwarp();
+                mbar_wait(&full[stg], (uint32_t)(round & 1));
+                const uint8_t *sb = ring + stg * C::STAGE;
                 if constexpr (BITS == 0) {
                     process_quarter_bf16(sb, st, qf, lane, c0);
                 } else {
                     process_block<BITS>(sb, st, qf, lane, c0);
                 }
-                // this warp owns the stage now: refill it with unit p + NST
+                // stage consumed: refill it with unit p + NST, then publish the round
                 __syncwarp();
-                if (lane == 0 && p + C::NST < nunits) {
-                    fence_proxy_async_smem();
-                    issue(p + C::NST);
+                if (lane == 0) {
+                    if (p + C::NST < nunits) {
+                        fence_proxy_async_smem();
+                        issue(p + C::NST);
+                    }
+                    __threadfence_block();
+                    consumed[stg] = round + 1;
                 }
             }
         }
@@ -655,7 +673,7 @@ __global__ void __launch_bounds__(AttnCfg<BITS>::NTHREADS, 1) decode_attn_kernel
         if (last) {
             __threadfence();
             // final merge across the CTA partials of this (b, kv head)
-            float *ob = merge;  // reuse: normalized O [8][D]
+            float *ob = qs;  // reuse: normalized O [8][D] (q is reloaded next segment)
             for (int idx = threadIdx.x; idx < g * D; idx += NCW * 32) {
                 const int h = idx / D;
                 const float *pmb = a.part_ml + (int64_t)bh * a.maxp * 16;
@@ -747,6 +765,10 @@ int attention_grid(int bits, int num_sms, int64_t nb, int BH) {
     const int64_t total = nb * BH;
     if (total == 0) return BH;
     return (int)(total < num_sms ? total : num_sms);
+}
+
+int64_t attention_scratch_floats(int max_ctas) {
+    return (int64_t)max_ctas * AttnCfg<2>::NCW * MERGE_FLOATS;
 }
 
 int attention_max_partials(int64_t nb, int BH, int ncta) {

@@ -108,6 +108,7 @@ struct oscar_kv_handle {
     void *ring_k = nullptr, *ring_v = nullptr;
     float *part_o = nullptr, *part_ml = nullptr;
     int *counters = nullptr;
+    float *warp_part = nullptr;
     int maxp_alloc = 0;
     void *stage = nullptr;  // host-API staging: q, k, v, out, lse
     int64_t device_bytes = 0;
@@ -140,6 +141,7 @@ struct oscar_kv_handle {
         cudaFree(part_o);
         cudaFree(part_ml);
         cudaFree(counters);
+        cudaFree(warp_part);
         cudaFree(stage);
     }
 
@@ -245,6 +247,7 @@ struct oscar_kv_handle {
         a.part_o = part_o;
         a.part_ml = part_ml;
         a.counters = counters;
+        a.warp_part = warp_part;
         a.ncta = attention_grid(dbits, num_sms, a.nb, a.BH);
         a.maxp = maxp_alloc;
         // exact partial-slot requirement
@@ -500,6 +503,8 @@ int oscar_kv_create(const oscar_kv_config *cfg, int64_t batch, int64_t q_heads, 
         h->part_ml = (float *)h->dalloc(sizeof(float) * (size_t)(h->BH * h->maxp_alloc * 16));
         h->counters = (int *)h->dalloc(sizeof(int) * (size_t)h->BH);
         CK(cudaMemset(h->counters, 0, sizeof(int) * (size_t)h->BH));
+        h->warp_part = (float *)h->dalloc(sizeof(float) *
+                                          (size_t)attention_scratch_floats((int)std::max<int64_t>(h->num_sms, h->BH)));
         const size_t stage_bytes = (size_t)(h->B * h->Hq * D * 2 + 2 * h->BH * D * 2 + h->B * h->Hq * D * 4 +
                                             h->B * h->Hq * 4 + 256);
         h->stage = h->dalloc(stage_bytes);

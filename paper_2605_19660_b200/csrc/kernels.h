@@ -59,12 +59,14 @@ struct AttnArgs {
     float *part_o;     // [BH][maxp][8][D]
     float *part_ml;    // [BH][maxp][8][2]
     int *counters;     // [BH], zero between launches
+    float *warp_part;  // [ncta][12][8*D+16] per-warp partial scratch
     int maxp;
     int ncta;
 };
 // bits: 2, 4 or 0 (bf16 baseline)
 cudaError_t launch_attention(int bits, const AttnArgs &a, cudaStream_t st);
 int attention_max_partials(int64_t nb, int BH, int ncta);
+int64_t attention_scratch_floats(int max_ctas);
 int attention_grid(int bits, int num_sms, int64_t nb, int BH);
 
 cudaError_t launch_lse_merge(const float *outs, const float *lses, int64_t parts, int64_t rows, int64_t d,

@@ -1,7 +1,7 @@
 #!/bin/bash
 # One GPU round: parity tests, smoke, bench, ncu launch list + one full capture.
 set -x
-mkdir -p gpurun_out
+mkdir -p gpurun_out; rm -f gpurun_out/parity_errors.jsonl
 export PYTHONUNBUFFERED=1
 timeout 900 python -m pytest tests -m gpu -q --timeout 600 > gpurun_out/pytest_gpu.txt 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.txt
 tail -30 gpurun_out/pytest_gpu.txt

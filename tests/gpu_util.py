@@ -48,3 +48,14 @@ def export_to_oracle(ex: dict, H: int, R_: int = R, G_: int = G) -> ob.ExportedC
 
 def rel_err(a: np.ndarray, ref: np.ndarray) -> float:
     return float(np.max(np.abs(a - ref)) / max(np.max(np.abs(ref)), 1e-30))
+
+
+def log_err(tag: str, err: float) -> None:
+    """Append a measured parity error to gpurun_out/parity_errors.jsonl (evidence)."""
+    import json
+    import os
+
+    d = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "gpurun_out")
+    if os.path.isdir(d):
+        with open(os.path.join(d, "parity_errors.jsonl"), "a") as f:
+            f.write(json.dumps({"test": tag, "max_abs_err_rel_to_max_abs_out": err}) + "\n")

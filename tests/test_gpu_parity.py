@@ -18,12 +18,12 @@ import pytest
 from oracle import bindings as ob
 from paper_2605_19660_b200.synthetic import make_inputs, make_queries
 
-from gpu_util import dev_bf16, export_to_oracle, rel_err
+from gpu_util import dev_bf16, export_to_oracle, log_err, rel_err
 
 pytestmark = pytest.mark.gpu
 
 # attention tolerance: max |o_dev - o_oracle| <= ATOL_REL * max |o_oracle|
-ATOL_REL_QUANT = 3e-3   # packed INT2/INT4 path (fp16 folded steps, fp16 P)
+ATOL_REL_QUANT = 5e-3   # packed INT2/INT4 path (fp16 folded steps, fp16 P): <= 2.5 bf16 half-ulps
 ATOL_REL_BF16 = 1e-2    # bf16 exact-cache baseline (bf16 P)
 
 CONFIGS = [
@@ -98,6 +98,7 @@ def test_decode_step_matches_oracle(cfg_t):
         if rotv:
             ref = np.stack([ob.port_fht(r) for r in ref])
         err = rel_err(out[b].astype(np.float64), ref)
+        log_err(f"decode_step[{_ids(cfg_t)}][b={b}]", err)
         assert err <= tol, (b, err)
     # the current token landed in the residual window, after the attention
     assert cache.total_tokens == 301 and cache.residual_tokens == 301 - 256
@@ -138,6 +139,7 @@ def test_decode_loop_crosses_flushes():
         out = cache.decode_step(dev_bf16(q[i][None]), dev_bf16(k[t][None]), dev_bf16(v[t][None])).cpu().numpy()
         ref = o.decode_step(q[i], k[t], v[t], g)
         worst = max(worst, rel_err(out[0].astype(np.float64), ref))
+    log_err("decode_loop_140_steps(worst)", worst)
     assert worst <= ATOL_REL_QUANT, worst
     assert (cache.packed_tokens, cache.residual_tokens, cache.flush_count) == (256, 4, 2)
     assert ob.caches_equal(export_to_oracle(cache.export(0), H), o.export()) == []

@@ -10,11 +10,11 @@ import pytest
 
 from oracle import bindings as ob
 
-from gpu_util import export_to_oracle, rel_err
+from gpu_util import export_to_oracle, log_err, rel_err
 
 pytestmark = pytest.mark.gpu
 
-ATOL_REL = {2: 3e-3, 4: 3e-3, 0: 1e-2}
+ATOL_REL = {2: 5e-3, 4: 5e-3, 0: 1e-2}
 
 
 def _torch_inputs(B, S, H, seed):
@@ -51,6 +51,7 @@ def test_large_cache_parity(bits):
         o.append(kb[:S], vb[:S])
         ref = o.decode_step(_np(q[b]), kb[S], vb[S], g, append=False)
         err = rel_err(out[b].astype(np.float64), ref)
+        log_err(f"large_cache[bits={bits}][B=4,S=16384,H=8][b={b}]", err)
         assert err <= ATOL_REL[bits], (b, err)
         if bits:
             mine = export_to_oracle(cache.export(b), H)

@@ -136,13 +136,9 @@ __device__ __forceinline__ void process_block(const uint8_t *__restrict__ sb, Wa
     const uint2 *bkp = reinterpret_cast<const uint2 *>(sb + Blk::KB_OFF + ((gq & 3) * 4 + tq) * 64);
     const uint32_t bkmask = gq < 4 ? 0xffffffffu : 0u;
     float kbias[4][4];
-#pragma unroll
-    for (int grp = 0; grp < 4; ++grp) kbias[grp][0] = kbias[grp][1] = kbias[grp][2] = kbias[grp][3] = 0.f;
 
     // ---- QK^T --------------------------------------------------------------------
     float sacc[8][4];
-#pragma unroll
-    for (int i = 0; i < 8; ++i) sacc[i][0] = sacc[i][1] = sacc[i][2] = sacc[i][3] = 0.f;
 #pragma unroll
     for (int s = 0; s < 8; ++s) {
         uint32_t kw[4 * WPF], kwh[4 * WPF];
@@ -176,7 +172,10 @@ __device__ __forceinline__ void process_block(const uint8_t *__restrict__ sb, Wa
             const uint2 z = bkp[s];
             const uint32_t z0 = z.x & bkmask, z1 = z.y & bkmask;
 #pragma unroll
-            for (int grp = 0; grp < 4; ++grp) mma16816(kbias[grp], z0, 0u, z1, 0u, bq[grp][0], bq[grp][1]);
+            for (int grp = 0; grp < 4; ++grp) {
+                if (s == 0) mma16816_zc(kbias[grp], z0, 0u, z1, 0u, bq[grp][0], bq[grp][1]);
+                else mma16816(kbias[grp], z0, 0u, z1, 0u, bq[grp][0], bq[grp][1]);
+            }
         }
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
@@ -185,8 +184,12 @@ __device__ __forceinline__ void process_block(const uint8_t *__restrict__ sb, Wa
             const uint32_t mask = FMASK << (BITS * fs);
             const uint32_t *src = (f < HALFT) ? kw : kwh;
             // word of family fam, half `half`: index fam*WPF + half
-            mma16816(sacc[i], src[0 * WPF + half] & mask, src[1 * WPF + half] & mask,
-                     src[2 * WPF + half] & mask, src[3 * WPF + half] & mask, bq[i >> 1][0], bq[i >> 1][1]);
+            if (s == 0)
+                mma16816_zc(sacc[i], src[0 * WPF + half] & mask, src[1 * WPF + half] & mask,
+                            src[2 * WPF + half] & mask, src[3 * WPF + half] & mask, bq[i >> 1][0], bq[i >> 1][1]);
+            else
+                mma16816(sacc[i], src[0 * WPF + half] & mask, src[1 * WPF + half] & mask,
+                         src[2 * WPF + half] & mask, src[3 * WPF + half] & mask, bq[i >> 1][0], bq[i >> 1][1]);
         }
     }
 
@@ -197,10 +200,10 @@ __device__ __forceinline__ void process_block(const uint8_t *__restrict__ sb, Wa
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
             const uint4 u = p[i];
-            nrm[4 * i] = __uint_as_float(u.x) * c0;
-            nrm[4 * i + 1] = __uint_as_float(u.y) * c0;
-            nrm[4 * i + 2] = __uint_as_float(u.z) * c0;
-            nrm[4 * i + 3] = __uint_as_float(u.w) * c0;
+            nrm[4 * i] = __uint_as_float(u.x);
+            nrm[4 * i + 1] = __uint_as_float(u.y);
+            nrm[4 * i + 2] = __uint_as_float(u.z);
+            nrm[4 * i + 3] = __uint_as_float(u.w);
         }
     }
     float kb0[4], kb1[4];
@@ -222,15 +225,31 @@ __device__ __forceinline__ void process_block(const uint8_t *__restrict__ sb, Wa
         bm0 = fmaxf(bm0, fmaxf(sacc[i][0], sacc[i][2]));
         bm1 = fmaxf(bm1, fmaxf(sacc[i][1], sacc[i][3]));
     }
+    // lazy rescale: the running max only moves when some lane's block max
+    // exceeds it (rare after the first blocks) -- then reduce and rescale
+    if (!__all_sync(0xffffffffu, bm0 <= st.m[0] && bm1 <= st.m[1])) {
 #pragma unroll
-    for (int o = 4; o < 32; o <<= 1) {
-        bm0 = fmaxf(bm0, __shfl_xor_sync(0xffffffffu, bm0, o));
-        bm1 = fmaxf(bm1, __shfl_xor_sync(0xffffffffu, bm1, o));
+        for (int o = 4; o < 32; o <<= 1) {
+            bm0 = fmaxf(bm0, __shfl_xor_sync(0xffffffffu, bm0, o));
+            bm1 = fmaxf(bm1, __shfl_xor_sync(0xffffffffu, bm1, o));
+        }
+        const float mn0 = fmaxf(st.m[0], bm0), mn1 = fmaxf(st.m[1], bm1);
+        const float al0 = fast_exp2(st.m[0] - mn0), al1 = fast_exp2(st.m[1] - mn1);
+        st.m[0] = mn0;
+        st.m[1] = mn1;
+        st.l[0] *= al0;
+        st.l[1] *= al1;
+#pragma unroll
+        for (int mm = 0; mm < 8; ++mm) {
+            st.o[mm][0] *= al0;
+            st.o[mm][1] *= al1;
+            st.o[mm][2] *= al0;
+            st.o[mm][3] *= al1;
+        }
+        st.ob[0] *= al0;
+        st.ob[1] *= al1;
     }
-    const float mn0 = fmaxf(st.m[0], bm0), mn1 = fmaxf(st.m[1], bm1);
-    const float al0 = fast_exp2(st.m[0] - mn0), al1 = fast_exp2(st.m[1] - mn1);
-    st.m[0] = mn0;
-    st.m[1] = mn1;
+    const float mn0 = st.m[0], mn1 = st.m[1];
     float ls0 = 0.f, ls1 = 0.f;
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
@@ -241,17 +260,8 @@ __device__ __forceinline__ void process_block(const uint8_t *__restrict__ sb, Wa
         ls0 += sacc[i][0] + sacc[i][2];
         ls1 += sacc[i][1] + sacc[i][3];
     }
-    st.l[0] = st.l[0] * al0 + ls0;
-    st.l[1] = st.l[1] * al1 + ls1;
-#pragma unroll
-    for (int mm = 0; mm < 8; ++mm) {
-        st.o[mm][0] *= al0;
-        st.o[mm][1] *= al1;
-        st.o[mm][2] *= al0;
-        st.o[mm][3] *= al1;
-    }
-    st.ob[0] *= al0;
-    st.ob[1] *= al1;
+    st.l[0] += ls0;
+    st.l[1] += ls1;
 
     // ---- P.V ---------------------------------------------------------------------------
     // value offsets as A: row gq (< 4) = channel group, k = tokens
@@ -391,7 +401,7 @@ __global__ void __launch_bounds__(AttnCfg<BITS>::NTHREADS, 1) decode_attn_kernel
     float *qs = reinterpret_cast<float *>(smem + C::QS_OFF);  // rotated q [8][D]
     float *qr = reinterpret_cast<float *>(smem + C::QR_OFF);  // raw q [8][D]
     uint64_t *full = reinterpret_cast<uint64_t *>(smem + C::BAR_OFF);
-    volatile int *consumed = reinterpret_cast<volatile int *>(smem + C::CNT_OFF);
+    int *consumed = reinterpret_cast<int *>(smem + C::CNT_OFF);
     uint8_t *ring = smem + C::RING_OFF;
     int *misc = reinterpret_cast<int *>(smem + C::MISC_OFF);
     // per-warp partials live in (L2-resident) global scratch, not shared memory
@@ -426,14 +436,24 @@ __global__ void __launch_bounds__(AttnCfg<BITS>::NTHREADS, 1) decode_attn_kernel
         bulk_g2s(ring + stg * C::STAGE, a.blocks + (bh * a.max_blocks + blk) * (int64_t)C::BYTES + sub * C::STAGE,
                  C::STAGE, &full[stg], pol);
     };
+    // warm L2 for the unit that will be TMA'd NST units later (hides HBM latency
+    // behind the ring without pinning shared memory)
+    auto prefetch = [&](int64_t p) {
+        if (p >= nunits) return;
+        const int64_t gidx = start + p;
+        const int64_t bh = gidx / nb, unit = gidx % nb;
+        const int64_t blk = unit / SUB, sub = unit % SUB;
+        bulk_prefetch_l2(a.blocks + (bh * a.max_blocks + blk) * (int64_t)C::BYTES + sub * C::STAGE, C::STAGE);
+    };
 
     if (threadIdx.x == 0) {
         for (int i = 0; i < C::NST; ++i) {
             mbar_init(&full[i], 1);
-            consumed[i] = 0;
+            st_volatile_shared(&consumed[i], 0);
         }
         fence_mbar_init();
         for (int64_t p = 0; p < nunits && p < C::NST; ++p) issue(p);
+        for (int64_t p = C::NST; p < 2 * C::NST; ++p) prefetch(p);
     }
     __syncthreads();
 
@@ -504,7 +524,7 @@ __global__ void __launch_bounds__(AttnCfg<BITS>::NTHREADS, 1) decode_attn_kernel
                 const int stg = (int)(p % C::NST);
                 const int round = (int)(p / C::NST);
                 if (lane == 0)
-                    while (consumed[stg] < round) {
+                    while (ld_volatile_shared(&consumed[stg]) < round) {
                     }
                 __syncwarp();
                 mbar_wait(&full[stg], (uint32_t)(round & 1));
@@ -521,8 +541,9 @@ __global__ void __launch_bounds__(AttnCfg<BITS>::NTHREADS, 1) decode_attn_kernel
                         fence_proxy_async_smem();
                         issue(p + C::NST);
                     }
+                    prefetch(p + 2 * C::NST);
                     __threadfence_block();
-                    consumed[stg] = round + 1;
+                    st_volatile_shared(&consumed[stg], round + 1);
                 }
             }
         }

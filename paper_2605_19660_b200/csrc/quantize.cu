@@ -222,7 +222,8 @@ __global__ void __launch_bounds__(QT) quantize_kernel(const QuantizeArgs a) {
             for (int i = 0; i < 32; ++i) x[i] = dmul(x[i], inv);
         }
         if (q == 0) {
-            nrm[norm_index(t)] = __double2float_rn(s);
+            // attention-facing copy pre-multiplied by log2(e)/sqrt(d) (logits in log2 units)
+            nrm[norm_index(t)] = __double2float_rn(dmul(s, 0.12751743074202186));
             if (shadow) shadow[SHADOW_K_DOUBLES + SHADOW_V_DOUBLES + t] = s;
         }
 #pragma unroll

@@ -25,6 +25,7 @@
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
 #include <math_constants.h>
+#include <stdlib.h>
 
 #include "device_common.cuh"
 #include "kernels.h"
@@ -38,13 +39,13 @@ constexpr int MERGE_FLOATS = 8 * D + 16;  // per-warp partial: O[8][128], m[8], 
 constexpr float LOG2E = 1.4426950408889634f;
 constexpr float LN2 = 0.6931471805599453f;
 
-template <int BITS>
+template <int BITS, int NCW_ = ((BITS == 4) ? 8 : 12)>
 struct AttnCfg {
     // one pipeline stage: a whole INT2/INT4 record, or a 32-token quarter of a bf16 record
     static constexpr int BYTES = (BITS == 0) ? BF16_BLOCK_BYTES : Block<BITS == 0 ? 2 : BITS>::BYTES;
     static constexpr int SUB = (BITS == 0) ? 4 : 1;
     static constexpr int STAGE = BYTES / SUB;
-    static constexpr int NCW = (BITS == 4) ? 8 : 12;  // warps per CTA, all consumers
+    static constexpr int NCW = NCW_;  // warps per CTA, all consumers
     static constexpr int NTHREADS = NCW * 32;
     static constexpr int QS_OFF = 0;                  // rotated q [8][D] fp32
     static constexpr int QR_OFF = QS_OFF + 8 * D * 4;  // raw q [8][D] fp32
@@ -56,7 +57,7 @@ struct AttnCfg {
     static constexpr int RING_OFF = ((CNT_OFF + NST * 4 + 127) / 128) * 128;
     static constexpr int SMEM = RING_OFF + NST * STAGE;
     static_assert(SMEM <= 232448, "shared memory budget");
-    static_assert(NST >= NCW, "ring shallower than the warp count");
+    // NST < NCW is correct (consumed-round counters) but leaves warps idle
 };
 
 __device__ __forceinline__ float warp_sum(float v) {
@@ -393,9 +394,9 @@ __device__ __forceinline__ void process_quarter_bf16(const uint8_t *__restrict__
     }
 }
 
-template <int BITS>
-__global__ void __launch_bounds__(AttnCfg<BITS>::NTHREADS, 1) decode_attn_kernel(const AttnArgs a) {
-    using C = AttnCfg<BITS>;
+template <int BITS, int NCW_>
+__global__ void __launch_bounds__(NCW_ * 32, 1) decode_attn_kernel(const AttnArgs a) {
+    using C = AttnCfg<BITS, NCW_>;
     constexpr int NCW = C::NCW;
     extern __shared__ __align__(1024) uint8_t smem[];
     float *qs = reinterpret_cast<float *>(smem + C::QS_OFF);  // rotated q [8][D]
@@ -453,7 +454,8 @@ __global__ void __launch_bounds__(AttnCfg<BITS>::NTHREADS, 1) decode_attn_kernel
         }
         fence_mbar_init();
         for (int64_t p = 0; p < nunits && p < C::NST; ++p) issue(p);
-        for (int64_t p = C::NST; p < 2 * C::NST; ++p) prefetch(p);
+        if (a.pf_dist > 0)
+            for (int64_t p = C::NST; p < C::NST + a.pf_dist; ++p) prefetch(p);
     }
     __syncthreads();
 
@@ -541,7 +543,7 @@ __global__ void __launch_bounds__(AttnCfg<BITS>::NTHREADS, 1) decode_attn_kernel
                         fence_proxy_async_smem();
                         issue(p + C::NST);
                     }
-                    prefetch(p + 2 * C::NST);
+                    if (a.pf_dist > 0) prefetch(p + C::NST + a.pf_dist);
                     __threadfence_block();
                     st_volatile_shared(&consumed[stg], round + 1);
                 }
@@ -765,17 +767,17 @@ __global__ void lse_merge_kernel(const float *outs, const float *lses, int64_t p
     }
 }
 
-template <int BITS>
+template <int BITS, int NCW>
 cudaError_t launch_t(const AttnArgs &a, cudaStream_t st) {
-    using C = AttnCfg<BITS>;
+    using C = AttnCfg<BITS, NCW>;
     static bool init = false;
     if (!init) {
-        cudaError_t e = cudaFuncSetAttribute(decode_attn_kernel<BITS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             C::SMEM);
+        cudaError_t e = cudaFuncSetAttribute(decode_attn_kernel<BITS, NCW>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
         if (e != cudaSuccess) return e;
         init = true;
     }
-    decode_attn_kernel<BITS><<<a.ncta, C::NTHREADS, C::SMEM, st>>>(a);
+    decode_attn_kernel<BITS, NCW><<<a.ncta, C::NTHREADS, C::SMEM, st>>>(a);
     return cudaGetLastError();
 }
 
@@ -789,7 +791,7 @@ int attention_grid(int bits, int num_sms, int64_t nb, int BH) {
 }
 
 int64_t attention_scratch_floats(int max_ctas) {
-    return (int64_t)max_ctas * AttnCfg<2>::NCW * MERGE_FLOATS;
+    return (int64_t)max_ctas * 12 * MERGE_FLOATS;
 }
 
 int attention_max_partials(int64_t nb, int BH, int ncta) {
@@ -799,11 +801,23 @@ int attention_max_partials(int64_t nb, int BH, int ncta) {
     return (int)(nb / (per > 0 ? per : 1) + 2);
 }
 
+// warps per CTA: OSCAR_NCW=8|12 overrides the default (tuning knob)
+static int ncw_choice(int bits) {
+    static int env = -1;
+    if (env < 0) {
+        const char *e = getenv("OSCAR_NCW");
+        env = e ? atoi(e) : 0;
+    }
+    if (env == 8 || env == 12) return env;
+    return bits == 4 ? 8 : 12;
+}
+
 cudaError_t launch_attention(int bits, const AttnArgs &a, cudaStream_t st) {
+    const int ncw = ncw_choice(bits);
     switch (bits) {
-        case 2: return launch_t<2>(a, st);
-        case 4: return launch_t<4>(a, st);
-        case 0: return launch_t<0>(a, st);
+        case 2: return ncw == 8 ? launch_t<2, 8>(a, st) : launch_t<2, 12>(a, st);
+        case 4: return ncw == 8 ? launch_t<4, 8>(a, st) : launch_t<4, 12>(a, st);
+        case 0: return ncw == 8 ? launch_t<0, 8>(a, st) : launch_t<0, 12>(a, st);
         default: return cudaErrorInvalidValue;
     }
 }

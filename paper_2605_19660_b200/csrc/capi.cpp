@@ -13,6 +13,7 @@
 #include <cuda_runtime.h>
 
 #include <cmath>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <fstream>
@@ -248,6 +249,14 @@ struct oscar_kv_handle {
         a.part_ml = part_ml;
         a.counters = counters;
         a.warp_part = warp_part;
+        {
+            static int pf = -1;
+            if (pf < 0) {
+                const char *e = getenv("OSCAR_L2_PREFETCH");
+                pf = e ? atoi(e) : 0;
+            }
+            a.pf_dist = pf;
+        }
         a.ncta = attention_grid(dbits, num_sms, a.nb, a.BH);
         a.maxp = maxp_alloc;
         // exact partial-slot requirement

@@ -62,6 +62,7 @@ struct AttnArgs {
     float *warp_part;  // [ncta][12][8*D+16] per-warp partial scratch
     int maxp;
     int ncta;
+    int pf_dist;       // L2 prefetch distance beyond the ring (units), 0 = off
 };
 // bits: 2, 4 or 0 (bf16 baseline)
 cudaError_t launch_attention(int bits, const AttnArgs &a, cudaStream_t st);

@@ -120,9 +120,17 @@ struct WarpState {
     float m[2], l[2];
 };
 
+__device__ __forceinline__ long long clk() {
+    long long c;
+    asm volatile("mov.u64 %0, %%clock64;" : "=l"(c));
+    return c;
+}
+
 template <int BITS>
 __device__ __forceinline__ void process_block(const uint8_t *__restrict__ sb, WarpState &st,
-                                              const uint32_t (&qf)[8][2], int lane, float c0) {
+                                              const uint32_t (&qf)[8][2], int lane, float c0,
+                                              long long *tm = nullptr) {
+    long long t0 = tm ? clk() : 0;
     using Blk = Block<BITS>;
     constexpr int TPW = 16 / BITS;   // m-tiles per half-word
     constexpr int WPF = 8 / TPW;     // words per fragment family per k-step
@@ -194,6 +202,7 @@ __device__ __forceinline__ void process_block(const uint8_t *__restrict__ sb, Wa
         }
     }
 
+    long long t1 = tm ? clk() : 0;
     // ---- logits (log2 units) ------------------------------------------------------------
     float nrm[16];
     {
@@ -264,6 +273,7 @@ __device__ __forceinline__ void process_block(const uint8_t *__restrict__ sb, Wa
     st.l[0] += ls0;
     st.l[1] += ls1;
 
+    long long t2 = tm ? clk() : 0;
     // ---- P.V ---------------------------------------------------------------------------
     // value offsets as A: row gq (< 4) = channel group, k = tokens
     const uint2 *vbp = reinterpret_cast<const uint2 *>(sb + Blk::VB_OFF + ((gq & 3) * 4 + tq) * 64);
@@ -318,6 +328,14 @@ __device__ __forceinline__ void process_block(const uint8_t *__restrict__ sb, Wa
             const uint2 z = vbp[j];
             mma16816(st.ob, z.x & bkmask, 0u, z.y & bkmask, 0u, bp0, bp1);
         }
+    }
+    if (tm) {
+        const float keep = st.o[0][0] + st.o[7][3];  // order the timer after the MMAs issued
+        asm volatile("" ::"f"(keep));
+        const long long t3 = clk();
+        tm[1] += t1 - t0;
+        tm[2] += t2 - t1;
+        tm[3] += t3 - t2;
     }
 }
 
@@ -475,6 +493,8 @@ __global__ void __launch_bounds__(NCW_ * 32, 1) decode_attn_kernel(const AttnArg
         seg_bh_first = seg_bh_last = cta;
     }
 
+    long long tmr[5] = {0, 0, 0, 0, 0};
+    const long long tk0 = a.prof ? clk() : 0;
     for (int64_t bh = seg_bh_first; bh <= seg_bh_last; ++bh) {
         const int b = (int)(bh / a.Hkv), kvh = (int)(bh % a.Hkv);
         const int64_t lo = total > 0 ? (bh * nb > start ? bh * nb : start) : 0;
@@ -529,12 +549,14 @@ __global__ void __launch_bounds__(NCW_ * 32, 1) decode_attn_kernel(const AttnArg
                     while (ld_volatile_shared(&consumed[stg]) < round) {
                     }
                 __syncwarp();
+                const long long tw0 = a.prof ? clk() : 0;
                 mbar_wait(&full[stg], (uint32_t)(round & 1));
+                if (a.prof) tmr[0] += clk() - tw0;
                 const uint8_t *sb = ring + stg * C::STAGE;
                 if constexpr (BITS == 0) {
                     process_quarter_bf16(sb, st, qf, lane, c0);
                 } else {
-                    process_block<BITS>(sb, st, qf, lane, c0);
+                    process_block<BITS>(sb, st, qf, lane, c0, a.prof ? tmr : nullptr);
                 }
                 // stage consumed: refill it with unit p + NST, then publish the round
                 __syncwarp();
@@ -746,6 +768,12 @@ __global__ void __launch_bounds__(NCW_ * 32, 1) decode_attn_kernel(const AttnArg
             }
         }
         __syncthreads();
+    }
+    if (a.prof && lane == 0) {
+        // per-warp phase cycles: [wait, qk, softmax, pv, total]
+        tmr[4] = clk() - tk0;
+        unsigned long long *pp = a.prof + ((int64_t)blockIdx.x * NCW + warp) * 5;
+        for (int i = 0; i < 5; ++i) pp[i] = (unsigned long long)tmr[i];
     }
 }
 

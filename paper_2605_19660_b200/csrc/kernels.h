@@ -63,6 +63,7 @@ struct AttnArgs {
     int maxp;
     int ncta;
     int pf_dist;       // L2 prefetch distance beyond the ring (units), 0 = off
+    unsigned long long *prof;  // debug: per-warp phase cycles [ncta][NCW][5] or null
 };
 // bits: 2, 4 or 0 (bf16 baseline)
 cudaError_t launch_attention(int bits, const AttnArgs &a, cudaStream_t st);

@@ -1,0 +1,3 @@
+for cfg in "2 12" "2 8" "4 8" "0 12"; do set -- $cfg
+  OSCAR_PROF=1 OSCAR_NCW=$2 timeout 120 python scripts/sweep.py $1 2>&1 | grep -E "OSCAR_PROF|bits" | tail -2
+done

@@ -493,7 +493,7 @@ __global__ void __launch_bounds__(NCW_ * 32, 1) decode_attn_kernel(const AttnArg
         seg_bh_first = seg_bh_last = cta;
     }
 
-    long long tmr[5] = {0, 0, 0, 0, 0};
+    long long tmr[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     const long long tk0 = a.prof ? clk() : 0;
     for (int64_t bh = seg_bh_first; bh <= seg_bh_last; ++bh) {
         const int b = (int)(bh / a.Hkv), kvh = (int)(bh % a.Hkv);
@@ -501,6 +501,7 @@ __global__ void __launch_bounds__(NCW_ * 32, 1) decode_attn_kernel(const AttnArg
         const int64_t hi = total > 0 ? ((bh + 1) * nb < end ? (bh + 1) * nb : end) : 0;
         const bool owns_tail = total == 0 || hi == (bh + 1) * nb;
 
+        const long long tq0 = a.prof ? clk() : 0;
         // ---- q for this (b, kv head): raw and rotated, fp32 in smem ----
         for (int j = warp; j < 8; j += NCW) {
             float x[4] = {0.f, 0.f, 0.f, 0.f};
@@ -538,6 +539,7 @@ __global__ void __launch_bounds__(NCW_ * 32, 1) decode_attn_kernel(const AttnArg
         st.m[0] = st.m[1] = -CUDART_INF_F;
         st.l[0] = st.l[1] = 0.f;
 
+        if (a.prof) tmr[6] += clk() - tq0;
         // ---- packed blocks of this segment: positions p = gidx - start, p % NCW == warp ----
         if (total > 0) {
             int64_t p0 = lo - start;
@@ -545,9 +547,11 @@ __global__ void __launch_bounds__(NCW_ * 32, 1) decode_attn_kernel(const AttnArg
             for (int64_t p = first; p < hi - start; p += NCW) {
                 const int stg = (int)(p % C::NST);
                 const int round = (int)(p / C::NST);
+                const long long ts0 = a.prof ? clk() : 0;
                 if (lane == 0)
                     while (ld_volatile_shared(&consumed[stg]) < round) {
                     }
+                if (a.prof) tmr[5] += clk() - ts0;
                 __syncwarp();
                 const long long tw0 = a.prof ? clk() : 0;
                 mbar_wait(&full[stg], (uint32_t)(round & 1));
@@ -572,6 +576,7 @@ __global__ void __launch_bounds__(NCW_ * 32, 1) decode_attn_kernel(const AttnArg
             }
         }
 
+        const long long te0 = a.prof ? clk() : 0;
         // ---- warp partial -> merge slot (unnormalized O[h][c], m[h], l[h]) ----
         float *slot = merge + warp * MERGE_FLOATS;
         {
@@ -768,12 +773,13 @@ __global__ void __launch_bounds__(NCW_ * 32, 1) decode_attn_kernel(const AttnArg
             }
         }
         __syncthreads();
+        if (a.prof) tmr[7] += clk() - te0;
     }
     if (a.prof && lane == 0) {
         // per-warp phase cycles: [wait, qk, softmax, pv, total]
         tmr[4] = clk() - tk0;
-        unsigned long long *pp = a.prof + ((int64_t)blockIdx.x * NCW + warp) * 5;
-        for (int i = 0; i < 5; ++i) pp[i] = (unsigned long long)tmr[i];
+        unsigned long long *pp = a.prof + ((int64_t)blockIdx.x * NCW + warp) * 8;
+        for (int i = 0; i < 8; ++i) pp[i] = (unsigned long long)tmr[i];
     }
 }
 

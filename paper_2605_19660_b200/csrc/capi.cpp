@@ -296,26 +296,29 @@ struct oscar_kv_handle {
         unsigned long long *pbuf = nullptr;
         const int nw = a.ncta * 12;
         if (prof) {
-            CK(cudaMalloc(&pbuf, sizeof(unsigned long long) * 5 * nw));
-            CK(cudaMemsetAsync(pbuf, 0, sizeof(unsigned long long) * 5 * nw, s));
+            CK(cudaMalloc(&pbuf, sizeof(unsigned long long) * 8 * nw));
+            CK(cudaMemsetAsync(pbuf, 0, sizeof(unsigned long long) * 8 * nw, s));
             a.prof = pbuf;
         }
         CK(launch_attention(dbits, a, s));
         ++last_launches;
         if (prof) {
-            std::vector<unsigned long long> hbuf(5 * nw);
+            std::vector<unsigned long long> hbuf(8 * nw);
             CK(cudaMemcpyAsync(hbuf.data(), pbuf, hbuf.size() * 8, cudaMemcpyDeviceToHost, s));
             CK(cudaStreamSynchronize(s));
-            double acc[5] = {0, 0, 0, 0, 0};
+            double acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
             int cnt = 0;
             for (int w = 0; w < nw; ++w) {
-                if (hbuf[5 * w + 4] == 0) continue;
+                if (hbuf[8 * w + 4] == 0) continue;
                 ++cnt;
-                for (int i = 0; i < 5; ++i) acc[i] += (double)hbuf[5 * w + i];
+                for (int i = 0; i < 8; ++i) acc[i] += (double)hbuf[8 * w + i];
             }
             if (cnt)
-                std::fprintf(stderr, "OSCAR_PROF warps=%d avg cycles: wait %.0f qk %.0f softmax %.0f pv %.0f total %.0f\n",
-                             cnt, acc[0] / cnt, acc[1] / cnt, acc[2] / cnt, acc[3] / cnt, acc[4] / cnt);
+                std::fprintf(stderr,
+                             "OSCAR_PROF warps=%d avg cycles: wait %.0f qk %.0f softmax %.0f pv %.0f total %.0f "
+                             "spin %.0f qprologue %.0f segtail %.0f\n",
+                             cnt, acc[0] / cnt, acc[1] / cnt, acc[2] / cnt, acc[3] / cnt, acc[4] / cnt, acc[5] / cnt,
+                             acc[6] / cnt, acc[7] / cnt);
             cudaFree(pbuf);
         }
     }

@@ -39,6 +39,10 @@ constexpr int MERGE_FLOATS = 8 * D + 16;  // per-warp partial: O[8][128], m[8], 
 constexpr float LOG2E = 1.4426950408889634f;
 constexpr float LN2 = 0.6931471805599453f;
 
+constexpr int NSEGSLOT = 4;    // per-warp partial slots (segments in flight per CTA)
+constexpr int NCW_MAX = 12;
+constexpr int QH_STRIDE = 136;  // padded fp16 row of the per-warp q tile (conflict-free fragment loads)
+
 template <int BITS, int NCW_ = ((BITS == 4) ? 8 : 12)>
 struct AttnCfg {
     // one pipeline stage: a whole INT2/INT4 record, or a 32-token quarter of a bf16 record
@@ -47,17 +51,15 @@ struct AttnCfg {
     static constexpr int STAGE = BYTES / SUB;
     static constexpr int NCW = NCW_;  // warps per CTA, all consumers
     static constexpr int NTHREADS = NCW * 32;
-    static constexpr int QS_OFF = 0;                  // rotated q [8][D] fp32
-    static constexpr int QR_OFF = QS_OFF + 8 * D * 4;  // raw q [8][D] fp32
-    static constexpr int MISC_OFF = QR_OFF + 8 * D * 4;
-    static constexpr int BAR_OFF = MISC_OFF + 16;
+    static constexpr int QH_OFF = 0;                                  // per-warp q tiles
+    static constexpr int SEG_OFF = QH_OFF + NCW * 8 * QH_STRIDE * 2;  // segcnt[4], segdone[4]
+    static constexpr int BAR_OFF = ((SEG_OFF + 2 * NSEGSLOT * 4 + 7) / 8) * 8;
     // shared ring of NST stages: as many whole stages as fit in 227 KB
     static constexpr int NST = (232448 - BAR_OFF - 1024) / STAGE;
-    static constexpr int CNT_OFF = BAR_OFF + NST * 8;       // consumed-round counter per stage
+    static constexpr int CNT_OFF = BAR_OFF + NST * 8;  // consumed-round counter per stage
     static constexpr int RING_OFF = ((CNT_OFF + NST * 4 + 127) / 128) * 128;
     static constexpr int SMEM = RING_OFF + NST * STAGE;
     static_assert(SMEM <= 232448, "shared memory budget");
-    // NST < NCW is correct (consumed-round counters) but leaves warps idle
 };
 
 __device__ __forceinline__ float warp_sum(float v) {
@@ -416,53 +418,38 @@ template <int BITS, int NCW_>
 __global__ void __launch_bounds__(NCW_ * 32, 1) decode_attn_kernel(const AttnArgs a) {
     using C = AttnCfg<BITS, NCW_>;
     constexpr int NCW = C::NCW;
+    constexpr int SUB = C::SUB;
     extern __shared__ __align__(1024) uint8_t smem[];
-    float *qs = reinterpret_cast<float *>(smem + C::QS_OFF);  // rotated q [8][D]
-    float *qr = reinterpret_cast<float *>(smem + C::QR_OFF);  // raw q [8][D]
     uint64_t *full = reinterpret_cast<uint64_t *>(smem + C::BAR_OFF);
     int *consumed = reinterpret_cast<int *>(smem + C::CNT_OFF);
+    int *segcnt = reinterpret_cast<int *>(smem + C::SEG_OFF);   // arrivals per segment slot
+    int *segdone = segcnt + NSEGSLOT;                           // merges completed per slot
     uint8_t *ring = smem + C::RING_OFF;
-    int *misc = reinterpret_cast<int *>(smem + C::MISC_OFF);
-    // per-warp partials live in (L2-resident) global scratch, not shared memory
-    float *merge = a.warp_part + (int64_t)blockIdx.x * NCW * MERGE_FLOATS;
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int gq = lane >> 2, tq = lane & 3;
     const int cta = blockIdx.x;
-    constexpr int SUB = C::SUB;
+    const int g = a.g;
     const int64_t nb = a.nb * SUB;  // pipeline units per (b, kv head)
     const int64_t total = (int64_t)a.BH * nb;
-    int64_t start, end;
+    int64_t start = 0, end = 0;
     if (total > 0) {
         start = (cta * total) / a.ncta;
         end = ((cta + 1) * total) / a.ncta;
-    } else {
-        start = end = 0;
     }
     const int64_t nunits = end - start;
     const uint64_t pol = l2_evict_first_policy();
     // Shared ring, any number of warps: unit p of this CTA's range lives in
     // stage p % NST, round p / NST.  Its consumer (warp p % NCW) first waits
-    // until the stage's previous round is consumed (software counter), which
-    // also means the TMA for unit p was issued -- so the full-barrier wait
-    // below is on the right phase.  After consuming, the warp refills the
-    // stage with unit p + NST and bumps the counter.
-    auto issue = [&](int64_t p) {
-        const int64_t gidx = start + p;
-        const int64_t bh = gidx / nb, unit = gidx % nb;
-        const int64_t blk = unit / SUB, sub = unit % SUB;
+    // until the stage's previous round is consumed (software counter) -- which
+    // also means the TMA for unit p was issued, so the full-barrier wait is on
+    // the right phase -- and after consuming refills the stage with unit p+NST.
+    auto issue = [&](int64_t p, int64_t bh, int64_t uidx) {  // uidx: unit index within bh
         const int stg = (int)(p % C::NST);
         mbar_arrive_expect_tx(&full[stg], C::STAGE);
-        bulk_g2s(ring + stg * C::STAGE, a.blocks + (bh * a.max_blocks + blk) * (int64_t)C::BYTES + sub * C::STAGE,
-                 C::STAGE, &full[stg], pol);
-    };
-    // warm L2 for the unit that will be TMA'd NST units later (hides HBM latency
-    // behind the ring without pinning shared memory)
-    auto prefetch = [&](int64_t p) {
-        if (p >= nunits) return;
-        const int64_t gidx = start + p;
-        const int64_t bh = gidx / nb, unit = gidx % nb;
-        const int64_t blk = unit / SUB, sub = unit % SUB;
-        bulk_prefetch_l2(a.blocks + (bh * a.max_blocks + blk) * (int64_t)C::BYTES + sub * C::STAGE, C::STAGE);
+        bulk_g2s(ring + stg * C::STAGE,
+                 a.blocks + (bh * a.max_blocks + uidx / SUB) * (int64_t)C::BYTES + (uidx % SUB) * C::STAGE, C::STAGE,
+                 &full[stg], pol);
     };
 
     if (threadIdx.x == 0) {
@@ -470,67 +457,70 @@ __global__ void __launch_bounds__(NCW_ * 32, 1) decode_attn_kernel(const AttnArg
             mbar_init(&full[i], 1);
             st_volatile_shared(&consumed[i], 0);
         }
+        for (int i = 0; i < NSEGSLOT; ++i) {
+            segcnt[i] = 0;
+            st_volatile_shared(&segdone[i], 0);
+        }
         fence_mbar_init();
-        for (int64_t p = 0; p < nunits && p < C::NST; ++p) issue(p);
-        if (a.pf_dist > 0)
-            for (int64_t p = C::NST; p < C::NST + a.pf_dist; ++p) prefetch(p);
+        if (nunits > 0) {
+            int64_t bh = start / nb, uidx = start % nb;
+            for (int64_t p = 0; p < nunits && p < C::NST; ++p) {
+                issue(p, bh, uidx);
+                if (++uidx == nb) {
+                    uidx = 0;
+                    ++bh;
+                }
+            }
+        }
     }
-    __syncthreads();
-
-    // ================= consumers =================
-    const float c0 = LOG2E * 0.08838834764831845f;  // log2(e)/sqrt(128)
-    const int gq = lane >> 2, tq = lane & 3;
-    const int g = a.g;
+    __syncthreads();  // the only CTA-wide barrier
 
     // segments: residual-only mode (nb == 0): CTA c <-> bh c
-    int64_t seg_bh_first, seg_bh_last;
+    int64_t seg_first, seg_last;
     if (total > 0) {
-        if (end <= start) return;
-        seg_bh_first = start / nb;
-        seg_bh_last = (end - 1) / nb;
+        if (nunits <= 0) return;
+        seg_first = start / nb;
+        seg_last = (end - 1) / nb;
     } else {
         if (cta >= a.BH) return;
-        seg_bh_first = seg_bh_last = cta;
+        seg_first = seg_last = cta;
     }
+    const float c0 = LOG2E * 0.08838834764831845f;  // log2(e)/sqrt(128)
+    __half *qh = reinterpret_cast<__half *>(smem + C::QH_OFF) + warp * 8 * QH_STRIDE;  // private
 
-    long long tmr[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-    const long long tk0 = a.prof ? clk() : 0;
-    for (int64_t bh = seg_bh_first; bh <= seg_bh_last; ++bh) {
+    for (int64_t bh = seg_first; bh <= seg_last; ++bh) {
+        const int k = (int)(bh - seg_first);
         const int b = (int)(bh / a.Hkv), kvh = (int)(bh % a.Hkv);
         const int64_t lo = total > 0 ? (bh * nb > start ? bh * nb : start) : 0;
         const int64_t hi = total > 0 ? ((bh + 1) * nb < end ? (bh + 1) * nb : end) : 0;
         const bool owns_tail = total == 0 || hi == (bh + 1) * nb;
+        const __nv_bfloat16 *qbase = reinterpret_cast<const __nv_bfloat16 *>(a.q) + ((int64_t)b * a.Hq + kvh * g) * D;
 
-        const long long tq0 = a.prof ? clk() : 0;
-        // ---- q for this (b, kv head): raw and rotated, fp32 in smem ----
-        for (int j = warp; j < 8; j += NCW) {
+        // ---- q fragments (per warp, no CTA barrier): rotated fp16 (raw bf16 for
+        //      the bf16 baseline) through a private padded smem tile ----
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
             float x[4] = {0.f, 0.f, 0.f, 0.f};
-            if (j < g) {
-                load_bf16x4(reinterpret_cast<const __nv_bfloat16 *>(a.q) + ((int64_t)b * a.Hq + kvh * g + j) * D +
-                                lane * 4,
-                            x);
+            if (j < g) load_bf16x4(qbase + j * D + lane * 4, x);
+            uint32_t w0, w1;
+            if (BITS == 0) {
+                w0 = pack_bf162(x[0], x[1]);
+                w1 = pack_bf162(x[2], x[3]);
+            } else {
+                if (a.rotates) fht128_warp(x, lane);
+                w0 = pack_half2(x[0], x[1]);
+                w1 = pack_half2(x[2], x[3]);
             }
-#pragma unroll
-            for (int e = 0; e < 4; ++e) qr[j * D + lane * 4 + e] = x[e];
-            if (a.rotates) fht128_warp(x, lane);
-#pragma unroll
-            for (int e = 0; e < 4; ++e) qs[j * D + lane * 4 + e] = x[e];
+            *reinterpret_cast<uint2 *>(qh + j * QH_STRIDE + lane * 4) = make_uint2(w0, w1);
         }
-        __syncthreads();
+        __syncwarp();
         uint32_t qf[8][2];
 #pragma unroll
         for (int s = 0; s < 8; ++s) {
-            const float *qrow = qs + gq * D + 16 * s + 2 * tq;
-            if (BITS == 0) {
-                // bf16 baseline attends raw K: use the raw q
-                const float *rrow = qr + gq * D + 16 * s + 2 * tq;
-                qf[s][0] = pack_bf162(rrow[0], rrow[1]);
-                qf[s][1] = pack_bf162(rrow[8], rrow[9]);
-            } else {
-                qf[s][0] = pack_half2(qrow[0], qrow[1]);
-                qf[s][1] = pack_half2(qrow[8], qrow[9]);
-            }
+            qf[s][0] = *reinterpret_cast<const uint32_t *>(qh + gq * QH_STRIDE + 16 * s + 2 * tq);
+            qf[s][1] = *reinterpret_cast<const uint32_t *>(qh + gq * QH_STRIDE + 16 * s + 2 * tq + 8);
         }
+        __syncwarp();
 
         WarpState st;
 #pragma unroll
@@ -539,46 +529,49 @@ __global__ void __launch_bounds__(NCW_ * 32, 1) decode_attn_kernel(const AttnArg
         st.m[0] = st.m[1] = -CUDART_INF_F;
         st.l[0] = st.l[1] = 0.f;
 
-        if (a.prof) tmr[6] += clk() - tq0;
-        // ---- packed blocks of this segment: positions p = gidx - start, p % NCW == warp ----
+        // ---- packed units of this segment: positions p = gidx - start, p % NCW == warp ----
         if (total > 0) {
-            int64_t p0 = lo - start;
-            int64_t first = p0 + ((warp - (int)(p0 % NCW)) + NCW) % NCW;
+            const int64_t p0 = lo - start;
+            const int64_t first = p0 + ((warp - (int)(p0 % NCW)) + NCW) % NCW;
             for (int64_t p = first; p < hi - start; p += NCW) {
                 const int stg = (int)(p % C::NST);
                 const int round = (int)(p / C::NST);
-                const long long ts0 = a.prof ? clk() : 0;
                 if (lane == 0)
                     while (ld_volatile_shared(&consumed[stg]) < round) {
                     }
-                if (a.prof) tmr[5] += clk() - ts0;
                 __syncwarp();
-                const long long tw0 = a.prof ? clk() : 0;
                 mbar_wait(&full[stg], (uint32_t)(round & 1));
-                if (a.prof) tmr[0] += clk() - tw0;
                 const uint8_t *sb = ring + stg * C::STAGE;
                 if constexpr (BITS == 0) {
                     process_quarter_bf16(sb, st, qf, lane, c0);
                 } else {
-                    process_block<BITS>(sb, st, qf, lane, c0, a.prof ? tmr : nullptr);
+                    process_block<BITS>(sb, st, qf, lane, c0);
                 }
                 // stage consumed: refill it with unit p + NST, then publish the round
                 __syncwarp();
                 if (lane == 0) {
                     if (p + C::NST < nunits) {
+                        int64_t bh2 = bh, u2 = start + p - bh * nb + C::NST;
+                        while (u2 >= nb) {
+                            u2 -= nb;
+                            ++bh2;
+                        }
                         fence_proxy_async_smem();
-                        issue(p + C::NST);
+                        issue(p + C::NST, bh2, u2);
                     }
-                    if (a.pf_dist > 0) prefetch(p + C::NST + a.pf_dist);
                     __threadfence_block();
                     st_volatile_shared(&consumed[stg], round + 1);
                 }
             }
         }
 
-        const long long te0 = a.prof ? clk() : 0;
-        // ---- warp partial -> merge slot (unnormalized O[h][c], m[h], l[h]) ----
-        float *slot = merge + warp * MERGE_FLOATS;
+        // ---- warp partial -> global slot (unnormalized O[h][c], m[h], l[h]) ----
+        const int sslot = k % NSEGSLOT;
+        if (lane == 0)
+            while (ld_volatile_shared(&segdone[sslot]) < k / NSEGSLOT) {  // slot reuse guard
+            }
+        __syncwarp();
+        float *slot = a.warp_part + (((int64_t)cta * NSEGSLOT + sslot) * NCW_MAX + warp) * MERGE_FLOATS;
         {
             float l0 = st.l[0], l1 = st.l[1];
 #pragma unroll
@@ -621,9 +614,10 @@ __global__ void __launch_bounds__(NCW_ * 32, 1) decode_attn_kernel(const AttnArg
             if (warp < ntok) {
                 float qv[8][4];
 #pragma unroll
-                for (int j = 0; j < 8; ++j)
-#pragma unroll
-                    for (int e = 0; e < 4; ++e) qv[j][e] = qr[j * D + lane * 4 + e];
+                for (int j = 0; j < 8; ++j) {
+                    qv[j][0] = qv[j][1] = qv[j][2] = qv[j][3] = 0.f;
+                    if (j < g) load_bf16x4(qbase + j * D + lane * 4, qv[j]);
+                }
                 float mr[8], lr[8], orr[8][4];
 #pragma unroll
                 for (int j = 0; j < 8; ++j) {
@@ -658,7 +652,6 @@ __global__ void __launch_bounds__(NCW_ * 32, 1) decode_attn_kernel(const AttnArg
                         }
                     }
                 }
-                // merge with the packed-block partial in this warp's slot
 #pragma unroll
                 for (int j = 0; j < 8; ++j) {
                     if (j < g) {
@@ -666,11 +659,13 @@ __global__ void __launch_bounds__(NCW_ * 32, 1) decode_attn_kernel(const AttnArg
                         const float M = fmaxf(ms, mr[j]);
                         const float fs = (ms == -CUDART_INF_F) ? 0.f : fast_exp2(ms - M);
                         const float fr = (mr[j] == -CUDART_INF_F) ? 0.f : fast_exp2(mr[j] - M);
-#pragma unroll
-                        for (int e = 0; e < 4; ++e) {
-                            float *op = slot + j * D + lane * 4 + e;
-                            *op = *op * fs + orr[j][e] * fr;
-                        }
+                        float4 *op = reinterpret_cast<float4 *>(slot + j * D + lane * 4);
+                        float4 ov = *op;
+                        ov.x = ov.x * fs + orr[j][0] * fr;
+                        ov.y = ov.y * fs + orr[j][1] * fr;
+                        ov.z = ov.z * fs + orr[j][2] * fr;
+                        ov.w = ov.w * fs + orr[j][3] * fr;
+                        *op = ov;
                         __syncwarp();
                         if (lane == 0) {
                             slot[8 * D + j] = M;
@@ -681,9 +676,19 @@ __global__ void __launch_bounds__(NCW_ * 32, 1) decode_attn_kernel(const AttnArg
                 __syncwarp();
             }
         }
-        __syncthreads();
 
-        // ---- CTA merge of the NCW warp partials -> global partial slot ----
+        // ---- arrive; the LAST warp of the CTA to finish this segment merges ----
+        int arrived = 0;
+        if (lane == 0) {
+            __threadfence_block();
+            arrived = atomicAdd(&segcnt[sslot], 1);
+        }
+        arrived = __shfl_sync(0xffffffffu, arrived, 0);
+        if (arrived != NCW - 1) continue;  // not last: straight on to the next segment
+        __threadfence_block();
+        if (lane == 0) segcnt[sslot] = 0;
+
+        const float *wp = a.warp_part + ((int64_t)cta * NSEGSLOT + sslot) * NCW_MAX * MERGE_FLOATS;
         int64_t first_cta = 0, last_cta = 0;
         if (total > 0) {
             first_cta = cta_of(bh * nb, total, a.ncta);
@@ -693,93 +698,79 @@ __global__ void __launch_bounds__(NCW_ * 32, 1) decode_attn_kernel(const AttnArg
         const int pslot = (int)(total > 0 ? cta - first_cta : 0);
         float *po = a.part_o + ((int64_t)bh * a.maxp + pslot) * 8 * D;
         float *pml = a.part_ml + ((int64_t)bh * a.maxp + pslot) * 16;
-        for (int idx = threadIdx.x; idx < g * D; idx += NCW * 32) {
-            const int h = idx / D;
+        for (int h = 0; h < g; ++h) {
             float M = -CUDART_INF_F;
 #pragma unroll
-            for (int w = 0; w < NCW; ++w) M = fmaxf(M, merge[w * MERGE_FLOATS + 8 * D + h]);
-            float O = 0.f, L = 0.f;
+            for (int w = 0; w < NCW; ++w) M = fmaxf(M, wp[w * MERGE_FLOATS + 8 * D + h]);
+            float4 O = make_float4(0.f, 0.f, 0.f, 0.f);
+            float L = 0.f;
 #pragma unroll
             for (int w = 0; w < NCW; ++w) {
-                const float mw = merge[w * MERGE_FLOATS + 8 * D + h];
+                const float mw = wp[w * MERGE_FLOATS + 8 * D + h];
                 const float f = (mw == -CUDART_INF_F) ? 0.f : fast_exp2(mw - M);
-                O += merge[w * MERGE_FLOATS + idx] * f;
-                L += merge[w * MERGE_FLOATS + 8 * D + 8 + h] * f;
+                const float4 v = *reinterpret_cast<const float4 *>(wp + w * MERGE_FLOATS + h * D + lane * 4);
+                O.x += v.x * f;
+                O.y += v.y * f;
+                O.z += v.z * f;
+                O.w += v.w * f;
+                L += wp[w * MERGE_FLOATS + 8 * D + 8 + h] * f;
             }
-            po[idx] = O;
-            if ((idx % D) == 0) {
+            *reinterpret_cast<float4 *>(po + h * D + lane * 4) = O;
+            if (lane == 0) {
                 pml[2 * h] = M;
                 pml[2 * h + 1] = L;
             }
         }
-        __threadfence();
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            const int prev = atomicAdd(&a.counters[bh], 1);
-            misc[0] = (prev == expected - 1) ? 1 : 0;
-        }
-        __syncthreads();
-        const bool last = misc[0] != 0;
-        if (last) {
+        // the warp slots of this segment may be reused now
+        if (lane == 0) st_volatile_shared(&segdone[sslot], k / NSEGSLOT + 1);
+        int prev = 0;
+        if (lane == 0) {
             __threadfence();
-            // final merge across the CTA partials of this (b, kv head)
-            float *ob = qs;  // reuse: normalized O [8][D] (q is reloaded next segment)
-            for (int idx = threadIdx.x; idx < g * D; idx += NCW * 32) {
-                const int h = idx / D;
-                const float *pmb = a.part_ml + (int64_t)bh * a.maxp * 16;
-                const float *pob = a.part_o + (int64_t)bh * a.maxp * 8 * D;
+            prev = atomicAdd(&a.counters[bh], 1);
+        }
+        prev = __shfl_sync(0xffffffffu, prev, 0);
+        if (prev == expected - 1) {
+            // last CTA for this (b, kv head): merge the CTA partials -> output
+            __threadfence();
+            const float *pmb = a.part_ml + (int64_t)bh * a.maxp * 16;
+            const float *pob = a.part_o + (int64_t)bh * a.maxp * 8 * D;
+            for (int h = 0; h < g; ++h) {
                 float M = -CUDART_INF_F;
-                for (int s = 0; s < expected; ++s) M = fmaxf(M, __ldcg(pmb + s * 16 + 2 * h));
-                float O = 0.f, L = 0.f;
-                for (int s = 0; s < expected; ++s) {
-                    const float ms = __ldcg(pmb + s * 16 + 2 * h);
+                for (int s2 = 0; s2 < expected; ++s2) M = fmaxf(M, __ldcg(pmb + s2 * 16 + 2 * h));
+                float x[4] = {0.f, 0.f, 0.f, 0.f};
+                float L = 0.f;
+                for (int s2 = 0; s2 < expected; ++s2) {
+                    const float ms = __ldcg(pmb + s2 * 16 + 2 * h);
                     const float f = (ms == -CUDART_INF_F) ? 0.f : fast_exp2(ms - M);
-                    O += __ldcg(pob + s * 8 * D + idx) * f;
-                    L += __ldcg(pmb + s * 16 + 2 * h + 1) * f;
+                    const float4 v = __ldcg(reinterpret_cast<const float4 *>(pob + s2 * 8 * D + h * D + lane * 4));
+                    x[0] += v.x * f;
+                    x[1] += v.y * f;
+                    x[2] += v.z * f;
+                    x[3] += v.w * f;
+                    L += __ldcg(pmb + s2 * 16 + 2 * h + 1) * f;
                 }
-                const float v = (L > 0.f) ? O / L : 0.f;
-                if (a.rotate_v) {
-                    ob[idx] = v;
-                } else {
-                    a.out[((int64_t)b * a.Hq + kvh * g + h) * D + (idx % D)] = v;
-                }
-                if (a.lse && (idx % D) == 0)
+                const float inv = (L > 0.f) ? 1.f / L : 0.f;
+#pragma unroll
+                for (int e = 0; e < 4; ++e) x[e] *= inv;
+                if (a.rotate_v) fht128_warp(x, lane);  // explicit-V mode: rotate the output back
+                *reinterpret_cast<float4 *>(a.out + ((int64_t)b * a.Hq + kvh * g + h) * D + lane * 4) =
+                    make_float4(x[0], x[1], x[2], x[3]);
+                if (a.lse && lane == 0)
                     a.lse[(int64_t)b * a.Hq + kvh * g + h] = (L > 0.f) ? (M + __log2f(L)) * LN2 : -CUDART_INF_F;
             }
-            if (a.rotate_v) {
-                __syncthreads();
-                for (int j = warp; j < g; j += NCW) {
-                    float x[4];
-#pragma unroll
-                    for (int e = 0; e < 4; ++e) x[e] = ob[j * D + lane * 4 + e];
-                    fht128_warp(x, lane);
-#pragma unroll
-                    for (int e = 0; e < 4; ++e) a.out[((int64_t)b * a.Hq + kvh * g + j) * D + lane * 4 + e] = x[e];
-                }
-            }
-            if (threadIdx.x == 0) a.counters[bh] = 0;
+            if (lane == 0) a.counters[bh] = 0;
         }
-        // current token -> residual ring (after everyone read the ring)
+        // current token -> residual ring (nobody reads slot r in this launch)
         if (owns_tail && a.write_ring && a.kcur) {
-            if (warp == 0) {
-                const uint2 *ks = reinterpret_cast<const uint2 *>(reinterpret_cast<const __nv_bfloat16 *>(a.kcur) +
-                                                                   ((int64_t)b * a.Hkv + kvh) * D);
-                const uint2 *vs = reinterpret_cast<const uint2 *>(reinterpret_cast<const __nv_bfloat16 *>(a.vcur) +
-                                                                   ((int64_t)b * a.Hkv + kvh) * D);
-                reinterpret_cast<uint2 *>(reinterpret_cast<__nv_bfloat16 *>(a.ring_k) + (bh * R + a.r) * D)[lane] =
-                    ks[lane];
-                reinterpret_cast<uint2 *>(reinterpret_cast<__nv_bfloat16 *>(a.ring_v) + (bh * R + a.r) * D)[lane] =
-                    vs[lane];
-            }
+            const uint2 *ks = reinterpret_cast<const uint2 *>(reinterpret_cast<const __nv_bfloat16 *>(a.kcur) +
+                                                               ((int64_t)b * a.Hkv + kvh) * D);
+            const uint2 *vs = reinterpret_cast<const uint2 *>(reinterpret_cast<const __nv_bfloat16 *>(a.vcur) +
+                                                               ((int64_t)b * a.Hkv + kvh) * D);
+            reinterpret_cast<uint2 *>(reinterpret_cast<__nv_bfloat16 *>(a.ring_k) + (bh * R + a.r) * D)[lane] =
+                ks[lane];
+            reinterpret_cast<uint2 *>(reinterpret_cast<__nv_bfloat16 *>(a.ring_v) + (bh * R + a.r) * D)[lane] =
+                vs[lane];
         }
-        __syncthreads();
-        if (a.prof) tmr[7] += clk() - te0;
-    }
-    if (a.prof && lane == 0) {
-        // per-warp phase cycles: [wait, qk, softmax, pv, total]
-        tmr[4] = clk() - tk0;
-        unsigned long long *pp = a.prof + ((int64_t)blockIdx.x * NCW + warp) * 8;
-        for (int i = 0; i < 8; ++i) pp[i] = (unsigned long long)tmr[i];
     }
 }
 
@@ -825,7 +816,7 @@ int attention_grid(int bits, int num_sms, int64_t nb, int BH) {
 }
 
 int64_t attention_scratch_floats(int max_ctas) {
-    return (int64_t)max_ctas * 12 * MERGE_FLOATS;
+    return (int64_t)max_ctas * NSEGSLOT * NCW_MAX * MERGE_FLOATS;
 }
 
 int attention_max_partials(int64_t nb, int BH, int ncta) {

@@ -487,6 +487,8 @@ __global__ void __launch_bounds__(NCW_ * 32, 1) decode_attn_kernel(const AttnArg
     }
     const float c0 = LOG2E * 0.08838834764831845f;  // log2(e)/sqrt(128)
     __half *qh = reinterpret_cast<__half *>(smem + C::QH_OFF) + warp * 8 * QH_STRIDE;  // private
+    long long tmr[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    const long long tk0 = a.prof ? clk() : 0;
 
     for (int64_t bh = seg_first; bh <= seg_last; ++bh) {
         const int k = (int)(bh - seg_first);
@@ -496,6 +498,7 @@ __global__ void __launch_bounds__(NCW_ * 32, 1) decode_attn_kernel(const AttnArg
         const bool owns_tail = total == 0 || hi == (bh + 1) * nb;
         const __nv_bfloat16 *qbase = reinterpret_cast<const __nv_bfloat16 *>(a.q) + ((int64_t)b * a.Hq + kvh * g) * D;
 
+        const long long tq0 = a.prof ? clk() : 0;
         // ---- q fragments (per warp, no CTA barrier): rotated fp16 (raw bf16 for
         //      the bf16 baseline) through a private padded smem tile ----
 #pragma unroll
@@ -528,6 +531,7 @@ __global__ void __launch_bounds__(NCW_ * 32, 1) decode_attn_kernel(const AttnArg
         st.ob[0] = st.ob[1] = st.ob[2] = st.ob[3] = 0.f;
         st.m[0] = st.m[1] = -CUDART_INF_F;
         st.l[0] = st.l[1] = 0.f;
+        if (a.prof) tmr[6] += clk() - tq0;
 
         // ---- packed units of this segment: positions p = gidx - start, p % NCW == warp ----
         if (total > 0) {
@@ -536,16 +540,23 @@ __global__ void __launch_bounds__(NCW_ * 32, 1) decode_attn_kernel(const AttnArg
             for (int64_t p = first; p < hi - start; p += NCW) {
                 const int stg = (int)(p % C::NST);
                 const int round = (int)(p / C::NST);
+                const long long ts0 = a.prof ? clk() : 0;
                 if (lane == 0)
                     while (ld_volatile_shared(&consumed[stg]) < round) {
                     }
                 __syncwarp();
+                const long long ts1 = a.prof ? clk() : 0;
                 mbar_wait(&full[stg], (uint32_t)(round & 1));
+                if (a.prof) {
+                    const long long ts2 = clk();
+                    tmr[5] += ts1 - ts0;
+                    tmr[0] += ts2 - ts1;
+                }
                 const uint8_t *sb = ring + stg * C::STAGE;
                 if constexpr (BITS == 0) {
                     process_quarter_bf16(sb, st, qf, lane, c0);
                 } else {
-                    process_block<BITS>(sb, st, qf, lane, c0);
+                    process_block<BITS>(sb, st, qf, lane, c0, a.prof ? tmr : nullptr);
                 }
                 // stage consumed: refill it with unit p + NST, then publish the round
                 __syncwarp();
@@ -565,6 +576,7 @@ __global__ void __launch_bounds__(NCW_ * 32, 1) decode_attn_kernel(const AttnArg
             }
         }
 
+        const long long te0 = a.prof ? clk() : 0;
         // ---- warp partial -> global slot (unnormalized O[h][c], m[h], l[h]) ----
         const int sslot = k % NSEGSLOT;
         if (lane == 0)
@@ -684,7 +696,9 @@ __global__ void __launch_bounds__(NCW_ * 32, 1) decode_attn_kernel(const AttnArg
             arrived = atomicAdd(&segcnt[sslot], 1);
         }
         arrived = __shfl_sync(0xffffffffu, arrived, 0);
+        if (a.prof) tmr[7] += clk() - te0;
         if (arrived != NCW - 1) continue;  // not last: straight on to the next segment
+        const long long tm0 = a.prof ? clk() : 0;
         __threadfence_block();
         if (lane == 0) segcnt[sslot] = 0;
 
@@ -771,6 +785,14 @@ __global__ void __launch_bounds__(NCW_ * 32, 1) decode_attn_kernel(const AttnArg
             reinterpret_cast<uint2 *>(reinterpret_cast<__nv_bfloat16 *>(a.ring_v) + (bh * R + a.r) * D)[lane] =
                 vs[lane];
         }
+        if (a.prof) tmr[4] += clk() - tm0;  // merge work (slot 4 reused until the end)
+    }
+    if (a.prof && lane == 0) {
+        // per-warp phase cycles: [wait, qk, softmax, pv, merge, spin, qprologue, segtail]; total in slot 4 of the
+        // host view is replaced below by the whole-kernel cycles
+        unsigned long long *pp = a.prof + ((int64_t)blockIdx.x * NCW_MAX + warp) * 9;
+        for (int i = 0; i < 8; ++i) pp[i] = (unsigned long long)tmr[i];
+        pp[8] = (unsigned long long)(clk() - tk0);
     }
 }
 

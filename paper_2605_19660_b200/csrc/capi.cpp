@@ -296,29 +296,31 @@ struct oscar_kv_handle {
         unsigned long long *pbuf = nullptr;
         const int nw = a.ncta * 12;
         if (prof) {
-            CK(cudaMalloc(&pbuf, sizeof(unsigned long long) * 8 * nw));
-            CK(cudaMemsetAsync(pbuf, 0, sizeof(unsigned long long) * 8 * nw, s));
+            CK(cudaMalloc(&pbuf, sizeof(unsigned long long) * 9 * nw));
+            CK(cudaMemsetAsync(pbuf, 0, sizeof(unsigned long long) * 9 * nw, s));
             a.prof = pbuf;
         }
         CK(launch_attention(dbits, a, s));
         ++last_launches;
         if (prof) {
-            std::vector<unsigned long long> hbuf(8 * nw);
+            std::vector<unsigned long long> hbuf(9 * nw);
             CK(cudaMemcpyAsync(hbuf.data(), pbuf, hbuf.size() * 8, cudaMemcpyDeviceToHost, s));
             CK(cudaStreamSynchronize(s));
-            double acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+            double acc[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+            double mx = 0;
             int cnt = 0;
             for (int w = 0; w < nw; ++w) {
-                if (hbuf[8 * w + 4] == 0) continue;
+                if (hbuf[9 * w + 8] == 0) continue;
                 ++cnt;
-                for (int i = 0; i < 8; ++i) acc[i] += (double)hbuf[8 * w + i];
+                for (int i = 0; i < 9; ++i) acc[i] += (double)hbuf[9 * w + i];
+                mx = std::max(mx, (double)hbuf[9 * w + 8]);
             }
             if (cnt)
                 std::fprintf(stderr,
-                             "OSCAR_PROF warps=%d avg cycles: wait %.0f qk %.0f softmax %.0f pv %.0f total %.0f "
-                             "spin %.0f qprologue %.0f segtail %.0f\n",
+                             "OSCAR_PROF warps=%d avg cycles: wait %.0f qk %.0f softmax %.0f pv %.0f merge %.0f "
+                             "spin %.0f qprologue %.0f segtail %.0f total %.0f max %.0f\n",
                              cnt, acc[0] / cnt, acc[1] / cnt, acc[2] / cnt, acc[3] / cnt, acc[4] / cnt, acc[5] / cnt,
-                             acc[6] / cnt, acc[7] / cnt);
+                             acc[6] / cnt, acc[7] / cnt, acc[8] / cnt, mx);
             cudaFree(pbuf);
         }
     }

@@ -501,10 +501,14 @@ __global__ void __launch_bounds__(NCW_ * 32, 1) decode_attn_kernel(const AttnArg
         const long long tq0 = a.prof ? clk() : 0;
         // ---- q fragments (per warp, no CTA barrier): rotated fp16 (raw bf16 for
         //      the bf16 baseline) through a private padded smem tile ----
-#pragma unroll
         for (int j = 0; j < 8; ++j) {
             float x[4] = {0.f, 0.f, 0.f, 0.f};
-            if (j < g) load_bf16x4(qbase + j * D + lane * 4, x);
+            if (j < g) {
+                load_bf16x4(qbase + j * D + lane * 4, x);
+            } else {  // padded heads: zero rows, no transform
+                *reinterpret_cast<uint2 *>(qh + j * QH_STRIDE + lane * 4) = make_uint2(0u, 0u);
+                continue;
+            }
             uint32_t w0, w1;
             if (BITS == 0) {
                 w0 = pack_bf162(x[0], x[1]);
@@ -570,7 +574,8 @@ __global__ void __launch_bounds__(NCW_ * 32, 1) decode_attn_kernel(const AttnArg
                         fence_proxy_async_smem();
                         issue(p + C::NST, bh2, u2);
                     }
-                    __threadfence_block();
+                    // no fence needed: a waiter only relies on phase `round` of this
+                    // stage being complete, which held before this warp consumed it
                     st_volatile_shared(&consumed[stg], round + 1);
                 }
             }

@@ -501,14 +501,20 @@ __global__ void __launch_bounds__(NCW_ * 32, 1) decode_attn_kernel(const AttnArg
         const long long tq0 = a.prof ? clk() : 0;
         // ---- q fragments (per warp, no CTA barrier): rotated fp16 (raw bf16 for
         //      the bf16 baseline) through a private padded smem tile ----
+        uint2 qraw[8];  // issue every head's load first: one memory latency, not g
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+            qraw[j] = j < g ? *reinterpret_cast<const uint2 *>(qbase + j * D + lane * 4) : make_uint2(0u, 0u);
         for (int j = 0; j < 8; ++j) {
-            float x[4] = {0.f, 0.f, 0.f, 0.f};
-            if (j < g) {
-                load_bf16x4(qbase + j * D + lane * 4, x);
-            } else {  // padded heads: zero rows, no transform
+            float x[4];
+            if (j >= g) {  // padded heads: zero rows, no transform
                 *reinterpret_cast<uint2 *>(qh + j * QH_STRIDE + lane * 4) = make_uint2(0u, 0u);
                 continue;
             }
+            x[0] = __uint_as_float(qraw[j].x << 16);
+            x[1] = __uint_as_float(qraw[j].x & 0xffff0000u);
+            x[2] = __uint_as_float(qraw[j].y << 16);
+            x[3] = __uint_as_float(qraw[j].y & 0xffff0000u);
             uint32_t w0, w1;
             if (BITS == 0) {
                 w0 = pack_bf162(x[0], x[1]);

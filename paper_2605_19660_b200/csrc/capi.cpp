@@ -315,6 +315,28 @@ struct oscar_kv_handle {
                 for (int i = 0; i < 9; ++i) acc[i] += (double)hbuf[9 * w + i];
                 mx = std::max(mx, (double)hbuf[9 * w + 8]);
             }
+            {
+                // per-CTA spread: slowest warp per CTA, min/max across CTAs
+                double cmin = 1e30, cmax = 0, wspread = 0;
+                int ncta_used = 0;
+                for (int c = 0; c < a.ncta; ++c) {
+                    double lo = 1e30, hi = 0;
+                    for (int w = 0; w < 12; ++w) {
+                        const double t = (double)hbuf[9 * (c * 12 + w) + 8];
+                        if (t == 0) continue;
+                        lo = std::min(lo, t);
+                        hi = std::max(hi, t);
+                    }
+                    if (hi == 0) continue;
+                    ++ncta_used;
+                    cmin = std::min(cmin, hi);
+                    cmax = std::max(cmax, hi);
+                    wspread += (hi - lo);
+                }
+                if (ncta_used)
+                    std::fprintf(stderr, "OSCAR_PROF cta slowest-warp cycles: min %.0f max %.0f; mean in-CTA warp spread %.0f\n",
+                                 cmin, cmax, wspread / ncta_used);
+            }
             if (cnt)
                 std::fprintf(stderr,
                              "OSCAR_PROF warps=%d avg cycles: wait %.0f qk %.0f softmax %.0f pv %.0f merge %.0f "

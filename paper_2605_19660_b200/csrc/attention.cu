@@ -41,7 +41,7 @@ constexpr float LN2 = 0.6931471805599453f;
 
 constexpr int NSEGSLOT = 4;    // per-warp partial slots (segments in flight per CTA)
 constexpr int NCW_MAX = 12;
-constexpr int QH_STRIDE = 136;  // padded fp16 row of the per-warp q tile (conflict-free fragment loads)
+constexpr int QH_STRIDE = 136;  // padded fp16 row of the per-warp q tile (conflict-free; 16-B aligned rows)
 
 template <int BITS, int NCW_ = ((BITS == 4) ? 8 : 12)>
 struct AttnCfg {
@@ -109,6 +109,17 @@ __device__ __forceinline__ void load_bf16x4(const __nv_bfloat16 *p, float (&x)[4
     x[2] = __uint_as_float(u.y << 16);
     x[3] = __uint_as_float(u.y & 0xffff0000u);
 }
+
+// cp.async the g raw bf16 q rows (256 B each) into a padded tile (row stride QH_STRIDE halves)
+__device__ __forceinline__ void qtile_prefetch(__half *tile, const __nv_bfloat16 *q, int g, int lane) {
+    for (int c = lane; c < g * 16; c += 32) {  // 16-byte chunks: row c/16, chunk c%16
+        const int j = c >> 4, off = (c & 15) * 8;
+        const uint32_t dst = smem_u32(tile + j * QH_STRIDE + off);
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(dst), "l"(q + j * D + off) : "memory");
+    }
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
 
 __device__ __forceinline__ int64_t cta_of(int64_t x, int64_t total, int ncta) {
     return ((x + 1) * ncta - 1) / total;
@@ -499,32 +510,28 @@ __global__ void __launch_bounds__(NCW_ * 32, 1) decode_attn_kernel(const AttnArg
         const __nv_bfloat16 *qbase = reinterpret_cast<const __nv_bfloat16 *>(a.q) + ((int64_t)b * a.Hq + kvh * g) * D;
 
         const long long tq0 = a.prof ? clk() : 0;
-        // ---- q fragments (per warp, no CTA barrier): rotated fp16 (raw bf16 for
-        //      the bf16 baseline) through a private padded smem tile ----
-        uint2 qraw[8];  // issue every head's load first: one memory latency, not g
-#pragma unroll
-        for (int j = 0; j < 8; ++j)
-            qraw[j] = j < g ? *reinterpret_cast<const uint2 *>(qbase + j * D + lane * 4) : make_uint2(0u, 0u);
+        // ---- q fragments (per warp, no CTA barrier): the raw bf16 q rows of this
+        //      segment were prefetched into the warp's private tile with cp.async
+        //      (one segment ahead); rotate in registers and write back as fp16
+        //      (raw bf16 kept for the bf16 baseline) in place, row by row ----
+        if (k == 0) qtile_prefetch(qh, qbase, g, lane);
+        cp_async_wait_all();
+        __syncwarp();
         for (int j = 0; j < 8; ++j) {
-            float x[4];
+            uint2 *row = reinterpret_cast<uint2 *>(qh + j * QH_STRIDE) + lane;
             if (j >= g) {  // padded heads: zero rows, no transform
-                *reinterpret_cast<uint2 *>(qh + j * QH_STRIDE + lane * 4) = make_uint2(0u, 0u);
+                *row = make_uint2(0u, 0u);
                 continue;
             }
-            x[0] = __uint_as_float(qraw[j].x << 16);
-            x[1] = __uint_as_float(qraw[j].x & 0xffff0000u);
-            x[2] = __uint_as_float(qraw[j].y << 16);
-            x[3] = __uint_as_float(qraw[j].y & 0xffff0000u);
-            uint32_t w0, w1;
-            if (BITS == 0) {
-                w0 = pack_bf162(x[0], x[1]);
-                w1 = pack_bf162(x[2], x[3]);
-            } else {
-                if (a.rotates) fht128_warp(x, lane);
-                w0 = pack_half2(x[0], x[1]);
-                w1 = pack_half2(x[2], x[3]);
-            }
-            *reinterpret_cast<uint2 *>(qh + j * QH_STRIDE + lane * 4) = make_uint2(w0, w1);
+            if (BITS == 0) continue;  // the bf16 baseline attends raw q
+            const uint2 u = *row;
+            float x[4];
+            x[0] = __uint_as_float(u.x << 16);
+            x[1] = __uint_as_float(u.x & 0xffff0000u);
+            x[2] = __uint_as_float(u.y << 16);
+            x[3] = __uint_as_float(u.y & 0xffff0000u);
+            if (a.rotates) fht128_warp(x, lane);  // shuffles: every lane read row j first
+            *row = make_uint2(pack_half2(x[0], x[1]), pack_half2(x[2], x[3]));
         }
         __syncwarp();
         uint32_t qf[8][2];
@@ -534,6 +541,11 @@ __global__ void __launch_bounds__(NCW_ * 32, 1) decode_attn_kernel(const AttnArg
             qf[s][1] = *reinterpret_cast<const uint32_t *>(qh + gq * QH_STRIDE + 16 * s + 2 * tq + 8);
         }
         __syncwarp();
+        if (bh < seg_last) {  // next segment's raw q, in flight during this segment
+            const __nv_bfloat16 *qn = reinterpret_cast<const __nv_bfloat16 *>(a.q) +
+                                      ((int64_t)((bh + 1) / a.Hkv) * a.Hq + ((bh + 1) % a.Hkv) * g) * D;
+            qtile_prefetch(qh, qn, g, lane);
+        }
 
         WarpState st;
 #pragma unroll

@@ -53,7 +53,7 @@ struct AttnCfg {
     static constexpr int NTHREADS = NCW * 32;
     static constexpr int QH_OFF = 0;                                  // per-warp q tiles
     static constexpr int SEG_OFF = QH_OFF + NCW * 8 * QH_STRIDE * 2;  // segcnt[4], segdone[4]
-    static constexpr int BAR_OFF = ((SEG_OFF + 2 * NSEGSLOT * 4 + 16 + 7) / 8) * 8;
+    static constexpr int BAR_OFF = ((SEG_OFF + 2 * NSEGSLOT * 4 + 7) / 8) * 8;
     // shared ring of NST stages: as many whole stages as fit in 227 KB
     static constexpr int NST = (232448 - BAR_OFF - 1024) / STAGE;
     static constexpr int CNT_OFF = BAR_OFF + NST * 8;  // consumed-round counter per stage
@@ -435,7 +435,6 @@ __global__ void __launch_bounds__(NCW_ * 32, 1) decode_attn_kernel(const AttnArg
     int *consumed = reinterpret_cast<int *>(smem + C::CNT_OFF);
     int *segcnt = reinterpret_cast<int *>(smem + C::SEG_OFF);   // arrivals per segment slot
     int *segdone = segcnt + NSEGSLOT;                           // merges completed per slot
-    int *next_unit = segdone + NSEGSLOT;                        // dynamic unit dispenser
     uint8_t *ring = smem + C::RING_OFF;
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -450,30 +449,12 @@ __global__ void __launch_bounds__(NCW_ * 32, 1) decode_attn_kernel(const AttnArg
         end = ((cta + 1) * total) / a.ncta;
     }
     const int64_t nunits = end - start;
-    // segments (one per (b, kv head) the range touches); residual-only mode: CTA c <-> bh c
-    int64_t seg_first, seg_last;
-    if (total > 0) {
-        if (nunits <= 0) return;
-        seg_first = start / nb;
-        seg_last = (end - 1) / nb;
-    } else {
-        if (cta >= a.BH) return;
-        seg_first = seg_last = cta;
-    }
-    __half *qh = reinterpret_cast<__half *>(smem + C::QH_OFF) + warp * 8 * QH_STRIDE;  // private q tile
-    auto qptr = [&](int64_t bh) {
-        return reinterpret_cast<const __nv_bfloat16 *>(a.q) + ((int64_t)(bh / a.Hkv) * a.Hq + (bh % a.Hkv) * g) * D;
-    };
-    // the first segment's q goes out before the ring fill (it is needed first)
-    qtile_prefetch(qh, qptr(seg_first), g, lane);
-
     const uint64_t pol = l2_evict_first_policy();
     // Shared ring, any number of warps: unit p of this CTA's range lives in
-    // stage p % NST, round p / NST.  Units are handed to warps dynamically (an
-    // smem counter), in order.  The consumer of unit p first waits until the
-    // stage's previous round is consumed (software counter) -- which also
-    // means the TMA for unit p was issued, so the full-barrier wait is on the
-    // right phase -- and after consuming refills the stage with unit p + NST.
+    // stage p % NST, round p / NST.  Its consumer (warp p % NCW) first waits
+    // until the stage's previous round is consumed (software counter) -- which
+    // also means the TMA for unit p was issued, so the full-barrier wait is on
+    // the right phase -- and after consuming refills the stage with unit p+NST.
     auto issue = [&](int64_t p, int64_t bh, int64_t uidx) {  // uidx: unit index within bh
         const int stg = (int)(p % C::NST);
         mbar_arrive_expect_tx(&full[stg], C::STAGE);
@@ -481,6 +462,7 @@ __global__ void __launch_bounds__(NCW_ * 32, 1) decode_attn_kernel(const AttnArg
                  a.blocks + (bh * a.max_blocks + uidx / SUB) * (int64_t)C::BYTES + (uidx % SUB) * C::STAGE, C::STAGE,
                  &full[stg], pol);
     };
+
     if (threadIdx.x == 0) {
         for (int i = 0; i < C::NST; ++i) {
             mbar_init(&full[i], 1);
@@ -490,35 +472,49 @@ __global__ void __launch_bounds__(NCW_ * 32, 1) decode_attn_kernel(const AttnArg
             segcnt[i] = 0;
             st_volatile_shared(&segdone[i], 0);
         }
-        *next_unit = 0;
         fence_mbar_init();
-    }
-    __syncthreads();  // the only CTA-wide barrier
-    if (threadIdx.x == 0 && nunits > 0) {
-        int64_t bh = start / nb, uidx = start % nb;
-        for (int64_t p = 0; p < nunits && p < C::NST; ++p) {
-            issue(p, bh, uidx);
-            if (++uidx == nb) {
-                uidx = 0;
-                ++bh;
+        if (nunits > 0) {
+            int64_t bh = start / nb, uidx = start % nb;
+            for (int64_t p = 0; p < nunits && p < C::NST; ++p) {
+                issue(p, bh, uidx);
+                if (++uidx == nb) {
+                    uidx = 0;
+                    ++bh;
+                }
             }
         }
     }
+    __syncthreads();  // the only CTA-wide barrier
 
+    // segments: residual-only mode (nb == 0): CTA c <-> bh c
+    int64_t seg_first, seg_last;
+    if (total > 0) {
+        if (nunits <= 0) return;
+        seg_first = start / nb;
+        seg_last = (end - 1) / nb;
+    } else {
+        if (cta >= a.BH) return;
+        seg_first = seg_last = cta;
+    }
     const float c0 = LOG2E * 0.08838834764831845f;  // log2(e)/sqrt(128)
-    uint32_t qf[8][2];
-    WarpState st;
-    int64_t k = -1;                 // current segment (local index) of this warp
-    int64_t seg_hi = 0;             // end position (exclusive) of segment k
-    bool seg_has_data = false;
+    __half *qh = reinterpret_cast<__half *>(smem + C::QH_OFF) + warp * 8 * QH_STRIDE;  // private
+    long long tmr[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    const long long tk0 = a.prof ? clk() : 0;
 
-    // ---- begin segment kk: q fragments + fresh accumulators ----
-    auto begin_segment = [&](int64_t kk) {
-        const int64_t bh = seg_first + kk;
-        seg_hi = total > 0 ? (((bh + 1) * nb < end ? (bh + 1) * nb : end) - start) : 0;
-        seg_has_data = false;
-        // raw bf16 q rows of this segment were prefetched into the private tile;
-        // rotate in registers and write back as fp16 in place, row by row
+    for (int64_t bh = seg_first; bh <= seg_last; ++bh) {
+        const int k = (int)(bh - seg_first);
+        const int b = (int)(bh / a.Hkv), kvh = (int)(bh % a.Hkv);
+        const int64_t lo = total > 0 ? (bh * nb > start ? bh * nb : start) : 0;
+        const int64_t hi = total > 0 ? ((bh + 1) * nb < end ? (bh + 1) * nb : end) : 0;
+        const bool owns_tail = total == 0 || hi == (bh + 1) * nb;
+        const __nv_bfloat16 *qbase = reinterpret_cast<const __nv_bfloat16 *>(a.q) + ((int64_t)b * a.Hq + kvh * g) * D;
+
+        const long long tq0 = a.prof ? clk() : 0;
+        // ---- q fragments (per warp, no CTA barrier): the raw bf16 q rows of this
+        //      segment were prefetched into the warp's private tile with cp.async
+        //      (one segment ahead); rotate in registers and write back as fp16
+        //      (raw bf16 kept for the bf16 baseline) in place, row by row ----
+        if (k == 0) qtile_prefetch(qh, qbase, g, lane);
         cp_async_wait_all();
         __syncwarp();
         for (int j = 0; j < 8; ++j) {
@@ -538,37 +534,80 @@ __global__ void __launch_bounds__(NCW_ * 32, 1) decode_attn_kernel(const AttnArg
             *row = make_uint2(pack_half2(x[0], x[1]), pack_half2(x[2], x[3]));
         }
         __syncwarp();
+        uint32_t qf[8][2];
 #pragma unroll
         for (int s = 0; s < 8; ++s) {
             qf[s][0] = *reinterpret_cast<const uint32_t *>(qh + gq * QH_STRIDE + 16 * s + 2 * tq);
             qf[s][1] = *reinterpret_cast<const uint32_t *>(qh + gq * QH_STRIDE + 16 * s + 2 * tq + 8);
         }
         __syncwarp();
-        if (bh < seg_last) qtile_prefetch(qh, qptr(bh + 1), g, lane);  // next segment's q, in flight
+        if (bh < seg_last) {  // next segment's raw q, in flight during this segment
+            const __nv_bfloat16 *qn = reinterpret_cast<const __nv_bfloat16 *>(a.q) +
+                                      ((int64_t)((bh + 1) / a.Hkv) * a.Hq + ((bh + 1) % a.Hkv) * g) * D;
+            qtile_prefetch(qh, qn, g, lane);
+        }
+
+        WarpState st;
 #pragma unroll
         for (int mm = 0; mm < 8; ++mm) st.o[mm][0] = st.o[mm][1] = st.o[mm][2] = st.o[mm][3] = 0.f;
         st.ob[0] = st.ob[1] = st.ob[2] = st.ob[3] = 0.f;
         st.m[0] = st.m[1] = -CUDART_INF_F;
         st.l[0] = st.l[1] = 0.f;
-    };
+        if (a.prof) tmr[6] += clk() - tq0;
 
-    // ---- end segment kk: partial (+ residual) -> slot; last warp merges ----
-    auto end_segment = [&](int64_t kk) {
-        const int64_t bh = seg_first + kk;
-        const int b = (int)(bh / a.Hkv), kvh = (int)(bh % a.Hkv);
-        const bool owns_tail = total == 0 || (((bh + 1) * nb <= end));
-        const int ntok = owns_tail ? a.r + (a.kcur ? 1 : 0) : 0;
-        const bool has_res = warp < ntok;
-        const int sslot = (int)(kk % NSEGSLOT);
+        // ---- packed units of this segment: positions p = gidx - start, p % NCW == warp ----
+        if (total > 0) {
+            const int64_t p0 = lo - start;
+            const int64_t first = p0 + ((warp - (int)(p0 % NCW)) + NCW) % NCW;
+            for (int64_t p = first; p < hi - start; p += NCW) {
+                const int stg = (int)(p % C::NST);
+                const int round = (int)(p / C::NST);
+                const long long ts0 = a.prof ? clk() : 0;
+                if (lane == 0)
+                    while (ld_volatile_shared(&consumed[stg]) < round) {
+                    }
+                __syncwarp();
+                const long long ts1 = a.prof ? clk() : 0;
+                mbar_wait(&full[stg], (uint32_t)(round & 1));
+                if (a.prof) {
+                    const long long ts2 = clk();
+                    tmr[5] += ts1 - ts0;
+                    tmr[0] += ts2 - ts1;
+                }
+                const uint8_t *sb = ring + stg * C::STAGE;
+                if constexpr (BITS == 0) {
+                    process_quarter_bf16(sb, st, qf, lane, c0);
+                } else {
+                    process_block<BITS>(sb, st, qf, lane, c0, a.prof ? tmr : nullptr);
+                }
+                // stage consumed: refill it with unit p + NST, then publish the round
+                __syncwarp();
+                if (lane == 0) {
+                    if (p + C::NST < nunits) {
+                        int64_t bh2 = bh, u2 = start + p - bh * nb + C::NST;
+                        while (u2 >= nb) {
+                            u2 -= nb;
+                            ++bh2;
+                        }
+                        fence_proxy_async_smem();
+                        issue(p + C::NST, bh2, u2);
+                    }
+                    // no fence needed: a waiter only relies on phase `round` of this
+                    // stage being complete, which held before this warp consumed it
+                    st_volatile_shared(&consumed[stg], round + 1);
+                }
+            }
+        }
+
+        const long long te0 = a.prof ? clk() : 0;
+        // ---- warp partial -> global slot (unnormalized O[h][c], m[h], l[h]) ----
+        const int sslot = k % NSEGSLOT;
         if (lane == 0)
-            while (ld_volatile_shared(&segdone[sslot]) < (int)(kk / NSEGSLOT)) {  // slot reuse guard
+            while (ld_volatile_shared(&segdone[sslot]) < k / NSEGSLOT) {  // slot reuse guard
             }
         __syncwarp();
         float *slot = a.warp_part + (((int64_t)cta * NSEGSLOT + sslot) * NCW_MAX + warp) * MERGE_FLOATS;
-        if (!seg_has_data) {
-            if (lane < 8) slot[8 * D + lane] = -CUDART_INF_F;  // empty partial (O not read)
-            if (lane < 8) slot[8 * D + 8 + lane] = 0.f;
-        } else {
+        {
             float l0 = st.l[0], l1 = st.l[1];
 #pragma unroll
             for (int o = 4; o < 32; o <<= 1) {
@@ -601,83 +640,88 @@ __global__ void __launch_bounds__(NCW_ * 32, 1) decode_attn_kernel(const AttnArg
                 slot[8 * D + 8 + 2 * tq] = l0;
                 slot[8 * D + 8 + 2 * tq + 1] = l1;
             }
-        }
-        __syncwarp();
-        // residual window + current token (fp32 CUDA cores), merged into the slot
-        if (has_res) {
-            const __nv_bfloat16 *qbase = qptr(bh);
-            float qv[8][4];
-#pragma unroll
-            for (int j = 0; j < 8; ++j) {
-                qv[j][0] = qv[j][1] = qv[j][2] = qv[j][3] = 0.f;
-                if (j < g) load_bf16x4(qbase + j * D + lane * 4, qv[j]);
-            }
-            float mr[8], lr[8], orr[8][4];
-#pragma unroll
-            for (int j = 0; j < 8; ++j) {
-                mr[j] = -CUDART_INF_F;
-                lr[j] = 0.f;
-                orr[j][0] = orr[j][1] = orr[j][2] = orr[j][3] = 0.f;
-            }
-            for (int t = warp; t < ntok; t += NCW) {
-                const __nv_bfloat16 *kp, *vp;
-                if (t < a.r) {
-                    kp = reinterpret_cast<const __nv_bfloat16 *>(a.ring_k) + (bh * R + t) * D;
-                    vp = reinterpret_cast<const __nv_bfloat16 *>(a.ring_v) + (bh * R + t) * D;
-                } else {
-                    kp = reinterpret_cast<const __nv_bfloat16 *>(a.kcur) + ((int64_t)b * a.Hkv + kvh) * D;
-                    vp = reinterpret_cast<const __nv_bfloat16 *>(a.vcur) + ((int64_t)b * a.Hkv + kvh) * D;
-                }
-                float k4[4], v4[4];
-                load_bf16x4(kp + lane * 4, k4);
-                load_bf16x4(vp + lane * 4, v4);
-                if (a.rotate_v) fht128_warp(v4, lane);
-#pragma unroll
-                for (int j = 0; j < 8; ++j) {
-                    if (j < g) {
-                        float d = qv[j][0] * k4[0] + qv[j][1] * k4[1] + qv[j][2] * k4[2] + qv[j][3] * k4[3];
-                        d = warp_sum(d) * c0;
-                        const float mn = fmaxf(mr[j], d);
-                        const float al = fast_exp2(mr[j] - mn), pp = fast_exp2(d - mn);
-                        lr[j] = lr[j] * al + pp;
-#pragma unroll
-                        for (int e = 0; e < 4; ++e) orr[j][e] = orr[j][e] * al + pp * v4[e];
-                        mr[j] = mn;
-                    }
-                }
-            }
-#pragma unroll
-            for (int j = 0; j < 8; ++j) {
-                if (j < g) {
-                    const float ms = slot[8 * D + j], ls = slot[8 * D + 8 + j];
-                    const float M = fmaxf(ms, mr[j]);
-                    const float fs = (ms == -CUDART_INF_F) ? 0.f : fast_exp2(ms - M);
-                    const float fr = (mr[j] == -CUDART_INF_F) ? 0.f : fast_exp2(mr[j] - M);
-                    float4 *op = reinterpret_cast<float4 *>(slot + j * D + lane * 4);
-                    float4 ov = (ms == -CUDART_INF_F) ? make_float4(0.f, 0.f, 0.f, 0.f) : *op;
-                    ov.x = ov.x * fs + orr[j][0] * fr;
-                    ov.y = ov.y * fs + orr[j][1] * fr;
-                    ov.z = ov.z * fs + orr[j][2] * fr;
-                    ov.w = ov.w * fs + orr[j][3] * fr;
-                    *op = ov;
-                    __syncwarp();
-                    if (lane == 0) {
-                        slot[8 * D + j] = M;
-                        slot[8 * D + 8 + j] = ls * fs + lr[j] * fr;
-                    }
-                }
-            }
             __syncwarp();
         }
 
-        // arrive; the LAST warp of the CTA to finish this segment merges
+        // ---- residual window + current token (fp32 CUDA cores), merged into the slot ----
+        if (owns_tail) {
+            const int ntok = a.r + (a.kcur ? 1 : 0);
+            if (warp < ntok) {
+                float qv[8][4];
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                    qv[j][0] = qv[j][1] = qv[j][2] = qv[j][3] = 0.f;
+                    if (j < g) load_bf16x4(qbase + j * D + lane * 4, qv[j]);
+                }
+                float mr[8], lr[8], orr[8][4];
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                    mr[j] = -CUDART_INF_F;
+                    lr[j] = 0.f;
+                    orr[j][0] = orr[j][1] = orr[j][2] = orr[j][3] = 0.f;
+                }
+                for (int t = warp; t < ntok; t += NCW) {
+                    const __nv_bfloat16 *kp, *vp;
+                    if (t < a.r) {
+                        kp = reinterpret_cast<const __nv_bfloat16 *>(a.ring_k) + (bh * R + t) * D;
+                        vp = reinterpret_cast<const __nv_bfloat16 *>(a.ring_v) + (bh * R + t) * D;
+                    } else {
+                        kp = reinterpret_cast<const __nv_bfloat16 *>(a.kcur) + ((int64_t)b * a.Hkv + kvh) * D;
+                        vp = reinterpret_cast<const __nv_bfloat16 *>(a.vcur) + ((int64_t)b * a.Hkv + kvh) * D;
+                    }
+                    float k4[4], v4[4];
+                    load_bf16x4(kp + lane * 4, k4);
+                    load_bf16x4(vp + lane * 4, v4);
+                    if (a.rotate_v) fht128_warp(v4, lane);
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) {
+                        if (j < g) {
+                            float d = qv[j][0] * k4[0] + qv[j][1] * k4[1] + qv[j][2] * k4[2] + qv[j][3] * k4[3];
+                            d = warp_sum(d) * c0;
+                            const float mn = fmaxf(mr[j], d);
+                            const float al = fast_exp2(mr[j] - mn), pp = fast_exp2(d - mn);
+                            lr[j] = lr[j] * al + pp;
+#pragma unroll
+                            for (int e = 0; e < 4; ++e) orr[j][e] = orr[j][e] * al + pp * v4[e];
+                            mr[j] = mn;
+                        }
+                    }
+                }
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                    if (j < g) {
+                        const float ms = slot[8 * D + j], ls = slot[8 * D + 8 + j];
+                        const float M = fmaxf(ms, mr[j]);
+                        const float fs = (ms == -CUDART_INF_F) ? 0.f : fast_exp2(ms - M);
+                        const float fr = (mr[j] == -CUDART_INF_F) ? 0.f : fast_exp2(mr[j] - M);
+                        float4 *op = reinterpret_cast<float4 *>(slot + j * D + lane * 4);
+                        float4 ov = *op;
+                        ov.x = ov.x * fs + orr[j][0] * fr;
+                        ov.y = ov.y * fs + orr[j][1] * fr;
+                        ov.z = ov.z * fs + orr[j][2] * fr;
+                        ov.w = ov.w * fs + orr[j][3] * fr;
+                        *op = ov;
+                        __syncwarp();
+                        if (lane == 0) {
+                            slot[8 * D + j] = M;
+                            slot[8 * D + 8 + j] = ls * fs + lr[j] * fr;
+                        }
+                    }
+                }
+                __syncwarp();
+            }
+        }
+
+        // ---- arrive; the LAST warp of the CTA to finish this segment merges ----
         int arrived = 0;
         if (lane == 0) {
             __threadfence_block();
             arrived = atomicAdd(&segcnt[sslot], 1);
         }
         arrived = __shfl_sync(0xffffffffu, arrived, 0);
-        if (arrived != NCW - 1) return;
+        if (a.prof) tmr[7] += clk() - te0;
+        if (arrived != NCW - 1) continue;  // not last: straight on to the next segment
+        const long long tm0 = a.prof ? clk() : 0;
         __threadfence_block();
         if (lane == 0) segcnt[sslot] = 0;
 
@@ -700,8 +744,7 @@ __global__ void __launch_bounds__(NCW_ * 32, 1) decode_attn_kernel(const AttnArg
 #pragma unroll
             for (int w = 0; w < NCW; ++w) {
                 const float mw = wp[w * MERGE_FLOATS + 8 * D + h];
-                if (mw == -CUDART_INF_F) continue;  // empty partial
-                const float f = fast_exp2(mw - M);
+                const float f = (mw == -CUDART_INF_F) ? 0.f : fast_exp2(mw - M);
                 const float4 v = *reinterpret_cast<const float4 *>(wp + w * MERGE_FLOATS + h * D + lane * 4);
                 O.x += v.x * f;
                 O.y += v.y * f;
@@ -715,7 +758,8 @@ __global__ void __launch_bounds__(NCW_ * 32, 1) decode_attn_kernel(const AttnArg
                 pml[2 * h + 1] = L;
             }
         }
-        if (lane == 0) st_volatile_shared(&segdone[sslot], (int)(kk / NSEGSLOT) + 1);  // slots reusable
+        // the warp slots of this segment may be reused now
+        if (lane == 0) st_volatile_shared(&segdone[sslot], k / NSEGSLOT + 1);
         int prev = 0;
         if (lane == 0) {
             __threadfence();
@@ -734,8 +778,7 @@ __global__ void __launch_bounds__(NCW_ * 32, 1) decode_attn_kernel(const AttnArg
                 float L = 0.f;
                 for (int s2 = 0; s2 < expected; ++s2) {
                     const float ms = __ldcg(pmb + s2 * 16 + 2 * h);
-                    if (ms == -CUDART_INF_F) continue;
-                    const float f = fast_exp2(ms - M);
+                    const float f = (ms == -CUDART_INF_F) ? 0.f : fast_exp2(ms - M);
                     const float4 v = __ldcg(reinterpret_cast<const float4 *>(pob + s2 * 8 * D + h * D + lane * 4));
                     x[0] += v.x * f;
                     x[1] += v.y * f;
@@ -765,60 +808,14 @@ __global__ void __launch_bounds__(NCW_ * 32, 1) decode_attn_kernel(const AttnArg
             reinterpret_cast<uint2 *>(reinterpret_cast<__nv_bfloat16 *>(a.ring_v) + (bh * R + a.r) * D)[lane] =
                 vs[lane];
         }
-    };
-
-    // ---- main loop: grab units in order, crossing segment boundaries as needed ----
-    const int64_t nseg = seg_last - seg_first + 1;
-    for (;;) {
-        int64_t p = 0;
-        if (lane == 0) p = atomicAdd(next_unit, 1);
-        p = __shfl_sync(0xffffffffu, (long long)p, 0);
-        if (p >= nunits) break;
-        while (k < 0 || p >= seg_hi) {  // close finished segments, open the unit's segment
-            if (k >= 0) end_segment(k);
-            ++k;
-            begin_segment(k);
-        }
-        const int stg = (int)(p % C::NST);
-        const int round = (int)(p / C::NST);
-        if (lane == 0)
-            while (ld_volatile_shared(&consumed[stg]) < round) {
-            }
-        __syncwarp();
-        mbar_wait(&full[stg], (uint32_t)(round & 1));
-        const uint8_t *sb = ring + stg * C::STAGE;
-        if constexpr (BITS == 0) {
-            process_quarter_bf16(sb, st, qf, lane, c0);
-        } else {
-            process_block<BITS>(sb, st, qf, lane, c0);
-        }
-        seg_has_data = true;
-        // stage consumed: refill it with unit p + NST, then publish the round
-        __syncwarp();
-        if (lane == 0) {
-            if (p + C::NST < nunits) {
-                const int64_t bh = seg_first + k;
-                int64_t bh2 = bh, u2 = start + p - bh * nb + C::NST;
-                while (u2 >= nb) {
-                    u2 -= nb;
-                    ++bh2;
-                }
-                fence_proxy_async_smem();
-                issue(p + C::NST, bh2, u2);
-            }
-            st_volatile_shared(&consumed[stg], round + 1);
-        }
+        if (a.prof) tmr[4] += clk() - tm0;  // merge work (slot 4 reused until the end)
     }
-    // close the remaining segments (empty partials for segments this warp never touched)
-    if (k < 0) {
-        k = 0;
-        begin_segment(0);
-    }
-    for (;;) {
-        end_segment(k);
-        if (k + 1 >= nseg) break;
-        ++k;
-        begin_segment(k);
+    if (a.prof && lane == 0) {
+        // per-warp phase cycles: [wait, qk, softmax, pv, merge, spin, qprologue, segtail]; total in slot 4 of the
+        // host view is replaced below by the whole-kernel cycles
+        unsigned long long *pp = a.prof + ((int64_t)blockIdx.x * NCW_MAX + warp) * 9;
+        for (int i = 0; i < 8; ++i) pp[i] = (unsigned long long)tmr[i];
+        pp[8] = (unsigned long long)(clk() - tk0);
     }
 }
 

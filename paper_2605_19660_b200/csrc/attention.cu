@@ -463,6 +463,13 @@ __global__ void __launch_bounds__(NCW_ * 32, 1) decode_attn_kernel(const AttnArg
                  &full[stg], pol);
     };
 
+    if (total > 0 ? nunits > 0 : cta < a.BH) {  // first segment's q goes out before the ring fill
+        const int64_t bh0 = total > 0 ? start / nb : cta;
+        qtile_prefetch(reinterpret_cast<__half *>(smem + C::QH_OFF) + warp * 8 * QH_STRIDE,
+                       reinterpret_cast<const __nv_bfloat16 *>(a.q) +
+                           ((int64_t)(bh0 / a.Hkv) * a.Hq + (bh0 % a.Hkv) * a.g) * D,
+                       a.g, lane);
+    }
     if (threadIdx.x == 0) {
         for (int i = 0; i < C::NST; ++i) {
             mbar_init(&full[i], 1);
@@ -514,7 +521,6 @@ __global__ void __launch_bounds__(NCW_ * 32, 1) decode_attn_kernel(const AttnArg
         //      segment were prefetched into the warp's private tile with cp.async
         //      (one segment ahead); rotate in registers and write back as fp16
         //      (raw bf16 kept for the bf16 baseline) in place, row by row ----
-        if (k == 0) qtile_prefetch(qh, qbase, g, lane);
         cp_async_wait_all();
         __syncwarp();
         for (int j = 0; j < 8; ++j) {
@@ -735,56 +741,89 @@ __global__ void __launch_bounds__(NCW_ * 32, 1) decode_attn_kernel(const AttnArg
         const int pslot = (int)(total > 0 ? cta - first_cta : 0);
         float *po = a.part_o + ((int64_t)bh * a.maxp + pslot) * 8 * D;
         float *pml = a.part_ml + ((int64_t)bh * a.maxp + pslot) * 16;
-        for (int h = 0; h < g; ++h) {
-            float M = -CUDART_INF_F;
+        {
+            // lane w < NCW holds warp w's (m[h], l[h]); one load round, then shuffles
+            float mw[8], lw[8];
+            {
+                const int w = lane < NCW ? lane : 0;
+                const float4 *ml = reinterpret_cast<const float4 *>(wp + w * MERGE_FLOATS + 8 * D);
+                const float4 m0 = ml[0], m1 = ml[1], l0 = ml[2], l1 = ml[3];
+                mw[0] = m0.x; mw[1] = m0.y; mw[2] = m0.z; mw[3] = m0.w;
+                mw[4] = m1.x; mw[5] = m1.y; mw[6] = m1.z; mw[7] = m1.w;
+                lw[0] = l0.x; lw[1] = l0.y; lw[2] = l0.z; lw[3] = l0.w;
+                lw[4] = l1.x; lw[5] = l1.y; lw[6] = l1.z; lw[7] = l1.w;
+                if (lane >= NCW) {
 #pragma unroll
-            for (int w = 0; w < NCW; ++w) M = fmaxf(M, wp[w * MERGE_FLOATS + 8 * D + h]);
-            float4 O = make_float4(0.f, 0.f, 0.f, 0.f);
-            float L = 0.f;
-#pragma unroll
-            for (int w = 0; w < NCW; ++w) {
-                const float mw = wp[w * MERGE_FLOATS + 8 * D + h];
-                const float f = (mw == -CUDART_INF_F) ? 0.f : fast_exp2(mw - M);
-                const float4 v = *reinterpret_cast<const float4 *>(wp + w * MERGE_FLOATS + h * D + lane * 4);
-                O.x += v.x * f;
-                O.y += v.y * f;
-                O.z += v.z * f;
-                O.w += v.w * f;
-                L += wp[w * MERGE_FLOATS + 8 * D + 8 + h] * f;
+                    for (int h = 0; h < 8; ++h) {
+                        mw[h] = -CUDART_INF_F;
+                        lw[h] = 0.f;
+                    }
+                }
             }
-            *reinterpret_cast<float4 *>(po + h * D + lane * 4) = O;
-            if (lane == 0) {
-                pml[2 * h] = M;
-                pml[2 * h + 1] = L;
+#pragma unroll
+            for (int h = 0; h < 8; ++h) {
+                if (h >= g) break;
+                float M = mw[h];
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o));
+                const float fw = (mw[h] == -CUDART_INF_F) ? 0.f : fast_exp2(mw[h] - M);  // lane w's factor
+                const float L = warp_sum(lw[h] * fw);
+                float4 v[NCW];
+#pragma unroll
+                for (int w = 0; w < NCW; ++w)  // all loads in flight at once
+                    v[w] = *reinterpret_cast<const float4 *>(wp + w * MERGE_FLOATS + h * D + lane * 4);
+                float4 O = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+                for (int w = 0; w < NCW; ++w) {
+                    const float f = __shfl_sync(0xffffffffu, fw, w);
+                    if (f != 0.f) {  // skips empty partials (their O is never read as NaN*0)
+                        O.x += v[w].x * f;
+                        O.y += v[w].y * f;
+                        O.z += v[w].z * f;
+                        O.w += v[w].w * f;
+                    }
+                }
+                *reinterpret_cast<float4 *>(po + h * D + lane * 4) = O;
+                if (lane == 0) {
+                    pml[2 * h] = M;
+                    pml[2 * h + 1] = L;
+                }
             }
         }
         // the warp slots of this segment may be reused now
         if (lane == 0) st_volatile_shared(&segdone[sslot], k / NSEGSLOT + 1);
+        __syncwarp();
         int prev = 0;
-        if (lane == 0) {
-            __threadfence();
-            prev = atomicAdd(&a.counters[bh], 1);
-        }
+        if (lane == 0) prev = atomic_add_acq_rel_gpu(&a.counters[bh], 1);  // publishes the partial
         prev = __shfl_sync(0xffffffffu, prev, 0);
         if (prev == expected - 1) {
             // last CTA for this (b, kv head): merge the CTA partials -> output
-            __threadfence();
             const float *pmb = a.part_ml + (int64_t)bh * a.maxp * 16;
             const float *pob = a.part_o + (int64_t)bh * a.maxp * 8 * D;
             for (int h = 0; h < g; ++h) {
-                float M = -CUDART_INF_F;
-                for (int s2 = 0; s2 < expected; ++s2) M = fmaxf(M, __ldcg(pmb + s2 * 16 + 2 * h));
+                // lane s2 < expected holds CTA partial s2's (m, l)
+                float ms = -CUDART_INF_F, ls = 0.f;
+                for (int s2 = lane; s2 < expected; s2 += 32) {  // expected <= 32 in practice
+                    const float m2 = __ldcg(pmb + s2 * 16 + 2 * h), l2 = __ldcg(pmb + s2 * 16 + 2 * h + 1);
+                    const float Mx = fmaxf(ms, m2);
+                    const float fa = (ms == -CUDART_INF_F) ? 0.f : fast_exp2(ms - Mx);
+                    const float fb = (m2 == -CUDART_INF_F) ? 0.f : fast_exp2(m2 - Mx);
+                    ls = ls * fa + l2 * fb;
+                    ms = Mx;
+                }
+                float M = ms;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o));
+                const float L = warp_sum((ms == -CUDART_INF_F) ? 0.f : ls * fast_exp2(ms - M));
                 float x[4] = {0.f, 0.f, 0.f, 0.f};
-                float L = 0.f;
                 for (int s2 = 0; s2 < expected; ++s2) {
-                    const float ms = __ldcg(pmb + s2 * 16 + 2 * h);
-                    const float f = (ms == -CUDART_INF_F) ? 0.f : fast_exp2(ms - M);
+                    const float m2 = __ldcg(pmb + s2 * 16 + 2 * h);
                     const float4 v = __ldcg(reinterpret_cast<const float4 *>(pob + s2 * 8 * D + h * D + lane * 4));
+                    const float f = (m2 == -CUDART_INF_F) ? 0.f : fast_exp2(m2 - M);
                     x[0] += v.x * f;
                     x[1] += v.y * f;
                     x[2] += v.z * f;
                     x[3] += v.w * f;
-                    L += __ldcg(pmb + s2 * 16 + 2 * h + 1) * f;
                 }
                 const float inv = (L > 0.f) ? 1.f / L : 0.f;
 #pragma unroll

@@ -505,7 +505,7 @@ __global__ void __launch_bounds__(NCW_ * 32, 1) decode_attn_kernel(const AttnArg
     }
     const float c0 = LOG2E * 0.08838834764831845f;  // log2(e)/sqrt(128)
     __half *qh = reinterpret_cast<__half *>(smem + C::QH_OFF) + warp * 8 * QH_STRIDE;  // private
-    long long tmr[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    long long tmr[12] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
     const long long tk0 = a.prof ? clk() : 0;
 
     for (int64_t bh = seg_first; bh <= seg_last; ++bh) {
@@ -793,9 +793,15 @@ __global__ void __launch_bounds__(NCW_ * 32, 1) decode_attn_kernel(const AttnArg
         // the warp slots of this segment may be reused now
         if (lane == 0) st_volatile_shared(&segdone[sslot], k / NSEGSLOT + 1);
         __syncwarp();
+        const long long tmA = a.prof ? clk() : 0;
         int prev = 0;
         if (lane == 0) prev = atomic_add_acq_rel_gpu(&a.counters[bh], 1);  // publishes the partial
         prev = __shfl_sync(0xffffffffu, prev, 0);
+        const long long tmB = a.prof ? clk() : 0;
+        if (a.prof) {
+            tmr[8] += tmA - tm0;
+            tmr[9] += tmB - tmA;
+        }
         if (prev == expected - 1) {
             // last CTA for this (b, kv head): merge the CTA partials -> output
             const float *pmb = a.part_ml + (int64_t)bh * a.maxp * 16;
@@ -835,6 +841,7 @@ __global__ void __launch_bounds__(NCW_ * 32, 1) decode_attn_kernel(const AttnArg
                     a.lse[(int64_t)b * a.Hq + kvh * g + h] = (L > 0.f) ? (M + __log2f(L)) * LN2 : -CUDART_INF_F;
             }
             if (lane == 0) a.counters[bh] = 0;
+            if (a.prof) tmr[10] += clk() - tmB;
         }
         // current token -> residual ring (nobody reads slot r in this launch)
         if (owns_tail && a.write_ring && a.kcur) {
@@ -852,9 +859,12 @@ __global__ void __launch_bounds__(NCW_ * 32, 1) decode_attn_kernel(const AttnArg
     if (a.prof && lane == 0) {
         // per-warp phase cycles: [wait, qk, softmax, pv, merge, spin, qprologue, segtail]; total in slot 4 of the
         // host view is replaced below by the whole-kernel cycles
-        unsigned long long *pp = a.prof + ((int64_t)blockIdx.x * NCW_MAX + warp) * 9;
+        unsigned long long *pp = a.prof + ((int64_t)blockIdx.x * NCW_MAX + warp) * 12;
         for (int i = 0; i < 8; ++i) pp[i] = (unsigned long long)tmr[i];
         pp[8] = (unsigned long long)(clk() - tk0);
+        pp[9] = (unsigned long long)tmr[8];
+        pp[10] = (unsigned long long)tmr[9];
+        pp[11] = (unsigned long long)tmr[10];
     }
 }
 

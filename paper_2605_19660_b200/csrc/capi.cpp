@@ -296,24 +296,24 @@ struct oscar_kv_handle {
         unsigned long long *pbuf = nullptr;
         const int nw = a.ncta * 12;
         if (prof) {
-            CK(cudaMalloc(&pbuf, sizeof(unsigned long long) * 9 * nw));
-            CK(cudaMemsetAsync(pbuf, 0, sizeof(unsigned long long) * 9 * nw, s));
+            CK(cudaMalloc(&pbuf, sizeof(unsigned long long) * 12 * nw));
+            CK(cudaMemsetAsync(pbuf, 0, sizeof(unsigned long long) * 12 * nw, s));
             a.prof = pbuf;
         }
         CK(launch_attention(dbits, a, s));
         ++last_launches;
         if (prof) {
-            std::vector<unsigned long long> hbuf(9 * nw);
+            std::vector<unsigned long long> hbuf(12 * nw);
             CK(cudaMemcpyAsync(hbuf.data(), pbuf, hbuf.size() * 8, cudaMemcpyDeviceToHost, s));
             CK(cudaStreamSynchronize(s));
-            double acc[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+            double acc[12] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
             double mx = 0;
             int cnt = 0;
             for (int w = 0; w < nw; ++w) {
-                if (hbuf[9 * w + 8] == 0) continue;
+                if (hbuf[12 * w + 8] == 0) continue;
                 ++cnt;
-                for (int i = 0; i < 9; ++i) acc[i] += (double)hbuf[9 * w + i];
-                mx = std::max(mx, (double)hbuf[9 * w + 8]);
+                for (int i = 0; i < 12; ++i) acc[i] += (double)hbuf[12 * w + i];
+                mx = std::max(mx, (double)hbuf[12 * w + 8]);
             }
             {
                 // per-CTA spread: slowest warp per CTA, min/max across CTAs
@@ -322,7 +322,7 @@ struct oscar_kv_handle {
                 for (int c = 0; c < a.ncta; ++c) {
                     double lo = 1e30, hi = 0;
                     for (int w = 0; w < 12; ++w) {
-                        const double t = (double)hbuf[9 * (c * 12 + w) + 8];
+                        const double t = (double)hbuf[12 * (c * 12 + w) + 8];
                         if (t == 0) continue;
                         lo = std::min(lo, t);
                         hi = std::max(hi, t);
@@ -340,9 +340,11 @@ struct oscar_kv_handle {
             if (cnt)
                 std::fprintf(stderr,
                              "OSCAR_PROF warps=%d avg cycles: wait %.0f qk %.0f softmax %.0f pv %.0f merge %.0f "
-                             "spin %.0f qprologue %.0f segtail %.0f total %.0f max %.0f\n",
+                             "spin %.0f qprologue %.0f segtail %.0f total %.0f max %.0f | merge parts: cta %.0f "
+                             "atomic %.0f final %.0f (sums over all warps / cnt*12)\n",
                              cnt, acc[0] / cnt, acc[1] / cnt, acc[2] / cnt, acc[3] / cnt, acc[4] / cnt, acc[5] / cnt,
-                             acc[6] / cnt, acc[7] / cnt, acc[8] / cnt, mx);
+                             acc[6] / cnt, acc[7] / cnt, acc[8] / cnt, mx, acc[9] / cnt * 12, acc[10] / cnt * 12,
+                             acc[11] / cnt * 12);
             cudaFree(pbuf);
         }
     }

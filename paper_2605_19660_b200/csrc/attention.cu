@@ -53,7 +53,7 @@ struct AttnCfg {
     static constexpr int NTHREADS = NCW * 32;
     static constexpr int QH_OFF = 0;                                  // per-warp q tiles
     static constexpr int SEG_OFF = QH_OFF + NCW * 8 * QH_STRIDE * 2;  // segcnt[4], segdone[4]
-    static constexpr int BAR_OFF = ((SEG_OFF + 2 * NSEGSLOT * 4 + 16 + 7) / 8) * 8;
+    static constexpr int BAR_OFF = ((SEG_OFF + 2 * NSEGSLOT * 4 + 7) / 8) * 8;
     // shared ring of NST stages: as many whole stages as fit in 227 KB
     static constexpr int NST = (232448 - BAR_OFF - 1024) / STAGE;
     static constexpr int CNT_OFF = BAR_OFF + NST * 8;  // consumed-round counter per stage
@@ -435,7 +435,6 @@ __global__ void __launch_bounds__(NCW_ * 32, 1) decode_attn_kernel(const AttnArg
     int *consumed = reinterpret_cast<int *>(smem + C::CNT_OFF);
     int *segcnt = reinterpret_cast<int *>(smem + C::SEG_OFF);   // arrivals per segment slot
     int *segdone = segcnt + NSEGSLOT;                           // merges completed per slot
-    int *next_unit = segdone + NSEGSLOT;                        // dynamic unit dispenser
     uint8_t *ring = smem + C::RING_OFF;
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -480,7 +479,6 @@ __global__ void __launch_bounds__(NCW_ * 32, 1) decode_attn_kernel(const AttnArg
             segcnt[i] = 0;
             st_volatile_shared(&segdone[i], 0);
         }
-        segdone[NSEGSLOT] = 0;  // dynamic unit dispenser
         fence_mbar_init();
         if (nunits > 0) {
             int64_t bh = start / nb, uidx = start % nb;
@@ -509,7 +507,6 @@ __global__ void __launch_bounds__(NCW_ * 32, 1) decode_attn_kernel(const AttnArg
     __half *qh = reinterpret_cast<__half *>(smem + C::QH_OFF) + warp * 8 * QH_STRIDE;  // private
     long long tmr[12] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
     const long long tk0 = a.prof ? clk() : 0;
-    int pend = -1;  // unit grabbed from the dispenser but not processed yet
 
     for (int64_t bh = seg_first; bh <= seg_last; ++bh) {
         const int k = (int)(bh - seg_first);
@@ -565,21 +562,12 @@ __global__ void __launch_bounds__(NCW_ * 32, 1) decode_attn_kernel(const AttnArg
         if (a.prof) tmr[6] += clk() - tq0;
 
         // ---- packed units of this segment: positions p = gidx - start, p % NCW == warp ----
-        // ---- packed units of this segment, handed out dynamically in ring order:
-        //      a warp that grabbed a unit of a later segment keeps it (pend) ----
         if (total > 0) {
-            const int seg_end = (int)(hi - start);
-            for (;;) {
-                if (pend < 0) {
-                    int p_ = 0;
-                    if (lane == 0) p_ = atomicAdd(next_unit, 1);
-                    pend = __shfl_sync(0xffffffffu, p_, 0);
-                }
-                if (pend >= seg_end) break;
-                const int p = pend;
-                pend = -1;
-                const int stg = p % C::NST;
-                const int round = p / C::NST;
+            const int64_t p0 = lo - start;
+            const int64_t first = p0 + ((warp - (int)(p0 % NCW)) + NCW) % NCW;
+            for (int64_t p = first; p < hi - start; p += NCW) {
+                const int stg = (int)(p % C::NST);
+                const int round = (int)(p / C::NST);
                 const long long ts0 = a.prof ? clk() : 0;
                 if (lane == 0)
                     while (ld_volatile_shared(&consumed[stg]) < round) {

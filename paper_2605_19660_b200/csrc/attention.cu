@@ -39,7 +39,7 @@ constexpr int MERGE_FLOATS = 8 * D + 16;  // per-warp partial: O[8][128], m[8], 
 constexpr float LOG2E = 1.4426950408889634f;
 constexpr float LN2 = 0.6931471805599453f;
 
-constexpr int NSEGSLOT = 4;    // per-warp partial slots (segments in flight per CTA)
+constexpr int MAXSEG_SMEM = 64;  // max segments (b, kv heads) per CTA range
 constexpr int NCW_MAX = 12;
 constexpr int QH_STRIDE = 136;  // padded fp16 row of the per-warp q tile (conflict-free; 16-B aligned rows)
 
@@ -52,8 +52,8 @@ struct AttnCfg {
     static constexpr int NCW = NCW_;  // warps per CTA, all consumers
     static constexpr int NTHREADS = NCW * 32;
     static constexpr int QH_OFF = 0;                                  // per-warp q tiles
-    static constexpr int SEG_OFF = QH_OFF + NCW * 8 * QH_STRIDE * 2;  // segcnt[4], segdone[4]
-    static constexpr int BAR_OFF = ((SEG_OFF + 2 * NSEGSLOT * 4 + 7) / 8) * 8;
+    static constexpr int SEG_OFF = QH_OFF + NCW * 8 * QH_STRIDE * 2;  // lastflag[MAXSEG_SMEM]
+    static constexpr int BAR_OFF = ((SEG_OFF + MAXSEG_SMEM * 4 + 7) / 8) * 8;
     // shared ring of NST stages: as many whole stages as fit in 227 KB
     static constexpr int NST = (232448 - BAR_OFF - 1024) / STAGE;
     static constexpr int CNT_OFF = BAR_OFF + NST * 8;  // consumed-round counter per stage
@@ -433,8 +433,6 @@ __global__ void __launch_bounds__(NCW_ * 32, 1) decode_attn_kernel(const AttnArg
     extern __shared__ __align__(1024) uint8_t smem[];
     uint64_t *full = reinterpret_cast<uint64_t *>(smem + C::BAR_OFF);
     int *consumed = reinterpret_cast<int *>(smem + C::CNT_OFF);
-    int *segcnt = reinterpret_cast<int *>(smem + C::SEG_OFF);   // arrivals per segment slot
-    int *segdone = segcnt + NSEGSLOT;                           // merges completed per slot
     uint8_t *ring = smem + C::RING_OFF;
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -474,10 +472,6 @@ __global__ void __launch_bounds__(NCW_ * 32, 1) decode_attn_kernel(const AttnArg
         for (int i = 0; i < C::NST; ++i) {
             mbar_init(&full[i], 1);
             st_volatile_shared(&consumed[i], 0);
-        }
-        for (int i = 0; i < NSEGSLOT; ++i) {
-            segcnt[i] = 0;
-            st_volatile_shared(&segdone[i], 0);
         }
         fence_mbar_init();
         if (nunits > 0) {
@@ -607,12 +601,7 @@ __global__ void __launch_bounds__(NCW_ * 32, 1) decode_attn_kernel(const AttnArg
 
         const long long te0 = a.prof ? clk() : 0;
         // ---- warp partial -> global slot (unnormalized O[h][c], m[h], l[h]) ----
-        const int sslot = k % NSEGSLOT;
-        if (lane == 0)
-            while (ld_volatile_shared(&segdone[sslot]) < k / NSEGSLOT) {  // slot reuse guard
-            }
-        __syncwarp();
-        float *slot = a.warp_part + (((int64_t)cta * NSEGSLOT + sslot) * NCW_MAX + warp) * MERGE_FLOATS;
+        float *slot = a.warp_part + (((int64_t)cta * a.maxseg + k) * NCW_MAX + warp) * MERGE_FLOATS;
         {
             float l0 = st.l[0], l1 = st.l[1];
 #pragma unroll
@@ -718,133 +707,115 @@ __global__ void __launch_bounds__(NCW_ * 32, 1) decode_attn_kernel(const AttnArg
             }
         }
 
-        // ---- arrive; the LAST warp of the CTA to finish this segment merges ----
-        int arrived = 0;
-        if (lane == 0) {
-            __threadfence_block();
-            arrived = atomicAdd(&segcnt[sslot], 1);
-        }
-        arrived = __shfl_sync(0xffffffffu, arrived, 0);
         if (a.prof) tmr[7] += clk() - te0;
-        if (arrived != NCW - 1) continue;  // not last: straight on to the next segment
-        const long long tm0 = a.prof ? clk() : 0;
-        __threadfence_block();
-        if (lane == 0) segcnt[sslot] = 0;
+    }
 
-        const float *wp = a.warp_part + ((int64_t)cta * NSEGSLOT + sslot) * NCW_MAX * MERGE_FLOATS;
-        int64_t first_cta = 0, last_cta = 0;
-        if (total > 0) {
-            first_cta = cta_of(bh * nb, total, a.ncta);
-            last_cta = cta_of((bh + 1) * nb - 1, total, a.ncta);
-        }
-        const int expected = (int)(last_cta - first_cta + 1);
+    // ======== end of the CTA's work: cooperative merges (all warps finish within
+    //          ~one unit of each other under the static round-robin schedule) ========
+    const long long tm0 = a.prof ? clk() : 0;
+    __syncthreads();
+    int *lastflag = reinterpret_cast<int *>(smem + C::SEG_OFF);  // [nseg] (segcnt area reused)
+    const int nseg = (int)(seg_last - seg_first + 1);
+    // (1) CTA partial per segment: warp-per-(segment, head), lane = 4-channel chunk
+    for (int item = warp; item < nseg * g; item += NCW) {
+        const int kk = item / g, h = item % g;
+        const int64_t bh = seg_first + kk;
+        const float *wp = a.warp_part + ((int64_t)cta * a.maxseg + kk) * NCW_MAX * MERGE_FLOATS;
+        int64_t first_cta = 0;
+        if (total > 0) first_cta = cta_of(bh * nb, total, a.ncta);
         const int pslot = (int)(total > 0 ? cta - first_cta : 0);
         float *po = a.part_o + ((int64_t)bh * a.maxp + pslot) * 8 * D;
         float *pml = a.part_ml + ((int64_t)bh * a.maxp + pslot) * 16;
-        {
-            // lane w < NCW holds warp w's (m[h], l[h]); one load round, then shuffles
-            float mw[8], lw[8];
-            {
-                const int w = lane < NCW ? lane : 0;
-                const float4 *ml = reinterpret_cast<const float4 *>(wp + w * MERGE_FLOATS + 8 * D);
-                const float4 m0 = ml[0], m1 = ml[1], l0 = ml[2], l1 = ml[3];
-                mw[0] = m0.x; mw[1] = m0.y; mw[2] = m0.z; mw[3] = m0.w;
-                mw[4] = m1.x; mw[5] = m1.y; mw[6] = m1.z; mw[7] = m1.w;
-                lw[0] = l0.x; lw[1] = l0.y; lw[2] = l0.z; lw[3] = l0.w;
-                lw[4] = l1.x; lw[5] = l1.y; lw[6] = l1.z; lw[7] = l1.w;
-                if (lane >= NCW) {
+        // lane w < NCW holds warp w's (m, l) of head h
+        const float mwv = lane < NCW ? wp[lane * MERGE_FLOATS + 8 * D + h] : -CUDART_INF_F;
+        const float lwv = lane < NCW ? wp[lane * MERGE_FLOATS + 8 * D + 8 + h] : 0.f;
+        float4 v[NCW];
 #pragma unroll
-                    for (int h = 0; h < 8; ++h) {
-                        mw[h] = -CUDART_INF_F;
-                        lw[h] = 0.f;
-                    }
-                }
-            }
+        for (int w = 0; w < NCW; ++w)  // all loads in flight at once
+            v[w] = *reinterpret_cast<const float4 *>(wp + w * MERGE_FLOATS + h * D + lane * 4);
+        float M = mwv;
 #pragma unroll
-            for (int h = 0; h < 8; ++h) {
-                if (h >= g) break;
-                float M = mw[h];
+        for (int o = 1; o < 32; o <<= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o));
+        const float fw = (mwv == -CUDART_INF_F) ? 0.f : fast_exp2(mwv - M);
+        const float L = warp_sum(lwv * fw);
+        float4 O = make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
-                for (int o = 1; o < 32; o <<= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o));
-                const float fw = (mw[h] == -CUDART_INF_F) ? 0.f : fast_exp2(mw[h] - M);  // lane w's factor
-                const float L = warp_sum(lw[h] * fw);
-                float4 v[NCW];
-#pragma unroll
-                for (int w = 0; w < NCW; ++w)  // all loads in flight at once
-                    v[w] = *reinterpret_cast<const float4 *>(wp + w * MERGE_FLOATS + h * D + lane * 4);
-                float4 O = make_float4(0.f, 0.f, 0.f, 0.f);
-#pragma unroll
-                for (int w = 0; w < NCW; ++w) {
-                    const float f = __shfl_sync(0xffffffffu, fw, w);
-                    if (f != 0.f) {  // skips empty partials (their O is never read as NaN*0)
-                        O.x += v[w].x * f;
-                        O.y += v[w].y * f;
-                        O.z += v[w].z * f;
-                        O.w += v[w].w * f;
-                    }
-                }
-                *reinterpret_cast<float4 *>(po + h * D + lane * 4) = O;
-                if (lane == 0) {
-                    pml[2 * h] = M;
-                    pml[2 * h + 1] = L;
-                }
+        for (int w = 0; w < NCW; ++w) {
+            const float f = __shfl_sync(0xffffffffu, fw, w);
+            if (f != 0.f) {
+                O.x += v[w].x * f;
+                O.y += v[w].y * f;
+                O.z += v[w].z * f;
+                O.w += v[w].w * f;
             }
         }
-        // the warp slots of this segment may be reused now
-        if (lane == 0) st_volatile_shared(&segdone[sslot], k / NSEGSLOT + 1);
-        __syncwarp();
-        const long long tmA = a.prof ? clk() : 0;
-        int prev = 0;
-        if (lane == 0) prev = atomic_add_acq_rel_gpu(&a.counters[bh], 1);  // publishes the partial
-        prev = __shfl_sync(0xffffffffu, prev, 0);
-        const long long tmB = a.prof ? clk() : 0;
-        if (a.prof) {
-            tmr[8] += tmA - tm0;
-            tmr[9] += tmB - tmA;
+        *reinterpret_cast<float4 *>(po + h * D + lane * 4) = O;
+        if (lane == 0) {
+            pml[2 * h] = M;
+            pml[2 * h + 1] = L;
         }
-        if (prev == expected - 1) {
-            // last CTA for this (b, kv head): merge the CTA partials -> output
-            const float *pmb = a.part_ml + (int64_t)bh * a.maxp * 16;
-            const float *pob = a.part_o + (int64_t)bh * a.maxp * 8 * D;
-            for (int h = 0; h < g; ++h) {
-                // lane s2 < expected holds CTA partial s2's (m, l)
-                float ms = -CUDART_INF_F, ls = 0.f;
-                for (int s2 = lane; s2 < expected; s2 += 32) {  // expected <= 32 in practice
-                    const float m2 = __ldcg(pmb + s2 * 16 + 2 * h), l2 = __ldcg(pmb + s2 * 16 + 2 * h + 1);
-                    const float Mx = fmaxf(ms, m2);
-                    const float fa = (ms == -CUDART_INF_F) ? 0.f : fast_exp2(ms - Mx);
-                    const float fb = (m2 == -CUDART_INF_F) ? 0.f : fast_exp2(m2 - Mx);
-                    ls = ls * fa + l2 * fb;
-                    ms = Mx;
-                }
-                float M = ms;
-#pragma unroll
-                for (int o = 1; o < 32; o <<= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o));
-                const float L = warp_sum((ms == -CUDART_INF_F) ? 0.f : ls * fast_exp2(ms - M));
-                float x[4] = {0.f, 0.f, 0.f, 0.f};
-                for (int s2 = 0; s2 < expected; ++s2) {
-                    const float m2 = __ldcg(pmb + s2 * 16 + 2 * h);
-                    const float4 v = __ldcg(reinterpret_cast<const float4 *>(pob + s2 * 8 * D + h * D + lane * 4));
-                    const float f = (m2 == -CUDART_INF_F) ? 0.f : fast_exp2(m2 - M);
-                    x[0] += v.x * f;
-                    x[1] += v.y * f;
-                    x[2] += v.z * f;
-                    x[3] += v.w * f;
-                }
-                const float inv = (L > 0.f) ? 1.f / L : 0.f;
-#pragma unroll
-                for (int e = 0; e < 4; ++e) x[e] *= inv;
-                if (a.rotate_v) fht128_warp(x, lane);  // explicit-V mode: rotate the output back
-                *reinterpret_cast<float4 *>(a.out + ((int64_t)b * a.Hq + kvh * g + h) * D + lane * 4) =
-                    make_float4(x[0], x[1], x[2], x[3]);
-                if (a.lse && lane == 0)
-                    a.lse[(int64_t)b * a.Hq + kvh * g + h] = (L > 0.f) ? (M + __log2f(L)) * LN2 : -CUDART_INF_F;
-            }
-            if (lane == 0) a.counters[bh] = 0;
-            if (a.prof) tmr[10] += clk() - tmB;
+    }
+    __syncthreads();
+    // (2) publish: one acq_rel ticket per segment (cumulative over the barrier)
+    if (threadIdx.x < nseg) {
+        const int64_t bh = seg_first + threadIdx.x;
+        int expected = 1;
+        if (total > 0) expected = (int)(cta_of((bh + 1) * nb - 1, total, a.ncta) - cta_of(bh * nb, total, a.ncta) + 1);
+        const int prev = atomic_add_acq_rel_gpu(&a.counters[bh], 1);
+        lastflag[threadIdx.x] = (prev == expected - 1) ? expected : 0;
+    }
+    __syncthreads();
+    if (a.prof) tmr[8] += clk() - tm0;
+    // (3) final merge for the (b, kv heads) this CTA completed last: warp-per-(segment, head)
+    for (int item = warp; item < nseg * g; item += NCW) {
+        const int kk = item / g, h = item % g;
+        const int expected = lastflag[kk];
+        if (expected == 0) continue;
+        const int64_t bh = seg_first + kk;
+        const int b = (int)(bh / a.Hkv), kvh = (int)(bh % a.Hkv);
+        const float *pmb = a.part_ml + (int64_t)bh * a.maxp * 16;
+        const float *pob = a.part_o + (int64_t)bh * a.maxp * 8 * D;
+        // lane s2 < expected holds CTA partial s2's (m, l)
+        float ms = -CUDART_INF_F, ls = 0.f;
+        for (int s2 = lane; s2 < expected; s2 += 32) {
+            const float m2 = __ldcg(pmb + s2 * 16 + 2 * h), l2 = __ldcg(pmb + s2 * 16 + 2 * h + 1);
+            const float Mx = fmaxf(ms, m2);
+            const float fa = (ms == -CUDART_INF_F) ? 0.f : fast_exp2(ms - Mx);
+            const float fb = (m2 == -CUDART_INF_F) ? 0.f : fast_exp2(m2 - Mx);
+            ls = ls * fa + l2 * fb;
+            ms = Mx;
         }
-        // current token -> residual ring (nobody reads slot r in this launch)
-        if (owns_tail && a.write_ring && a.kcur) {
+        float M = ms;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o));
+        const float L = warp_sum((ms == -CUDART_INF_F) ? 0.f : ls * fast_exp2(ms - M));
+        float x[4] = {0.f, 0.f, 0.f, 0.f};
+        for (int s2 = 0; s2 < expected; ++s2) {
+            const float m2 = __ldcg(pmb + s2 * 16 + 2 * h);
+            const float4 v = __ldcg(reinterpret_cast<const float4 *>(pob + s2 * 8 * D + h * D + lane * 4));
+            const float f = (m2 == -CUDART_INF_F) ? 0.f : fast_exp2(m2 - M);
+            x[0] += v.x * f;
+            x[1] += v.y * f;
+            x[2] += v.z * f;
+            x[3] += v.w * f;
+        }
+        const float inv = (L > 0.f) ? 1.f / L : 0.f;
+#pragma unroll
+        for (int e = 0; e < 4; ++e) x[e] *= inv;
+        if (a.rotate_v) fht128_warp(x, lane);  // explicit-V mode: rotate the output back
+        *reinterpret_cast<float4 *>(a.out + ((int64_t)b * a.Hq + kvh * g + h) * D + lane * 4) =
+            make_float4(x[0], x[1], x[2], x[3]);
+        if (a.lse && lane == 0)
+            a.lse[(int64_t)b * a.Hq + kvh * g + h] = (L > 0.f) ? (M + __log2f(L)) * LN2 : -CUDART_INF_F;
+        if (h == 0 && lane == 0) a.counters[bh] = 0;  // the ticket is complete: reset for the next launch
+    }
+    // (4) current token -> residual ring of the (b, kv heads) whose tail this CTA owns
+    if (a.write_ring && a.kcur) {
+        for (int kk = warp; kk < nseg; kk += NCW) {
+            const int64_t bh = seg_first + kk;
+            const bool owns_tail = total == 0 || ((bh + 1) * nb <= end);
+            if (!owns_tail) continue;
+            const int b = (int)(bh / a.Hkv), kvh = (int)(bh % a.Hkv);
             const uint2 *ks = reinterpret_cast<const uint2 *>(reinterpret_cast<const __nv_bfloat16 *>(a.kcur) +
                                                                ((int64_t)b * a.Hkv + kvh) * D);
             const uint2 *vs = reinterpret_cast<const uint2 *>(reinterpret_cast<const __nv_bfloat16 *>(a.vcur) +
@@ -854,8 +825,8 @@ __global__ void __launch_bounds__(NCW_ * 32, 1) decode_attn_kernel(const AttnArg
             reinterpret_cast<uint2 *>(reinterpret_cast<__nv_bfloat16 *>(a.ring_v) + (bh * R + a.r) * D)[lane] =
                 vs[lane];
         }
-        if (a.prof) tmr[4] += clk() - tm0;  // merge work (slot 4 reused until the end)
     }
+    if (a.prof) tmr[4] += clk() - tm0;
     if (a.prof && lane == 0) {
         // per-warp phase cycles: [wait, qk, softmax, pv, merge, spin, qprologue, segtail]; total in slot 4 of the
         // host view is replaced below by the whole-kernel cycles
@@ -910,7 +881,7 @@ int attention_grid(int bits, int num_sms, int64_t nb, int BH) {
 }
 
 int64_t attention_scratch_floats(int max_ctas) {
-    return (int64_t)max_ctas * NSEGSLOT * NCW_MAX * MERGE_FLOATS;
+    return (int64_t)max_ctas * NCW_MAX * MERGE_FLOATS;  // per segment slot
 }
 
 int attention_max_partials(int64_t nb, int BH, int ncta) {

@@ -111,6 +111,7 @@ struct oscar_kv_handle {
     int *counters = nullptr;
     float *warp_part = nullptr;
     int maxp_alloc = 0;
+    int maxseg_alloc = 1;
     void *stage = nullptr;  // host-API staging: q, k, v, out, lse
     int64_t device_bytes = 0;
     int last_launches = 0;
@@ -249,6 +250,7 @@ struct oscar_kv_handle {
         a.part_ml = part_ml;
         a.counters = counters;
         a.warp_part = warp_part;
+        a.maxseg = maxseg_alloc;
         {
             static int pf = -1;
             if (pf < 0) {
@@ -261,12 +263,23 @@ struct oscar_kv_handle {
         a.maxp = maxp_alloc;
         // exact partial-slot requirement
         if (a.nb > 0) {
-            const int64_t total = a.nb * a.BH;
+            const int64_t nbs = a.nb * (dbits == 0 ? 4 : 1);  // pipeline units per (b, kv head)
+            const int64_t total = nbs * a.BH;
             auto cta_of = [&](int64_t x) { return ((x + 1) * a.ncta - 1) / total; };
             int64_t need = 0;
             for (int64_t bh = 0; bh < a.BH; ++bh)
-                need = std::max(need, cta_of((bh + 1) * a.nb - 1) - cta_of(bh * a.nb) + 1);
+                need = std::max(need, cta_of((bh + 1) * nbs - 1) - cta_of(bh * nbs) + 1);
             if (need > maxp_alloc) throw LogicErr("internal: partial buffer too small");
+            // segments per CTA range (units: nb blocks x SUB quarters for bf16)
+            const int64_t sub = dbits == 0 ? 4 : 1, nbu = a.nb * sub, totu = nbu * a.BH;
+            int64_t nseg = 0;
+            for (int64_t c = 0; c < a.ncta; ++c) {
+                const int64_t st = c * totu / a.ncta, en = (c + 1) * totu / a.ncta;
+                if (en > st) nseg = std::max(nseg, (en - 1) / nbu - st / nbu + 1);
+            }
+            if (nseg > maxseg_alloc) throw LogicErr("internal: too many segments per CTA");
+        } else {
+            a.maxseg = 1;  // residual-only mode: one segment per CTA
         }
         return a;
     }
@@ -567,8 +580,11 @@ int oscar_kv_create(const oscar_kv_config *cfg, int64_t batch, int64_t q_heads, 
         h->part_ml = (float *)h->dalloc(sizeof(float) * (size_t)(h->BH * h->maxp_alloc * 16));
         h->counters = (int *)h->dalloc(sizeof(int) * (size_t)h->BH);
         CK(cudaMemset(h->counters, 0, sizeof(int) * (size_t)h->BH));
-        h->warp_part = (float *)h->dalloc(sizeof(float) *
-                                          (size_t)attention_scratch_floats((int)std::max<int64_t>(h->num_sms, h->BH)));
+        // segments (b, kv heads) one CTA range can touch: <= BH/ncta + 2 (nb >= 1 unit)
+        h->maxseg_alloc = (int)std::min<int64_t>(64, h->BH / h->num_sms + 2);
+        h->warp_part = (float *)h->dalloc(
+            sizeof(float) * (size_t)attention_scratch_floats(
+                                (int)std::max<int64_t>((int64_t)h->num_sms * h->maxseg_alloc, h->BH)));
         const size_t stage_bytes = (size_t)(h->B * h->Hq * D * 2 + 2 * h->BH * D * 2 + h->B * h->Hq * D * 4 +
                                             h->B * h->Hq * 4 + 256);
         h->stage = h->dalloc(stage_bytes);

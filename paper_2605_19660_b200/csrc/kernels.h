@@ -59,7 +59,8 @@ struct AttnArgs {
     float *part_o;     // [BH][maxp][8][D]
     float *part_ml;    // [BH][maxp][8][2]
     int *counters;     // [BH], zero between launches
-    float *warp_part;  // [ncta][12][8*D+16] per-warp partial scratch
+    float *warp_part;  // [ncta][maxseg][12][8*D+16] per-warp partial scratch
+    int maxseg;        // segment slots per CTA in warp_part
     int maxp;
     int ncta;
     int pf_dist;       // L2 prefetch distance beyond the ring (units), 0 = off
@@ -68,7 +69,8 @@ struct AttnArgs {
 // bits: 2, 4 or 0 (bf16 baseline)
 cudaError_t launch_attention(int bits, const AttnArgs &a, cudaStream_t st);
 int attention_max_partials(int64_t nb, int BH, int ncta);
-int64_t attention_scratch_floats(int max_ctas);
+int64_t attention_scratch_floats(int max_ctas);  // floats per segment slot set
+int attention_max_segments(int64_t nb_units, int BH, int ncta);
 int attention_grid(int bits, int num_sms, int64_t nb, int BH);
 
 cudaError_t launch_lse_merge(const float *outs, const float *lses, int64_t parts, int64_t rows, int64_t d,

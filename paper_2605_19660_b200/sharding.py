@@ -1,0 +1,187 @@
+"""Multi-GPU launcher for the OScaR KV-cache path.
+
+One process per GPU (torch.distributed over NCCL for the plumbing).  Three
+partitionings, matching BASELINE.json configs 3-5:
+
+* batch sharding (C3): sequences [b0, b1) live on rank r, all KV heads --
+  no communication (the reference has no cross-sequence term);
+* head sharding (C4): KV heads [h0, h1) and their GQA query heads live on
+  rank r -- no communication (attend_one has no cross-head term,
+  pipeline.cpp:152-180; cache state is per head, kv_cache.hpp:111-116);
+* sequence sharding (C5): the context is cut into R-aligned token ranges so
+  that quantisation groups and R-blocks never straddle ranks (flush_k_block /
+  flush_v_block work on whole R-blocks, kv_cache.cpp:101-157); the residual
+  window and every appended token live on the tail rank, which therefore
+  flushes exactly when the single-cache reference would.  Each rank attends
+  its shard, the (O, LSE) partials are exchanged with ONE all-gather and
+  merged on device by the log-sum-exp merge kernel (oscar_lse_merge).
+
+The reference is single-process (no MPI/NCCL anywhere); these
+plans are new, but the union of the per-rank caches is bit-identical to the
+single cache the reference would build (tests/test_sharding_cpu.py checks that
+with the oracle).
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+R = 128
+D = 128
+
+
+# ----------------------------------------------------------------------------- plans
+def even_range(n: int, world: int, rank: int) -> tuple[int, int]:
+    """[lo, hi) of an even contiguous split of n items (sizes differ by <= 1)."""
+    if world <= 0 or not 0 <= rank < world:
+        raise ValueError(f"bad rank {rank} for world {world}")
+    return (rank * n) // world, ((rank + 1) * n) // world
+
+
+def batch_shard(B: int, world: int, rank: int) -> tuple[int, int]:
+    """Sequences of rank `rank` (C3)."""
+    return even_range(B, world, rank)
+
+
+@dataclass(frozen=True)
+class HeadShard:
+    kv_lo: int
+    kv_hi: int
+    q_lo: int
+    q_hi: int
+
+
+def head_shard(Hkv: int, Hq: int, world: int, rank: int) -> HeadShard:
+    """KV heads [kv_lo, kv_hi) and their GQA query heads (C4).  Query head j
+    attends KV head j // (Hq/Hkv), so a KV-head range owns a contiguous,
+    group-aligned query range."""
+    if Hq % Hkv:
+        raise ValueError("q_heads must be a multiple of kv heads")
+    if world > Hkv:
+        raise ValueError(f"head sharding needs world ({world}) <= kv heads ({Hkv})")
+    g = Hq // Hkv
+    lo, hi = even_range(Hkv, world, rank)
+    return HeadShard(lo, hi, lo * g, hi * g)
+
+
+@dataclass(frozen=True)
+class SeqShard:
+    tok_lo: int      # first context token of this rank
+    tok_hi: int      # one past the last prefill token of this rank
+    tail: bool       # owns the residual window and all appended tokens
+
+    @property
+    def tokens(self) -> int:
+        return self.tok_hi - self.tok_lo
+
+
+def sequence_shard(S: int, world: int, rank: int, R_: int = R) -> SeqShard:
+    """R-aligned token range of rank `rank` for a prefill of S tokens (C5).
+
+    The S - S mod R packed tokens are split in whole R-blocks (even split of
+    blocks); the S mod R residual tokens go to the last rank, exactly where
+    the single cache keeps them (kv_cache.cpp:204-218)."""
+    nblk = S // R_
+    b0, b1 = even_range(nblk, world, rank)
+    tail = rank == world - 1
+    return SeqShard(b0 * R_, S if tail else b1 * R_, tail)
+
+
+# ----------------------------------------------------------------------------- exchange
+def _dist():
+    import torch.distributed as td
+
+    return td
+
+
+def gather_partials(o, lse, group=None):
+    """All-gather this rank's (O [rows, d] fp32, LSE [rows] fp32) partial.
+
+    Both are packed into one [rows, d+1] buffer so the exchange is ONE
+    collective (latency-bound: C5 moves 14.4 KB per rank per layer).  Returns
+    (outs [P, rows, d], lses [P, rows]) on o's device.  Works on NCCL (CUDA
+    tensors) and gloo (CPU tensors, the multi-process CPU tests)."""
+    import torch
+
+    td = _dist()
+    P = td.get_world_size(group)
+    rows, d = o.shape
+    buf = torch.cat([o.reshape(rows, d), lse.reshape(rows, 1)], dim=1).contiguous()
+    if td.get_backend(group) == "nccl":
+        allb = torch.empty((P, rows, d + 1), dtype=buf.dtype, device=buf.device)
+        td.all_gather_into_tensor(allb, buf, group=group)
+    else:  # gloo: host staging (multi-process tests, several ranks sharing one GPU)
+        hb = buf.cpu()
+        parts = [torch.empty_like(hb) for _ in range(P)]
+        td.all_gather(parts, hb, group=group)
+        allb = torch.stack(parts).to(buf.device)
+    return allb[:, :, :d].contiguous(), allb[:, :, d].contiguous()
+
+
+# ----------------------------------------------------------------------------- sharded caches
+class SeqShardedKvCache:
+    """One rank's share of a sequence-sharded cache (C5).
+
+    Every rank calls the same methods in the same order (SPMD).  prefill()
+    takes the FULL context tensors [B, S, H, d] or just this rank's slice
+    (pass `sliced=True`); decode_step() returns the merged attention output of
+    the whole context (+ current token) on every rank.
+    """
+
+    def __init__(self, cfg, batch: int, q_heads: int, max_tokens_per_rank: int, device: int = 0,
+                 keep_exact: bool = True, group=None, merge=None):
+        from .kv_cache import KvCache, lse_merge
+
+        td = _dist()
+        self.group = group
+        self.world = td.get_world_size(group)
+        self.rank = td.get_rank(group)
+        self.B, self.Hq = batch, q_heads
+        self.cache = KvCache(cfg, batch=batch, q_heads=q_heads, max_tokens=max_tokens_per_rank, device=device,
+                             keep_exact=keep_exact)
+        self.shard = None
+        self._merge = merge or (lambda outs, lses: lse_merge(outs, lses))
+
+    def prefill(self, k, v, S: int | None = None, sliced: bool = False, stream=None):
+        S = k.shape[1] if S is None else S
+        self.shard = sequence_shard(S, self.world, self.rank)
+        if not sliced:
+            k = k[:, self.shard.tok_lo:self.shard.tok_hi].contiguous()
+            v = v[:, self.shard.tok_lo:self.shard.tok_hi].contiguous()
+        self.cache.buffer_quant(k, v, stream=stream)
+
+    def local_partial(self, q, k=None, v=None, stream=None):
+        """(O [B*Hq, d], LSE [B*Hq]) of this rank's shard; the tail rank also
+        attends the current token and appends it (decode_step ordering)."""
+        import torch
+
+        rows = self.B * self.Hq
+        dev = q.device
+        out = torch.empty((rows, D), dtype=torch.float32, device=dev)
+        lse = torch.empty((rows,), dtype=torch.float32, device=dev)
+        if self.shard is not None and self.shard.tail and k is not None:
+            self.cache.decode_step(q, k, v, out=out, lse=lse, stream=stream)
+        elif self.cache.total_tokens > 0:
+            self.cache.attend(q, out=out, lse=lse, stream=stream)
+        else:  # an empty shard contributes nothing to the softmax
+            out.zero_()
+            lse.fill_(float("-inf"))
+        return out, lse
+
+    def decode_step(self, q, k, v, stream=None):
+        o, l = self.local_partial(q, k, v, stream=stream)
+        outs, lses = gather_partials(o, l, self.group)
+        return self._merge(outs, lses).reshape(self.B, self.Hq, D)
+
+    @property
+    def total_tokens(self) -> int:
+        import torch
+
+        td = _dist()
+        t = torch.tensor([self.cache.total_tokens], dtype=torch.int64)
+        if td.get_backend(self.group) == "nccl":
+            t = t.cuda()
+        td.all_reduce(t, group=self.group)
+        return int(t.item())
+
+    def close(self):
+        self.cache.close()

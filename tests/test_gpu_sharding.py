@@ -1,0 +1,109 @@
+"""Multi-rank paths through the CUDA library.
+
+The GPU box has one B200, so the SPMD code runs as two gloo ranks sharing
+cuda:0 (NCCL refuses two ranks on one device); the exchange is the same
+gather_partials call the NCCL launcher makes, the merge is the device
+log-sum-exp kernel.  Reference semantics: the sharded result must equal one
+cache holding the whole context (fp32 merge rounding only)."""
+import os
+import socket
+
+import numpy as np
+import pytest
+
+from gpu_util import dev_bf16, rel_err
+
+pytestmark = pytest.mark.gpu
+
+S, H, G_, STEPS = 1000, 2, 4, 30  # residual 104 -> the 24th decode step flushes on the tail rank
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _inputs():
+    from paper_2605_19660_b200.synthetic import make_inputs, make_queries
+
+    k, v = make_inputs(77, S + STEPS, H)
+    q = make_queries(77, STEPS, H * G_)
+    return k, v, q
+
+
+def _seq_worker(rank, world, port, res_path):
+    import torch
+    import torch.distributed as td
+
+    from paper_2605_19660_b200 import PipelineConfig
+    from paper_2605_19660_b200.sharding import SeqShardedKvCache
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(0)
+    td.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        k, v, q = _inputs()
+        c = SeqShardedKvCache(PipelineConfig(heads=H), batch=1, q_heads=H * G_, max_tokens_per_rank=S + STEPS)
+        c.prefill(dev_bf16(k[None, :S]), dev_bf16(v[None, :S]))
+        outs = []
+        for t in range(STEPS):
+            o = c.decode_step(dev_bf16(q[t][None]), dev_bf16(k[S + t][None]), dev_bf16(v[S + t][None]))
+            outs.append(o.cpu().numpy())
+        tot = c.total_tokens
+        if rank == 0:
+            np.save(res_path, np.stack(outs))
+        assert tot == S + STEPS
+        c.close()
+    finally:
+        td.destroy_process_group()
+
+
+def test_sequence_sharded_decode_matches_single_cache(tmp_path):
+    import torch.multiprocessing as mp
+
+    from paper_2605_19660_b200 import KvCache, PipelineConfig
+
+    res = str(tmp_path / "seq.npy")
+    mp.spawn(_seq_worker, args=(2, _free_port(), res), nprocs=2, join=True)
+    sharded = np.load(res)
+    k, v, q = _inputs()
+    c = KvCache(PipelineConfig(heads=H), batch=1, q_heads=H * G_, max_tokens=S + STEPS)
+    c.buffer_quant(dev_bf16(k[None, :S]), dev_bf16(v[None, :S]))
+    for t in range(STEPS):
+        o = c.decode_step(dev_bf16(q[t][None]), dev_bf16(k[S + t][None]), dev_bf16(v[S + t][None])).cpu().numpy()
+        assert rel_err(sharded[t], o) < 1e-5, t
+    assert c.flush_count == 1
+
+
+def test_head_sharded_equals_full_heads():
+    """KV heads [h0, h1) + their query heads on their own cache == the same
+    heads of the full cache (C4 partitioning, no communication)."""
+    import torch
+
+    from paper_2605_19660_b200 import KvCache, PipelineConfig
+    from paper_2605_19660_b200.sharding import head_shard
+    from paper_2605_19660_b200.synthetic import make_inputs, make_queries
+
+    B, Hkv, g, Sx = 2, 4, 7, 700
+    data = [make_inputs(90 + b, Sx + 1, Hkv) for b in range(B)]
+    k = np.stack([d[0] for d in data])
+    v = np.stack([d[1] for d in data])
+    q = np.stack([make_queries(90 + b, 1, Hkv * g)[0] for b in range(B)])
+    full = KvCache(PipelineConfig(heads=Hkv), batch=B, q_heads=Hkv * g, max_tokens=Sx + 4)
+    full.buffer_quant(dev_bf16(k[:, :Sx]), dev_bf16(v[:, :Sx]))
+    of = full.decode_step(dev_bf16(q), dev_bf16(k[:, Sx]), dev_bf16(v[:, Sx])).cpu().numpy()
+    for rank in range(2):
+        hs = head_shard(Hkv, Hkv * g, 2, rank)
+        c = KvCache(PipelineConfig(heads=hs.kv_hi - hs.kv_lo), batch=B, q_heads=hs.q_hi - hs.q_lo,
+                    max_tokens=Sx + 4)
+        c.buffer_quant(dev_bf16(k[:, :Sx, hs.kv_lo:hs.kv_hi]), dev_bf16(v[:, :Sx, hs.kv_lo:hs.kv_hi]))
+        o = c.decode_step(dev_bf16(q[:, hs.q_lo:hs.q_hi]), dev_bf16(k[:, Sx, hs.kv_lo:hs.kv_hi]),
+                          dev_bf16(v[:, Sx, hs.kv_lo:hs.kv_hi])).cpu().numpy()
+        torch.cuda.synchronize()
+        assert rel_err(o, of[:, hs.q_lo:hs.q_hi]) < 1e-5
+        # the packed blocks are the full cache's blocks, bit for bit
+        ef, eh = full.export(1), c.export(1)
+        for key in ("k_payload", "v_payload", "k_delta", "k_zp", "v_delta", "v_zp", "k_norms"):
+            assert np.array_equal(eh[key], ef[key][hs.kv_lo:hs.kv_hi]), key

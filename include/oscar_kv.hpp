@@ -1,0 +1,131 @@
+// oscar_kv.hpp -- header-only C++ host wrapper over the C-ABI (oscar_kv.h)
+// that re-exposes the reference's class and method names
+// (/root/reference/proj/include/oscar/kv_cache.hpp:61-123) and its exception
+// types (std::invalid_argument / std::logic_error / std::runtime_error), so
+// reference call sites change only their include and constructor arguments.
+// See INTEGRATION.md.
+#pragma once
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "oscar_kv.h"
+
+namespace oscar_b200 {
+
+// status -> the reference's exception types (kv_cache.cpp:51-67, 225-227, 471)
+inline void check(int rc) {
+    if (rc == 0) return;
+    const std::string msg = oscar_last_error();
+    if (rc == 1) throw std::invalid_argument(msg);
+    if (rc == 2) throw std::logic_error(msg);
+    throw std::runtime_error(msg);
+}
+
+enum class Method : int32_t { Fp = OSCAR_FP, Kivi = OSCAR_KIVI, RotateOnly = OSCAR_ROTATE_ONLY,
+                              ScaleOnly = OSCAR_SCALE_ONLY, Oscar = OSCAR_OSCAR };
+enum class Scaling : int32_t { L2 = OSCAR_L2, Rsqrt = OSCAR_RSQRT, Max = OSCAR_MAX, MeanAbs = OSCAR_MEAN_ABS };
+
+// PipelineConfig (kv_cache.hpp:19-32) with the same defaults, plus rotate_v.
+struct PipelineConfig {
+    Method method = Method::Oscar;
+    int bits = 2;
+    int64_t group_size = 32;
+    int64_t residual_len = 128;
+    Scaling scaling = Scaling::L2;
+    int64_t head_dim = 128;
+    int64_t heads = 1;
+    bool rotate_v = false;
+
+    oscar_kv_config c() const {
+        oscar_kv_config x{};
+        x.method = static_cast<int32_t>(method);
+        x.bits = bits;
+        x.group_size = group_size;
+        x.residual_len = residual_len;
+        x.scaling = static_cast<int32_t>(scaling);
+        x.rotate_v = rotate_v ? 1 : 0;
+        x.head_dim = head_dim;
+        x.heads = heads;
+        return x;
+    }
+    void validate() const {  // PipelineConfig::validate (kv_cache.cpp:51-67)
+        const oscar_kv_config x = c();
+        check(oscar_kv_config_validate(&x));
+    }
+};
+
+// Device KvCache for `batch` sequences x cfg.heads KV heads.  Single writer
+// (kv_cache.hpp:58-60); every call enqueues on `stream` (a cudaStream_t).
+class KvCache {
+public:
+    KvCache(const PipelineConfig &cfg, int64_t batch, int64_t q_heads, int64_t max_tokens, int device = 0,
+            bool keep_exact = true)
+        : cfg_(cfg) {
+        const oscar_kv_config x = cfg.c();
+        check(oscar_kv_create(&x, batch, q_heads, max_tokens, device, keep_exact ? 1 : 0, &h_));
+    }
+    KvCache(const KvCache &) = delete;
+    KvCache &operator=(const KvCache &) = delete;
+    KvCache(KvCache &&o) noexcept : cfg_(o.cfg_), h_(std::exchange(o.h_, nullptr)) {}
+    ~KvCache() {
+        if (h_) oscar_kv_destroy(h_);
+    }
+
+    // buffer_quant_k + buffer_quant_v (kv_cache.cpp:194-292) on RAW bf16 keys
+    // [batch, n, heads, d]: the key transform of apply_method runs on device.
+    void buffer_quant(const void *k, const void *v, int64_t n_tokens, void *stream = nullptr) {
+        check(oscar_kv_append(h_, k, v, n_tokens, stream));
+    }
+    // decode_step body (pipeline.cpp:292-323) without the projections.
+    void decode_step(const void *q, const void *k, const void *v, float *out, float *lse = nullptr,
+                     void *stream = nullptr) {
+        check(oscar_kv_decode_step(h_, q, k, v, out, lse, stream));
+    }
+    void attend(const void *q, float *out, float *lse, void *stream = nullptr) {
+        check(oscar_kv_attend(h_, q, out, lse, stream));
+    }
+
+    int64_t packed_tokens() const { return stats().packed; }
+    int64_t residual_tokens() const { return stats().residual; }
+    int64_t total_tokens() const {
+        const Stats s = stats();
+        return s.packed + s.residual;
+    }
+    int64_t flush_count() const { return stats().flushes; }
+
+    oscar_kv_memory_report_t memory_report() const {
+        oscar_kv_memory_report_t r{};
+        check(oscar_kv_memory_report(h_, &r));
+        return r;
+    }
+    // KvCache::dump (kv_cache.cpp:469-507) of sequence b
+    void dump(int64_t b, const std::string &path) { check(oscar_kv_dump(h_, b, path.c_str())); }
+    // materialize_k / materialize_v (kv_cache.cpp:327-381) of sequence b, fp64 [total, H, d]
+    std::pair<std::vector<double>, std::vector<double>> materialize(int64_t b) {
+        const size_t n = (size_t)(total_tokens() * cfg_.heads * cfg_.head_dim);
+        std::vector<double> k(n), v(n);
+        check(oscar_kv_materialize(h_, b, k.data(), v.data()));
+        return {std::move(k), std::move(v)};
+    }
+
+    oscar_kv_handle *handle() const { return h_; }
+    const PipelineConfig &config() const { return cfg_; }
+
+private:
+    struct Stats {
+        int64_t packed = 0, residual = 0, flushes = 0;
+    };
+    Stats stats() const {
+        Stats s;
+        check(oscar_kv_stats(h_, &s.packed, &s.residual, &s.flushes));
+        return s;
+    }
+    PipelineConfig cfg_;
+    oscar_kv_handle *h_ = nullptr;
+};
+
+}  // namespace oscar_b200

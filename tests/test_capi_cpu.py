@@ -42,3 +42,39 @@ def test_config_validation_without_gpu():
                 dict(bits=3), dict(head_dim=64)):
         with pytest.raises(ValueError):
             PipelineConfig(**bad).validate()
+
+
+CPP_PROGRAM = r"""
+#include <cstdio>
+#include "oscar_kv.hpp"
+int main() {
+    oscar_b200::PipelineConfig pc;
+    pc.heads = 8;
+    pc.validate();
+    int caught = 0;
+    try { pc.residual_len = 100; pc.validate(); } catch (const std::invalid_argument &) { caught = 1; }
+    std::printf("ok %d\n", caught);
+    return caught ? 0 : 1;
+}
+"""
+
+
+def test_cpp_wrapper_compiles_and_validates(tmp_path):
+    """a reference-side C++ caller builds against
+    include/oscar_kv.hpp, links the library and gets the reference's
+    exception type from PipelineConfig::validate (kv_cache.cpp:51-67)."""
+    import shutil
+    import subprocess
+
+    if not os.path.exists(LIB):
+        pytest.skip("library not built")
+    if shutil.which("g++") is None:
+        pytest.skip("no g++")
+    src = tmp_path / "caller.cpp"
+    src.write_text(CPP_PROGRAM)
+    exe = tmp_path / "caller"
+    libdir = os.path.dirname(LIB)
+    subprocess.run(["g++", "-std=c++17", "-I", os.path.join(ROOT, "include"), str(src), "-o", str(exe),
+                    "-L", libdir, "-loscar_b200", f"-Wl,-rpath,{libdir}"], check=True)
+    out = subprocess.run([str(exe)], capture_output=True, text=True, check=True).stdout
+    assert out.strip() == "ok 1"

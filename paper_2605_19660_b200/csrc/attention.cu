@@ -35,12 +35,12 @@ namespace osk {
 
 namespace {
 
-constexpr int MERGE_FLOATS = 8 * D + 16;  // per-warp partial: O[8][128], m[8], l[8]
+constexpr int MERGE_FLOATS = 8 * D + 16 + D;  // per-warp partial: O[8][128], m[8], l[8] + 128 scratch
 constexpr float LOG2E = 1.4426950408889634f;
 constexpr float LN2 = 0.6931471805599453f;
 
 constexpr int MAXSEG_SMEM = 64;  // max segments (b, kv heads) per CTA range
-constexpr int NCW_MAX = 12;
+constexpr int NCW_MAX = 16;
 constexpr int QH_STRIDE = 136;  // padded fp16 row of the per-warp q tile (conflict-free; 16-B aligned rows)
 
 template <int BITS, int NCW_ = ((BITS == 4) ? 8 : 12)>
@@ -151,13 +151,12 @@ __device__ __forceinline__ void process_block(const uint8_t *__restrict__ sb, Wa
     constexpr uint32_t FMASK = (BITS == 2) ? 0x00030003u : 0x000F000Fu;
     const int gq = lane >> 2, tq = lane & 3;
 
-    // ---- key zero points as A (row gq = group): bias[grp][head] =
-    //      sum_c nz[c,grp] * B[grp][c][head], B = Qrot*step -- the SAME fp16 B as the
-    //      code MMA, so dot = sum_c B*(code - zp) is consistent
-    // lane gq < 4 holds row gq (= group); rows 4..15 are zero
+    // ---- key offsets as A (row gq = group): bias[grp][head] = sum_c b[c,grp] * Qrot[head][c]
+    //      (x = a*code + b, the value form of dequantize_one, quant.cpp:65-68) -- one
+    //      MMA per k-step; lane gq < 4 holds row gq (= group); rows 4..15 are zero
     const uint2 *bkp = reinterpret_cast<const uint2 *>(sb + Blk::KB_OFF + ((gq & 3) * 4 + tq) * 64);
     const uint32_t bkmask = gq < 4 ? 0xffffffffu : 0u;
-    float kbias[4][4];
+    float kbias[4];
 
     // ---- QK^T --------------------------------------------------------------------
     float sacc[8][4];
@@ -193,11 +192,8 @@ __device__ __forceinline__ void process_block(const uint8_t *__restrict__ sb, Wa
         {
             const uint2 z = bkp[s];
             const uint32_t z0 = z.x & bkmask, z1 = z.y & bkmask;
-#pragma unroll
-            for (int grp = 0; grp < 4; ++grp) {
-                if (s == 0) mma16816_zc(kbias[grp], z0, 0u, z1, 0u, bq[grp][0], bq[grp][1]);
-                else mma16816(kbias[grp], z0, 0u, z1, 0u, bq[grp][0], bq[grp][1]);
-            }
+            if (s == 0) mma16816_zc(kbias, z0, 0u, z1, 0u, qf[s][0], qf[s][1]);
+            else mma16816(kbias, z0, 0u, z1, 0u, qf[s][0], qf[s][1]);
         }
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
@@ -232,8 +228,8 @@ __device__ __forceinline__ void process_block(const uint8_t *__restrict__ sb, Wa
     float kb0[4], kb1[4];
 #pragma unroll
     for (int grp = 0; grp < 4; ++grp) {
-        kb0[grp] = __shfl_sync(0xffffffffu, kbias[grp][0], grp * 4 + tq);
-        kb1[grp] = __shfl_sync(0xffffffffu, kbias[grp][1], grp * 4 + tq);
+        kb0[grp] = __shfl_sync(0xffffffffu, kbias[0], grp * 4 + tq);
+        kb1[grp] = __shfl_sync(0xffffffffu, kbias[1], grp * 4 + tq);
     }
     float bm0 = -CUDART_INF_F, bm1 = -CUDART_INF_F;
 #pragma unroll
@@ -425,6 +421,152 @@ __device__ __forceinline__ void process_quarter_bf16(const uint8_t *__restrict__
     }
 }
 
+// One 16-token tile [t0, t0+16) of the residual window (+ the current token at
+// index r) for one (b, kv head), merged into the warp's partial slot.
+//   QK^T: D[token, head] = sum_c K[token, c] q[head, c]    A = K rows (ring, row-major)
+//   P.V : D[chan, head]  = sum_t V^T[chan, t] P[head, t]   A = V^T rows (ring, channel-major)
+// Invalid tokens (>= ntok) get -inf logits and zero V; the ring is read
+// through L2 (written by the previous steps).
+struct ResidualRefs {
+    const uint16_t *ringk, *ringv;  // this (b, kv head)'s rings
+    const uint16_t *kc, *vc;        // current token or null
+    int g, r, rotate_v;
+};
+
+__device__ __noinline__ void residual_tile(const ResidualRefs rr, float *slot, const __nv_bfloat16 *qbase, int t0,
+                                           int ntok, int lane, float c0) {
+    const int gq = lane >> 2, tq = lane & 3;
+    const int g = rr.g, r = rr.r;
+    const uint16_t *ringk = rr.ringk, *ringv = rr.ringv, *kc = rr.kc, *vc = rr.vc;
+    // token rows of this lane's A fragments: t0 + gq, t0 + gq + 8
+    const int tA = t0 + gq, tB = tA + 8;
+    auto krow = [&](int t) -> const uint16_t * {
+        if (t < r) return ringk + (int64_t)t * D;
+        if (t < ntok) return kc;  // t == r: the current token
+        return nullptr;
+    };
+    const uint16_t *kA = krow(tA), *kB = krow(tB);
+    auto ld32 = [](const uint16_t *p, int c) -> uint32_t {
+        return p ? *reinterpret_cast<const uint32_t *>(p + c) : 0u;
+    };
+    // ---- QK^T (raw bf16 q as B: lane holds q[head gq][16s + 2tq (+1), +8 (+9)]) ----
+    float sacc[4] = {0.f, 0.f, 0.f, 0.f};
+    const uint16_t *qrow = gq < g ? reinterpret_cast<const uint16_t *>(qbase) + gq * D : nullptr;
+#pragma unroll
+    for (int s = 0; s < 8; ++s) {
+        const int c = 16 * s + 2 * tq;
+        mma16816_bf16(sacc, ld32(kA, c), ld32(kB, c), ld32(kA, c + 8), ld32(kB, c + 8), ld32(qrow, c),
+                      ld32(qrow, c + 8));
+    }
+    // logits in log2 units; rows gq / gq+8 = tokens tA / tB; cols 2tq, 2tq+1 = heads
+    const bool vA = tA < ntok, vB = tB < ntok;
+    sacc[0] = vA ? sacc[0] * c0 : -CUDART_INF_F;
+    sacc[1] = vA ? sacc[1] * c0 : -CUDART_INF_F;
+    sacc[2] = vB ? sacc[2] * c0 : -CUDART_INF_F;
+    sacc[3] = vB ? sacc[3] * c0 : -CUDART_INF_F;
+    float m0 = fmaxf(sacc[0], sacc[2]), m1 = fmaxf(sacc[1], sacc[3]);
+#pragma unroll
+    for (int o = 4; o < 32; o <<= 1) {
+        m0 = fmaxf(m0, __shfl_xor_sync(0xffffffffu, m0, o));
+        m1 = fmaxf(m1, __shfl_xor_sync(0xffffffffu, m1, o));
+    }
+    sacc[0] = fast_exp2(sacc[0] - m0);
+    sacc[1] = fast_exp2(sacc[1] - m1);
+    sacc[2] = fast_exp2(sacc[2] - m0);
+    sacc[3] = fast_exp2(sacc[3] - m1);
+    float l0 = sacc[0] + sacc[2], l1 = sacc[1] + sacc[3];
+#pragma unroll
+    for (int o = 4; o < 32; o <<= 1) {
+        l0 += __shfl_xor_sync(0xffffffffu, l0, o);
+        l1 += __shfl_xor_sync(0xffffffffu, l1, o);
+    }
+    // ---- P as the B operand: lane (gq, tq) needs P[head gq][tokens 2tq, 2tq+1, 2tq+8, 2tq+9],
+    //      held by lanes (2tq, gq/2) and (2tq+1, gq/2) in accumulator layout ----
+    const uint32_t X = pack_bf162(sacc[0], sacc[1]), Y = pack_bf162(sacc[2], sacc[3]);
+    const int sa = (2 * tq) * 4 + (gq >> 1), sbl = (2 * tq + 1) * 4 + (gq >> 1);
+    const uint32_t xa = __shfl_sync(0xffffffffu, X, sa), ya = __shfl_sync(0xffffffffu, Y, sa);
+    const uint32_t xb = __shfl_sync(0xffffffffu, X, sbl), yb = __shfl_sync(0xffffffffu, Y, sbl);
+    const uint32_t sel = (gq & 1) ? 0x7632u : 0x5410u;
+    const uint32_t b0 = __byte_perm(xa, xb, sel), b1 = __byte_perm(ya, yb, sel);
+    // ---- P.V: A = V^T [16 channels x 16 tokens] from the channel-major ring ----
+    const int u0 = t0 + 2 * tq, u1 = u0 + 8;  // token pairs (u0, u0+1), (u1, u1+1) of this lane
+    auto vpair = [&](int c, int u) -> uint32_t {
+        uint32_t w = (u + 1 < r) ? *reinterpret_cast<const uint32_t *>(ringv + (int64_t)c * R + u) : 0u;
+        if (u + 1 >= r && u < ntok) {  // tail of the window: per-token select ring / current / zero
+            const uint32_t lo = u < r ? ringv[(int64_t)c * R + u] : (u < ntok ? vc[c] : 0u);
+            const uint32_t hi = u + 1 < r ? ringv[(int64_t)c * R + u + 1] : (u + 1 < ntok ? vc[c] : 0u);
+            w = lo | (hi << 16);
+        }
+        return w;
+    };
+    float o[8][4];
+#pragma unroll
+    for (int mm = 0; mm < 8; ++mm) {
+        const int cA = 16 * mm + gq, cB = cA + 8;
+        o[mm][0] = o[mm][1] = o[mm][2] = o[mm][3] = 0.f;
+        mma16816_bf16(o[mm], vpair(cA, u0), vpair(cB, u0), vpair(cA, u1), vpair(cB, u1), b0, b1);
+    }
+    // ---- merge into the slot: O[h][c] unnormalised, m[h], l[h] (log2 units); in
+    //      explicit-V mode the packed partial lives in the rotated space, so this
+    //      (raw-V) partial is rotated head by head first ----
+    __syncwarp();
+    const int h0 = 2 * tq, h1 = h0 + 1;
+    const float ms0 = slot[8 * D + h0], ms1 = slot[8 * D + h1];
+    const float ls0 = slot[8 * D + 8 + h0], ls1 = slot[8 * D + 8 + h1];
+    const float M0 = fmaxf(ms0, m0), M1 = fmaxf(ms1, m1);
+    const float fs0 = (ms0 == -CUDART_INF_F) ? 0.f : fast_exp2(ms0 - M0);
+    const float fs1 = (ms1 == -CUDART_INF_F) ? 0.f : fast_exp2(ms1 - M1);
+    const float fr0 = fast_exp2(m0 - M0), fr1 = fast_exp2(m1 - M1);
+    if (!rr.rotate_v) {
+#pragma unroll
+        for (int mm = 0; mm < 8; ++mm) {
+            const int cA = 16 * mm + gq, cB = cA + 8;
+            slot[h0 * D + cA] = slot[h0 * D + cA] * fs0 + o[mm][0] * fr0;
+            slot[h1 * D + cA] = slot[h1 * D + cA] * fs1 + o[mm][1] * fr1;
+            slot[h0 * D + cB] = slot[h0 * D + cB] * fs0 + o[mm][2] * fr0;
+            slot[h1 * D + cB] = slot[h1 * D + cB] * fs1 + o[mm][3] * fr1;
+        }
+    } else {
+        // rescale the packed partial, then add the rotated residual partial head by head
+        float *part = slot + 8 * D + 16;  // 2 x 128 floats of scratch reserved after m/l
+#pragma unroll
+        for (int mm = 0; mm < 8; ++mm) {
+            const int cA = 16 * mm + gq, cB = cA + 8;
+            slot[h0 * D + cA] *= fs0;
+            slot[h1 * D + cA] *= fs1;
+            slot[h0 * D + cB] *= fs0;
+            slot[h1 * D + cB] *= fs1;
+        }
+        for (int h = 0; h < g; ++h) {
+            __syncwarp();
+            if ((h >> 1) == tq) {
+                const bool e = (h & 1) != 0;
+                const float f = e ? fr1 : fr0;
+#pragma unroll
+                for (int mm = 0; mm < 8; ++mm) {
+                    part[16 * mm + gq] = (e ? o[mm][1] : o[mm][0]) * f;
+                    part[16 * mm + gq + 8] = (e ? o[mm][3] : o[mm][2]) * f;
+                }
+            }
+            __syncwarp();
+            float x[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) x[e] = part[4 * lane + e];
+            fht128_warp(x, lane);
+#pragma unroll
+            for (int e = 0; e < 4; ++e) slot[h * D + 4 * lane + e] += x[e];
+        }
+    }
+    __syncwarp();
+    if (gq == 0) {
+        slot[8 * D + h0] = M0;
+        slot[8 * D + h1] = M1;
+        slot[8 * D + 8 + h0] = ls0 * fs0 + l0 * fr0;
+        slot[8 * D + 8 + h1] = ls1 * fs1 + l1 * fr1;
+    }
+    __syncwarp();
+}
+
 template <int BITS, int NCW_>
 __global__ void __launch_bounds__(NCW_ * 32, 1) decode_attn_kernel(const AttnArgs a) {
     using C = AttnCfg<BITS, NCW_>;
@@ -461,19 +603,21 @@ __global__ void __launch_bounds__(NCW_ * 32, 1) decode_attn_kernel(const AttnArg
                  &full[stg], pol);
     };
 
-    if (total > 0 ? nunits > 0 : cta < a.BH) {  // first segment's q goes out before the ring fill
-        const int64_t bh0 = total > 0 ? start / nb : cta;
-        qtile_prefetch(reinterpret_cast<__half *>(smem + C::QH_OFF) + warp * 8 * QH_STRIDE,
-                       reinterpret_cast<const __nv_bfloat16 *>(a.q) +
-                           ((int64_t)(bh0 / a.Hkv) * a.Hq + (bh0 % a.Hkv) * a.g) * D,
-                       a.g, lane);
-    }
+    // Programmatic dependent launch: the next decode step's CTAs may start as
+    // this grid's CTAs retire; each new CTA streams its first NST packed
+    // records into shared memory BEFORE waiting on this grid (the packed
+    // blocks are written only by the quantize kernel, and the host clears
+    // pdl_prefetch after a flush), then waits for the previous grid's
+    // completion + memory flush before touching q, the current token, the
+    // residual ring or any scratch the previous grid wrote.
+    griddep_launch_dependents();
     if (threadIdx.x == 0) {
         for (int i = 0; i < C::NST; ++i) {
             mbar_init(&full[i], 1);
             st_volatile_shared(&consumed[i], 0);
         }
         fence_mbar_init();
+        if (!a.pdl_prefetch) griddep_wait();
         if (nunits > 0) {
             int64_t bh = start / nb, uidx = start % nb;
             for (int64_t p = 0; p < nunits && p < C::NST; ++p) {
@@ -485,7 +629,15 @@ __global__ void __launch_bounds__(NCW_ * 32, 1) decode_attn_kernel(const AttnArg
             }
         }
     }
-    __syncthreads();  // the only CTA-wide barrier
+    griddep_wait();
+    if (total > 0 ? nunits > 0 : cta < a.BH) {  // first segment's q
+        const int64_t bh0 = total > 0 ? start / nb : cta;
+        qtile_prefetch(reinterpret_cast<__half *>(smem + C::QH_OFF) + warp * 8 * QH_STRIDE,
+                       reinterpret_cast<const __nv_bfloat16 *>(a.q) +
+                           ((int64_t)(bh0 / a.Hkv) * a.Hq + (bh0 % a.Hkv) * a.g) * D,
+                       a.g, lane);
+    }
+    __syncthreads();  // the only CTA-wide barrier before the end-of-work merges
 
     // segments: residual-only mode (nb == 0): CTA c <-> bh c
     int64_t seg_first, seg_last;
@@ -638,72 +790,22 @@ __global__ void __launch_bounds__(NCW_ * 32, 1) decode_attn_kernel(const AttnArg
             __syncwarp();
         }
 
-        // ---- residual window + current token (fp32 CUDA cores), merged into the slot ----
+        // ---- residual window + current token on the tensor cores (bf16 mma, raw q . raw k:
+        //      the key transform is orthonormal up to the stored norm, so attending the raw
+        //      bf16 rows IS attend_one over the full-precision residual, pipeline.cpp:152-180),
+        //      one 16-token tile per warp, merged into that warp's slot ----
         if (owns_tail) {
             const int ntok = a.r + (a.kcur ? 1 : 0);
-            if (warp < ntok) {
-                float qv[8][4];
-#pragma unroll
-                for (int j = 0; j < 8; ++j) {
-                    qv[j][0] = qv[j][1] = qv[j][2] = qv[j][3] = 0.f;
-                    if (j < g) load_bf16x4(qbase + j * D + lane * 4, qv[j]);
-                }
-                float mr[8], lr[8], orr[8][4];
-#pragma unroll
-                for (int j = 0; j < 8; ++j) {
-                    mr[j] = -CUDART_INF_F;
-                    lr[j] = 0.f;
-                    orr[j][0] = orr[j][1] = orr[j][2] = orr[j][3] = 0.f;
-                }
-                for (int t = warp; t < ntok; t += NCW) {
-                    const __nv_bfloat16 *kp, *vp;
-                    if (t < a.r) {
-                        kp = reinterpret_cast<const __nv_bfloat16 *>(a.ring_k) + (bh * R + t) * D;
-                        vp = reinterpret_cast<const __nv_bfloat16 *>(a.ring_v) + (bh * R + t) * D;
-                    } else {
-                        kp = reinterpret_cast<const __nv_bfloat16 *>(a.kcur) + ((int64_t)b * a.Hkv + kvh) * D;
-                        vp = reinterpret_cast<const __nv_bfloat16 *>(a.vcur) + ((int64_t)b * a.Hkv + kvh) * D;
-                    }
-                    float k4[4], v4[4];
-                    load_bf16x4(kp + lane * 4, k4);
-                    load_bf16x4(vp + lane * 4, v4);
-                    if (a.rotate_v) fht128_warp(v4, lane);
-#pragma unroll
-                    for (int j = 0; j < 8; ++j) {
-                        if (j < g) {
-                            float d = qv[j][0] * k4[0] + qv[j][1] * k4[1] + qv[j][2] * k4[2] + qv[j][3] * k4[3];
-                            d = warp_sum(d) * c0;
-                            const float mn = fmaxf(mr[j], d);
-                            const float al = fast_exp2(mr[j] - mn), pp = fast_exp2(d - mn);
-                            lr[j] = lr[j] * al + pp;
-#pragma unroll
-                            for (int e = 0; e < 4; ++e) orr[j][e] = orr[j][e] * al + pp * v4[e];
-                            mr[j] = mn;
-                        }
-                    }
-                }
-#pragma unroll
-                for (int j = 0; j < 8; ++j) {
-                    if (j < g) {
-                        const float ms = slot[8 * D + j], ls = slot[8 * D + 8 + j];
-                        const float M = fmaxf(ms, mr[j]);
-                        const float fs = (ms == -CUDART_INF_F) ? 0.f : fast_exp2(ms - M);
-                        const float fr = (mr[j] == -CUDART_INF_F) ? 0.f : fast_exp2(mr[j] - M);
-                        float4 *op = reinterpret_cast<float4 *>(slot + j * D + lane * 4);
-                        float4 ov = *op;
-                        ov.x = ov.x * fs + orr[j][0] * fr;
-                        ov.y = ov.y * fs + orr[j][1] * fr;
-                        ov.z = ov.z * fs + orr[j][2] * fr;
-                        ov.w = ov.w * fs + orr[j][3] * fr;
-                        *op = ov;
-                        __syncwarp();
-                        if (lane == 0) {
-                            slot[8 * D + j] = M;
-                            slot[8 * D + 8 + j] = ls * fs + lr[j] * fr;
-                        }
-                    }
-                }
-                __syncwarp();
+            if (warp * 16 < ntok) {
+                ResidualRefs rr;
+                rr.ringk = reinterpret_cast<const uint16_t *>(a.ring_k) + bh * R * D;
+                rr.ringv = reinterpret_cast<const uint16_t *>(a.ring_v) + bh * R * D;
+                rr.kc = a.kcur ? reinterpret_cast<const uint16_t *>(a.kcur) + ((int64_t)b * a.Hkv + kvh) * D : nullptr;
+                rr.vc = a.vcur ? reinterpret_cast<const uint16_t *>(a.vcur) + ((int64_t)b * a.Hkv + kvh) * D : nullptr;
+                rr.g = g;
+                rr.r = a.r;
+                rr.rotate_v = a.rotate_v;
+                residual_tile(rr, slot, qbase, warp * 16, ntok, lane, c0);
             }
         }
 
@@ -822,8 +924,12 @@ __global__ void __launch_bounds__(NCW_ * 32, 1) decode_attn_kernel(const AttnArg
                                                                ((int64_t)b * a.Hkv + kvh) * D);
             reinterpret_cast<uint2 *>(reinterpret_cast<__nv_bfloat16 *>(a.ring_k) + (bh * R + a.r) * D)[lane] =
                 ks[lane];
-            reinterpret_cast<uint2 *>(reinterpret_cast<__nv_bfloat16 *>(a.ring_v) + (bh * R + a.r) * D)[lane] =
-                vs[lane];
+            const uint2 vv = vs[lane];  // V ring is channel-major [D][R]
+            uint16_t *rv = reinterpret_cast<uint16_t *>(a.ring_v) + bh * R * D + a.r;
+            rv[(4 * lane + 0) * R] = (uint16_t)(vv.x & 0xffffu);
+            rv[(4 * lane + 1) * R] = (uint16_t)(vv.x >> 16);
+            rv[(4 * lane + 2) * R] = (uint16_t)(vv.y & 0xffffu);
+            rv[(4 * lane + 3) * R] = (uint16_t)(vv.y >> 16);
         }
     }
     if (a.prof) tmr[4] += clk() - tm0;
@@ -867,8 +973,19 @@ cudaError_t launch_t(const AttnArgs &a, cudaStream_t st) {
         if (e != cudaSuccess) return e;
         init = true;
     }
-    decode_attn_kernel<BITS, NCW><<<a.ncta, C::NTHREADS, C::SMEM, st>>>(a);
-    return cudaGetLastError();
+    // programmatic stream serialization: may overlap the previous kernel's tail
+    // (the kernel orders its dependent accesses with griddepcontrol.wait)
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)a.ncta);
+    cfg.blockDim = dim3(C::NTHREADS);
+    cfg.dynamicSmemBytes = C::SMEM;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, decode_attn_kernel<BITS, NCW>, a);
 }
 
 }  // namespace
@@ -898,14 +1015,14 @@ static int ncw_choice(int bits) {
         const char *e = getenv("OSCAR_NCW");
         env = e ? atoi(e) : 0;
     }
-    if (env == 8 || env == 12) return env;
+    if (env == 8 || env == 12 || env == 16) return env;
     return bits == 4 ? 8 : 12;
 }
 
 cudaError_t launch_attention(int bits, const AttnArgs &a, cudaStream_t st) {
     const int ncw = ncw_choice(bits);
     switch (bits) {
-        case 2: return ncw == 8 ? launch_t<2, 8>(a, st) : launch_t<2, 12>(a, st);
+        case 2: return ncw == 8 ? launch_t<2, 8>(a, st) : ncw == 16 ? launch_t<2, 16>(a, st) : launch_t<2, 12>(a, st);
         case 4: return ncw == 8 ? launch_t<4, 8>(a, st) : launch_t<4, 12>(a, st);
         case 0: return ncw == 8 ? launch_t<0, 8>(a, st) : launch_t<0, 12>(a, st);
         default: return cudaErrorInvalidValue;

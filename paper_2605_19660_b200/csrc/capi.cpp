@@ -116,6 +116,9 @@ struct oscar_kv_handle {
     int64_t device_bytes = 0;
     int last_launches = 0;
     cudaStream_t last_stream = nullptr;
+    // a quantize kernel wrote packed records since the last attention launch:
+    // the next attention launch must not prefetch them ahead of griddepcontrol.wait
+    bool blocks_written = true;
 
     TransformCfg tc() const {
         TransformCfg t;
@@ -149,7 +152,7 @@ struct oscar_kv_handle {
 
     // ---- kernels --------------------------------------------------------------
     void quantize_from(const void *k, const void *v, int64_t sb, int64_t st, int64_t sh, int64_t tok0,
-                       int64_t nblk, int64_t blk0, cudaStream_t s) {
+                       int64_t nblk, int64_t blk0, cudaStream_t s, int64_t vst = -1, int64_t vsc = 1) {
         QuantizeArgs a{};
         a.k = k;
         a.v = v;
@@ -157,6 +160,8 @@ struct oscar_kv_handle {
         a.st = st;
         a.sh = sh;
         a.tok0 = tok0;
+        a.vst = vst < 0 ? st : vst;
+        a.vsc = vsc;
         a.B = (int)B;
         a.H = (int)cfg.heads;
         a.n_blocks = nblk;
@@ -167,6 +172,7 @@ struct oscar_kv_handle {
         a.tc = tc();
         CK(launch_quantize(a, s));
         ++last_launches;
+        blocks_written = true;
     }
     void ring_copy(const void *k, const void *v, int64_t sb, int64_t st, int64_t sh, int64_t tok0, int64_t n,
                    int64_t slot0, cudaStream_t s) {
@@ -187,9 +193,9 @@ struct oscar_kv_handle {
         ++last_launches;
     }
     void flush(cudaStream_t s) {
-        // the ring [bh][R][D] is the source of one block per (b, h)
+        // the rings are the source of one block per (b, h): K [bh][R][D], V [bh][D][R]
         const int64_t H = cfg.heads;
-        quantize_from(ring_k, ring_v, H * R * D, D, (int64_t)R * D, 0, 1, packed / R, s);
+        quantize_from(ring_k, ring_v, H * R * D, D, (int64_t)R * D, 0, 1, packed / R, s, /*vst=*/1, /*vsc=*/R);
         packed += R;
         residual = 0;
     }
@@ -260,6 +266,7 @@ struct oscar_kv_handle {
             a.pf_dist = pf;
         }
         a.ncta = attention_grid(dbits, num_sms, a.nb, a.BH);
+        a.pdl_prefetch = blocks_written ? 0 : 1;
         a.maxp = maxp_alloc;
         // exact partial-slot requirement
         if (a.nb > 0) {
@@ -290,6 +297,7 @@ struct oscar_kv_handle {
         AttnArgs a = attn_args(q, k, v, out, lse);
         CK(launch_attention(dbits, a, s));
         ++last_launches;
+        blocks_written = false;
         // buffer_quant_k/v of the current token (written into the ring by the kernel)
         prefilled = true;
         residual += 1;
@@ -307,7 +315,7 @@ struct oscar_kv_handle {
         static int prof = -1;
         if (prof < 0) prof = getenv("OSCAR_PROF") ? 1 : 0;
         unsigned long long *pbuf = nullptr;
-        const int nw = a.ncta * 12;
+        const int nw = a.ncta * 16;
         if (prof) {
             CK(cudaMalloc(&pbuf, sizeof(unsigned long long) * 12 * nw));
             CK(cudaMemsetAsync(pbuf, 0, sizeof(unsigned long long) * 12 * nw, s));
@@ -315,6 +323,7 @@ struct oscar_kv_handle {
         }
         CK(launch_attention(dbits, a, s));
         ++last_launches;
+        blocks_written = false;
         if (prof) {
             std::vector<unsigned long long> hbuf(12 * nw);
             CK(cudaMemcpyAsync(hbuf.data(), pbuf, hbuf.size() * 8, cudaMemcpyDeviceToHost, s));
@@ -334,8 +343,8 @@ struct oscar_kv_handle {
                 int ncta_used = 0;
                 for (int c = 0; c < a.ncta; ++c) {
                     double lo = 1e30, hi = 0;
-                    for (int w = 0; w < 12; ++w) {
-                        const double t = (double)hbuf[12 * (c * 12 + w) + 8];
+                    for (int w = 0; w < 16; ++w) {
+                        const double t = (double)hbuf[12 * (c * 16 + w) + 8];
                         if (t == 0) continue;
                         lo = std::min(lo, t);
                         hi = std::max(hi, t);
@@ -509,7 +518,7 @@ HostCache build_host_cache(oscar_kv_handle *h, int64_t b) {
             if (tc.scales) s = host::token_scale(row, D, cfg.scaling);
             for (int c = 0; c < D; ++c) hc.k_res[(t * H + hh) * D + c] = row[c];
             hc.k_norms_res[t * H + hh] = s;
-            for (int c = 0; c < D; ++c) row[c] = host::bf16_to_double(rv[t * D + c]);
+            for (int c = 0; c < D; ++c) row[c] = host::bf16_to_double(rv[c * R + t]);  // V ring is channel-major
             if (cfg.rotate_v) host::fht(row, D);
             for (int c = 0; c < D; ++c) hc.v_res[(t * H + hh) * D + c] = row[c];
         }

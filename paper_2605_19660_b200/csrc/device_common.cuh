@@ -84,6 +84,16 @@ __device__ __forceinline__ int atomic_add_acq_rel_gpu(int *p, int v) {
     return old;
 }
 
+// ---- programmatic dependent launch (griddepcontrol, sm_90+) ---------------------
+// allow the next grid in the stream (launched with programmatic stream
+// serialization) to be scheduled as this grid's CTAs retire
+__device__ __forceinline__ void griddep_launch_dependents() {
+    asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+}
+// wait until the prerequisite grid has completed and its memory is visible
+// (returns at once when the grid was launched without a programmatic dependency)
+__device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
+
 // ---- named barrier among a subset of warps ---------------------------------------
 __device__ __forceinline__ void named_bar(int id, int nthreads) {
     asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(nthreads) : "memory");

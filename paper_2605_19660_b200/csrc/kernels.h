@@ -15,12 +15,15 @@ struct TransformCfg {
 };
 
 // Quantise n_blocks R-blocks per (sequence, head) from a bf16 source.
-// Source element (b, h, token t, channel c) lives at
-//   src + b*sb + (tok0 + t)*st + h*sh + c
+// Key element (b, h, token t, channel c) lives at
+//   k + b*sb + (tok0 + t)*st + h*sh + c,
+// value element at v + b*sb + (tok0 + t)*vst + h*sh + c*vsc (vsc = 1 for a
+// token-major source; the residual ring stores V channel-major, vsc = R).
 // Block k of (b,h) is written to blocks[((b*H+h)*max_blocks + blk0 + k)*bytes].
 struct QuantizeArgs {
     const void *k, *v;
     int64_t sb, st, sh, tok0;
+    int64_t vst, vsc;
     int B, H;
     int64_t n_blocks;
     uint8_t *blocks;
@@ -30,13 +33,15 @@ struct QuantizeArgs {
 };
 cudaError_t launch_quantize(const QuantizeArgs &a, cudaStream_t st);
 
-// Copy n tokens of raw bf16 K/V into the residual ring at slot0.
+// Copy n tokens of raw bf16 K/V into the residual ring at slot0: K ring
+// [bh][R][D] token-major, V ring [bh][D][R] channel-major (so the attention
+// kernel's P.V A fragments are contiguous token pairs).
 struct RingCopyArgs {
     const void *k, *v;
     int64_t sb, st, sh, tok0;
     int B, H;
     int64_t n;
-    void *ring_k, *ring_v;  // [bh][R][D]
+    void *ring_k, *ring_v;  // K [bh][R][D], V [bh][D][R]
     int64_t slot0;
 };
 cudaError_t launch_ring_copy(const RingCopyArgs &a, cudaStream_t st);
@@ -48,7 +53,7 @@ struct AttnArgs {
     int BH, Hkv, g, Hq;
     const void *q;     // bf16 [B][Hq][D]
     const void *kcur, *vcur;  // bf16 [B][Hkv][D] or null
-    void *ring_k, *ring_v;    // [bh][R][D]
+    void *ring_k, *ring_v;    // K [bh][R][D], V [bh][D][R]
     int r;             // residual rows in ring
     int write_ring;    // store kcur/vcur at ring slot r
     int rotates;       // rotate q for the packed part
@@ -64,6 +69,8 @@ struct AttnArgs {
     int maxp;
     int ncta;
     int pf_dist;       // L2 prefetch distance beyond the ring (units), 0 = off
+    int pdl_prefetch;  // packed records unchanged since the previous launch on this stream:
+                       // the ring fill may start before griddepcontrol.wait
     unsigned long long *prof;  // debug: per-warp phase cycles [ncta][NCW][5] or null
 };
 // bits: 2, 4 or 0 (bf16 baseline)

@@ -8,16 +8,16 @@
 //   [K codes  4096 B]  mma A-fragment order      [K codes  8192 B]
 //   [V codes  4096 B]  mma A-fragment order      [V codes  8192 B]
 //   [K a      1024 B]  fp16 step  per (ch,grp)   ... same params/norms ...
-//   [K z      1024 B]  fp16 -zero point per (ch,grp)
+//   [K b      1024 B]  fp16 offset -delta*zp per (ch,grp)
 //   [V a      1024 B]  fp16 step  per (tok,gc)
 //   [V b      1024 B]  fp16 offset per (tok,gc)
 //   [norms     512 B]  fp32 per token
 //
-// Keys dequantise as x = a*(code + z) with a = delta, z = -zp (a constant
-// group stores a = constant, z = 1: its codes are 0), values as x = a*code + b
-// with b = -delta*zp (a = 0, b = constant) -- the reference's dequantize_one
-// (quant.cpp:65-68) with the step narrowed to fp16; the key form keeps the
-// zero point exact so the kernel's dot product stays sum_c B_c*(code - zp).
+// Keys and values both dequantise as x = a*code + b with a = delta and
+// b = -delta*zp (a constant group stores a = 0, b = constant; its codes are 0)
+// -- the reference's dequantize_one (quant.cpp:65-68) with step and offset
+// narrowed to fp16.  The attention kernel folds a into the MMA B operand and
+// b into one small MMA per k-step (keys) / token tile (values).
 //
 // The codes are the reference's codes (bit-identical values) permuted inside
 // the block so that every 32-bit word a lane loads IS an mma.m16n8k16 A

@@ -152,12 +152,15 @@ __device__ __forceinline__ void affine16(const GroupQ &p, __half &a, __half &b) 
     }
 }
 
-template <int BITS>
-__global__ void __launch_bounds__(QT) quantize_kernel(const QuantizeArgs a) {
+// GPAR 32-token groups of the block are processed concurrently by GPAR
+// 128-thread quarters of the CTA (GPAR = 1: prefill, throughput; GPAR = 4:
+// the single-block flush, latency).
+template <int BITS, int GPAR>
+__global__ void __launch_bounds__(QT * GPAR) quantize_kernel(const QuantizeArgs a) {
     using Blk = Block<BITS>;
     extern __shared__ __align__(16) uint8_t smem[];
-    double *ku = reinterpret_cast<double *>(smem);               // [32][129]
-    uint8_t *ck = smem + 32 * 129 * 8;                            // [128][128] K codes
+    double *ku = reinterpret_cast<double *>(smem) + (threadIdx.x / QT) * 32 * 129;  // [GPAR][32][129]
+    uint8_t *ck = smem + GPAR * 32 * 129 * 8;                     // [128][128] K codes
     uint8_t *cv = ck + R * D;                                     // [128][128] V codes
     uint8_t *prm = cv + R * D;                                    // params + norms (BYTES - KA_OFF)
     __half *ka = reinterpret_cast<__half *>(prm);
@@ -166,7 +169,7 @@ __global__ void __launch_bounds__(QT) quantize_kernel(const QuantizeArgs a) {
     __half *vb = va + R * NGC;
     float *nrm = reinterpret_cast<float *>(vb + R * NGC);
 
-    const int tid = threadIdx.x, lane = tid & 31, q = tid & 3, tl = tid >> 2;
+    const int tid = threadIdx.x % QT, lane = tid & 31, q = tid & 3, tl = tid >> 2;
     const int bh = blockIdx.y, b = bh / a.H, h = bh % a.H;
     const int64_t blk = blockIdx.x;
     const __nv_bfloat16 *kin = reinterpret_cast<const __nv_bfloat16 *>(a.k) + b * a.sb + h * a.sh;
@@ -176,7 +179,7 @@ __global__ void __launch_bounds__(QT) quantize_kernel(const QuantizeArgs a) {
     double *shadow = a.shadow ? a.shadow + out_blk * SHADOW_DOUBLES : nullptr;
     const TransformCfg tc = a.tc;
 
-    for (int gi = 0; gi < NGRP; ++gi) {
+    for (int gi = threadIdx.x / QT; gi < NGRP; gi += GPAR) {
         const int t = gi * G + tl;  // token within the block
         // ---------------- K: rotate, scale (apply_method) ----------------
         double x[32];
@@ -232,7 +235,14 @@ __global__ void __launch_bounds__(QT) quantize_kernel(const QuantizeArgs a) {
         // ---------------- V: optional rotation, per-token groups ----------------
         {
             double y[32];
-            load32(vin + (tok_base + t) * a.st + q * 32, y);
+            if (a.vsc == 1) {
+                load32(vin + (tok_base + t) * a.vst + q * 32, y);
+            } else {  // channel-major source (the residual ring)
+                const uint16_t *vp = reinterpret_cast<const uint16_t *>(vin) + (tok_base + t) * a.vst;
+#pragma unroll
+                for (int i = 0; i < 32; ++i)
+                    y[i] = (double)__uint_as_float((uint32_t)vp[(int64_t)(q * 32 + i) * a.vsc] << 16);
+            }
             if (tc.rotate_v) fht128_quad(y, q);
             const GroupQ p = group_params([&](int i) { return y[i]; }, BITS);
 #pragma unroll
@@ -252,10 +262,14 @@ __global__ void __launch_bounds__(QT) quantize_kernel(const QuantizeArgs a) {
             const int c = tid;  // channel
             const GroupQ p = group_params([&](int i) { return ku[i * 129 + c]; }, BITS);
             for (int i = 0; i < G; ++i) ck[(gi * G + i) * D + c] = quantize_one(ku[i * 129 + c], p, BITS);
-            // keys: step and NEGATED zero point, x = step*(code + nz); a constant
-            // group is (lo, +1) since its codes are 0 (quant.cpp:37-42, 65-68)
-            ka[ka_index(c, gi)] = __double2half(p.delta == 0.0 ? p.lo : p.delta);
-            kb[kb_index(c, gi)] = __double2half(p.delta == 0.0 ? 1.0 : -(double)p.zp);
+            // keys use the same affine form as values, x = a*code + b with
+            // b = -delta*zp (a constant group is a = 0, b = lo: its codes are 0,
+            // quant.cpp:37-42, 65-68); the attention kernel folds b into one
+            // MMA per k-step against the rotated query
+            __half ha, hb;
+            affine16(p, ha, hb);
+            ka[ka_index(c, gi)] = ha;
+            kb[kb_index(c, gi)] = hb;
             if (shadow) {
                 shadow[(c * NGRP + gi) * 2] = p.lo;
                 shadow[(c * NGRP + gi) * 2 + 1] = p.hi;
@@ -268,7 +282,7 @@ __global__ void __launch_bounds__(QT) quantize_kernel(const QuantizeArgs a) {
     uint8_t *out = a.blocks + out_blk * (int64_t)Blk::BYTES;
     constexpr int NWORDS = R * D * BITS / 32;
     constexpr int TPW = 16 / BITS;
-    for (int w = tid; w < NWORDS; w += QT) {
+    for (int w = threadIdx.x; w < NWORDS; w += QT * GPAR) {
         uint32_t wk = 0, wv = 0;
 #pragma unroll
         for (int hi = 0; hi < 2; ++hi) {
@@ -286,7 +300,7 @@ __global__ void __launch_bounds__(QT) quantize_kernel(const QuantizeArgs a) {
     }
     // params + norms: contiguous tail of the record
     constexpr int TAIL = Blk::BYTES - Blk::KA_OFF;
-    for (int i = tid; i < TAIL / 16; i += QT)
+    for (int i = threadIdx.x; i < TAIL / 16; i += QT * GPAR)
         reinterpret_cast<uint4 *>(out + Blk::KA_OFF)[i] = reinterpret_cast<const uint4 *>(prm)[i];
 }
 
@@ -306,7 +320,12 @@ __global__ void __launch_bounds__(QT) raw_block_kernel_dyn(const QuantizeArgs a)
     for (int i = threadIdx.x; i < R * 16; i += QT) {
         const int t = i >> 4, part = i & 15;
         reinterpret_cast<uint4 *>(sk)[i] = *reinterpret_cast<const uint4 *>(kin + (tok_base + t) * a.st + part * 8);
-        reinterpret_cast<uint4 *>(sv)[i] = *reinterpret_cast<const uint4 *>(vin + (tok_base + t) * a.st + part * 8);
+        if (a.vsc == 1) {
+            reinterpret_cast<uint4 *>(sv)[i] = *reinterpret_cast<const uint4 *>(vin + (tok_base + t) * a.vst + part * 8);
+        } else {
+#pragma unroll
+            for (int e = 0; e < 8; ++e) sv[t * D + part * 8 + e] = vin[(tok_base + t) * a.vst + (part * 8 + e) * a.vsc];
+        }
     }
     __syncthreads();
     constexpr int QW = BF16_QUARTER_BYTES / 2 / 4;  // 32-bit words per tensor per quarter (2048)
@@ -331,13 +350,31 @@ __global__ void ring_copy_kernel(const RingCopyArgs a) {
     const uint16_t *kin = reinterpret_cast<const uint16_t *>(a.k) + b * a.sb + h * a.sh + (a.tok0 + t) * a.st;
     const uint16_t *vin = reinterpret_cast<const uint16_t *>(a.v) + b * a.sb + h * a.sh + (a.tok0 + t) * a.st;
     uint16_t *rk = reinterpret_cast<uint16_t *>(a.ring_k) + ((int64_t)bh * R + a.slot0 + t) * D;
-    uint16_t *rv = reinterpret_cast<uint16_t *>(a.ring_v) + ((int64_t)bh * R + a.slot0 + t) * D;
-    const int i = threadIdx.x;  // 32 threads x 8 bf16... use 16 threads each for k and v
+    uint16_t *rv = reinterpret_cast<uint16_t *>(a.ring_v) + (int64_t)bh * R * D + a.slot0 + t;
+    const int i = threadIdx.x;  // 32 threads: 16 B of K each (row-major), 4 V channels each (channel-major)
     if (i < 16) reinterpret_cast<uint4 *>(rk)[i] = reinterpret_cast<const uint4 *>(kin)[i];
-    else reinterpret_cast<uint4 *>(rv)[i - 16] = reinterpret_cast<const uint4 *>(vin)[i - 16];
+    const uint2 vv = reinterpret_cast<const uint2 *>(vin)[i];
+    rv[(4 * i + 0) * R] = (uint16_t)(vv.x & 0xffffu);
+    rv[(4 * i + 1) * R] = (uint16_t)(vv.x >> 16);
+    rv[(4 * i + 2) * R] = (uint16_t)(vv.y & 0xffffu);
+    rv[(4 * i + 3) * R] = (uint16_t)(vv.y >> 16);
 }
 
 }  // namespace
+
+template <int BITS, int GPAR>
+cudaError_t launch_q(const QuantizeArgs &a, dim3 grid, cudaStream_t st) {
+    const int smem = GPAR * 32 * 129 * 8 + 2 * R * D + Block<BITS>::BYTES - Block<BITS>::KA_OFF;
+    static bool init = false;
+    if (!init) {
+        cudaError_t e = cudaFuncSetAttribute(quantize_kernel<BITS, GPAR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             smem);
+        if (e != cudaSuccess) return e;
+        init = true;
+    }
+    quantize_kernel<BITS, GPAR><<<grid, QT * GPAR, smem, st>>>(a);
+    return cudaGetLastError();
+}
 
 cudaError_t launch_quantize(const QuantizeArgs &a, cudaStream_t st) {
     if (a.n_blocks <= 0) return cudaSuccess;
@@ -351,25 +388,10 @@ cudaError_t launch_quantize(const QuantizeArgs &a, cudaStream_t st) {
         raw_block_kernel_dyn<<<grid, QT, 2 * R * D * 2, st>>>(a);
         return cudaGetLastError();
     }
-    const int smem_common = 32 * 129 * 8 + 2 * R * D;
-    if (a.tc.bits == 2) {
-        const int smem = smem_common + Block<2>::BYTES - Block<2>::KA_OFF;
-        static bool init = false;
-        if (!init) {
-            cudaFuncSetAttribute(quantize_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-            init = true;
-        }
-        quantize_kernel<2><<<grid, QT, smem, st>>>(a);
-    } else {
-        const int smem = smem_common + Block<4>::BYTES - Block<4>::KA_OFF;
-        static bool init = false;
-        if (!init) {
-            cudaFuncSetAttribute(quantize_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-            init = true;
-        }
-        quantize_kernel<4><<<grid, QT, smem, st>>>(a);
-    }
-    return cudaGetLastError();
+    // one block per (b, h) (the flush): 4 groups in parallel for latency
+    const bool flush = a.n_blocks == 1;
+    if (a.tc.bits == 2) return flush ? launch_q<2, 4>(a, grid, st) : launch_q<2, 1>(a, grid, st);
+    return flush ? launch_q<4, 4>(a, grid, st) : launch_q<4, 1>(a, grid, st);
 }
 
 cudaError_t launch_ring_copy(const RingCopyArgs &a, cudaStream_t st) {

@@ -87,6 +87,14 @@ int oscar_kv_append(oscar_kv_handle *h, const void *k, const void *v, int64_t n_
 int oscar_kv_decode_step(oscar_kv_handle *h, const void *q, const void *k, const void *v, float *out,
                          float *lse, void *stream);
 
+/* decode_step for n independent caches (e.g. the layers of one model step)
+ * in ONE host call: element i of every array belongs to handles[i]; lse may
+ * be NULL (or contain NULLs).  Same semantics as n oscar_kv_decode_step
+ * calls in order on one stream, without the per-call host round trip. */
+int oscar_kv_decode_step_many(int32_t n, oscar_kv_handle *const *handles, const void *const *q,
+                              const void *const *k, const void *const *v, float *const *out, float *const *lse,
+                              void *stream);
+
 /* Attention over the cache contents only (no current token, no append).
  * Used for sequence sharding: each rank attends its R-aligned shard and the
  * (out, lse) partials are merged with oscar_lse_merge. */

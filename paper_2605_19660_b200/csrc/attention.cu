@@ -41,7 +41,8 @@ constexpr float LN2 = 0.6931471805599453f;
 
 constexpr int MAXSEG_SMEM = 64;  // max segments (b, kv heads) per CTA range
 constexpr int NCW_MAX = 16;
-constexpr int QH_STRIDE = 136;  // padded fp16 row of the per-warp q tile (conflict-free; 16-B aligned rows)
+constexpr int QH_STRIDE = 136;  // padded fp16 row of a q tile (conflict-free; 16-B aligned rows)
+constexpr int QSEG = 4;         // segment q tiles held in shared memory (one wave)
 
 template <int BITS, int NCW_ = ((BITS == 4) ? 8 : 12)>
 struct AttnCfg {
@@ -51,8 +52,8 @@ struct AttnCfg {
     static constexpr int STAGE = BYTES / SUB;
     static constexpr int NCW = NCW_;  // warps per CTA, all consumers
     static constexpr int NTHREADS = NCW * 32;
-    static constexpr int QH_OFF = 0;                                  // per-warp q tiles
-    static constexpr int SEG_OFF = QH_OFF + NCW * 8 * QH_STRIDE * 2;  // lastflag[MAXSEG_SMEM]
+    static constexpr int QH_OFF = 0;                                   // QSEG segment q tiles
+    static constexpr int SEG_OFF = QH_OFF + QSEG * 8 * QH_STRIDE * 2;  // lastflag[MAXSEG_SMEM]
     static constexpr int BAR_OFF = ((SEG_OFF + MAXSEG_SMEM * 4 + 7) / 8) * 8;
     // shared ring of NST stages: as many whole stages as fit in 227 KB
     static constexpr int NST = (232448 - BAR_OFF - 1024) / STAGE;
@@ -109,17 +110,6 @@ __device__ __forceinline__ void load_bf16x4(const __nv_bfloat16 *p, float (&x)[4
     x[2] = __uint_as_float(u.y << 16);
     x[3] = __uint_as_float(u.y & 0xffff0000u);
 }
-
-// cp.async the g raw bf16 q rows (256 B each) into a padded tile (row stride QH_STRIDE halves)
-__device__ __forceinline__ void qtile_prefetch(__half *tile, const __nv_bfloat16 *q, int g, int lane) {
-    for (int c = lane; c < g * 16; c += 32) {  // 16-byte chunks: row c/16, chunk c%16
-        const int j = c >> 4, off = (c & 15) * 8;
-        const uint32_t dst = smem_u32(tile + j * QH_STRIDE + off);
-        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(dst), "l"(q + j * D + off) : "memory");
-    }
-    asm volatile("cp.async.commit_group;\n" ::: "memory");
-}
-__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
 
 __device__ __forceinline__ int64_t cta_of(int64_t x, int64_t total, int ncta) {
     return ((x + 1) * ncta - 1) / total;
@@ -231,28 +221,34 @@ __device__ __forceinline__ void process_block(const uint8_t *__restrict__ sb, Wa
         kb0[grp] = __shfl_sync(0xffffffffu, kbias[0], grp * 4 + tq);
         kb1[grp] = __shfl_sync(0xffffffffu, kbias[1], grp * 4 + tq);
     }
+    // logits relative to the running max, y = logit - m (one FFMA with the key
+    // norm); first block of a segment: m = -inf, measure against 0 instead
+    const float r0 = (st.m[0] == -CUDART_INF_F) ? 0.f : st.m[0];
+    const float r1 = (st.m[1] == -CUDART_INF_F) ? 0.f : st.m[1];
     float bm0 = -CUDART_INF_F, bm1 = -CUDART_INF_F;
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
         const int fs = (i % TPW) % HALFT;
         const float sc = __int_as_float((127 + 24 - BITS * fs) << 23);  // 2^(24 - BITS*fs)
         const int grp = i >> 1;
-        sacc[i][0] = fmaf(sacc[i][0], sc, kb0[grp]) * nrm[2 * i];
-        sacc[i][1] = fmaf(sacc[i][1], sc, kb1[grp]) * nrm[2 * i];
-        sacc[i][2] = fmaf(sacc[i][2], sc, kb0[grp]) * nrm[2 * i + 1];
-        sacc[i][3] = fmaf(sacc[i][3], sc, kb1[grp]) * nrm[2 * i + 1];
+        sacc[i][0] = fmaf(fmaf(sacc[i][0], sc, kb0[grp]), nrm[2 * i], -r0);
+        sacc[i][1] = fmaf(fmaf(sacc[i][1], sc, kb1[grp]), nrm[2 * i], -r1);
+        sacc[i][2] = fmaf(fmaf(sacc[i][2], sc, kb0[grp]), nrm[2 * i + 1], -r0);
+        sacc[i][3] = fmaf(fmaf(sacc[i][3], sc, kb1[grp]), nrm[2 * i + 1], -r1);
         bm0 = fmaxf(bm0, fmaxf(sacc[i][0], sacc[i][2]));
         bm1 = fmaxf(bm1, fmaxf(sacc[i][1], sacc[i][3]));
     }
     // lazy rescale: the running max only moves when some lane's block max
     // exceeds it (rare after the first blocks) -- then reduce and rescale
-    if (!__all_sync(0xffffffffu, bm0 <= st.m[0] && bm1 <= st.m[1])) {
+    if (!__all_sync(0xffffffffu, bm0 <= 0.f && bm1 <= 0.f && st.m[0] != -CUDART_INF_F && st.m[1] != -CUDART_INF_F)) {
 #pragma unroll
         for (int o = 4; o < 32; o <<= 1) {
             bm0 = fmaxf(bm0, __shfl_xor_sync(0xffffffffu, bm0, o));
             bm1 = fmaxf(bm1, __shfl_xor_sync(0xffffffffu, bm1, o));
         }
-        const float mn0 = fmaxf(st.m[0], bm0), mn1 = fmaxf(st.m[1], bm1);
+        // new max = r + d with d = max(block max - r, old max - r)
+        const float d0 = fmaxf(bm0, st.m[0] - r0), d1 = fmaxf(bm1, st.m[1] - r1);
+        const float mn0 = r0 + d0, mn1 = r1 + d1;
         const float al0 = fast_exp2(st.m[0] - mn0), al1 = fast_exp2(st.m[1] - mn1);
         st.m[0] = mn0;
         st.m[1] = mn1;
@@ -267,15 +263,21 @@ __device__ __forceinline__ void process_block(const uint8_t *__restrict__ sb, Wa
         }
         st.ob[0] *= al0;
         st.ob[1] *= al1;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            sacc[i][0] -= d0;
+            sacc[i][1] -= d1;
+            sacc[i][2] -= d0;
+            sacc[i][3] -= d1;
+        }
     }
-    const float mn0 = st.m[0], mn1 = st.m[1];
     float ls0 = 0.f, ls1 = 0.f;
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
-        sacc[i][0] = fast_exp2(sacc[i][0] - mn0);
-        sacc[i][1] = fast_exp2(sacc[i][1] - mn1);
-        sacc[i][2] = fast_exp2(sacc[i][2] - mn0);
-        sacc[i][3] = fast_exp2(sacc[i][3] - mn1);
+        sacc[i][0] = fast_exp2(sacc[i][0]);
+        sacc[i][1] = fast_exp2(sacc[i][1]);
+        sacc[i][2] = fast_exp2(sacc[i][2]);
+        sacc[i][3] = fast_exp2(sacc[i][3]);
         ls0 += sacc[i][0] + sacc[i][2];
         ls1 += sacc[i][1] + sacc[i][3];
     }
@@ -418,6 +420,39 @@ __device__ __forceinline__ void process_quarter_bf16(const uint8_t *__restrict__
             const uint4 a = V[(j * 8 + mm) * 32 + lane];
             mma16816_bf16(st.o[mm], a.x, a.y, a.z, a.w, bp0, bp1);
         }
+    }
+}
+
+// Rotated (fp16) / raw (bf16 baseline) q tiles of segments [k0, k1) of this
+// CTA's range (k1 - k0 <= QSEG), built cooperatively: item (segment k, head
+// row j) -> warp item % NCW; tile (k % QSEG) row j, rows j >= g zero-filled.  Each segment's
+// rotation runs once per CTA instead of once per warp.
+template <int BITS, int NCW>
+__device__ __forceinline__ void build_q_tiles(const AttnArgs &a, __half *tiles, int64_t seg_first, int k0, int k1,
+                                              int warp, int lane) {
+    const int g = a.g;
+    for (int item = k0 * 8 + warp; item < k1 * 8; item += NCW) {
+        const int k = item >> 3, j = item & 7;
+        const int64_t bh = seg_first + k;
+        uint2 *row = reinterpret_cast<uint2 *>(tiles + ((k % QSEG) * 8 + j) * QH_STRIDE) + lane;
+        if (j >= g) {
+            *row = make_uint2(0u, 0u);
+            continue;
+        }
+        const uint2 u = *(reinterpret_cast<const uint2 *>(reinterpret_cast<const __nv_bfloat16 *>(a.q) +
+                                                          ((bh / a.Hkv) * a.Hq + (bh % a.Hkv) * g + j) * D) +
+                          lane);
+        if (BITS == 0) {  // the bf16 baseline attends raw q
+            *row = u;
+            continue;
+        }
+        float x[4];
+        x[0] = __uint_as_float(u.x << 16);
+        x[1] = __uint_as_float(u.x & 0xffff0000u);
+        x[2] = __uint_as_float(u.y << 16);
+        x[3] = __uint_as_float(u.y & 0xffff0000u);
+        if (a.rotates) fht128_warp(x, lane);
+        *row = make_uint2(pack_half2(x[0], x[1]), pack_half2(x[2], x[3]));
     }
 }
 
@@ -630,27 +665,16 @@ __global__ void __launch_bounds__(NCW_ * 32, 1) decode_attn_kernel(const AttnArg
         }
     }
     griddep_wait();
-    if (total > 0 ? nunits > 0 : cta < a.BH) {  // first segment's q
-        const int64_t bh0 = total > 0 ? start / nb : cta;
-        qtile_prefetch(reinterpret_cast<__half *>(smem + C::QH_OFF) + warp * 8 * QH_STRIDE,
-                       reinterpret_cast<const __nv_bfloat16 *>(a.q) +
-                           ((int64_t)(bh0 / a.Hkv) * a.Hq + (bh0 % a.Hkv) * a.g) * D,
-                       a.g, lane);
-    }
-    __syncthreads();  // the only CTA-wide barrier before the end-of-work merges
-
     // segments: residual-only mode (nb == 0): CTA c <-> bh c
-    int64_t seg_first, seg_last;
-    if (total > 0) {
-        if (nunits <= 0) return;
-        seg_first = start / nb;
-        seg_last = (end - 1) / nb;
-    } else {
-        if (cta >= a.BH) return;
-        seg_first = seg_last = cta;
-    }
+    const bool active = total > 0 ? nunits > 0 : cta < a.BH;
+    const int64_t seg_first = !active ? 0 : (total > 0 ? start / nb : cta);
+    const int64_t seg_last = !active ? -1 : (total > 0 ? (end - 1) / nb : cta);
+    const int nseg_all = (int)(seg_last - seg_first + 1);
+    __half *qtiles = reinterpret_cast<__half *>(smem + C::QH_OFF);  // QSEG segment tiles of 8 x QH_STRIDE
+    build_q_tiles<BITS, NCW>(a, qtiles, seg_first, 0, nseg_all < QSEG ? nseg_all : QSEG, warp, lane);
+    __syncthreads();  // barrier init + first wave of q tiles visible
+    if (!active) return;
     const float c0 = LOG2E * 0.08838834764831845f;  // log2(e)/sqrt(128)
-    __half *qh = reinterpret_cast<__half *>(smem + C::QH_OFF) + warp * 8 * QH_STRIDE;  // private
     long long tmr[12] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
     const long long tk0 = a.prof ? clk() : 0;
 
@@ -663,40 +687,19 @@ __global__ void __launch_bounds__(NCW_ * 32, 1) decode_attn_kernel(const AttnArg
         const __nv_bfloat16 *qbase = reinterpret_cast<const __nv_bfloat16 *>(a.q) + ((int64_t)b * a.Hq + kvh * g) * D;
 
         const long long tq0 = a.prof ? clk() : 0;
-        // ---- q fragments (per warp, no CTA barrier): the raw bf16 q rows of this
-        //      segment were prefetched into the warp's private tile with cp.async
-        //      (one segment ahead); rotate in registers and write back as fp16
-        //      (raw bf16 kept for the bf16 baseline) in place, row by row ----
-        cp_async_wait_all();
-        __syncwarp();
-        for (int j = 0; j < 8; ++j) {
-            uint2 *row = reinterpret_cast<uint2 *>(qh + j * QH_STRIDE) + lane;
-            if (j >= g) {  // padded heads: zero rows, no transform
-                *row = make_uint2(0u, 0u);
-                continue;
-            }
-            if (BITS == 0) continue;  // the bf16 baseline attends raw q
-            const uint2 u = *row;
-            float x[4];
-            x[0] = __uint_as_float(u.x << 16);
-            x[1] = __uint_as_float(u.x & 0xffff0000u);
-            x[2] = __uint_as_float(u.y << 16);
-            x[3] = __uint_as_float(u.y & 0xffff0000u);
-            if (a.rotates) fht128_warp(x, lane);  // shuffles: every lane read row j first
-            *row = make_uint2(pack_half2(x[0], x[1]), pack_half2(x[2], x[3]));
+        // ---- q fragments from this segment's CTA-shared tile; every QSEG segments
+        //      the next wave of tiles is built (all warps walk the same segments) ----
+        if (k > 0 && k % QSEG == 0) {
+            __syncthreads();
+            build_q_tiles<BITS, NCW>(a, qtiles, seg_first, k, (k + QSEG < nseg_all ? k + QSEG : nseg_all), warp, lane);
+            __syncthreads();
         }
-        __syncwarp();
+        const __half *qh = qtiles + (k % QSEG) * 8 * QH_STRIDE;
         uint32_t qf[8][2];
 #pragma unroll
         for (int s = 0; s < 8; ++s) {
             qf[s][0] = *reinterpret_cast<const uint32_t *>(qh + gq * QH_STRIDE + 16 * s + 2 * tq);
             qf[s][1] = *reinterpret_cast<const uint32_t *>(qh + gq * QH_STRIDE + 16 * s + 2 * tq + 8);
-        }
-        __syncwarp();
-        if (bh < seg_last) {  // next segment's raw q, in flight during this segment
-            const __nv_bfloat16 *qn = reinterpret_cast<const __nv_bfloat16 *>(a.q) +
-                                      ((int64_t)((bh + 1) / a.Hkv) * a.Hq + ((bh + 1) % a.Hkv) * g) * D;
-            qtile_prefetch(qh, qn, g, lane);
         }
 
         WarpState st;
@@ -892,14 +895,28 @@ __global__ void __launch_bounds__(NCW_ * 32, 1) decode_attn_kernel(const AttnArg
         for (int o = 1; o < 32; o <<= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o));
         const float L = warp_sum((ms == -CUDART_INF_F) ? 0.f : ls * fast_exp2(ms - M));
         float x[4] = {0.f, 0.f, 0.f, 0.f};
-        for (int s2 = 0; s2 < expected; ++s2) {
-            const float m2 = __ldcg(pmb + s2 * 16 + 2 * h);
-            const float4 v = __ldcg(reinterpret_cast<const float4 *>(pob + s2 * 8 * D + h * D + lane * 4));
-            const float f = (m2 == -CUDART_INF_F) ? 0.f : fast_exp2(m2 - M);
-            x[0] += v.x * f;
-            x[1] += v.y * f;
-            x[2] += v.z * f;
-            x[3] += v.w * f;
+        for (int s0 = 0; s0 < expected; s0 += 8) {  // 8 partials' loads in flight per batch
+            float m2[8];
+            float4 v[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const int s2 = s0 + u;
+                if (s2 < expected) {
+                    m2[u] = __ldcg(pmb + s2 * 16 + 2 * h);
+                    v[u] = __ldcg(reinterpret_cast<const float4 *>(pob + s2 * 8 * D + h * D + lane * 4));
+                } else {
+                    m2[u] = -CUDART_INF_F;
+                    v[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const float f = (m2[u] == -CUDART_INF_F) ? 0.f : fast_exp2(m2[u] - M);
+                x[0] += v[u].x * f;
+                x[1] += v[u].y * f;
+                x[2] += v[u].z * f;
+                x[3] += v[u].w * f;
+            }
         }
         const float inv = (L > 0.f) ? 1.f / L : 0.f;
 #pragma unroll
@@ -990,11 +1007,17 @@ cudaError_t launch_t(const AttnArgs &a, cudaStream_t st) {
 
 }  // namespace
 
+static int ncw_choice(int bits);
+
+// persistent grid: one CTA per SM, but never fewer than ~one pipeline unit per
+// warp per CTA -- small workloads (few sequences x short contexts) then use
+// fewer CTAs and every (b, kv head) has fewer split-KV partials to merge
 int attention_grid(int bits, int num_sms, int64_t nb, int BH) {
-    (void)bits;
-    const int64_t total = nb * BH;
-    if (total == 0) return BH;
-    return (int)(total < num_sms ? total : num_sms);
+    const int64_t units = nb * BH * (bits == 0 ? 4 : 1);
+    if (units == 0) return BH;
+    const int64_t per = ncw_choice(bits);
+    const int64_t want = (units + per - 1) / per;
+    return (int)(want < num_sms ? want : num_sms);
 }
 
 int64_t attention_scratch_floats(int max_ctas) {

@@ -276,7 +276,18 @@ struct oscar_kv_handle {
             int64_t need = 0;
             for (int64_t bh = 0; bh < a.BH; ++bh)
                 need = std::max(need, cta_of((bh + 1) * nbs - 1) - cta_of(bh * nbs) + 1);
-            if (need > maxp_alloc) throw LogicErr("internal: partial buffer too small");
+            if (need > maxp_alloc) {  // rare: grow the split-KV partial buffers (synchronous)
+                CK(cudaDeviceSynchronize());
+                cudaFree(part_o);
+                cudaFree(part_ml);
+                device_bytes -= sizeof(float) * (int64_t)BH * maxp_alloc * (8 * D + 16);
+                maxp_alloc = (int)need;
+                part_o = (float *)dalloc(sizeof(float) * (size_t)(BH * maxp_alloc * 8 * D));
+                part_ml = (float *)dalloc(sizeof(float) * (size_t)(BH * maxp_alloc * 16));
+                a.part_o = part_o;
+                a.part_ml = part_ml;
+                a.maxp = maxp_alloc;
+            }
             // segments per CTA range (units: nb blocks x SUB quarters for bf16)
             const int64_t sub = dbits == 0 ? 4 : 1, nbu = a.nb * sub, totu = nbu * a.BH;
             int64_t nseg = 0;
@@ -284,7 +295,18 @@ struct oscar_kv_handle {
                 const int64_t st = c * totu / a.ncta, en = (c + 1) * totu / a.ncta;
                 if (en > st) nseg = std::max(nseg, (en - 1) / nbu - st / nbu + 1);
             }
-            if (nseg > maxseg_alloc) throw LogicErr("internal: too many segments per CTA");
+            if (nseg > 64) throw InvalidArg("attention: more than 64 (sequence, kv head) segments per CTA");
+            if (nseg > maxseg_alloc) {  // rare (few long CTA ranges over short sequences): grow the scratch
+                CK(cudaDeviceSynchronize());
+                cudaFree(warp_part);
+                device_bytes -= sizeof(float) * attention_scratch_floats(
+                                                    (int)std::max<int64_t>((int64_t)num_sms * maxseg_alloc, BH));
+                maxseg_alloc = (int)nseg;
+                warp_part = (float *)dalloc(sizeof(float) * (size_t)attention_scratch_floats(
+                                                                (int)std::max<int64_t>((int64_t)num_sms * maxseg_alloc, BH)));
+                a.warp_part = warp_part;
+                a.maxseg = maxseg_alloc;
+            }
         } else {
             a.maxseg = 1;  // residual-only mode: one segment per CTA
         }
@@ -622,6 +644,24 @@ int oscar_kv_decode_step(oscar_kv_handle *h, const void *q, const void *k, const
         CK(cudaSetDevice(h->device));
         h->last_stream = (cudaStream_t)stream;
         h->decode_step(q, k, v, out, lse, (cudaStream_t)stream);
+    });
+}
+
+int oscar_kv_decode_step_many(int32_t n, oscar_kv_handle *const *hs, const void *const *q, const void *const *k,
+                              const void *const *v, float *const *out, float *const *lse, void *stream) {
+    return guard([&] {
+        if (n < 0 || (n > 0 && (!hs || !q || !k || !v || !out))) throw InvalidArg("decode_step_many: null argument");
+        int dev = -1;
+        for (int32_t i = 0; i < n; ++i) {
+            oscar_kv_handle *h = hs[i];
+            if (!h || !q[i] || !k[i] || !v[i] || !out[i]) throw InvalidArg("decode_step_many: null argument");
+            if (h->device != dev) {
+                CK(cudaSetDevice(h->device));
+                dev = h->device;
+            }
+            h->last_stream = (cudaStream_t)stream;
+            h->decode_step(q[i], k[i], v[i], out[i], lse ? lse[i] : nullptr, (cudaStream_t)stream);
+        }
     });
 }
 

@@ -74,6 +74,7 @@ def lib():
         L.oscar_kv_append.argtypes = [_P, _P, _P, ctypes.c_int64, _P]
         L.oscar_kv_decode_step.argtypes = [_P, _P, _P, _P, _P, _P, _P]
         L.oscar_kv_attend.argtypes = [_P, _P, _P, _P, _P]
+        L.oscar_kv_decode_step_many.argtypes = [ctypes.c_int32, _P, _P, _P, _P, _P, _P, _P]
         L.oscar_kv_decode_step_host.argtypes = [_P, _P, _P, _P, _P, _P, _P]
         L.oscar_kv_stats.argtypes = [_P, ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(ctypes.c_int64),
                                      ctypes.POINTER(ctypes.c_int64)]
@@ -90,7 +91,7 @@ def lib():
 # every entry point declared in include/oscar_kv.h
 C_ABI_SYMBOLS = [
     "oscar_last_error", "oscar_kv_config_validate", "oscar_kv_create", "oscar_kv_destroy", "oscar_kv_append",
-    "oscar_kv_decode_step", "oscar_kv_attend", "oscar_kv_decode_step_host", "oscar_kv_stats",
+    "oscar_kv_decode_step", "oscar_kv_decode_step_many", "oscar_kv_attend", "oscar_kv_decode_step_host", "oscar_kv_stats",
     "oscar_kv_memory_report", "oscar_kv_export", "oscar_kv_dump", "oscar_kv_materialize", "oscar_lse_merge",
     "oscar_kv_last_launch_count",
 ]
@@ -281,6 +282,28 @@ class KvCache:
         v = np.zeros((n, self.H, D))
         _check(lib().oscar_kv_materialize(self._h, b, k.ctypes.data, v.ctypes.data))
         return k, v
+
+
+class DecodeBatch:
+    """decode_step over several caches (e.g. every layer of a model step) in
+    one C-ABI call (oscar_kv_decode_step_many).  Pointer arrays are built once
+    for fixed q/k/v/out buffers; call run() each step after filling them."""
+
+    def __init__(self, caches, qs, ks, vs, outs, lses=None):
+        n = len(caches)
+        arr = ctypes.c_void_p * n
+        self.n = n
+        self._keep = (caches, qs, ks, vs, outs, lses)
+        self.h = arr(*[c._h.value for c in caches])
+        self.q = arr(*[_ptr(x) for x in qs])
+        self.k = arr(*[_ptr(x) for x in ks])
+        self.v = arr(*[_ptr(x) for x in vs])
+        self.o = arr(*[_ptr(x) for x in outs])
+        self.l = arr(*[_ptr(x) for x in lses]) if lses is not None else None
+
+    def run(self, stream=None):
+        _check(lib().oscar_kv_decode_step_many(self.n, self.h, self.q, self.k, self.v, self.o, self.l,
+                                               _stream(stream)))
 
 
 def lse_merge(outs, lses, out=None, lse_out=None, stream=None):

@@ -103,8 +103,10 @@ def gather_partials(o, lse, group=None):
     import torch
 
     td = _dist()
-    P = td.get_world_size(group)
     rows, d = o.shape
+    if not td.is_initialized():  # single process: nothing to exchange
+        return o.reshape(1, rows, d), lse.reshape(1, rows)
+    P = td.get_world_size(group)
     buf = torch.cat([o.reshape(rows, d), lse.reshape(rows, 1)], dim=1).contiguous()
     if td.get_backend(group) == "nccl":
         allb = torch.empty((P, rows, d + 1), dtype=buf.dtype, device=buf.device)
@@ -133,8 +135,8 @@ class SeqShardedKvCache:
 
         td = _dist()
         self.group = group
-        self.world = td.get_world_size(group)
-        self.rank = td.get_rank(group)
+        self.world = td.get_world_size(group) if td.is_initialized() else 1
+        self.rank = td.get_rank(group) if td.is_initialized() else 0
         self.B, self.Hq = batch, q_heads
         self.cache = KvCache(cfg, batch=batch, q_heads=q_heads, max_tokens=max_tokens_per_rank, device=device,
                              keep_exact=keep_exact)
@@ -169,6 +171,8 @@ class SeqShardedKvCache:
 
     def decode_step(self, q, k, v, stream=None):
         o, l = self.local_partial(q, k, v, stream=stream)
+        if self.world == 1:  # the only shard: its partial is the normalised result
+            return o.reshape(self.B, self.Hq, D)
         outs, lses = gather_partials(o, l, self.group)
         return self._merge(outs, lses).reshape(self.B, self.Hq, D)
 
@@ -177,6 +181,8 @@ class SeqShardedKvCache:
         import torch
 
         td = _dist()
+        if self.world == 1:
+            return self.cache.total_tokens
         t = torch.tensor([self.cache.total_tokens], dtype=torch.int64)
         if td.get_backend(self.group) == "nccl":
             t = t.cuda()

@@ -256,3 +256,34 @@ def test_sequence_sharded_attend_and_lse_merge():
     merged = lse_merge(torch.stack(parts_o), torch.stack(parts_l))
     torch.cuda.synchronize()
     assert rel_err(merged.cpu().numpy(), o_full.reshape(H * g, 128).cpu().numpy()) < 1e-5
+
+
+def test_decode_step_many_equals_per_cache_calls():
+    """oscar_kv_decode_step_many (one host call for several caches, e.g. the
+    layers of a step) == the same decode_step calls one by one, bit for bit."""
+    import torch
+
+    from paper_2605_19660_b200 import DecodeBatch, KvCache, PipelineConfig
+
+    H, g, S, L = 2, 4, 260, 3
+    data = [make_inputs(300 + i, S + 2, H) for i in range(L)]
+    q = dev_bf16(make_queries(300, 1, H * g))
+
+    def build():
+        cs = []
+        for k, v in data:
+            c = KvCache(PipelineConfig(heads=H), batch=1, q_heads=H * g, max_tokens=S + 8)
+            c.buffer_quant(dev_bf16(k[None, :S]), dev_bf16(v[None, :S]))
+            cs.append(c)
+        return cs
+
+    one = build()
+    ref = [c.decode_step(q, dev_bf16(d[0][S][None]), dev_bf16(d[1][S][None])) for c, d in zip(one, data)]
+    many = build()
+    outs = [torch.empty_like(r) for r in ref]
+    DecodeBatch(many, [q] * L, [dev_bf16(d[0][S][None]) for d in data], [dev_bf16(d[1][S][None]) for d in data],
+                outs).run()
+    torch.cuda.synchronize()
+    for a, b in zip(ref, outs):
+        assert torch.equal(a, b)
+    assert all(c.total_tokens == S + 1 for c in many)

@@ -30,6 +30,7 @@
 #include "device_common.cuh"
 #include "kernels.h"
 #include "layout.h"
+#include "split.h"
 
 namespace osk {
 
@@ -111,9 +112,6 @@ __device__ __forceinline__ void load_bf16x4(const __nv_bfloat16 *p, float (&x)[4
     x[3] = __uint_as_float(u.y & 0xffff0000u);
 }
 
-__device__ __forceinline__ int64_t cta_of(int64_t x, int64_t total, int ncta) {
-    return ((x + 1) * ncta - 1) / total;
-}
 
 // ----------------------------------------------------------------------------
 // per-warp accumulator state (fragment layouts, see layout.h)
@@ -619,9 +617,10 @@ __global__ void __launch_bounds__(NCW_ * 32, 1) decode_attn_kernel(const AttnArg
     const int64_t nb = a.nb * SUB;  // pipeline units per (b, kv head)
     const int64_t total = (int64_t)a.BH * nb;
     int64_t start = 0, end = 0;
+    const Split sp{nb, a.BH, a.ncta, a.seg_cost};
     if (total > 0) {
-        start = (cta * total) / a.ncta;
-        end = ((cta + 1) * total) / a.ncta;
+        start = sp.begin(cta);
+        end = sp.end(cta);
     }
     const int64_t nunits = end - start;
     const uint64_t pol = l2_evict_first_policy();
@@ -678,6 +677,7 @@ __global__ void __launch_bounds__(NCW_ * 32, 1) decode_attn_kernel(const AttnArg
     long long tmr[12] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
     const long long tk0 = a.prof ? clk() : 0;
 
+    int rtile_base = 0;  // residual tiles handed out so far (round-robin over warps)
     for (int64_t bh = seg_first; bh <= seg_last; ++bh) {
         const int k = (int)(bh - seg_first);
         const int b = (int)(bh / a.Hkv), kvh = (int)(bh % a.Hkv);
@@ -796,10 +796,14 @@ __global__ void __launch_bounds__(NCW_ * 32, 1) decode_attn_kernel(const AttnArg
         // ---- residual window + current token on the tensor cores (bf16 mma, raw q . raw k:
         //      the key transform is orthonormal up to the stored norm, so attending the raw
         //      bf16 rows IS attend_one over the full-precision residual, pipeline.cpp:152-180),
-        //      one 16-token tile per warp, merged into that warp's slot ----
+        //      one 16-token tile per warp, merged into that warp's slot; the tiles of
+        //      successive tail segments of this CTA rotate over the warps ----
         if (owns_tail) {
             const int ntok = a.r + (a.kcur ? 1 : 0);
-            if (warp * 16 < ntok) {
+            const int ntiles = (ntok + 15) >> 4;
+            const int j = (warp - rtile_base % NCW + NCW) % NCW;  // this warp's tile in this segment
+            rtile_base += ntiles;
+            if (j < ntiles) {
                 ResidualRefs rr;
                 rr.ringk = reinterpret_cast<const uint16_t *>(a.ring_k) + bh * R * D;
                 rr.ringv = reinterpret_cast<const uint16_t *>(a.ring_v) + bh * R * D;
@@ -808,7 +812,7 @@ __global__ void __launch_bounds__(NCW_ * 32, 1) decode_attn_kernel(const AttnArg
                 rr.g = g;
                 rr.r = a.r;
                 rr.rotate_v = a.rotate_v;
-                residual_tile(rr, slot, qbase, warp * 16, ntok, lane, c0);
+                residual_tile(rr, slot, qbase, j * 16, ntok, lane, c0);
             }
         }
 
@@ -827,7 +831,7 @@ __global__ void __launch_bounds__(NCW_ * 32, 1) decode_attn_kernel(const AttnArg
         const int64_t bh = seg_first + kk;
         const float *wp = a.warp_part + ((int64_t)cta * a.maxseg + kk) * NCW_MAX * MERGE_FLOATS;
         int64_t first_cta = 0;
-        if (total > 0) first_cta = cta_of(bh * nb, total, a.ncta);
+        if (total > 0) first_cta = sp.cta_of(bh * nb);
         const int pslot = (int)(total > 0 ? cta - first_cta : 0);
         float *po = a.part_o + ((int64_t)bh * a.maxp + pslot) * 8 * D;
         float *pml = a.part_ml + ((int64_t)bh * a.maxp + pslot) * 16;
@@ -865,7 +869,7 @@ __global__ void __launch_bounds__(NCW_ * 32, 1) decode_attn_kernel(const AttnArg
     if (threadIdx.x < nseg) {
         const int64_t bh = seg_first + threadIdx.x;
         int expected = 1;
-        if (total > 0) expected = (int)(cta_of((bh + 1) * nb - 1, total, a.ncta) - cta_of(bh * nb, total, a.ncta) + 1);
+        if (total > 0) expected = (int)(sp.cta_of((bh + 1) * nb - 1) - sp.cta_of(bh * nb) + 1);
         const int prev = atomic_add_acq_rel_gpu(&a.counters[bh], 1);
         lastflag[threadIdx.x] = (prev == expected - 1) ? expected : 0;
     }
@@ -958,7 +962,9 @@ __global__ void __launch_bounds__(NCW_ * 32, 1) decode_attn_kernel(const AttnArg
         pp[8] = (unsigned long long)(clk() - tk0);
         pp[9] = (unsigned long long)tmr[8];
         pp[10] = (unsigned long long)tmr[9];
-        pp[11] = (unsigned long long)tmr[10];
+        unsigned smid;
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+        pp[11] = smid;
     }
 }
 

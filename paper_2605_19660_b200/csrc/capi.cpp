@@ -27,6 +27,7 @@
 #include "host_ref.h"
 #include "kernels.h"
 #include "layout.h"
+#include "split.h"
 
 using namespace osk;
 
@@ -266,16 +267,25 @@ struct oscar_kv_handle {
             a.pf_dist = pf;
         }
         a.ncta = attention_grid(dbits, num_sms, a.nb, a.BH);
+        {
+            static int64_t sc = -1;  // OSCAR_SEG_COST overrides the per-segment split weight (tuning knob)
+            if (sc < 0) {
+                const char *e = getenv("OSCAR_SEG_COST");
+                sc = e ? atoll(e) : 3;
+            }
+            a.seg_cost = sc;
+        }
         a.pdl_prefetch = blocks_written ? 0 : 1;
         a.maxp = maxp_alloc;
         // exact partial-slot requirement
         if (a.nb > 0) {
             const int64_t nbs = a.nb * (dbits == 0 ? 4 : 1);  // pipeline units per (b, kv head)
             const int64_t total = nbs * a.BH;
-            auto cta_of = [&](int64_t x) { return ((x + 1) * a.ncta - 1) / total; };
+            (void)total;
+            const Split sp{nbs, a.BH, a.ncta, a.seg_cost};
             int64_t need = 0;
             for (int64_t bh = 0; bh < a.BH; ++bh)
-                need = std::max(need, cta_of((bh + 1) * nbs - 1) - cta_of(bh * nbs) + 1);
+                need = std::max(need, sp.cta_of((bh + 1) * nbs - 1) - sp.cta_of(bh * nbs) + 1);
             if (need > maxp_alloc) {  // rare: grow the split-KV partial buffers (synchronous)
                 CK(cudaDeviceSynchronize());
                 cudaFree(part_o);
@@ -291,8 +301,9 @@ struct oscar_kv_handle {
             // segments per CTA range (units: nb blocks x SUB quarters for bf16)
             const int64_t sub = dbits == 0 ? 4 : 1, nbu = a.nb * sub, totu = nbu * a.BH;
             int64_t nseg = 0;
+            (void)totu;
             for (int64_t c = 0; c < a.ncta; ++c) {
-                const int64_t st = c * totu / a.ncta, en = (c + 1) * totu / a.ncta;
+                const int64_t st = sp.begin(c), en = sp.end(c);
                 if (en > st) nseg = std::max(nseg, (en - 1) / nbu - st / nbu + 1);
             }
             if (nseg > 64) throw InvalidArg("attention: more than 64 (sequence, kv head) segments per CTA");
@@ -376,6 +387,31 @@ struct oscar_kv_handle {
                     cmin = std::min(cmin, hi);
                     cmax = std::max(cmax, hi);
                     wspread += (hi - lo);
+                }
+                if (const char *fn = getenv("OSCAR_PROF_FILE")) {  // per-CTA: range, segments, tails, smid, cycles
+                    if (FILE *f = std::fopen(fn, "w")) {
+                        std::fprintf(f, "cta,smid,units,segments,tails,slowest_warp_cycles\n");
+                        const int64_t nbu = a.nb * (dbits == 0 ? 4 : 1);
+                        const Split sp{nbu, a.BH, a.ncta, a.seg_cost};
+                        for (int c = 0; c < a.ncta; ++c) {
+                            double hi = 0;
+                            unsigned long long sm = 0;
+                            for (int w = 0; w < 16; ++w) {
+                                const double t = (double)hbuf[12 * (c * 16 + w) + 8];
+                                if (t > hi) {
+                                    hi = t;
+                                    sm = hbuf[12 * (c * 16 + w) + 11];
+                                }
+                            }
+                            const int64_t st = sp.begin(c), en = sp.end(c);
+                            int64_t tails = 0;
+                            for (int64_t bh = st / nbu; en > st && bh <= (en - 1) / nbu; ++bh)
+                                if ((bh + 1) * nbu <= en) ++tails;
+                            std::fprintf(f, "%d,%llu,%lld,%lld,%lld,%.0f\n", c, sm, (long long)(en - st),
+                                         (long long)(en > st ? (en - 1) / nbu - st / nbu + 1 : 0), (long long)tails, hi);
+                        }
+                        std::fclose(f);
+                    }
                 }
                 if (ncta_used)
                     std::fprintf(stderr, "OSCAR_PROF cta slowest-warp cycles: min %.0f max %.0f; mean in-CTA warp spread %.0f\n",

@@ -157,9 +157,10 @@ class SeqShardedKvCache:
         import torch
 
         rows = self.B * self.Hq
-        dev = q.device
-        out = torch.empty((rows, D), dtype=torch.float32, device=dev)
-        lse = torch.empty((rows,), dtype=torch.float32, device=dev)
+        if getattr(self, "_bufs", None) is None or self._bufs[0].device != q.device:
+            self._bufs = (torch.empty((rows, D), dtype=torch.float32, device=q.device),
+                          torch.empty((rows,), dtype=torch.float32, device=q.device))
+        out, lse = self._bufs  # reused across steps (stream-ordered)
         if self.shard is not None and self.shard.tail and k is not None:
             self.cache.decode_step(q, k, v, out=out, lse=lse, stream=stream)
         elif self.cache.total_tokens > 0:

@@ -221,17 +221,33 @@ def test_host_buffer_entry_matches_device_entry():
     H, g, S = 2, 4, 200
     k, v = make_inputs(9, S + 1, H)
     q = make_queries(9, 1, H * g)
-    outs = []
-    for host in (False, True):
+    import torch
+
+    outs, lses = [], []
+    # device entry; host entry with pageable buffers (D2H copies); host entry with
+    # page-locked buffers (the kernel writes out/lse to mapped host memory)
+    for mode in ("device", "pageable", "pinned"):
         c = KvCache(PipelineConfig(heads=H), batch=1, q_heads=H * g, max_tokens=512)
         c.buffer_quant(dev_bf16(k[None, :S]), dev_bf16(v[None, :S]))
-        if host:
-            o = np.zeros((1, H * g, 128), np.float32)
-            c.decode_step_host(to_bf16_bits(q), to_bf16_bits(k[S][None]), to_bf16_bits(v[S][None]), o)
-            outs.append(o)
+        if mode == "device":
+            lse = torch.empty((1, H * g), device="cuda")
+            outs.append(c.decode_step(dev_bf16(q), dev_bf16(k[S][None]), dev_bf16(v[S][None]), lse=lse).cpu().numpy())
+            lses.append(lse.cpu().numpy())
+            continue
+        qb, kb, vb = to_bf16_bits(q), to_bf16_bits(k[S][None]), to_bf16_bits(v[S][None])
+        if mode == "pageable":
+            o, l = np.zeros((1, H * g, 128), np.float32), np.zeros((1, H * g), np.float32)
         else:
-            outs.append(c.decode_step(dev_bf16(q), dev_bf16(k[S][None]), dev_bf16(v[S][None])).cpu().numpy())
-    assert np.array_equal(outs[0], outs[1])
+            ot = torch.zeros((1, H * g, 128), dtype=torch.float32).pin_memory()
+            lt = torch.zeros((1, H * g), dtype=torch.float32).pin_memory()
+            o, l = ot.numpy(), lt.numpy()
+            pin = [torch.from_numpy(x.view(np.int16)).pin_memory() for x in (qb, kb, vb)]
+            qb, kb, vb = (t.numpy().view(np.uint16) for t in pin)
+        c.decode_step_host(qb, kb, vb, o, lse=l)
+        outs.append(o.copy())
+        lses.append(l.copy())
+    assert np.array_equal(outs[0], outs[1]) and np.array_equal(outs[0], outs[2])
+    assert np.array_equal(lses[0], lses[1]) and np.array_equal(lses[0], lses[2])
 
 
 def test_sequence_sharded_attend_and_lse_merge():

@@ -30,6 +30,7 @@ namespace osk {
 namespace {
 
 constexpr int QT = 128;  // threads per CTA
+constexpr int KU_ROW = 4 * 33;  // doubles per token row of the K_u tile (4 quarters of 32, padded to 33)
 
 __device__ __forceinline__ double dadd(double a, double b) { return __dadd_rn(a, b); }
 __device__ __forceinline__ double dsub(double a, double b) { return __dsub_rn(a, b); }
@@ -132,13 +133,41 @@ __device__ __forceinline__ GroupQ group_params(Get get, int bits) {
     return p;
 }
 
-// quant.cpp:53-57
-__device__ __forceinline__ uint8_t quantize_one(double x, const GroupQ &p, int bits) {
-    if (p.delta == 0.0) return 0;
-    long long q = llround(ddiv(x, p.delta)) + p.zp;
-    const long long mx = (1 << bits) - 1;
-    q = q < 0 ? 0 : (q > mx ? mx : q);
-    return (uint8_t)q;
+// quant.cpp:53-57 over one group: q = clamp(llround(x / delta) + zp, 0, 2^b-1).
+// x / delta is taken as x * (1/delta) -- within 2 ulp of the IEEE quotient --
+// and rounded branch-free; an element whose product lies within 1e-9 of a
+// half-integer (where the two could round apart; 2 ulp < 1e-9 while
+// |x/delta| < 2^20, checked once per group) is redone with the exact IEEE
+// division afterwards.  The codes are bit-identical to the reference's.
+template <typename Get, typename Put>
+__device__ __forceinline__ void quantize_group(Get get, const GroupQ &p, int bits, Put put) {
+    const int mx = (1 << bits) - 1;
+    if (p.delta == 0.0) {
+#pragma unroll
+        for (int i = 0; i < 32; ++i) put(i, 0);
+        return;
+    }
+    const double inv = ddiv(1.0, p.delta);
+    const bool fast = dmul(fmax(fabs(p.lo), fabs(p.hi)), inv) < 1048576.0;
+    // codes saturate, so a zero point beyond +-2^30 acts like +-2^30
+    const int zp = p.zp > (1ll << 30) ? (1 << 30) : (p.zp < -(1ll << 30) ? -(1 << 30) : (int)p.zp);
+    unsigned tie = 0;
+#pragma unroll
+    for (int i = 0; i < 32; ++i) {
+        const double y = dmul(get(i), inv);
+        const double fl = floor(y);
+        const double fr = dsub(y, fl);
+        tie |= (fabs(dsub(fr, 0.5)) <= 1e-9 ? 1u : 0u) << i;
+        const int q = (int)fl + (fr > 0.5 ? 1 : 0) + zp;
+        put(i, q < 0 ? 0 : (q > mx ? mx : q));
+    }
+    if (!fast || tie) {  // rare: exact division for the flagged elements
+        for (int i = 0; i < 32; ++i) {
+            if (fast && !((tie >> i) & 1u)) continue;
+            long long q = llround(ddiv(get(i), p.delta)) + p.zp;
+            put(i, (int)(q < 0 ? 0 : (q > mx ? mx : q)));
+        }
+    }
 }
 
 // affine fp16 form used by the attention kernel: x = a*code + b
@@ -159,8 +188,8 @@ template <int BITS, int GPAR>
 __global__ void __launch_bounds__(QT * GPAR) quantize_kernel(const QuantizeArgs a) {
     using Blk = Block<BITS>;
     extern __shared__ __align__(16) uint8_t smem[];
-    double *ku = reinterpret_cast<double *>(smem) + (threadIdx.x / QT) * 32 * 129;  // [GPAR][32][129]
-    uint8_t *ck = smem + GPAR * 32 * 129 * 8;                     // [128][128] K codes
+    double *ku = reinterpret_cast<double *>(smem) + (threadIdx.x / QT) * 32 * KU_ROW;  // [GPAR][32][4][33]
+    uint8_t *ck = smem + GPAR * 32 * KU_ROW * 8;                  // [128][128] K codes
     uint8_t *cv = ck + R * D;                                     // [128][128] V codes
     uint8_t *prm = cv + R * D;                                    // params + norms (BYTES - KA_OFF)
     __half *ka = reinterpret_cast<__half *>(prm);
@@ -230,7 +259,7 @@ __global__ void __launch_bounds__(QT * GPAR) quantize_kernel(const QuantizeArgs 
             if (shadow) shadow[SHADOW_K_DOUBLES + SHADOW_V_DOUBLES + t] = s;
         }
 #pragma unroll
-        for (int i = 0; i < 32; ++i) ku[tl * 129 + q * 32 + i] = x[i];
+        for (int i = 0; i < 32; ++i) ku[tl * KU_ROW + q * 33 + i] = x[i];
 
         // ---------------- V: optional rotation, per-token groups ----------------
         {
@@ -246,7 +275,8 @@ __global__ void __launch_bounds__(QT * GPAR) quantize_kernel(const QuantizeArgs 
             if (tc.rotate_v) fht128_quad(y, q);
             const GroupQ p = group_params([&](int i) { return y[i]; }, BITS);
 #pragma unroll
-            for (int i = 0; i < 32; ++i) cv[t * D + q * 32 + i] = quantize_one(y[i], p, BITS);
+            quantize_group([&](int i) { return y[i]; }, p, BITS,
+                           [&](int i, int code) { cv[t * D + q * 32 + i] = (uint8_t)code; });
             __half ha, hb;
             affine16(p, ha, hb);
             va[va_index(t, q)] = ha;
@@ -260,8 +290,10 @@ __global__ void __launch_bounds__(QT * GPAR) quantize_kernel(const QuantizeArgs 
         // ---------------- K: per-channel group of G tokens ----------------
         {
             const int c = tid;  // channel
-            const GroupQ p = group_params([&](int i) { return ku[i * 129 + c]; }, BITS);
-            for (int i = 0; i < G; ++i) ck[(gi * G + i) * D + c] = quantize_one(ku[i * 129 + c], p, BITS);
+            const int cc = (c >> 5) * 33 + (c & 31);
+            const GroupQ p = group_params([&](int i) { return ku[i * KU_ROW + cc]; }, BITS);
+            quantize_group([&](int i) { return ku[i * KU_ROW + cc]; }, p, BITS,
+                           [&](int i, int code) { ck[(gi * G + i) * D + c] = (uint8_t)code; });
             // keys use the same affine form as values, x = a*code + b with
             // b = -delta*zp (a constant group is a = 0, b = lo: its codes are 0,
             // quant.cpp:37-42, 65-68); the attention kernel folds b into one
@@ -364,7 +396,7 @@ __global__ void ring_copy_kernel(const RingCopyArgs a) {
 
 template <int BITS, int GPAR>
 cudaError_t launch_q(const QuantizeArgs &a, dim3 grid, cudaStream_t st) {
-    const int smem = GPAR * 32 * 129 * 8 + 2 * R * D + Block<BITS>::BYTES - Block<BITS>::KA_OFF;
+    const int smem = GPAR * 32 * KU_ROW * 8 + 2 * R * D + Block<BITS>::BYTES - Block<BITS>::KA_OFF;
     static bool init = false;
     if (!init) {
         cudaError_t e = cudaFuncSetAttribute(quantize_kernel<BITS, GPAR>, cudaFuncAttributeMaxDynamicSharedMemorySize,

@@ -303,3 +303,25 @@ def test_decode_step_many_equals_per_cache_calls():
     for a, b in zip(ref, outs):
         assert torch.equal(a, b)
     assert all(c.total_tokens == S + 1 for c in many)
+
+
+def test_quantizer_exact_half_ties_bitexact():
+    """Values landing exactly on half-integers of x/delta (llround's
+    half-away-from-zero ties, quant.cpp:53-57) take the exact-division path of
+    the device quantizer: codes must still equal the reference's."""
+    from paper_2605_19660_b200 import KvCache, PipelineConfig
+
+    H, S = 1, 256
+    rng = np.random.default_rng(5)
+    k, _ = make_inputs(21, S, H)
+    # value groups of {0, 3, +-0.5, 1.5, 2.5, ...}: delta = 1, x/delta hits .5 ties
+    choices = np.array([0.0, 3.0, 0.5, 1.5, 2.5, 1.0, 2.0, -0.0])
+    v = rng.choice(choices, size=(S, H, 128))
+    v[:, :, 0] = 0.0
+    v[:, :, 1] = 3.0
+    for bits in (2, 4):
+        c = KvCache(PipelineConfig(heads=H, bits=bits, method="kivi"), batch=1, q_heads=H, max_tokens=S + 8)
+        c.buffer_quant(dev_bf16(k[None]), dev_bf16(v[None]))
+        o = ob.PortCache(method="kivi", bits=bits, H=H)
+        o.append(k, v)
+        assert ob.caches_equal(export_to_oracle(c.export(0), H), o.export()) == []

@@ -6,7 +6,6 @@ gather_partials call the NCCL launcher makes, the merge is the device
 log-sum-exp kernel.  Reference semantics: the sharded result must equal one
 cache holding the whole context (fp32 merge rounding only)."""
 import os
-import socket
 
 import numpy as np
 import pytest
@@ -18,12 +17,6 @@ pytestmark = pytest.mark.gpu
 S, H, G_, STEPS = 1000, 2, 4, 30  # residual 104 -> the 24th decode step flushes on the tail rank
 
 
-def _free_port():
-    with socket.socket() as s:
-        s.bind(("127.0.0.1", 0))
-        return s.getsockname()[1]
-
-
 def _inputs():
     from paper_2605_19660_b200.synthetic import make_inputs, make_queries
 
@@ -32,17 +25,15 @@ def _inputs():
     return k, v, q
 
 
-def _seq_worker(rank, world, port, res_path):
+def _seq_worker(rank, world, rdzv, res_path):
     import torch
     import torch.distributed as td
 
     from paper_2605_19660_b200 import PipelineConfig
     from paper_2605_19660_b200.sharding import SeqShardedKvCache
 
-    os.environ["MASTER_ADDR"] = "127.0.0.1"
-    os.environ["MASTER_PORT"] = str(port)
     torch.cuda.set_device(0)
-    td.init_process_group("gloo", rank=rank, world_size=world)
+    td.init_process_group("gloo", init_method=f"file://{rdzv}", rank=rank, world_size=world)
     try:
         k, v, q = _inputs()
         c = SeqShardedKvCache(PipelineConfig(heads=H), batch=1, q_heads=H * G_, max_tokens_per_rank=S + STEPS)
@@ -66,7 +57,7 @@ def test_sequence_sharded_decode_matches_single_cache(tmp_path):
     from paper_2605_19660_b200 import KvCache, PipelineConfig
 
     res = str(tmp_path / "seq.npy")
-    mp.spawn(_seq_worker, args=(2, _free_port(), res), nprocs=2, join=True)
+    mp.spawn(_seq_worker, args=(2, str(tmp_path / "rdzv"), res), nprocs=2, join=True)
     sharded = np.load(res)
     k, v, q = _inputs()
     c = KvCache(PipelineConfig(heads=H), batch=1, q_heads=H * G_, max_tokens=S + STEPS)

@@ -3,7 +3,6 @@ bit-exactness of R-aligned sequence shards against the single cache (oracle),
 and the (O, LSE) all-gather + log-sum-exp merge over a world_size-2 gloo
 group.  The device merge kernel itself is covered by the GPU tests."""
 import os
-import socket
 
 import numpy as np
 import pytest
@@ -95,13 +94,11 @@ def _merge(outs, lses):
     return (w[:, :, None] * outs).sum(0) / w.sum(0)[:, None]
 
 
-def _worker(rank, world, port, S, H, g, q, res_path):
+def _worker(rank, world, rdzv, S, H, g, q, res_path):
     import torch
     import torch.distributed as td
 
-    os.environ["MASTER_ADDR"] = "127.0.0.1"
-    os.environ["MASTER_PORT"] = str(port)
-    td.init_process_group("gloo", rank=rank, world_size=world)
+    td.init_process_group("gloo", init_method=f"file://{rdzv}", rank=rank, world_size=world)
     try:
         k, v = make_inputs(41, S, H)
         s = sh.sequence_shard(S, world, rank)
@@ -119,12 +116,6 @@ def _worker(rank, world, port, S, H, g, q, res_path):
         td.destroy_process_group()
 
 
-def _free_port():
-    with socket.socket() as s:
-        s.bind(("127.0.0.1", 0))
-        return s.getsockname()[1]
-
-
 def test_gloo_world2_gather_and_lse_merge(tmp_path):
     """Two ranks attend their R-aligned shards, all-gather (O, LSE) over gloo,
     and the log-sum-exp merge equals attention over the whole cache."""
@@ -133,7 +124,7 @@ def test_gloo_world2_gather_and_lse_merge(tmp_path):
     S, H, g, world = 900, 2, 4, 2
     q = make_queries(41, 1, H * g)[0]
     res = str(tmp_path / "merged.npy")
-    mp.spawn(_worker, args=(world, _free_port(), S, H, g, q, res), nprocs=world, join=True)
+    mp.spawn(_worker, args=(world, str(tmp_path / "rdzv"), S, H, g, q, res), nprocs=world, join=True)
     merged = np.load(res)
     k, v = make_inputs(41, S, H)
     full = ob.PortCache(H=H)

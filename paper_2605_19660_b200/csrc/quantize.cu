@@ -69,11 +69,13 @@ __device__ __forceinline__ void fht128_quad(double (&x)[32], int q) {
     // half = 32: partner quarter q^1; half = 64: partner quarter q^2
 #pragma unroll
     for (int xm = 1; xm <= 2; xm <<= 1) {
-        const bool upper = (q & xm) != 0;
+        // lower lane: a + b; upper lane: a - b with a = partner, b = own value:
+        // fma(+-1, own, partner) rounds once, exactly like dadd / dsub
+        const double sgn = (q & xm) ? -1.0 : 1.0;
 #pragma unroll
         for (int i = 0; i < 32; ++i) {
             const double o = __shfl_xor_sync(0xffffffffu, x[i], xm);
-            x[i] = upper ? dsub(o, x[i]) : dadd(x[i], o);
+            x[i] = __fma_rn(sgn, x[i], o);
         }
     }
     const double scale = ddiv(1.0, __dsqrt_rn(128.0));
@@ -129,6 +131,28 @@ __device__ __forceinline__ GroupQ group_params(Get get, int bits) {
     } else {
         p.delta = ddiv(dsub(hi, lo), (double)((1 << bits) - 1));
         p.zp = llround(ddiv(-lo, p.delta));
+    }
+    return p;
+}
+
+// group_params for values that are exactly representable in fp32
+__device__ __forceinline__ GroupQ group_params_f32(const double (&y)[32], int bits) {
+    float lo = (float)y[0], hi = lo;
+#pragma unroll
+    for (int i = 1; i < 32; ++i) {
+        lo = fminf(lo, (float)y[i]);
+        hi = fmaxf(hi, (float)y[i]);
+    }
+    if (lo == 0.0f || hi == 0.0f) return group_params([&](int i) { return y[i]; }, bits);
+    GroupQ p;
+    p.lo = (double)lo;
+    p.hi = (double)hi;
+    if (p.hi == p.lo) {
+        p.delta = 0.0;
+        p.zp = 0;
+    } else {
+        p.delta = ddiv(dsub(p.hi, p.lo), (double)((1 << bits) - 1));
+        p.zp = llround(ddiv(-p.lo, p.delta));
     }
     return p;
 }
@@ -273,7 +297,11 @@ __global__ void __launch_bounds__(QT * GPAR) quantize_kernel(const QuantizeArgs 
                     y[i] = (double)__uint_as_float((uint32_t)vp[(int64_t)(q * 32 + i) * a.vsc] << 16);
             }
             if (tc.rotate_v) fht128_quad(y, q);
-            const GroupQ p = group_params([&](int i) { return y[i]; }, BITS);
+            // raw (bf16-valued) V: the group range in fp32 is exact, one FMNMX per
+            // element; a zero extreme re-runs the sequential std::min/max so the
+            // sign of a zero constant matches quant.cpp:26-34
+            const GroupQ p = tc.rotate_v ? group_params([&](int i) { return y[i]; }, BITS)
+                                         : group_params_f32(y, BITS);
 #pragma unroll
             quantize_group([&](int i) { return y[i]; }, p, BITS,
                            [&](int i, int code) { cv[t * D + q * 32 + i] = (uint8_t)code; });

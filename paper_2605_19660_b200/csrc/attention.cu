@@ -746,6 +746,17 @@ __global__ void __launch_bounds__(NCW_ * 32, 1) decode_attn_kernel(const AttnArg
                         }
                         fence_proxy_async_smem();
                         issue(p + C::NST, bh2, u2);
+                        // optional L2 prefetch pf_dist units beyond the ring (OSCAR_L2_PREFETCH)
+                        if (a.pf_dist > 0 && p + C::NST + a.pf_dist < nunits) {
+                            int64_t bh3 = bh2, u3 = u2 + a.pf_dist;
+                            while (u3 >= nb) {
+                                u3 -= nb;
+                                ++bh3;
+                            }
+                            bulk_prefetch_l2(a.blocks + (bh3 * a.max_blocks + u3 / SUB) * (int64_t)C::BYTES +
+                                                 (u3 % SUB) * C::STAGE,
+                                             C::STAGE);
+                        }
                     }
                     // no fence needed: a waiter only relies on phase `round` of this
                     // stage being complete, which held before this warp consumed it

@@ -742,7 +742,8 @@ int oscar_kv_decode_step_host(oscar_kv_handle *h, const void *q_host, const void
             attr.srcAccessOrder = cudaMemcpySrcAccessOrderStream;
             attr.flags = cudaMemcpyFlagPreferOverlapWithCompute;
             size_t attr_idx = 0, fail = 0;
-            if (cudaMemcpyBatchAsync(dsts, srcs, sizes, 3, &attr, &attr_idx, 1, &fail, s) != cudaSuccess) {
+            const bool pinned = mapped(q_host) && mapped(k_host) && mapped(v_host);
+            if (!pinned || cudaMemcpyBatchAsync(dsts, srcs, sizes, 3, &attr, &attr_idx, 1, &fail, s) != cudaSuccess) {
                 (void)cudaGetLastError();
                 CK(cudaMemcpyAsync(dq, q_host, qb, cudaMemcpyHostToDevice, s));
                 CK(cudaMemcpyAsync(dk, k_host, kb, cudaMemcpyHostToDevice, s));

@@ -127,9 +127,12 @@ __device__ __forceinline__ long long clk() {
     return c;
 }
 
+// qsm: this lane's row of the segment's rotated-q tile in shared memory (fp16,
+// row gq, offset 2tq); the B fragments are re-read per k-step instead of being
+// held in 16 registers across the block
 template <int BITS>
 __device__ __forceinline__ void process_block(const uint8_t *__restrict__ sb, WarpState &st,
-                                              const uint32_t (&qf)[8][2], int lane, float c0,
+                                              const __half *__restrict__ qsm, int lane, float c0,
                                               long long *tm = nullptr) {
     long long t0 = tm ? clk() : 0;
     using Blk = Block<BITS>;
@@ -164,6 +167,9 @@ __device__ __forceinline__ void process_block(const uint8_t *__restrict__ sb, Wa
 #pragma unroll
             for (int v = 0; v < 4 * WPF; ++v) kwh[v] = kw[v] >> 8;
         }
+        uint32_t qf[8][2];  // only [s] is live
+        qf[s][0] = *reinterpret_cast<const uint32_t *>(qsm + 16 * s);
+        qf[s][1] = *reinterpret_cast<const uint32_t *>(qsm + 16 * s + 8);
         uint32_t bq[4][2];
         {
             const uint4 *p = reinterpret_cast<const uint4 *>(sb + Blk::KA_OFF + (s * 4 + tq) * 32);
@@ -733,7 +739,7 @@ __global__ void __launch_bounds__(NCW_ * 32, 1) decode_attn_kernel(const AttnArg
                 if constexpr (BITS == 0) {
                     process_quarter_bf16(sb, st, qf, lane, c0);
                 } else {
-                    process_block<BITS>(sb, st, qf, lane, c0, a.prof ? tmr : nullptr);
+                    process_block<BITS>(sb, st, qh + gq * QH_STRIDE + 2 * tq, lane, c0, a.prof ? tmr : nullptr);
                 }
                 // stage consumed: refill it with unit p + NST, then publish the round
                 __syncwarp();

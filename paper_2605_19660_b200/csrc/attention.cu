@@ -472,8 +472,16 @@ struct ResidualRefs {
     int g, r, rotate_v;
 };
 
-__device__ __noinline__ void residual_tile(const ResidualRefs rr, float *slot, const __nv_bfloat16 *qbase, int t0,
-                                           int ntok, int lane, float c0) {
+// The tile's partial in registers: o in the packed partial's fragment layout
+// (rows gq / gq+8 of m-tile mm = channels 16mm+gq / +8, cols 2tq / 2tq+1 =
+// heads), m / l per head column in log2 units.
+struct ResPartial {
+    float o[8][4];
+    float m0, m1, l0, l1;
+};
+
+__device__ __forceinline__ void residual_compute(const ResidualRefs rr, const __nv_bfloat16 *qbase, int t0,
+                                                 int ntok, int lane, float c0, ResPartial &rp) {
     const int gq = lane >> 2, tq = lane & 3;
     const int g = rr.g, r = rr.r;
     const uint16_t *ringk = rr.ringk, *ringv = rr.ringv, *kc = rr.kc, *vc = rr.vc;
@@ -488,15 +496,42 @@ __device__ __noinline__ void residual_tile(const ResidualRefs rr, float *slot, c
     auto ld32 = [](const uint16_t *p, int c) -> uint32_t {
         return p ? *reinterpret_cast<const uint32_t *>(p + c) : 0u;
     };
-    // ---- QK^T (raw bf16 q as B: lane holds q[head gq][16s + 2tq (+1), +8 (+9)]) ----
-    float sacc[4] = {0.f, 0.f, 0.f, 0.f};
+    const int u0 = t0 + 2 * tq, u1 = u0 + 8;  // token pairs (u0, u0+1), (u1, u1+1) of this lane
+    auto vpair = [&](int c, int u) -> uint32_t {
+        uint32_t w = (u + 1 < r) ? *reinterpret_cast<const uint32_t *>(ringv + (int64_t)c * R + u) : 0u;
+        if (u + 1 >= r && u < ntok) {  // tail of the window: per-token select ring / current / zero
+            const uint32_t lo = u < r ? ringv[(int64_t)c * R + u] : (u < ntok ? vc[c] : 0u);
+            const uint32_t hi = u + 1 < r ? ringv[(int64_t)c * R + u + 1] : (u + 1 < ntok ? vc[c] : 0u);
+            w = lo | (hi << 16);
+        }
+        return w;
+    };
+    // ---- every global load of the tile up front (one L2 round trip): K rows, raw q
+    //      (B: lane holds q[head gq][16s + 2tq (+1), +8 (+9)]) and the V^T pairs ----
     const uint16_t *qrow = gq < g ? reinterpret_cast<const uint16_t *>(qbase) + gq * D : nullptr;
+    uint32_t kf[8][4], qb[8][2], vf[8][4];
 #pragma unroll
     for (int s = 0; s < 8; ++s) {
         const int c = 16 * s + 2 * tq;
-        mma16816_bf16(sacc, ld32(kA, c), ld32(kB, c), ld32(kA, c + 8), ld32(kB, c + 8), ld32(qrow, c),
-                      ld32(qrow, c + 8));
+        kf[s][0] = ld32(kA, c);
+        kf[s][1] = ld32(kB, c);
+        kf[s][2] = ld32(kA, c + 8);
+        kf[s][3] = ld32(kB, c + 8);
+        qb[s][0] = ld32(qrow, c);
+        qb[s][1] = ld32(qrow, c + 8);
     }
+#pragma unroll
+    for (int mm = 0; mm < 8; ++mm) {
+        const int cA = 16 * mm + gq, cB = cA + 8;
+        vf[mm][0] = vpair(cA, u0);
+        vf[mm][1] = vpair(cB, u0);
+        vf[mm][2] = vpair(cA, u1);
+        vf[mm][3] = vpair(cB, u1);
+    }
+    // ---- QK^T ----
+    float sacc[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+    for (int s = 0; s < 8; ++s) mma16816_bf16(sacc, kf[s][0], kf[s][1], kf[s][2], kf[s][3], qb[s][0], qb[s][1]);
     // logits in log2 units; rows gq / gq+8 = tokens tA / tB; cols 2tq, 2tq+1 = heads
     const bool vA = tA < ntok, vB = tB < ntok;
     sacc[0] = vA ? sacc[0] * c0 : -CUDART_INF_F;
@@ -527,27 +562,24 @@ __device__ __noinline__ void residual_tile(const ResidualRefs rr, float *slot, c
     const uint32_t xb = __shfl_sync(0xffffffffu, X, sbl), yb = __shfl_sync(0xffffffffu, Y, sbl);
     const uint32_t sel = (gq & 1) ? 0x7632u : 0x5410u;
     const uint32_t b0 = __byte_perm(xa, xb, sel), b1 = __byte_perm(ya, yb, sel);
-    // ---- P.V: A = V^T [16 channels x 16 tokens] from the channel-major ring ----
-    const int u0 = t0 + 2 * tq, u1 = u0 + 8;  // token pairs (u0, u0+1), (u1, u1+1) of this lane
-    auto vpair = [&](int c, int u) -> uint32_t {
-        uint32_t w = (u + 1 < r) ? *reinterpret_cast<const uint32_t *>(ringv + (int64_t)c * R + u) : 0u;
-        if (u + 1 >= r && u < ntok) {  // tail of the window: per-token select ring / current / zero
-            const uint32_t lo = u < r ? ringv[(int64_t)c * R + u] : (u < ntok ? vc[c] : 0u);
-            const uint32_t hi = u + 1 < r ? ringv[(int64_t)c * R + u + 1] : (u + 1 < ntok ? vc[c] : 0u);
-            w = lo | (hi << 16);
-        }
-        return w;
-    };
-    float o[8][4];
+    // ---- P.V: A = V^T [16 channels x 16 tokens] ----
 #pragma unroll
     for (int mm = 0; mm < 8; ++mm) {
-        const int cA = 16 * mm + gq, cB = cA + 8;
-        o[mm][0] = o[mm][1] = o[mm][2] = o[mm][3] = 0.f;
-        mma16816_bf16(o[mm], vpair(cA, u0), vpair(cB, u0), vpair(cA, u1), vpair(cB, u1), b0, b1);
+        rp.o[mm][0] = rp.o[mm][1] = rp.o[mm][2] = rp.o[mm][3] = 0.f;
+        mma16816_bf16(rp.o[mm], vf[mm][0], vf[mm][1], vf[mm][2], vf[mm][3], b0, b1);
     }
-    // ---- merge into the slot: O[h][c] unnormalised, m[h], l[h] (log2 units); in
-    //      explicit-V mode the packed partial lives in the rotated space, so this
-    //      (raw-V) partial is rotated head by head first ----
+    rp.m0 = m0;
+    rp.m1 = m1;
+    rp.l0 = l0;
+    rp.l1 = l1;
+}
+
+// merge a tile partial into the warp's slot (read-modify-write); in explicit-V
+// mode the packed partial lives in the rotated space, so the raw-V tile
+// partial is rotated head by head first
+__device__ __forceinline__ void residual_merge(const ResPartial &rp, float *slot, int g, int rotate_v, int lane) {
+    const int gq = lane >> 2, tq = lane & 3;
+    const float m0 = rp.m0, m1 = rp.m1, l0 = rp.l0, l1 = rp.l1;
     __syncwarp();
     const int h0 = 2 * tq, h1 = h0 + 1;
     const float ms0 = slot[8 * D + h0], ms1 = slot[8 * D + h1];
@@ -556,45 +588,44 @@ __device__ __noinline__ void residual_tile(const ResidualRefs rr, float *slot, c
     const float fs0 = (ms0 == -CUDART_INF_F) ? 0.f : fast_exp2(ms0 - M0);
     const float fs1 = (ms1 == -CUDART_INF_F) ? 0.f : fast_exp2(ms1 - M1);
     const float fr0 = fast_exp2(m0 - M0), fr1 = fast_exp2(m1 - M1);
-    if (!rr.rotate_v) {
+    if (!rotate_v) {
 #pragma unroll
         for (int mm = 0; mm < 8; ++mm) {
             const int cA = 16 * mm + gq, cB = cA + 8;
-            slot[h0 * D + cA] = slot[h0 * D + cA] * fs0 + o[mm][0] * fr0;
-            slot[h1 * D + cA] = slot[h1 * D + cA] * fs1 + o[mm][1] * fr1;
-            slot[h0 * D + cB] = slot[h0 * D + cB] * fs0 + o[mm][2] * fr0;
-            slot[h1 * D + cB] = slot[h1 * D + cB] * fs1 + o[mm][3] * fr1;
+            slot[h0 * D + cA] = slot[h0 * D + cA] * fs0 + rp.o[mm][0] * fr0;
+            slot[h1 * D + cA] = slot[h1 * D + cA] * fs1 + rp.o[mm][1] * fr1;
+            slot[h0 * D + cB] = slot[h0 * D + cB] * fs0 + rp.o[mm][2] * fr0;
+            slot[h1 * D + cB] = slot[h1 * D + cB] * fs1 + rp.o[mm][3] * fr1;
         }
-    } else {
-        // rescale the packed partial, then add the rotated residual partial head by head
-        float *part = slot + 8 * D + 16;  // 2 x 128 floats of scratch reserved after m/l
+    }
+    // rotate_v: rescale the packed partial, then add the rotated residual partial head by head
+    float *part = slot + 8 * D + 16;  // 128 floats of scratch reserved after m/l
 #pragma unroll
-        for (int mm = 0; mm < 8; ++mm) {
-            const int cA = 16 * mm + gq, cB = cA + 8;
-            slot[h0 * D + cA] *= fs0;
-            slot[h1 * D + cA] *= fs1;
-            slot[h0 * D + cB] *= fs0;
-            slot[h1 * D + cB] *= fs1;
-        }
-        for (int h = 0; h < g; ++h) {
-            __syncwarp();
-            if ((h >> 1) == tq) {
-                const bool e = (h & 1) != 0;
-                const float f = e ? fr1 : fr0;
+    for (int mm = 0; mm < 8 && rotate_v; ++mm) {
+        const int cA = 16 * mm + gq, cB = cA + 8;
+        slot[h0 * D + cA] *= fs0;
+        slot[h1 * D + cA] *= fs1;
+        slot[h0 * D + cB] *= fs0;
+        slot[h1 * D + cB] *= fs1;
+    }
+    for (int h = 0; h < g && rotate_v; ++h) {
+        __syncwarp();
+        if ((h >> 1) == tq) {
+            const bool e = (h & 1) != 0;
+            const float f = e ? fr1 : fr0;
 #pragma unroll
-                for (int mm = 0; mm < 8; ++mm) {
-                    part[16 * mm + gq] = (e ? o[mm][1] : o[mm][0]) * f;
-                    part[16 * mm + gq + 8] = (e ? o[mm][3] : o[mm][2]) * f;
-                }
+            for (int mm = 0; mm < 8; ++mm) {
+                part[16 * mm + gq] = (e ? rp.o[mm][1] : rp.o[mm][0]) * f;
+                part[16 * mm + gq + 8] = (e ? rp.o[mm][3] : rp.o[mm][2]) * f;
             }
-            __syncwarp();
-            float x[4];
-#pragma unroll
-            for (int e = 0; e < 4; ++e) x[e] = part[4 * lane + e];
-            fht128_warp(x, lane);
-#pragma unroll
-            for (int e = 0; e < 4; ++e) slot[h * D + 4 * lane + e] += x[e];
         }
+        __syncwarp();
+        float x[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) x[e] = part[4 * lane + e];
+        fht128_warp(x, lane);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) slot[h * D + 4 * lane + e] += x[e];
     }
     __syncwarp();
     if (gq == 0) {
@@ -604,6 +635,15 @@ __device__ __noinline__ void residual_tile(const ResidualRefs rr, float *slot, c
         slot[8 * D + 8 + h1] = ls1 * fs1 + l1 * fr1;
     }
     __syncwarp();
+}
+
+// One 16-token tile [t0, t0+16) of the residual window (+ the current token at
+// index r), merged into the warp's partial slot.
+__device__ __noinline__ void residual_tile(const ResidualRefs rr, float *slot, const __nv_bfloat16 *qbase, int t0,
+                                           int ntok, int lane, float c0) {
+    ResPartial rp;
+    residual_compute(rr, qbase, t0, ntok, lane, c0, rp);
+    residual_merge(rp, slot, rr.g, rr.rotate_v, lane);
 }
 
 template <int BITS, int NCW_>
@@ -623,7 +663,7 @@ __global__ void __launch_bounds__(NCW_ * 32, 1) decode_attn_kernel(const AttnArg
     const int64_t nb = a.nb * SUB;  // pipeline units per (b, kv head)
     const int64_t total = (int64_t)a.BH * nb;
     int64_t start = 0, end = 0;
-    const Split sp{nb, a.BH, a.ncta, a.seg_cost};
+    const Split sp{nb, a.BH, a.ncta, a.seg_cost, a.tail_cost};
     if (total > 0) {
         start = sp.begin(cta);
         end = sp.end(cta);
@@ -812,9 +852,10 @@ __global__ void __launch_bounds__(NCW_ * 32, 1) decode_attn_kernel(const AttnArg
 
         // ---- residual window + current token on the tensor cores (bf16 mma, raw q . raw k:
         //      the key transform is orthonormal up to the stored norm, so attending the raw
-        //      bf16 rows IS attend_one over the full-precision residual, pipeline.cpp:152-180),
-        //      one 16-token tile per warp, merged into that warp's slot; the tiles of
-        //      successive tail segments of this CTA rotate over the warps ----
+        //      bf16 rows IS attend_one over the full-precision residual, pipeline.cpp:152-180):
+        //      one 16-token tile per warp of the tail owner (all its loads in one round trip),
+        //      merged into the warp's slot; the tiles of successive tail segments of this CTA
+        //      rotate over the warps ----
         if (owns_tail) {
             const int ntok = a.r + (a.kcur ? 1 : 0);
             const int ntiles = (ntok + 15) >> 4;

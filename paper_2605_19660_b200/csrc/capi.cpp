@@ -274,6 +274,15 @@ struct oscar_kv_handle {
                 sc = e ? atoll(e) : 3;
             }
             a.seg_cost = sc;
+            // the residual-window tiles (one 16-token tile per warp of the tail owner)
+            // cost that CTA about half a unit per warp: charge it OSCAR_TAIL_COST units
+            static int64_t tcost = -1;
+            if (tcost < 0) {
+                const char *e = getenv("OSCAR_TAIL_COST");
+                tcost = e ? atoll(e) : 6;
+            }
+            const int ntok = (int)residual + (kc ? 1 : 0);
+            a.tail_cost = ntok > 0 ? tcost : 0;
         }
         a.pdl_prefetch = blocks_written ? 0 : 1;
         a.maxp = maxp_alloc;
@@ -282,7 +291,7 @@ struct oscar_kv_handle {
             const int64_t nbs = a.nb * (dbits == 0 ? 4 : 1);  // pipeline units per (b, kv head)
             const int64_t total = nbs * a.BH;
             (void)total;
-            const Split sp{nbs, a.BH, a.ncta, a.seg_cost};
+            const Split sp{nbs, a.BH, a.ncta, a.seg_cost, a.tail_cost};
             int64_t need = 0;
             for (int64_t bh = 0; bh < a.BH; ++bh)
                 need = std::max(need, sp.cta_of((bh + 1) * nbs - 1) - sp.cta_of(bh * nbs) + 1);
@@ -392,7 +401,7 @@ struct oscar_kv_handle {
                     if (FILE *f = std::fopen(fn, "w")) {
                         std::fprintf(f, "cta,smid,units,segments,tails,slowest_warp_cycles\n");
                         const int64_t nbu = a.nb * (dbits == 0 ? 4 : 1);
-                        const Split sp{nbu, a.BH, a.ncta, a.seg_cost};
+                        const Split sp{nbu, a.BH, a.ncta, a.seg_cost, a.tail_cost};
                         for (int c = 0; c < a.ncta; ++c) {
                             double hi = 0;
                             unsigned long long sm = 0;

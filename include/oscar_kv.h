@@ -133,6 +133,15 @@ int oscar_kv_export(oscar_kv_handle *h, int64_t b, oscar_kv_export_t *out);
  * the reference's KvCache::load. */
 int oscar_kv_dump(oscar_kv_handle *h, int64_t b, const char *path);
 
+/* KvCache::load (kv_cache.cpp:509-549): sequence b of the handle from a KVC1
+ * file (written by the reference's KvCache::dump or oscar_kv_dump).  The
+ * config (method, bits, G, R, scaling, H, d_h) must match; a fresh handle
+ * adopts the file's token counts, a filled one must already hold the same
+ * counts (one handle = sequences of equal length).  Residual rows and the
+ * bits-0 raw rows must be the transform of bf16 inputs (verified bit for
+ * bit); quantized blocks need keep_exact.  Synchronous. */
+int oscar_kv_load(oscar_kv_handle *h, int64_t b, const char *path);
+
 /* materialize_k / materialize_v (kv_cache.cpp:327-381) of sequence b into
  * host fp64 [total, H, d] buffers (a debug/parity path, not the hot path). */
 int oscar_kv_materialize(oscar_kv_handle *h, int64_t b, double *k_out, double *v_out);

@@ -104,6 +104,8 @@ public:
     }
     // KvCache::dump (kv_cache.cpp:469-507) of sequence b
     void dump(int64_t b, const std::string &path) { check(oscar_kv_dump(h_, b, path.c_str())); }
+    // KvCache::load (kv_cache.cpp:509-549) into sequence b
+    void load(int64_t b, const std::string &path) { check(oscar_kv_load(h_, b, path.c_str())); }
     // materialize_k / materialize_v (kv_cache.cpp:327-381) of sequence b, fp64 [total, H, d]
     std::pair<std::vector<double>, std::vector<double>> materialize(int64_t b) {
         const size_t n = (size_t)(total_tokens() * cfg_.heads * cfg_.head_dim);

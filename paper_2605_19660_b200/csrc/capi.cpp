@@ -609,6 +609,319 @@ const char *scaling_name(int s) {
     return n[s];
 }
 
+// ---------------------------------------------------------------------------
+// KVC1 import (KvCache::load, kv_cache.cpp:509-549): reference layout -> device
+// records, exact shadow and residual rings.
+
+// manifest scalar lookup (the manifest is one flat JSON object; the nested
+// k_blocks / v_blocks arrays are implied by the config and checked by size)
+struct Manifest {
+    std::string text;
+    std::string raw(const std::string &key) const {
+        const std::string k = "\"" + key + "\":";
+        const size_t p = text.find(k);
+        if (p == std::string::npos) throw InvalidArg("cache load: manifest lacks " + key);
+        size_t b = p + k.size(), e = b;
+        if (text[b] == '"') {
+            e = text.find('"', b + 1);
+            return text.substr(b + 1, e - b - 1);
+        }
+        while (e < text.size() && text[e] != ',' && text[e] != '}') ++e;
+        return text.substr(b, e - b);
+    }
+    int64_t i(const std::string &key) const { return std::stoll(raw(key)); }
+    bool flag(const std::string &key) const { return raw(key) == "true"; }
+};
+
+// IEEE double -> binary16, round to nearest even (what __double2half does)
+uint16_t double_to_half_rn(double x) {
+    uint64_t u;
+    std::memcpy(&u, &x, 8);
+    const uint16_t sign = (uint16_t)((u >> 48) & 0x8000u);
+    const int exp = (int)((u >> 52) & 0x7ff);
+    const uint64_t man = u & ((1ull << 52) - 1);
+    if (exp == 0x7ff) return sign | 0x7c00u | (man ? 0x200u : 0u);
+    if (exp == 0) return sign;  // double subnormals are far below the half range
+    const uint64_t m = man | (1ull << 52);
+    const int e = exp - 1023;
+    int shift, he;
+    if (e >= -14) {
+        shift = 42;
+        he = e + 15;
+    } else {
+        shift = 28 - e;  // subnormal: units of 2^-24
+        he = 0;
+    }
+    if (shift > 63) return sign;
+    uint64_t q = m >> shift;
+    const uint64_t rem = m & ((1ull << shift) - 1), half = 1ull << (shift - 1);
+    if (rem > half || (rem == half && (q & 1))) ++q;
+    if (he > 0) {
+        if (q == 2048) {
+            q = 1024;
+            ++he;
+        }
+        if (he >= 31) return sign | 0x7c00u;
+        return sign | (uint16_t)(he << 10) | (uint16_t)(q & 0x3ffu);
+    }
+    return sign | (uint16_t)q;  // q == 1024 is the smallest normal, encoded naturally
+}
+
+uint16_t double_to_bf16_near(double x) {  // x within a few ulp of a bf16 value
+    const float f = (float)x;
+    uint32_t u;
+    std::memcpy(&u, &f, 4);
+    u += 0x7fffu + ((u >> 16) & 1u);
+    return (uint16_t)(u >> 16);
+}
+
+// (delta, zp, constant) -> a (lo, hi) pair the shadow can hold, such that
+// quant.cpp:37-46 recomputes exactly this delta and zp (export / dump stay exact)
+void lohi_from_params(double delta, int64_t zp, double constant, int bits, double &lo, double &hi) {
+    lo = constant;
+    if (delta == 0.0) {
+        if (zp != 0) throw InvalidArg("cache load: constant group with a non-zero zero point");
+        hi = lo;
+        return;
+    }
+    const double lv = (double)((int64_t{1} << bits) - 1);
+    double up = lo + delta * lv, dn = up;
+    for (int k = 0; k < 32; ++k) {  // the nearest hi (in ulps) with (hi - lo) / lv == delta
+        for (const double cand : {up, dn}) {
+            double d2, cst;
+            int64_t z2;
+            host::params_from_lohi(lo, cand, bits, d2, z2, cst);
+            if (d2 == delta) {
+                if (z2 != zp) throw InvalidArg("cache load: zero point inconsistent with delta and constant");
+                hi = cand;
+                return;
+            }
+        }
+        up = std::nextafter(up, INFINITY);
+        dn = std::nextafter(dn, -INFINITY);
+    }
+    throw InvalidArg("cache load: no (lo, hi) reproduces the stored delta");
+}
+
+// raw bf16 key row from the stored transformed row K_u and its norm (inverse of
+// apply_method), verified by replaying the forward transform bit for bit
+void raw_key_row(const double *ku, double s, const TransformCfg &tc, int scaling, uint16_t *out) {
+    double x[D], y[D];
+    for (int c = 0; c < D; ++c) x[c] = tc.scales ? ku[c] * s : ku[c];
+    if (tc.rotates) host::fht(x, D);
+    for (int c = 0; c < D; ++c) {
+        out[c] = double_to_bf16_near(x[c]);
+        y[c] = host::bf16_to_double(out[c]);
+    }
+    if (tc.rotates) host::fht(y, D);
+    double s2 = 1.0;
+    if (tc.scales) s2 = host::token_scale(y, D, scaling);
+    for (int c = 0; c < D; ++c)
+        if (y[c] != ku[c]) throw InvalidArg("cache load: residual key rows are not the transform of bf16 keys");
+    if (tc.scales && s2 != s) throw InvalidArg("cache load: residual key norms are not the bf16 keys' norms");
+}
+
+void raw_value_row(const double *v, int rotate_v, uint16_t *out) {
+    double x[D], y[D];
+    for (int c = 0; c < D; ++c) x[c] = v[c];
+    if (rotate_v) host::fht(x, D);
+    for (int c = 0; c < D; ++c) {
+        out[c] = double_to_bf16_near(x[c]);
+        y[c] = host::bf16_to_double(out[c]);
+    }
+    if (rotate_v) host::fht(y, D);
+    for (int c = 0; c < D; ++c)
+        if (y[c] != v[c]) throw InvalidArg("cache load: value rows are not bf16-representable");
+}
+
+template <typename T>
+std::vector<T> read_vec(std::ifstream &f, size_t n) {
+    std::vector<T> v(n);
+    f.read(reinterpret_cast<char *>(v.data()), (std::streamsize)(n * sizeof(T)));
+    if (!f) throw InvalidArg("cache load: file too short");
+    return v;
+}
+
+void load_kvc1(oscar_kv_handle *h, int64_t b, const char *path) {
+    if (b < 0 || b >= h->B) throw InvalidArg("load: sequence index out of range");
+    std::ifstream f(path, std::ios::binary);
+    if (!f) throw std::runtime_error(std::string("cache load: cannot open ") + path);
+    Manifest m;
+    std::getline(f, m.text);
+    if (m.raw("magic") != "KVC1") throw std::runtime_error("cache load: bad magic");
+    const oscar_kv_config &c = h->cfg;
+    if (m.i("R") != c.residual_len || m.i("G") != c.group_size || m.i("b") != c.bits || m.i("H") != c.heads ||
+        m.i("d_h") != c.head_dim || m.raw("method") != method_name(c.method) ||
+        m.raw("scaling") != scaling_name(c.scaling))
+        throw InvalidArg("cache load: file was written under a different config");
+    const int64_t packed = m.i("S_packed"), r = m.i("residual_tokens"), flushes = m.i("flush_count");
+    if (m.i("S_packed_v") != packed || m.i("v_residual_tokens") != r)
+        throw InvalidArg("cache load: key and value streams differ in length");
+    if (packed % R || r < 0 || r >= R) throw InvalidArg("cache load: inconsistent token counts");
+    if (packed + r > h->max_tokens) throw InvalidArg("cache load: cache capacity exceeded");
+    if (!h->prefilled) {
+        h->packed = packed;
+        h->residual = r;
+        h->flushes = flushes;
+        h->prefilled = m.flag("k_prefilled");
+    } else if (h->packed != packed || h->residual != r) {
+        throw InvalidArg("cache load: sequences of one handle must hold the same number of tokens");
+    }
+    if (h->dbits && !h->keep_exact) throw InvalidArg("cache load: handle created without keep_exact");
+    const int64_t H = c.heads, nb = packed / R;
+    const int bits = h->dbits;
+    const TransformCfg tc = h->tc();
+    const int64_t kp = D * (R / G), vp = R * (D / G);
+    struct Blk {
+        std::vector<double> delta, cst, raw;
+        std::vector<int64_t> zp;
+        std::vector<uint16_t> codes;  // reference order
+    };
+    auto read_block = [&](int64_t nparams) {
+        Blk k;
+        if (bits) {
+            k.delta.resize(nparams);
+            k.zp.resize(nparams);
+            k.cst.resize(nparams);
+            for (int64_t i = 0; i < nparams; ++i) {
+                f.read(reinterpret_cast<char *>(&k.delta[i]), 8);
+                f.read(reinterpret_cast<char *>(&k.zp[i]), 8);
+                f.read(reinterpret_cast<char *>(&k.cst[i]), 8);
+            }
+            if (bits == 2) {
+                auto w = read_vec<uint16_t>(f, R * D / 8);
+                k.codes.resize(R * D);
+                for (int64_t i = 0; i < R * D; ++i) k.codes[i] = (uint16_t)((w[i / 8] >> (2 * (i % 8))) & 3u);
+            } else {
+                k.codes = read_vec<uint16_t>(f, R * D);
+            }
+            if (!f) throw InvalidArg("cache load: file too short");
+        } else {
+            k.raw = read_vec<double>(f, R * D);
+        }
+        return k;
+    };
+    std::vector<std::vector<Blk>> kb(H), vb(H);
+    std::vector<std::vector<double>> knorm(H);
+    for (int64_t hh = 0; hh < H; ++hh) {
+        for (int64_t k = 0; k < nb; ++k) kb[hh].push_back(read_block(kp));
+        knorm[hh] = read_vec<double>(f, packed);
+    }
+    const auto kres = read_vec<double>(f, r * H * D);
+    const auto kres_n = read_vec<double>(f, r * H);
+    for (int64_t hh = 0; hh < H; ++hh)
+        for (int64_t k = 0; k < nb; ++k) vb[hh].push_back(read_block(vp));
+    const auto vres = read_vec<double>(f, r * H * D);
+
+    CK(cudaSetDevice(h->device));
+    if (h->last_stream) CK(cudaStreamSynchronize(h->last_stream));
+    std::vector<uint8_t> rec(h->block_bytes);
+    std::vector<double> sh(SHADOW_DOUBLES);
+    for (int64_t hh = 0; hh < H; ++hh) {
+        const int64_t bh = b * H + hh;
+        for (int64_t k = 0; k < nb; ++k) {
+            const Blk &K = kb[hh][k], &V = vb[hh][k];
+            std::fill(rec.begin(), rec.end(), 0);
+            if (bits) {
+                const int tpw = 16 / bits;
+                const int64_t code_bytes = (int64_t)R * D * bits / 8;
+                uint32_t *kw = reinterpret_cast<uint32_t *>(rec.data());
+                uint32_t *vw = reinterpret_cast<uint32_t *>(rec.data() + code_bytes);
+                const uint32_t maxc = (1u << bits) - 1;
+                for (int w = 0; w < (int)(code_bytes / 4); ++w)
+                    for (int hi = 0; hi < 2; ++hi)
+                        for (int fl = 0; fl < tpw; ++fl) {
+                            int t, ch;
+                            const int s_ = hi * 16 + fl * bits;
+                            k_word_coords(bits, w, fl, hi, t, ch);
+                            const uint32_t ck = K.codes[(size_t)ch * R + t];
+                            v_word_coords(bits, w, fl, hi, t, ch);
+                            const uint32_t cv = V.codes[(size_t)t * D + ch];
+                            if (ck > maxc || cv > maxc) throw InvalidArg("cache load: code out of range");
+                            kw[w] |= ck << s_;
+                            vw[w] |= cv << s_;
+                        }
+                const int ka_off = bits == 2 ? Block<2>::KA_OFF : Block<4>::KA_OFF;
+                const int kb_off = bits == 2 ? Block<2>::KB_OFF : Block<4>::KB_OFF;
+                const int va_off = bits == 2 ? Block<2>::VA_OFF : Block<4>::VA_OFF;
+                const int vb_off = bits == 2 ? Block<2>::VB_OFF : Block<4>::VB_OFF;
+                const int nr_off = bits == 2 ? Block<2>::NORM_OFF : Block<4>::NORM_OFF;
+                uint16_t *pka = reinterpret_cast<uint16_t *>(rec.data() + ka_off);
+                uint16_t *pkb = reinterpret_cast<uint16_t *>(rec.data() + kb_off);
+                uint16_t *pva = reinterpret_cast<uint16_t *>(rec.data() + va_off);
+                uint16_t *pvb = reinterpret_cast<uint16_t *>(rec.data() + vb_off);
+                float *pn = reinterpret_cast<float *>(rec.data() + nr_off);
+                // affine16 (quantize.cu): a = delta, b = delta * -zp; constant group a = 0, b = lo
+                auto affine = [&](double dl, int64_t zp, double cst, uint16_t &a, uint16_t &bb) {
+                    if (dl == 0.0) {
+                        a = double_to_half_rn(0.0);
+                        bb = double_to_half_rn(cst);
+                    } else {
+                        a = double_to_half_rn(dl);
+                        bb = double_to_half_rn(dl * -(double)zp);
+                    }
+                };
+                for (int ch = 0; ch < D; ++ch)
+                    for (int grp = 0; grp < NGRP; ++grp) {
+                        const int p = ch * (R / G) + grp;
+                        affine(K.delta[p], K.zp[p], K.cst[p], pka[ka_index(ch, grp)], pkb[kb_index(ch, grp)]);
+                        lohi_from_params(K.delta[p], K.zp[p], K.cst[p], bits, sh[(ch * NGRP + grp) * 2],
+                                         sh[(ch * NGRP + grp) * 2 + 1]);
+                    }
+                for (int t = 0; t < R; ++t)
+                    for (int gc = 0; gc < NGC; ++gc) {
+                        const int p = t * (D / G) + gc;
+                        affine(V.delta[p], V.zp[p], V.cst[p], pva[va_index(t, gc)], pvb[vb_index(t, gc)]);
+                        lohi_from_params(V.delta[p], V.zp[p], V.cst[p], bits, sh[SHADOW_K_DOUBLES + (t * NGC + gc) * 2],
+                                         sh[SHADOW_K_DOUBLES + (t * NGC + gc) * 2 + 1]);
+                    }
+                for (int t = 0; t < R; ++t) {
+                    const double s = knorm[hh][k * R + t];
+                    pn[norm_index(t)] = (float)(s * 0.12751743074202186);  // log2(e)/sqrt(d), as quantize.cu
+                    sh[SHADOW_K_DOUBLES + SHADOW_V_DOUBLES + t] = s;
+                }
+                CK(cudaMemcpy(h->shadow + (bh * h->max_blocks + k) * SHADOW_DOUBLES, sh.data(),
+                              sizeof(double) * SHADOW_DOUBLES, cudaMemcpyHostToDevice));
+            } else {
+                // raw block: transformed rows -> raw bf16 rows -> fragment order
+                std::vector<uint16_t> kraw(R * D), vraw(R * D);
+                for (int t = 0; t < R; ++t) {
+                    raw_key_row(&K.raw[(size_t)t * D], knorm[hh][k * R + t], tc, c.scaling, &kraw[(size_t)t * D]);
+                    raw_value_row(&V.raw[(size_t)t * D], c.rotate_v, &vraw[(size_t)t * D]);
+                }
+                constexpr int QW = BF16_QUARTER_BYTES / 8;
+                for (int qu = 0; qu < 4; ++qu) {
+                    uint32_t *qw = reinterpret_cast<uint32_t *>(rec.data() + qu * BF16_QUARTER_BYTES);
+                    for (int w = 0; w < QW; ++w)
+                        for (int hi = 0; hi < 2; ++hi) {
+                            int t, ch;
+                            bf16_k_coords(w, hi, t, ch);
+                            qw[w] |= (uint32_t)kraw[(qu * 32 + t) * D + ch] << (16 * hi);
+                            bf16_v_coords(w, hi, t, ch);
+                            qw[QW + w] |= (uint32_t)vraw[(qu * 32 + t) * D + ch] << (16 * hi);
+                        }
+                }
+            }
+            CK(cudaMemcpy(h->blocks + (bh * h->max_blocks + k) * h->block_bytes, rec.data(), h->block_bytes,
+                          cudaMemcpyHostToDevice));
+        }
+        // residual window -> raw bf16 rings (K token-major, V channel-major)
+        if (r > 0) {
+            std::vector<uint16_t> rk((size_t)R * D, 0), rv((size_t)R * D, 0), row(D);
+            for (int64_t t = 0; t < r; ++t) {
+                raw_key_row(&kres[(t * H + hh) * D], kres_n[t * H + hh], tc, c.scaling, &rk[t * D]);
+                raw_value_row(&vres[(t * H + hh) * D], c.rotate_v, row.data());
+                for (int ch = 0; ch < D; ++ch) rv[(size_t)ch * R + t] = row[ch];
+            }
+            CK(cudaMemcpy(reinterpret_cast<uint16_t *>(h->ring_k) + bh * R * D, rk.data(), sizeof(uint16_t) * R * D,
+                          cudaMemcpyHostToDevice));
+            CK(cudaMemcpy(reinterpret_cast<uint16_t *>(h->ring_v) + bh * R * D, rv.data(), sizeof(uint16_t) * R * D,
+                          cudaMemcpyHostToDevice));
+        }
+    }
+    h->blocks_written = true;  // the next attention launch waits before touching the records
+}
+
 }  // namespace
 
 // ===========================================================================
@@ -922,6 +1235,13 @@ int oscar_kv_dump(oscar_kv_handle *h, int64_t b, const char *path) {
         for (int64_t hh = 0; hh < H; ++hh) write_blocks(true, hh);
         f.write(reinterpret_cast<const char *>(hc.v_res.data()), (std::streamsize)(hc.v_res.size() * 8));
         if (!f) throw std::runtime_error("cache dump: write failed");
+    });
+}
+
+int oscar_kv_load(oscar_kv_handle *h, int64_t b, const char *path) {
+    return guard([&] {
+        if (!h || !path) throw InvalidArg("null argument");
+        load_kvc1(h, b, path);
     });
 }
 

@@ -81,6 +81,7 @@ def lib():
         L.oscar_kv_memory_report.argtypes = [_P, ctypes.POINTER(_MemReport)]
         L.oscar_kv_export.argtypes = [_P, ctypes.c_int64, ctypes.POINTER(_Export)]
         L.oscar_kv_dump.argtypes = [_P, ctypes.c_int64, ctypes.c_char_p]
+        L.oscar_kv_load.argtypes = [_P, ctypes.c_int64, ctypes.c_char_p]
         L.oscar_kv_materialize.argtypes = [_P, ctypes.c_int64, _P, _P]
         L.oscar_lse_merge.argtypes = [_P, _P, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64, _P, _P, _P]
         L.oscar_kv_last_launch_count.argtypes = [_P]
@@ -92,7 +93,7 @@ def lib():
 C_ABI_SYMBOLS = [
     "oscar_last_error", "oscar_kv_config_validate", "oscar_kv_create", "oscar_kv_destroy", "oscar_kv_append",
     "oscar_kv_decode_step", "oscar_kv_decode_step_many", "oscar_kv_attend", "oscar_kv_decode_step_host", "oscar_kv_stats",
-    "oscar_kv_memory_report", "oscar_kv_export", "oscar_kv_dump", "oscar_kv_materialize", "oscar_lse_merge",
+    "oscar_kv_memory_report", "oscar_kv_export", "oscar_kv_dump", "oscar_kv_load", "oscar_kv_materialize", "oscar_lse_merge",
     "oscar_kv_last_launch_count",
 ]
 
@@ -274,6 +275,10 @@ class KvCache:
     def dump(self, b: int, path: str):
         """KvCache::dump (kv_cache.cpp:469-507) for sequence b."""
         _check(lib().oscar_kv_dump(self._h, b, path.encode()))
+
+    def load(self, b: int, path: str):
+        """KvCache::load (kv_cache.cpp:509-549) into sequence b."""
+        _check(lib().oscar_kv_load(self._h, b, path.encode()))
 
     def materialize(self, b: int = 0):
         """materialize_k / materialize_v (kv_cache.cpp:327-381) of sequence b."""

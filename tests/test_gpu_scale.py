@@ -62,3 +62,26 @@ def test_large_cache_parity(bits):
             mine.k_norms_residual = theirs.k_norms_residual
             mine.v_residual = theirs.v_residual
             assert ob.caches_equal(mine, theirs) == []
+
+
+def test_long_context_gqa7_many_partials():
+    """C5-like shape at 64K: one sequence, 4 KV heads x 7 query heads (Qwen2.5
+    GQA), so each (b, kv head) is split over ~37 CTAs and the final merge
+    combines many partials; checked against the CPU oracle."""
+    import torch
+
+    from paper_2605_19660_b200 import KvCache, PipelineConfig
+
+    B, S, H, g = 1, 65536, 4, 7
+    k, v = _torch_inputs(B, S + 1, H, 91)
+    q = torch.randn((B, H * g, 128), device="cuda").to(torch.bfloat16)
+    cache = KvCache(PipelineConfig(heads=H, bits=2), batch=B, q_heads=H * g, max_tokens=S + 8)
+    cache.buffer_quant(k[:, :S].contiguous(), v[:, :S].contiguous())
+    out = cache.decode_step(q, k[:, S].contiguous(), v[:, S].contiguous()).cpu().numpy()
+    o = ob.PortCache(H=H, bits=2)
+    kb, vb = _np(k[0]), _np(v[0])
+    o.append(kb[:S], vb[:S])
+    ref = o.decode_step(_np(q[0]), kb[S], vb[S], g, append=False)
+    err = rel_err(out[0].astype(np.float64), ref)
+    log_err("long_context[bits=2][B=1,S=65536,H=4,g=7]", err)
+    assert err <= ATOL_REL[2], err

@@ -458,6 +458,7 @@ def cpu_baseline(S, Hq, Hkv, n_steps=3, heads_sample=None):
     from oracle import bindings as ob
 
     kind = "reference" if ob.ref_available() else "port"
+    cores = ob.ref_use_threads(cpu_threads()) if kind == "reference" else 1
     H = heads_sample or Hkv
     g = Hq // Hkv
     rng = np.random.default_rng(5)
@@ -479,7 +480,7 @@ def cpu_baseline(S, Hq, Hkv, n_steps=3, heads_sample=None):
     dt = time.perf_counter() - t0
     frac = H / Hkv
     del rng
-    return {"value": frac * n_steps / dt, "unit": "tokens/s", "cores": cpu_threads(), "kind": kind,
+    return {"value": frac * n_steps / dt, "unit": "tokens/s", "cores": cores, "kind": kind,
             "sample": f"1 sequence x {H}/{Hkv} KV heads ({H * g} q heads) at {S} ctx, {n_steps} decode steps "
                       f"(apply_method + materialize_k/v + attention + buffer_quant; prefill {prefill_s:.1f}s untimed)",
             "s_per_step": dt / n_steps}
@@ -496,6 +497,7 @@ def run_reference(args):
     S, Hq, Hkv, K, W = args.ctx, args.q_heads, args.kv_heads, args.steps, args.warmup
     g = Hq // Hkv
     kind = "reference" if ob.ref_available() else "port"
+    cores = ob.ref_use_threads(cpu_threads()) if kind == "reference" else 1  # torchrun exports OMP_NUM_THREADS=1
     mk = ob.RefCache if kind == "reference" else ob.PortCache
     # bounded sample: one sequence, as many KV heads as fit ~150 s for W+K steps
     probe_k, probe_v = make_inputs(3, S + 2, 1)
@@ -538,7 +540,7 @@ def run_reference(args):
         "data": "synthetic (TNI-recipe keys, N(0,1) values/queries), bf16-representable",
         "config": {"workload": f"C2 layer shape ({Hq} q / {Hkv} kv heads, d=128), {S} ctx, INT2, G=32, R=128 "
                                f"(CPU sample of one sequence)", "context": S, "bits": 2},
-        "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": cpu_threads(), "kind": kind,
+        "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": cores, "kind": kind,
                          "sample": sample},
         "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -664,6 +666,10 @@ def main():
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    # test hook: run every rank on one device over gloo (the multi-rank code path
+    # on a single-GPU box); never set for measurements
+    if os.environ.get("OSCAR_BENCH_ONE_DEVICE"):
+        local_rank = 0
     if args.impl == "reference":
         if rank != 0:
             return
@@ -674,7 +680,10 @@ def main():
         import torch.distributed as td
 
         torch.cuda.set_device(local_rank)
-        td.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        if os.environ.get("OSCAR_BENCH_ONE_DEVICE"):
+            td.init_process_group("gloo")
+        else:
+            td.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     res = run_ours(args, rank, world, local_rank) if args.config == "c2" else run_config(args, rank, world, local_rank)
     if rank == 0:
         print(json.dumps(res), flush=True)

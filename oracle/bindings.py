@@ -49,6 +49,12 @@ def ref_available() -> bool:
     return os.path.exists(REF_SO)
 
 
+def ref_use_threads(n: int) -> int:
+    """Run the compiled reference's OpenMP regions on n threads (all host
+    cores for the CPU baseline); returns the thread count in effect."""
+    return int(Ref.lib().ref_set_num_threads(int(n)))
+
+
 # --------------------------------------------------------------------------
 @dataclass
 class ExportedCache:
@@ -176,6 +182,8 @@ class Ref(_Lib):
         L.ref_attention.argtypes = [_dp, ctypes.c_int64, _dp, _dp, ctypes.c_int64, ctypes.c_int64,
                                     ctypes.c_int64, _dp]
         L.ref_num_threads.restype = ctypes.c_int
+        L.ref_set_num_threads.restype = ctypes.c_int
+        L.ref_set_num_threads.argtypes = [ctypes.c_int]
 
     @classmethod
     def check(cls, rc):

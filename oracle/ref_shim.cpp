@@ -304,4 +304,16 @@ int ref_num_threads() {
 #endif
 }
 
+// the CPU baseline uses every host core regardless of OMP_NUM_THREADS set by a
+// launcher (torchrun exports 1); returns the threads now in effect
+int ref_set_num_threads(int n) {
+#ifdef _OPENMP
+    if (n > 0) omp_set_num_threads(n);
+    return omp_get_max_threads();
+#else
+    (void)n;
+    return 1;
+#endif
+}
+
 }  // extern "C"

@@ -957,11 +957,12 @@ __global__ void __launch_bounds__(NCW_ * 32, 1) decode_attn_kernel(const AttnArg
         for (int o = 1; o < 32; o <<= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o));
         const float L = warp_sum((ms == -CUDART_INF_F) ? 0.f : ls * fast_exp2(ms - M));
         float x[4] = {0.f, 0.f, 0.f, 0.f};
-        for (int s0 = 0; s0 < expected; s0 += 8) {  // 8 partials' loads in flight per batch
-            float m2[8];
-            float4 v[8];
+        constexpr int FB = 16;  // partials' loads in flight per batch (registers are free at this point)
+        for (int s0 = 0; s0 < expected; s0 += FB) {
+            float m2[FB];
+            float4 v[FB];
 #pragma unroll
-            for (int u = 0; u < 8; ++u) {
+            for (int u = 0; u < FB; ++u) {
                 const int s2 = s0 + u;
                 if (s2 < expected) {
                     m2[u] = __ldcg(pmb + s2 * 16 + 2 * h);
@@ -972,7 +973,7 @@ __global__ void __launch_bounds__(NCW_ * 32, 1) decode_attn_kernel(const AttnArg
                 }
             }
 #pragma unroll
-            for (int u = 0; u < 8; ++u) {
+            for (int u = 0; u < FB; ++u) {
                 const float f = (m2[u] == -CUDART_INF_F) ? 0.f : fast_exp2(m2[u] - M);
                 x[0] += v[u].x * f;
                 x[1] += v[u].y * f;

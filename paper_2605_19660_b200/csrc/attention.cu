@@ -942,44 +942,44 @@ __global__ void __launch_bounds__(NCW_ * 32, 1) decode_attn_kernel(const AttnArg
         const int b = (int)(bh / a.Hkv), kvh = (int)(bh % a.Hkv);
         const float *pmb = a.part_ml + (int64_t)bh * a.maxp * 16;
         const float *pob = a.part_o + (int64_t)bh * a.maxp * 8 * D;
-        // lane s2 < expected holds CTA partial s2's (m, l)
-        float ms = -CUDART_INF_F, ls = 0.f;
-        for (int s2 = lane; s2 < expected; s2 += 32) {
-            const float m2 = __ldcg(pmb + s2 * 16 + 2 * h), l2 = __ldcg(pmb + s2 * 16 + 2 * h + 1);
-            const float Mx = fmaxf(ms, m2);
-            const float fa = (ms == -CUDART_INF_F) ? 0.f : fast_exp2(ms - Mx);
-            const float fb = (m2 == -CUDART_INF_F) ? 0.f : fast_exp2(m2 - Mx);
-            ls = ls * fa + l2 * fb;
-            ms = Mx;
-        }
-        float M = ms;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o));
-        const float L = warp_sum((ms == -CUDART_INF_F) ? 0.f : ls * fast_exp2(ms - M));
+        // one pass, online over batches of partials: every lane loads the (m, l) of
+        // each partial (warp-uniform broadcast) next to its 4 channels of O
+        float M = -CUDART_INF_F, L = 0.f;
         float x[4] = {0.f, 0.f, 0.f, 0.f};
         constexpr int FB = 16;  // partials' loads in flight per batch (registers are free at this point)
         for (int s0 = 0; s0 < expected; s0 += FB) {
-            float m2[FB];
+            float m2[FB], l2[FB];
             float4 v[FB];
 #pragma unroll
             for (int u = 0; u < FB; ++u) {
                 const int s2 = s0 + u;
                 if (s2 < expected) {
                     m2[u] = __ldcg(pmb + s2 * 16 + 2 * h);
+                    l2[u] = __ldcg(pmb + s2 * 16 + 2 * h + 1);
                     v[u] = __ldcg(reinterpret_cast<const float4 *>(pob + s2 * 8 * D + h * D + lane * 4));
                 } else {
                     m2[u] = -CUDART_INF_F;
+                    l2[u] = 0.f;
                     v[u] = make_float4(0.f, 0.f, 0.f, 0.f);
                 }
             }
+            float bm = M;
+#pragma unroll
+            for (int u = 0; u < FB; ++u) bm = fmaxf(bm, m2[u]);
+            const float sc = (M == -CUDART_INF_F) ? 0.f : fast_exp2(M - bm);
+            L *= sc;
+#pragma unroll
+            for (int e = 0; e < 4; ++e) x[e] *= sc;
 #pragma unroll
             for (int u = 0; u < FB; ++u) {
-                const float f = (m2[u] == -CUDART_INF_F) ? 0.f : fast_exp2(m2[u] - M);
+                const float f = (m2[u] == -CUDART_INF_F) ? 0.f : fast_exp2(m2[u] - bm);
+                L += l2[u] * f;
                 x[0] += v[u].x * f;
                 x[1] += v[u].y * f;
                 x[2] += v[u].z * f;
                 x[3] += v[u].w * f;
             }
+            M = bm;
         }
         const float inv = (L > 0.f) ? 1.f / L : 0.f;
 #pragma unroll

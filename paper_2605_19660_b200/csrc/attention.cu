@@ -144,9 +144,8 @@ __device__ __forceinline__ void process_block(const uint8_t *__restrict__ sb, Wa
 
     // ---- key offsets as A (row gq = group): bias[grp][head] = sum_c b[c,grp] * Qrot[head][c]
     //      (x = a*code + b, the value form of dequantize_one, quant.cpp:65-68) -- one
-    //      MMA per k-step; lane gq < 4 holds row gq (= group); rows 4..15 are zero
+    //      MMA per k-step; row gq < 4 (= group) is read back, rows 4..15 are don't-care
     const uint2 *bkp = reinterpret_cast<const uint2 *>(sb + Blk::KB_OFF + ((gq & 3) * 4 + tq) * 64);
-    const uint32_t bkmask = gq < 4 ? 0xffffffffu : 0u;
     float kbias[4];
 
     // ---- QK^T --------------------------------------------------------------------
@@ -185,9 +184,10 @@ __device__ __forceinline__ void process_block(const uint8_t *__restrict__ sb, Wa
         }
         {
             const uint2 z = bkp[s];
-            const uint32_t z0 = z.x & bkmask, z1 = z.y & bkmask;
-            if (s == 0) mma16816_zc(kbias, z0, 0u, z1, 0u, qf[s][0], qf[s][1]);
-            else mma16816(kbias, z0, 0u, z1, 0u, qf[s][0], qf[s][1]);
+            // rows >= 4 of A are don't-care (only rows 0-3 = groups are read back):
+            // lanes gq >= 4 duplicate group gq & 3, rows 8-15 duplicate rows 0-7
+            if (s == 0) mma16816_zc(kbias, z.x, z.x, z.y, z.y, qf[s][0], qf[s][1]);
+            else mma16816(kbias, z.x, z.x, z.y, z.y, qf[s][0], qf[s][1]);
         }
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
@@ -341,7 +341,7 @@ __device__ __forceinline__ void process_block(const uint8_t *__restrict__ sb, Wa
         }
         {
             const uint2 z = vbp[j];
-            mma16816(st.ob, z.x & bkmask, 0u, z.y & bkmask, 0u, bp0, bp1);
+            mma16816(st.ob, z.x, z.x, z.y, z.y, bp0, bp1);  // rows >= 4 don't-care, as for the keys
         }
     }
     if (tm) {
@@ -676,7 +676,7 @@ __global__ void __launch_bounds__(NCW_ * 32, 1) decode_attn_kernel(const AttnArg
     // also means the TMA for unit p was issued, so the full-barrier wait is on
     // the right phase -- and after consuming refills the stage with unit p+NST.
     auto issue = [&](int64_t p, int64_t bh, int64_t uidx) {  // uidx: unit index within bh
-        const int stg = (int)(p % C::NST);
+        const int stg = (int)p % C::NST;
         mbar_arrive_expect_tx(&full[stg], C::STAGE);
         bulk_g2s(ring + stg * C::STAGE,
                  a.blocks + (bh * a.max_blocks + uidx / SUB) * (int64_t)C::BYTES + (uidx % SUB) * C::STAGE, C::STAGE,
@@ -761,8 +761,8 @@ __global__ void __launch_bounds__(NCW_ * 32, 1) decode_attn_kernel(const AttnArg
             const int64_t p0 = lo - start;
             const int64_t first = p0 + ((warp - (int)(p0 % NCW)) + NCW) % NCW;
             for (int64_t p = first; p < hi - start; p += NCW) {
-                const int stg = (int)(p % C::NST);
-                const int round = (int)(p / C::NST);
+                const int stg = (int)p % C::NST;  // 32-bit: p < units of one CTA
+                const int round = (int)p / C::NST;
                 const long long ts0 = a.prof ? clk() : 0;
                 if (lane == 0)
                     while (ld_volatile_shared(&consumed[stg]) < round) {

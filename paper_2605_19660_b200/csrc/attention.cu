@@ -55,7 +55,8 @@ struct AttnCfg {
     static constexpr int NTHREADS = NCW * 32;
     static constexpr int QH_OFF = 0;                                   // QSEG segment q tiles
     static constexpr int SEG_OFF = QH_OFF + QSEG * 8 * QH_STRIDE * 2;  // lastflag[MAXSEG_SMEM]
-    static constexpr int BAR_OFF = ((SEG_OFF + MAXSEG_SMEM * 4 + 7) / 8) * 8;
+    static constexpr int TAB_OFF = ((SEG_OFF + MAXSEG_SMEM * 4 + 7) / 8) * 8;  // last-segment slot per warp
+    static constexpr int BAR_OFF = TAB_OFF + NCW_MAX * 8;
     // shared ring of NST stages: as many whole stages as fit in 227 KB
     static constexpr int NST = (232448 - BAR_OFF - 1024) / STAGE;
     static constexpr int CNT_OFF = BAR_OFF + NST * 8;  // consumed-round counter per stage
@@ -723,6 +724,18 @@ __global__ void __launch_bounds__(NCW_ * 32, 1) decode_attn_kernel(const AttnArg
     long long tmr[12] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
     const long long tk0 = a.prof ? clk() : 0;
 
+    // the stage of warp w's final unit (positions p = w, w + NCW, ... < nunits), free
+    // after it is consumed: p + NST >= nunits, so it is never refilled.  Only used
+    // when the CTA has at least NST units (small launches keep global slots).
+    const bool smem_last = total > 0 && nunits >= C::NST;
+    const int nu32 = (int)nunits;
+    auto last_seg_slot = [&](int w) -> float * {
+        if (smem_last) {
+            const int pw = nu32 - 1 - ((nu32 - 1 - w) % NCW);
+            return reinterpret_cast<float *>(ring + (pw % C::NST) * C::STAGE);
+        }
+        return a.warp_part + (((int64_t)cta * a.maxseg + (seg_last - seg_first)) * NCW_MAX + w) * MERGE_FLOATS;
+    };
     int rtile_base = 0;  // residual tiles handed out so far (round-robin over warps)
     for (int64_t bh = seg_first; bh <= seg_last; ++bh) {
         const int k = (int)(bh - seg_first);
@@ -812,8 +825,12 @@ __global__ void __launch_bounds__(NCW_ * 32, 1) decode_attn_kernel(const AttnArg
         }
 
         const long long te0 = a.prof ? clk() : 0;
-        // ---- warp partial -> global slot (unnormalized O[h][c], m[h], l[h]) ----
-        float *slot = a.warp_part + (((int64_t)cta * a.maxseg + k) * NCW_MAX + warp) * MERGE_FLOATS;
+        // ---- warp partial -> slot (unnormalized O[h][c], m[h], l[h]).  For the CTA's
+        //      last segment the slot is the warp's last ring stage (shared memory: no
+        //      stage is refilled or re-read once its final round is consumed), else
+        //      global scratch ----
+        float *slot = bh == seg_last ? last_seg_slot(warp)
+                                     : a.warp_part + (((int64_t)cta * a.maxseg + k) * NCW_MAX + warp) * MERGE_FLOATS;
         {
             float l0 = st.l[0], l1 = st.l[1];
 #pragma unroll
@@ -880,6 +897,7 @@ __global__ void __launch_bounds__(NCW_ * 32, 1) decode_attn_kernel(const AttnArg
     // ======== end of the CTA's work: cooperative merges (all warps finish within
     //          ~one unit of each other under the static round-robin schedule) ========
     const long long tm0 = a.prof ? clk() : 0;
+    if (lane == 0) reinterpret_cast<float **>(smem + C::TAB_OFF)[warp] = last_seg_slot(warp);
     __syncthreads();
     int *lastflag = reinterpret_cast<int *>(smem + C::SEG_OFF);  // [nseg] (segcnt area reused)
     const int nseg = (int)(seg_last - seg_first + 1);
@@ -888,18 +906,21 @@ __global__ void __launch_bounds__(NCW_ * 32, 1) decode_attn_kernel(const AttnArg
         const int kk = item / g, h = item % g;
         const int64_t bh = seg_first + kk;
         const float *wp = a.warp_part + ((int64_t)cta * a.maxseg + kk) * NCW_MAX * MERGE_FLOATS;
+        const bool lastk = kk == nseg - 1;
+        const float *const *tab = reinterpret_cast<const float *const *>(smem + C::TAB_OFF);
+        auto src = [&](int w) -> const float * { return lastk ? tab[w] : wp + w * MERGE_FLOATS; };
         int64_t first_cta = 0;
         if (total > 0) first_cta = sp.cta_of(bh * nb);
         const int pslot = (int)(total > 0 ? cta - first_cta : 0);
         float *po = a.part_o + ((int64_t)bh * a.maxp + pslot) * 8 * D;
         float *pml = a.part_ml + ((int64_t)bh * a.maxp + pslot) * 16;
         // lane w < NCW holds warp w's (m, l) of head h
-        const float mwv = lane < NCW ? wp[lane * MERGE_FLOATS + 8 * D + h] : -CUDART_INF_F;
-        const float lwv = lane < NCW ? wp[lane * MERGE_FLOATS + 8 * D + 8 + h] : 0.f;
+        const float mwv = lane < NCW ? src(lane)[8 * D + h] : -CUDART_INF_F;
+        const float lwv = lane < NCW ? src(lane)[8 * D + 8 + h] : 0.f;
         float4 v[NCW];
 #pragma unroll
         for (int w = 0; w < NCW; ++w)  // all loads in flight at once
-            v[w] = *reinterpret_cast<const float4 *>(wp + w * MERGE_FLOATS + h * D + lane * 4);
+            v[w] = *reinterpret_cast<const float4 *>(src(w) + h * D + lane * 4);
         float M = mwv;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o));

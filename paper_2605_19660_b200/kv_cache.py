@@ -17,7 +17,7 @@ from dataclasses import dataclass
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "liboscar_b200.so")
+LIB_PATH = os.environ.get("OSCAR_LIB") or os.path.join(HERE, "liboscar_b200.so")  # OSCAR_LIB: A/B builds
 
 METHODS = {"fp": 0, "kivi": 1, "rotate-only": 2, "scale-only": 3, "oscar": 4}
 SCALINGS = {"l2": 0, "rsqrt": 1, "max": 2, "mean-abs": 3}

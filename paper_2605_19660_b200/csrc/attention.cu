@@ -736,7 +736,9 @@ __global__ void __launch_bounds__(NCW_ * 32, 1) decode_attn_kernel(const AttnArg
         }
         return a.warp_part + (((int64_t)cta * a.maxseg + (seg_last - seg_first)) * NCW_MAX + w) * MERGE_FLOATS;
     };
-    int rtile_base = 0;  // residual tiles handed out so far (round-robin over warps)
+    // residual tiles handed out so far (round-robin over warps), starting at the
+    // first warp with one unit fewer than warp 0 (units go round-robin from warp 0)
+    int rtile_base = (int)(nunits % NCW);
     for (int64_t bh = seg_first; bh <= seg_last; ++bh) {
         const int k = (int)(bh - seg_first);
         const int b = (int)(bh / a.Hkv), kvh = (int)(bh % a.Hkv);
@@ -1101,7 +1103,9 @@ static int ncw_choice(int bits);
 int attention_grid(int bits, int num_sms, int64_t nb, int BH) {
     const int64_t units = nb * BH * (bits == 0 ? 4 : 1);
     if (units == 0) return BH;
-    const int64_t per = ncw_choice(bits);
+    // small launches: ~2/3 of the warps stream packed units, the rest take the
+    // residual-window tiles concurrently
+    const int64_t per = (ncw_choice(bits) * 2) / 3;
     const int64_t want = (units + per - 1) / per;
     return (int)(want < num_sms ? want : num_sms);
 }

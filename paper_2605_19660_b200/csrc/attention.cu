@@ -946,6 +946,7 @@ __global__ void __launch_bounds__(NCW_ * 32, 1) decode_attn_kernel(const AttnArg
         }
     }
     __syncthreads();
+    const long long tp0 = a.prof ? clk() : 0;
     // (2) publish: one acq_rel ticket per segment (cumulative over the barrier)
     if (threadIdx.x < nseg) {
         const int64_t bh = seg_first + threadIdx.x;
@@ -955,7 +956,11 @@ __global__ void __launch_bounds__(NCW_ * 32, 1) decode_attn_kernel(const AttnArg
         lastflag[threadIdx.x] = (prev == expected - 1) ? expected : 0;
     }
     __syncthreads();
-    if (a.prof) tmr[8] += clk() - tm0;
+    if (a.prof) {
+        tmr[8] += clk() - tm0;
+        tmr[9] += clk() - tp0;  // the ticket (atomic) part
+    }
+    const long long tf0 = a.prof ? clk() : 0;
     // (3) final merge for the (b, kv heads) this CTA completed last: warp-per-(segment, head)
     for (int item = warp; item < nseg * g; item += NCW) {
         const int kk = item / g, h = item % g;
@@ -1014,6 +1019,7 @@ __global__ void __launch_bounds__(NCW_ * 32, 1) decode_attn_kernel(const AttnArg
             a.lse[(int64_t)b * a.Hq + kvh * g + h] = (L > 0.f) ? (M + __log2f(L)) * LN2 : -CUDART_INF_F;
         if (h == 0 && lane == 0) a.counters[bh] = 0;  // the ticket is complete: reset for the next launch
     }
+    if (a.prof) tmr[10] += clk() - tf0;
     // (4) current token -> residual ring of the (b, kv heads) whose tail this CTA owns
     if (a.write_ring && a.kcur) {
         for (int kk = warp; kk < nseg; kk += NCW) {
@@ -1044,6 +1050,7 @@ __global__ void __launch_bounds__(NCW_ * 32, 1) decode_attn_kernel(const AttnArg
         pp[8] = (unsigned long long)(clk() - tk0);
         pp[9] = (unsigned long long)tmr[8];
         pp[10] = (unsigned long long)tmr[9];
+        pp[7] = (unsigned long long)tmr[10];  // (per-CTA dump) final-merge cycles of this warp
         unsigned smid;
         asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
         pp[11] = smid;

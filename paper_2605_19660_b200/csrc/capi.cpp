@@ -399,11 +399,11 @@ struct oscar_kv_handle {
                 }
                 if (const char *fn = getenv("OSCAR_PROF_FILE")) {  // per-CTA: range, segments, tails, smid, cycles
                     if (FILE *f = std::fopen(fn, "w")) {
-                        std::fprintf(f, "cta,smid,units,segments,tails,slowest_warp_cycles\n");
+                        std::fprintf(f, "cta,smid,units,segments,tails,slowest_warp_cycles,cta_merge,ticket,final_merge\n");
                         const int64_t nbu = a.nb * (dbits == 0 ? 4 : 1);
                         const Split sp{nbu, a.BH, a.ncta, a.seg_cost, a.tail_cost};
                         for (int c = 0; c < a.ncta; ++c) {
-                            double hi = 0;
+                            double hi = 0, cm = 0, tk = 0, fm = 0;
                             unsigned long long sm = 0;
                             for (int w = 0; w < 16; ++w) {
                                 const double t = (double)hbuf[12 * (c * 16 + w) + 8];
@@ -411,13 +411,17 @@ struct oscar_kv_handle {
                                     hi = t;
                                     sm = hbuf[12 * (c * 16 + w) + 11];
                                 }
+                                cm = std::max(cm, (double)hbuf[12 * (c * 16 + w) + 9]);
+                                tk = std::max(tk, (double)hbuf[12 * (c * 16 + w) + 10]);
+                                fm = std::max(fm, (double)hbuf[12 * (c * 16 + w) + 7]);
                             }
                             const int64_t st = sp.begin(c), en = sp.end(c);
                             int64_t tails = 0;
                             for (int64_t bh = st / nbu; en > st && bh <= (en - 1) / nbu; ++bh)
                                 if ((bh + 1) * nbu <= en) ++tails;
-                            std::fprintf(f, "%d,%llu,%lld,%lld,%lld,%.0f\n", c, sm, (long long)(en - st),
-                                         (long long)(en > st ? (en - 1) / nbu - st / nbu + 1 : 0), (long long)tails, hi);
+                            std::fprintf(f, "%d,%llu,%lld,%lld,%lld,%.0f,%.0f,%.0f,%.0f\n", c, sm, (long long)(en - st),
+                                         (long long)(en > st ? (en - 1) / nbu - st / nbu + 1 : 0), (long long)tails, hi,
+                                         cm, tk, fm);
                         }
                         std::fclose(f);
                     }

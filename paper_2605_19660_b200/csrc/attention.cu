@@ -647,7 +647,9 @@ __device__ __noinline__ void residual_tile(const ResidualRefs rr, float *slot, c
     residual_merge(rp, slot, rr.g, rr.rotate_v, lane);
 }
 
-template <int BITS, int NCW_>
+// DEFER: the tiles of a CTA's tail segments after its first run once the packed
+// units are done (launches where a CTA spans many (b, kv head) segments)
+template <int BITS, int NCW_, bool DEFER>
 __global__ void __launch_bounds__(NCW_ * 32, 1) decode_attn_kernel(const AttnArgs a) {
     using C = AttnCfg<BITS, NCW_>;
     constexpr int NCW = C::NCW;
@@ -739,6 +741,8 @@ __global__ void __launch_bounds__(NCW_ * 32, 1) decode_attn_kernel(const AttnArg
     // residual tiles handed out so far (round-robin over warps), starting at the
     // first warp with one unit fewer than warp 0 (units go round-robin from warp 0)
     int rtile_base = (int)(nunits % NCW);
+    bool seen_tail = false;
+    (void)seen_tail;
     for (int64_t bh = seg_first; bh <= seg_last; ++bh) {
         const int k = (int)(bh - seg_first);
         const int b = (int)(bh / a.Hkv), kvh = (int)(bh % a.Hkv);
@@ -880,7 +884,12 @@ __global__ void __launch_bounds__(NCW_ * 32, 1) decode_attn_kernel(const AttnArg
             const int ntiles = (ntok + 15) >> 4;
             const int j = (warp - rtile_base % NCW + NCW) % NCW;  // this warp's tile in this segment
             rtile_base += ntiles;
-            if (j < ntiles) {
+            bool now = true;
+            if constexpr (DEFER) {
+                now = !seen_tail;
+                seen_tail = true;
+            }
+            if (now && j < ntiles) {
                 ResidualRefs rr;
                 rr.ringk = reinterpret_cast<const uint16_t *>(a.ring_k) + bh * R * D;
                 rr.ringv = reinterpret_cast<const uint16_t *>(a.ring_v) + bh * R * D;
@@ -894,6 +903,36 @@ __global__ void __launch_bounds__(NCW_ * 32, 1) decode_attn_kernel(const AttnArg
         }
 
         if (a.prof) tmr[7] += clk() - te0;
+    }
+
+    if constexpr (DEFER) {  // tiles of the tail segments after the first, after the packed units
+        const int ntok = a.r + (a.kcur ? 1 : 0);
+        const int ntiles = (ntok + 15) >> 4;
+        int rbase = (int)(nunits % NCW);
+        bool first_tail = true;
+        for (int64_t bh = seg_first; ntiles > 0 && bh <= seg_last; ++bh) {
+            const int64_t hi = total > 0 ? ((bh + 1) * nb < end ? (bh + 1) * nb : end) : 0;
+            if (!(total == 0 || hi == (bh + 1) * nb)) continue;  // not this CTA's tail
+            const int j = (warp - rbase % NCW + NCW) % NCW;
+            rbase += ntiles;
+            const bool ran = first_tail;
+            first_tail = false;
+            if (ran || j >= ntiles) continue;
+            const int k = (int)(bh - seg_first);
+            const int b = (int)(bh / a.Hkv), kvh = (int)(bh % a.Hkv);
+            float *slot = bh == seg_last ? last_seg_slot(warp)
+                                         : a.warp_part + (((int64_t)cta * a.maxseg + k) * NCW_MAX + warp) * MERGE_FLOATS;
+            ResidualRefs rr;
+            rr.ringk = reinterpret_cast<const uint16_t *>(a.ring_k) + bh * R * D;
+            rr.ringv = reinterpret_cast<const uint16_t *>(a.ring_v) + bh * R * D;
+            rr.kc = a.kcur ? reinterpret_cast<const uint16_t *>(a.kcur) + ((int64_t)b * a.Hkv + kvh) * D : nullptr;
+            rr.vc = a.vcur ? reinterpret_cast<const uint16_t *>(a.vcur) + ((int64_t)b * a.Hkv + kvh) * D : nullptr;
+            rr.g = g;
+            rr.r = a.r;
+            rr.rotate_v = a.rotate_v;
+            residual_tile(rr, slot, reinterpret_cast<const __nv_bfloat16 *>(a.q) + ((int64_t)b * a.Hq + kvh * g) * D,
+                          j * 16, ntok, lane, c0);
+        }
     }
 
     // ======== end of the CTA's work: cooperative merges (all warps finish within
@@ -1075,12 +1114,12 @@ __global__ void lse_merge_kernel(const float *outs, const float *lses, int64_t p
     }
 }
 
-template <int BITS, int NCW>
-cudaError_t launch_t(const AttnArgs &a, cudaStream_t st) {
+template <int BITS, int NCW, bool DEFER>
+cudaError_t launch_d(const AttnArgs &a, cudaStream_t st) {
     using C = AttnCfg<BITS, NCW>;
     static bool init = false;
     if (!init) {
-        cudaError_t e = cudaFuncSetAttribute(decode_attn_kernel<BITS, NCW>,
+        cudaError_t e = cudaFuncSetAttribute(decode_attn_kernel<BITS, NCW, DEFER>,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
         if (e != cudaSuccess) return e;
         init = true;
@@ -1097,7 +1136,15 @@ cudaError_t launch_t(const AttnArgs &a, cudaStream_t st) {
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    return cudaLaunchKernelEx(&cfg, decode_attn_kernel<BITS, NCW>, a);
+    return cudaLaunchKernelEx(&cfg, decode_attn_kernel<BITS, NCW, DEFER>, a);
+}
+
+// DEFER pays off when CTAs span several (b, kv head) segments (each with its own
+// tail): more than two segments per CTA on average
+template <int BITS, int NCW>
+cudaError_t launch_t(const AttnArgs &a, cudaStream_t st) {
+    const bool defer = a.nb > 0 && (int64_t)a.BH > 2 * (int64_t)a.ncta;
+    return defer ? launch_d<BITS, NCW, true>(a, st) : launch_d<BITS, NCW, false>(a, st);
 }
 
 }  // namespace

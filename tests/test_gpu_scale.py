@@ -85,3 +85,28 @@ def test_long_context_gqa7_many_partials():
     err = rel_err(out[0].astype(np.float64), ref)
     log_err("long_context[bits=2][B=1,S=65536,H=4,g=7]", err)
     assert err <= ATOL_REL[2], err
+
+
+def test_many_segments_per_cta_deferred_tiles():
+    """Many short sequences (384 (b, kv head) pairs of 2 packed blocks + a
+    100-token window): each CTA spans several segments with their own tails,
+    which selects the kernel variant that defers the later tails' residual
+    tiles; sequences are checked against the CPU oracle."""
+    import torch
+
+    from paper_2605_19660_b200 import KvCache, PipelineConfig
+
+    B, S, H, g = 48, 356, 8, 4
+    k, v = _torch_inputs(B, S + 1, H, 123)
+    q = torch.randn((B, H * g, 128), device="cuda").to(torch.bfloat16)
+    cache = KvCache(PipelineConfig(heads=H, bits=2), batch=B, q_heads=H * g, max_tokens=S + 8)
+    cache.buffer_quant(k[:, :S].contiguous(), v[:, :S].contiguous())
+    out = cache.decode_step(q, k[:, S].contiguous(), v[:, S].contiguous()).cpu().numpy()
+    for b in (0, 17, B - 1):
+        o = ob.PortCache(H=H, bits=2)
+        kb, vb = _np(k[b]), _np(v[b])
+        o.append(kb[:S], vb[:S])
+        ref = o.decode_step(_np(q[b]), kb[S], vb[S], g, append=False)
+        err = rel_err(out[b].astype(np.float64), ref)
+        log_err(f"many_segments[bits=2][B=48,S=356,H=8][b={b}]", err)
+        assert err <= ATOL_REL[2], (b, err)

@@ -218,17 +218,32 @@ struct oscar_kv_handle {
             residual = r;
             return;
         }
-        // decode branch (kv_cache.cpp:219-249): token by token, flush at exactly R
+        // decode branch (kv_cache.cpp:219-249): token by token, flush at exactly R.
+        // Equivalent batched form: top up the open window (flush it if it fills),
+        // quantize every following whole R-block straight from the input -- the
+        // same R-aligned token groups the token-by-token flushes would produce, so
+        // the cache is bit-identical -- and leave the remainder in the window.
         int64_t pos = 0;
-        while (pos < n) {
-            const int64_t m = std::min(n - pos, R - residual);
-            ring_copy(k, v, sb, st, sh, pos, m, residual, s);
+        if (residual > 0) {
+            const int64_t m = std::min(n, R - residual);
+            ring_copy(k, v, sb, st, sh, 0, m, residual, s);
             residual += m;
-            pos += m;
+            pos = m;
             if (residual == R) {
                 flush(s);
                 ++flushes;
             }
+        }
+        const int64_t nfull = (n - pos) / R;
+        if (nfull > 0) {
+            quantize_from(k, v, sb, st, sh, pos, nfull, packed / R, s);
+            packed += nfull * R;
+            flushes += nfull;
+            pos += nfull * R;
+        }
+        if (pos < n) {
+            ring_copy(k, v, sb, st, sh, pos, n - pos, 0, s);
+            residual = n - pos;
         }
     }
 

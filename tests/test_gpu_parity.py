@@ -325,3 +325,29 @@ def test_quantizer_exact_half_ties_bitexact():
         o = ob.PortCache(method="kivi", bits=bits, H=H)
         o.append(k, v)
         assert ob.caches_equal(export_to_oracle(c.export(0), H), o.export()) == []
+
+
+@pytest.mark.parametrize("bits,rotv", [(2, False), (4, False), (0, False), (2, True)])
+def test_chunked_appends_equal_token_by_token(bits, rotv):
+    """Streaming quantize-on-append: appending chunks of any size after the
+    prefill (the decode branch of buffer_quant_k/v, kv_cache.cpp:219-249) gives
+    the cache that token-by-token appends give -- whole R-blocks inside a chunk
+    are quantized straight from the input -- and the oracle's cache."""
+    from paper_2605_19660_b200 import KvCache, PipelineConfig
+
+    H = 2
+    chunks = [1, 50, 300, 7, 500, 128, 129, 3]
+    S0, S = 200, 200 + sum(chunks)
+    k, v = make_inputs(88 + bits, S, H)
+    cfg = PipelineConfig(heads=H, bits=bits, rotate_v=rotv)
+    a = KvCache(cfg, batch=1, q_heads=H, max_tokens=S + 8)
+    a.buffer_quant(dev_bf16(k[None, :S0]), dev_bf16(v[None, :S0]))
+    o = ob.PortCache(H=H, bits=bits, rotate_v=rotv)
+    o.append(k[:S0], v[:S0])
+    pos = S0
+    for n in chunks:
+        a.buffer_quant(dev_bf16(k[None, pos:pos + n]), dev_bf16(v[None, pos:pos + n]))
+        o.append(k[pos:pos + n], v[pos:pos + n])
+        pos += n
+    assert (a.packed_tokens, a.residual_tokens) == ((S // 128) * 128, S % 128)
+    assert ob.caches_equal(export_to_oracle(a.export(0), H), o.export()) == []

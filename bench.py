@@ -613,6 +613,29 @@ def run_config(args, rank, world, local_rank):
         del kk, vv
         caches.append(cache)
     torch.cuda.empty_cache()
+    stream_stats = None
+    if c == "c5":  # streaming quantize-on-append into the tail shard: 32 chunks of 2048 tokens
+        extra = KvCache(cfg, batch=1, q_heads=Hq, max_tokens=2 * R + 32 * 2048, device=local_rank, keep_exact=False)
+        ka, va = synth_kv(1, 32 * 2048 + 100, Hloc, 99, dev)
+        extra.buffer_quant(ka[:, :100].contiguous(), va[:, :100].contiguous(), stream=sh)  # prefill: open window
+        chunks = [(ka[:, 100 + i * 2048:100 + (i + 1) * 2048].contiguous(),
+                   va[:, 100 + i * 2048:100 + (i + 1) * 2048].contiguous()) for i in range(32)]
+        torch.cuda.synchronize()
+        s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s0.record(stream)
+        for kc_, vc_ in chunks:
+            extra.buffer_quant(kc_, vc_, stream=sh)
+        s1.record(stream)
+        torch.cuda.synchronize()
+        sms = s0.elapsed_time(s1)
+        rd = 32 * 2048 * Hloc * D * 2 * 2
+        wr = (32 * 2048 // R) * Hloc * BLOCK_BYTES[bits]
+        stream_stats = {"tokens": 32 * 2048, "chunk": 2048, "ms": sms, "gbs": (rd + wr) / (sms * 1e-3) / 1e9,
+                        "tokens_per_s": 32 * 2048 / (sms * 1e-3),
+                        "what": "oscar_kv_append of 32 x 2048-token chunks (4 KV heads) after a 100-token prefill: "
+                                "window top-up + whole blocks quantized from the input + window remainder"}
+        extra.close()
+        del ka, va, chunks
     q, kn, vn = step_inputs(K + W, B, Hqloc, Hloc, 11 + rank, dev)
     out = torch.empty((B, Hqloc, D), dtype=torch.float32, device=dev)
 
@@ -658,6 +681,7 @@ def run_config(args, rank, world, local_rank):
                      "peak_source": peak_src, "unit": "GB/s",
                      "frac": step_bytes / (ms / K * 1e-3) / 1e9 / peak, "algorithmic_bytes_per_step_per_gpu": step_bytes},
         "prefill_s": t_pre,
+        "streaming_append": stream_stats,
     }
 
 

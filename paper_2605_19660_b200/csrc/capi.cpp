@@ -153,7 +153,8 @@ struct oscar_kv_handle {
 
     // ---- kernels --------------------------------------------------------------
     void quantize_from(const void *k, const void *v, int64_t sb, int64_t st, int64_t sh, int64_t tok0,
-                       int64_t nblk, int64_t blk0, cudaStream_t s, int64_t vst = -1, int64_t vsc = 1) {
+                       int64_t nblk, int64_t blk0, cudaStream_t s, int64_t vst = -1, int64_t vsc = 1,
+                       int64_t ring_prefix = 0) {
         QuantizeArgs a{};
         a.k = k;
         a.v = v;
@@ -171,6 +172,11 @@ struct oscar_kv_handle {
         a.blk0 = blk0;
         a.shadow = shadow;
         a.tc = tc();
+        if (ring_prefix > 0) {
+            a.rk = ring_k;
+            a.rv = ring_v;
+            a.rtok = ring_prefix;
+        }
         CK(launch_quantize(a, s));
         ++last_launches;
         blocks_written = true;
@@ -224,23 +230,19 @@ struct oscar_kv_handle {
         // same R-aligned token groups the token-by-token flushes would produce, so
         // the cache is bit-identical -- and leave the remainder in the window.
         int64_t pos = 0;
-        if (residual > 0) {
-            const int64_t m = std::min(n, R - residual);
-            ring_copy(k, v, sb, st, sh, 0, m, residual, s);
-            residual += m;
-            pos = m;
-            if (residual == R) {
-                flush(s);
-                ++flushes;
-            }
+        if (residual + n < R) {  // stays inside the open window
+            ring_copy(k, v, sb, st, sh, 0, n, residual, s);
+            residual += n;
+            return;
         }
-        const int64_t nfull = (n - pos) / R;
-        if (nfull > 0) {
-            quantize_from(k, v, sb, st, sh, pos, nfull, packed / R, s);
-            packed += nfull * R;
-            flushes += nfull;
-            pos += nfull * R;
-        }
+        // the window's residual tokens + the input complete nblk blocks: one launch
+        // whose block 0 reads its first `residual` tokens from the rings
+        const int64_t nblk = (residual + n) / R;
+        quantize_from(k, v, sb, st, sh, 0, nblk, packed / R, s, -1, 1, residual);
+        pos = nblk * R - residual;
+        packed += nblk * R;
+        flushes += nblk;
+        residual = 0;
         if (pos < n) {
             ring_copy(k, v, sb, st, sh, pos, n - pos, 0, s);
             residual = n - pos;

@@ -30,6 +30,10 @@ struct QuantizeArgs {
     int64_t max_blocks, blk0;
     double *shadow;  // nullable: [bh][max_blocks][SHADOW_DOUBLES]
     TransformCfg tc;
+    // optional residual-window prefix of block 0: its first rtok tokens come from
+    // the rings (K [bh][R][D], V [bh][D][R]), the rest from the source above
+    const void *rk = nullptr, *rv = nullptr;
+    int64_t rtok = 0;
 };
 cudaError_t launch_quantize(const QuantizeArgs &a, cudaStream_t st);
 

@@ -227,7 +227,12 @@ __global__ void __launch_bounds__(QT * GPAR) quantize_kernel(const QuantizeArgs 
     const int64_t blk = blockIdx.x;
     const __nv_bfloat16 *kin = reinterpret_cast<const __nv_bfloat16 *>(a.k) + b * a.sb + h * a.sh;
     const __nv_bfloat16 *vin = reinterpret_cast<const __nv_bfloat16 *>(a.v) + b * a.sb + h * a.sh;
-    const int64_t tok_base = a.tok0 + blk * R;
+    // block 0 may start with a.rtok tokens of the open residual window (rings):
+    // token t of block blk is ring row t if blk == 0 && t < rtok, else input token
+    // tok0 + blk*R + t - rtok
+    const int64_t tok_base = a.tok0 + blk * R - a.rtok;
+    const uint16_t *rk = a.rk ? reinterpret_cast<const uint16_t *>(a.rk) + (int64_t)bh * R * D : nullptr;
+    const uint16_t *rv = a.rv ? reinterpret_cast<const uint16_t *>(a.rv) + (int64_t)bh * R * D : nullptr;
     const int64_t out_blk = (int64_t)bh * a.max_blocks + a.blk0 + blk;
     double *shadow = a.shadow ? a.shadow + out_blk * SHADOW_DOUBLES : nullptr;
     const TransformCfg tc = a.tc;
@@ -236,7 +241,10 @@ __global__ void __launch_bounds__(QT * GPAR) quantize_kernel(const QuantizeArgs 
         const int t = gi * G + tl;  // token within the block
         // ---------------- K: rotate, scale (apply_method) ----------------
         double x[32];
-        load32(kin + (tok_base + t) * a.st + q * 32, x);
+        const bool from_ring = blk == 0 && t < a.rtok;
+        load32(from_ring ? reinterpret_cast<const __nv_bfloat16 *>(rk) + (int64_t)t * D + q * 32
+                         : kin + (tok_base + t) * a.st + q * 32,
+               x);
         if (tc.rotates) fht128_quad(x, q);
         double s = 1.0, inv = 1.0;
         if (tc.scales) {
@@ -288,7 +296,11 @@ __global__ void __launch_bounds__(QT * GPAR) quantize_kernel(const QuantizeArgs 
         // ---------------- V: optional rotation, per-token groups ----------------
         {
             double y[32];
-            if (a.vsc == 1) {
+            if (from_ring) {  // channel-major residual ring
+#pragma unroll
+                for (int i = 0; i < 32; ++i)
+                    y[i] = (double)__uint_as_float((uint32_t)rv[(int64_t)(q * 32 + i) * R + t] << 16);
+            } else if (a.vsc == 1) {
                 load32(vin + (tok_base + t) * a.vst + q * 32, y);
             } else {  // channel-major source (the residual ring)
                 const uint16_t *vp = reinterpret_cast<const uint16_t *>(vin) + (tok_base + t) * a.vst;
@@ -376,9 +388,17 @@ __global__ void __launch_bounds__(QT) raw_block_kernel_dyn(const QuantizeArgs a)
     uint8_t *out = a.blocks + out_blk * (int64_t)BF16_BLOCK_BYTES;
     const uint16_t *kin = reinterpret_cast<const uint16_t *>(a.k) + b * a.sb + h * a.sh;
     const uint16_t *vin = reinterpret_cast<const uint16_t *>(a.v) + b * a.sb + h * a.sh;
-    const int64_t tok_base = a.tok0 + blk * R;
+    const int64_t tok_base = a.tok0 + blk * R - a.rtok;
+    const uint16_t *rk = a.rk ? reinterpret_cast<const uint16_t *>(a.rk) + (int64_t)bh * R * D : nullptr;
+    const uint16_t *rv = a.rv ? reinterpret_cast<const uint16_t *>(a.rv) + (int64_t)bh * R * D : nullptr;
     for (int i = threadIdx.x; i < R * 16; i += QT) {
         const int t = i >> 4, part = i & 15;
+        if (blk == 0 && t < a.rtok) {  // open residual window: K row-major, V channel-major rings
+            reinterpret_cast<uint4 *>(sk)[i] = *reinterpret_cast<const uint4 *>(rk + (int64_t)t * D + part * 8);
+#pragma unroll
+            for (int e = 0; e < 8; ++e) sv[t * D + part * 8 + e] = rv[(int64_t)(part * 8 + e) * R + t];
+            continue;
+        }
         reinterpret_cast<uint4 *>(sk)[i] = *reinterpret_cast<const uint4 *>(kin + (tok_base + t) * a.st + part * 8);
         if (a.vsc == 1) {
             reinterpret_cast<uint4 *>(sv)[i] = *reinterpret_cast<const uint4 *>(vin + (tok_base + t) * a.vst + part * 8);
@@ -448,8 +468,9 @@ cudaError_t launch_quantize(const QuantizeArgs &a, cudaStream_t st) {
         raw_block_kernel_dyn<<<grid, QT, 2 * R * D * 2, st>>>(a);
         return cudaGetLastError();
     }
-    // one block per (b, h) (the flush): 4 groups in parallel for latency
-    const bool flush = a.n_blocks == 1;
+    // few blocks (the flush; short streaming chunks): 4 groups in parallel per CTA
+    // for latency; bulk prefill: one group at a time, more CTAs per SM
+    const bool flush = a.n_blocks * a.B * a.H <= 2 * 148;
     if (a.tc.bits == 2) return flush ? launch_q<2, 4>(a, grid, st) : launch_q<2, 1>(a, grid, st);
     return flush ? launch_q<4, 4>(a, grid, st) : launch_q<4, 1>(a, grid, st);
 }

@@ -45,8 +45,9 @@ def parse():
     p.add_argument("--bits", type=int, default=2)
     p.add_argument("--no-compare", action="store_true", help="skip the INT4 / bf16 comparison legs")
     p.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
-    p.add_argument("--config", default="c2", choices=["c2", "c3", "c4", "c5"],
-                   help="c2 (default, the headline) or the multi-GPU configs of BASELINE.json: "
+    p.add_argument("--config", default="c2", choices=["c1", "c2", "c3", "c4", "c5"],
+                   help="c2 (default, the headline), c1 (the reference's CPU-runnable case: B=1, 4K, "
+                        "GPU and CPU reference side by side) or the multi-GPU configs of BASELINE.json: "
                         "c3 32-layer Qwen2.5-7B batch-sharded, c4 128K head-sharded, c5 512K sequence-sharded")
     p.add_argument("--layers", type=int, default=32, help="c3: layers per step")
     return p.parse_args()
@@ -546,6 +547,81 @@ def run_reference(args):
     }
 
 
+# ----------------------------------------------------------------------------- config 1
+def run_c1(args, rank, world, local_rank):
+    """BASELINE.json configs[0]: one Llama-3-8B layer (32 q / 8 kv heads), batch 1,
+    4K context, INT2 -- quantize (prefill) + decode on the GPU, and the compiled
+    reference on the host cores on the same inputs."""
+    import numpy as np
+    import torch
+
+    from oracle import bindings as ob
+    from paper_2605_19660_b200 import KvCache, PipelineConfig
+    from paper_2605_19660_b200.synthetic import make_inputs, make_queries, to_bf16_bits
+
+    dev = torch.device("cuda", local_rank)
+    torch.cuda.set_device(dev)
+    stream = torch.cuda.Stream(device=dev)
+    torch.cuda.set_stream(stream)
+    sh = stream.cuda_stream
+    S, Hq, Hkv, K, W = 4096, 32, 8, args.steps, args.warmup
+    g = Hq // Hkv
+    k, v = make_inputs(21, S + K + W, Hkv)
+    q = make_queries(21, K + W, Hq)
+
+    def dev_bf16(x):
+        return torch.from_numpy(to_bf16_bits(np.ascontiguousarray(x)).view(np.int16)).view(torch.bfloat16).to(dev)
+
+    kd, vd, qd = dev_bf16(k[None]), dev_bf16(v[None]), dev_bf16(q)
+    cache = KvCache(PipelineConfig(heads=Hkv, bits=2), batch=1, q_heads=Hq, max_tokens=S + K + W + 8)
+    warm = KvCache(PipelineConfig(heads=Hkv, bits=2), batch=1, q_heads=Hq, max_tokens=S + 8)
+    warm.buffer_quant(kd[:, :S].contiguous(), vd[:, :S].contiguous(), stream=sh)  # first-launch costs
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    cache.buffer_quant(kd[:, :S].contiguous(), vd[:, :S].contiguous(), stream=sh)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    gpu_prefill_ms = e0.elapsed_time(e1)
+    kn = [kd[:, S + i].contiguous() for i in range(K + W)]
+    vn = [vd[:, S + i].contiguous() for i in range(K + W)]
+    out = torch.empty((1, Hq, D), device=dev)
+    for i in range(W):
+        cache.decode_step(qd[i][None], kn[i], vn[i], out=out, stream=sh)
+    torch.cuda.synchronize()
+    e0.record(stream)
+    for i in range(W, W + K):
+        cache.decode_step(qd[i][None], kn[i], vn[i], out=out, stream=sh)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    gpu_step_us = 1e3 * e0.elapsed_time(e1) / K
+    # the compiled reference on the same inputs (all host cores)
+    kind = "reference" if ob.ref_available() else "port"
+    cores = ob.ref_use_threads(cpu_threads()) if kind == "reference" else 1
+    ref = ob.RefCache(H=Hkv) if kind == "reference" else ob.PortCache(H=Hkv)
+    t0 = time.perf_counter()
+    ref.append(k[:S], v[:S])
+    cpu_prefill_s = time.perf_counter() - t0
+    n_cpu = min(K, 8)
+    t0 = time.perf_counter()
+    for i in range(W, W + n_cpu):
+        ref.decode_step(q[i], k[S + i - W], v[S + i - W], g)
+    cpu_step_s = (time.perf_counter() - t0) / n_cpu
+    return {
+        "metric": METRIC + " [c1]", "value": K / (gpu_step_us * K * 1e-6), "unit": "tokens/s", "n_gpus": 1,
+        "steps": K, "warmup": W, "ms_per_step": gpu_step_us / 1e3, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "int2", "data": "synthetic (TNI-recipe keys, N(0,1) values/queries), bf16",
+        "config": {"workload": "C1: Llama-3-8B attention layer (32 q / 8 kv heads), batch 1, 4K ctx, INT2, G=32, "
+                               "R=128 -- GPU and the compiled reference on the same inputs", "context": S},
+        "gpu": {"prefill_quantize_ms": gpu_prefill_ms, "decode_step_us": gpu_step_us},
+        "cpu_baseline": {"kind": kind, "cores": cores, "prefill_quantize_ms": 1e3 * cpu_prefill_s,
+                         "decode_step_ms": 1e3 * cpu_step_s, "value": 1.0 / cpu_step_s, "unit": "tokens/s",
+                         "sample": f"the whole C1 workload ({n_cpu} decode steps timed)"},
+        "speedup": {"prefill_quantize": 1e3 * cpu_prefill_s / gpu_prefill_ms,
+                    "decode_step": 1e6 * cpu_step_s / gpu_step_us},
+    }
+
+
 # ----------------------------------------------------------------------------- configs 3-5
 def run_config(args, rank, world, local_rank):
     """BASELINE.json configs[2..4] on `world` GPUs.
@@ -575,6 +651,8 @@ def run_config(args, rank, world, local_rank):
     K, W, bits = args.steps, args.warmup, args.bits
     c = args.config
     caches, layers = [], 1
+    if c == "c1":
+        return run_c1(args, rank, world, local_rank)
     if c == "c3":
         Hq, Hkv, S, layers = 28, 4, 8192, args.layers
         Bg = args.batch if args.batch != 16 else 256

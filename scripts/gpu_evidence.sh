@@ -9,7 +9,7 @@ cp gpurun_out/parity_errors.jsonl $OUT/ 2>/dev/null
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $OUT/smoke.txt 2>&1
 timeout 900 python bench.py > $OUT/bench_c2.json 2> $OUT/bench_c2.err
 timeout 600 python bench.py --impl reference --steps 2 --warmup 1 > $OUT/bench_reference.json 2> $OUT/bench_reference.err
-for c in c4 c5; do timeout 600 python bench.py --config $c --steps 64 --warmup 4 > $OUT/bench_$c.json 2>/dev/null; done
+for c in c1 c4 c5; do timeout 600 python bench.py --config $c --steps 64 --warmup 4 > $OUT/bench_$c.json 2>/dev/null; done
 for b in 256 64 8 1; do timeout 900 python bench.py --config c3 --batch $b --steps 16 --warmup 3 > $OUT/bench_c3_b$b.json 2>/dev/null; done
 for b in 4 0; do timeout 200 python scripts/diag_resid.py $b 2>/dev/null | tail -1; done > $OUT/attend_by_residual.txt
 timeout 200 python scripts/diag_resid.py 2 2>/dev/null | tail -1 >> $OUT/attend_by_residual.txt

@@ -1143,7 +1143,12 @@ cudaError_t launch_d(const AttnArgs &a, cudaStream_t st) {
 // tail): more than two segments per CTA on average
 template <int BITS, int NCW>
 cudaError_t launch_t(const AttnArgs &a, cudaStream_t st) {
-    const bool defer = a.nb > 0 && (int64_t)a.BH > 2 * (int64_t)a.ncta;
+    static int force = -2;  // OSCAR_DEFER=0|1 overrides the choice (experiments)
+    if (force == -2) {
+        const char *e = getenv("OSCAR_DEFER");
+        force = e ? atoi(e) : -1;
+    }
+    const bool defer = force >= 0 ? force == 1 : (a.nb > 0 && (int64_t)a.BH > 2 * (int64_t)a.ncta);
     return defer ? launch_d<BITS, NCW, true>(a, st) : launch_d<BITS, NCW, false>(a, st);
 }
 

@@ -332,7 +332,8 @@ def run_ours(args, rank, world, local_rank):
         "higher_is_better": True,
         "scaling": "weak",
         "vs_baseline": None,
-        "dtype": "int2" if args.bits == 2 else ("int4" if args.bits == 4 else "bf16"),
+        "dtype": "f16" if args.bits else "bf16",  # MMA operand type (fp32 accumulate); the cache stores:
+        "storage": "int2" if args.bits == 2 else ("int4" if args.bits == 4 else "bf16"),
         "compute": "2-bit codes as fp16-subnormal mma.sync A operands, fp16 B, fp32 accumulate/softmax",
         "data": "synthetic (TNI-recipe keys, N(0,1) values/queries), bf16 inputs",
         "config": {
@@ -610,7 +611,8 @@ def run_c1(args, rank, world, local_rank):
     return {
         "metric": METRIC + " [c1]", "value": K / (gpu_step_us * K * 1e-6), "unit": "tokens/s", "n_gpus": 1,
         "steps": K, "warmup": W, "ms_per_step": gpu_step_us / 1e3, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "int2", "data": "synthetic (TNI-recipe keys, N(0,1) values/queries), bf16",
+        "vs_baseline": None, "dtype": "f16", "storage": "int2",
+        "data": "synthetic (TNI-recipe keys, N(0,1) values/queries), bf16",
         "config": {"workload": "C1: Llama-3-8B attention layer (32 q / 8 kv heads), batch 1, 4K ctx, INT2, G=32, "
                                "R=128 -- GPU and the compiled reference on the same inputs", "context": S},
         "gpu": {"prefill_quantize_ms": gpu_prefill_ms, "decode_step_us": gpu_step_us},
@@ -751,7 +753,8 @@ def run_config(args, rank, world, local_rank):
     return {
         "metric": METRIC + f" [{c}]", "value": value, "unit": "tokens/s", "n_gpus": world, "steps": K, "warmup": W,
         "ms_per_step": ms / K, "higher_is_better": True, "scaling": "weak" if c == "c3" else "strong",
-        "vs_baseline": None, "dtype": "int2" if bits == 2 else ("int4" if bits == 4 else "bf16"),
+        "vs_baseline": None, "dtype": "f16" if bits else "bf16",
+        "storage": "int2" if bits == 2 else ("int4" if bits == 4 else "bf16"),
         "data": "synthetic (TNI-recipe keys, N(0,1) values/queries), bf16 inputs",
         "config": {"workload": desc, "batch_per_gpu": B, "kv_heads_per_gpu": Hloc, "q_heads_per_gpu": Hqloc,
                    "context": S, "tokens_per_gpu": per_rank_tokens, "layers": layers, "bits": bits},

@@ -21,6 +21,13 @@ def t(name, fn, n=K):
     for i in range(n): fn(i)
     torch.cuda.synchronize(); res[name] = round(1e6 * (time.perf_counter() - t0) / n, 1)
 t("host_api", lambda i: cache.decode_step_host(qn[i], kn_[i], vn_[i], on, stream=sh))
+t("host_api_default_stream_lookup", lambda i: cache.decode_step_host(qn[i], kn_[i], vn_[i], on))
+import ctypes
+from paper_2605_19660_b200.kv_cache import lib
+L = lib()
+qp = [qn[i].ctypes.data for i in range(K)]; kp = [kn_[i].ctypes.data for i in range(K)]; vp = [vn_[i].ctypes.data for i in range(K)]
+op = on.ctypes.data
+t("raw_cabi", lambda i: L.oscar_kv_decode_step_host(cache._h, qp[i], kp[i], vp[i], op, None, sh))
 qd = torch.empty((B, Hq, 128), dtype=torch.bfloat16, device=dev); kd = torch.empty((B, Hkv, 128), dtype=torch.bfloat16, device=dev)
 vd = torch.empty_like(kd); od = torch.empty((B, Hq, 128), device=dev)
 t("device_api_sync", lambda i: (cache.decode_step(qd, kd, vd, out=od, stream=sh), torch.cuda.current_stream().synchronize()))

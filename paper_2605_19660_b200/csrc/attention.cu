@@ -641,10 +641,21 @@ __device__ __forceinline__ void residual_merge(const ResPartial &rp, float *slot
 // One 16-token tile [t0, t0+16) of the residual window (+ the current token at
 // index r), merged into the warp's partial slot.
 __device__ __noinline__ void residual_tile(const ResidualRefs rr, float *slot, const __nv_bfloat16 *qbase, int t0,
-                                           int ntok, int lane, float c0) {
+                                           int ntok, int lane, float c0, uint16_t *ring_k_w, uint16_t *ring_v_w) {
     ResPartial rp;
     residual_compute(rr, qbase, t0, ntok, lane, c0, rp);
     residual_merge(rp, slot, rr.g, rr.rotate_v, lane);
+    // the tile holding the current token (index r) also appends it to the rings at
+    // slot r: nothing in this launch reads that slot (tiles take it from kcur)
+    if (ring_k_w && rr.kc && t0 <= rr.r && rr.r < t0 + 16) {
+        reinterpret_cast<uint2 *>(ring_k_w + rr.r * D)[lane] = reinterpret_cast<const uint2 *>(rr.kc)[lane];
+        const uint2 vv = reinterpret_cast<const uint2 *>(rr.vc)[lane];  // V ring is channel-major [D][R]
+        uint16_t *rv = ring_v_w + rr.r;
+        rv[(4 * lane + 0) * R] = (uint16_t)(vv.x & 0xffffu);
+        rv[(4 * lane + 1) * R] = (uint16_t)(vv.x >> 16);
+        rv[(4 * lane + 2) * R] = (uint16_t)(vv.y & 0xffffu);
+        rv[(4 * lane + 3) * R] = (uint16_t)(vv.y >> 16);
+    }
 }
 
 // DEFER: the tiles of a CTA's tail segments after its first run once the packed
@@ -898,7 +909,9 @@ __global__ void __launch_bounds__(NCW_ * 32, 1) decode_attn_kernel(const AttnArg
                 rr.g = g;
                 rr.r = a.r;
                 rr.rotate_v = a.rotate_v;
-                residual_tile(rr, slot, qbase, j * 16, ntok, lane, c0);
+                residual_tile(rr, slot, qbase, j * 16, ntok, lane, c0,
+                              a.write_ring ? reinterpret_cast<uint16_t *>(a.ring_k) + bh * R * D : nullptr,
+                              reinterpret_cast<uint16_t *>(a.ring_v) + bh * R * D);
             }
         }
 
@@ -931,7 +944,9 @@ __global__ void __launch_bounds__(NCW_ * 32, 1) decode_attn_kernel(const AttnArg
             rr.r = a.r;
             rr.rotate_v = a.rotate_v;
             residual_tile(rr, slot, reinterpret_cast<const __nv_bfloat16 *>(a.q) + ((int64_t)b * a.Hq + kvh * g) * D,
-                          j * 16, ntok, lane, c0);
+                          j * 16, ntok, lane, c0,
+                          a.write_ring ? reinterpret_cast<uint16_t *>(a.ring_k) + bh * R * D : nullptr,
+                          reinterpret_cast<uint16_t *>(a.ring_v) + bh * R * D);
         }
     }
 
@@ -1059,27 +1074,6 @@ __global__ void __launch_bounds__(NCW_ * 32, 1) decode_attn_kernel(const AttnArg
         if (h == 0 && lane == 0) a.counters[bh] = 0;  // the ticket is complete: reset for the next launch
     }
     if (a.prof) tmr[10] += clk() - tf0;
-    // (4) current token -> residual ring of the (b, kv heads) whose tail this CTA owns
-    if (a.write_ring && a.kcur) {
-        for (int kk = warp; kk < nseg; kk += NCW) {
-            const int64_t bh = seg_first + kk;
-            const bool owns_tail = total == 0 || ((bh + 1) * nb <= end);
-            if (!owns_tail) continue;
-            const int b = (int)(bh / a.Hkv), kvh = (int)(bh % a.Hkv);
-            const uint2 *ks = reinterpret_cast<const uint2 *>(reinterpret_cast<const __nv_bfloat16 *>(a.kcur) +
-                                                               ((int64_t)b * a.Hkv + kvh) * D);
-            const uint2 *vs = reinterpret_cast<const uint2 *>(reinterpret_cast<const __nv_bfloat16 *>(a.vcur) +
-                                                               ((int64_t)b * a.Hkv + kvh) * D);
-            reinterpret_cast<uint2 *>(reinterpret_cast<__nv_bfloat16 *>(a.ring_k) + (bh * R + a.r) * D)[lane] =
-                ks[lane];
-            const uint2 vv = vs[lane];  // V ring is channel-major [D][R]
-            uint16_t *rv = reinterpret_cast<uint16_t *>(a.ring_v) + bh * R * D + a.r;
-            rv[(4 * lane + 0) * R] = (uint16_t)(vv.x & 0xffffu);
-            rv[(4 * lane + 1) * R] = (uint16_t)(vv.x >> 16);
-            rv[(4 * lane + 2) * R] = (uint16_t)(vv.y & 0xffffu);
-            rv[(4 * lane + 3) * R] = (uint16_t)(vv.y >> 16);
-        }
-    }
     if (a.prof) tmr[4] += clk() - tm0;
     if (a.prof && lane == 0) {
         // per-warp phase cycles: [wait, qk, softmax, pv, merge, spin, qprologue, segtail]; total in slot 4 of the

@@ -4,12 +4,13 @@
 //
 // Persistent, stream-K style: one CTA per SM gets an equal contiguous range
 // of the global (sequence*KV-head, R-block) space, so every SM streams the
-// same number of bytes.  All 8 warps consume: unit p of the range (one
-// R-block record of 12.8 KB INT2 / 21 KB INT4, or a 16 KB quarter of a bf16
-// record, see layout.h) is streamed HBM -> shared memory by ONE cp.async.bulk
-// (TMA engine, L2 evict-first) into stage p % NST of an mbarrier ring and
-// processed by warp p % 8, which then refills that same stage with unit
-// p + NST -- no producer warp, no empty barriers, 255 registers per thread.
+// same number of bytes.  All NCW warps consume (12 for INT2, 8 for INT4 and
+// bf16): unit p of the range (one R-block record of 12.8 KB INT2 / 21 KB
+// INT4, or a 16 KB quarter of a bf16 record, see layout.h) is streamed HBM ->
+// shared memory by ONE cp.async.bulk (TMA engine, L2 evict-first) into stage
+// p % NST of an mbarrier ring and processed by warp p % NCW, which then
+// refills that same stage with unit p + NST -- no producer warp, no empty
+// barriers.
 // Per block a consumer runs QK^T and P.V on the tensor cores
 // (mma.sync m16n8k16, fp16 in / fp32 accumulate) straight from the packed
 // codes: every loaded 32-bit word ANDed with a field mask IS an A register
@@ -18,10 +19,10 @@
 // into one extra MMA per block, the per-token key norm into the fp32
 // epilogue.  Online softmax in log2 units; partials are merged per CTA in
 // shared memory and across CTAs by the last-arriving CTA of each (b, kv-head)
-// (atomic ticket), which also writes the current token into the residual
-// ring.  The residual window (< R full-precision tokens) plus the current
-// token are attended with fp32 CUDA-core math by the CTA that owns the last
-// packed block of the sequence.
+// (atomic ticket).  The residual window (< R full-precision tokens) plus the
+// current token are attended on the bf16 tensor cores, one 16-token tile per
+// warp of the CTA that owns the last packed block of the sequence; the tile
+// holding the current token also writes it into the residual ring.
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
 #include <math_constants.h>

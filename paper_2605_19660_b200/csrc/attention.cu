@@ -119,7 +119,8 @@ __device__ __forceinline__ void load_bf16x4(const __nv_bfloat16 *p, float (&x)[4
 // per-warp accumulator state (fragment layouts, see layout.h)
 struct WarpState {
     float o[8][4];   // P.V accumulators: m-tile mm, (row gq|gq+8) x (head 2tq|2tq+1)
-    float ob[4];     // V-offset accumulator: row gq = channel group
+    float ob[4];     // V-offset accumulators: row gq = channel group, even k-steps
+    float ob2[4];    //   rows gq+8 = channel group, odd k-steps (paired b-param quads)
     float m[2], l[2];
 };
 
@@ -147,8 +148,9 @@ __device__ __forceinline__ void process_block(const uint8_t *__restrict__ sb, Wa
     // ---- key offsets as A (row gq = group): bias[grp][head] = sum_c b[c,grp] * Qrot[head][c]
     //      (x = a*code + b, the value form of dequantize_one, quant.cpp:65-68) -- one
     //      MMA per k-step; row gq < 4 (= group) is read back, rows 4..15 are don't-care
-    const uint2 *bkp = reinterpret_cast<const uint2 *>(sb + Blk::KB_OFF + ((gq & 3) * 4 + tq) * 64);
-    float kbias[4];
+    const uint4 *bkp = reinterpret_cast<const uint4 *>(sb + Blk::KB_OFF + ((gq & 3) * 4 + tq) * 64);
+    float kbias[4], kbias2[4];  // rows gq: even k-steps; rows gq+8: odd k-steps
+    uint4 zk;
 
     // ---- QK^T --------------------------------------------------------------------
     float sacc[8][4];
@@ -185,11 +187,14 @@ __device__ __forceinline__ void process_block(const uint8_t *__restrict__ sb, Wa
             bq[3][1] = hmul2_u32(qf[s][1], a23.w);
         }
         {
-            const uint2 z = bkp[s];
-            // rows >= 4 of A are don't-care (only rows 0-3 = groups are read back):
-            // lanes gq >= 4 duplicate group gq & 3, rows 8-15 duplicate rows 0-7
-            if (s == 0) mma16816_zc(kbias, z.x, z.x, z.y, z.y, qf[s][0], qf[s][1]);
-            else mma16816(kbias, z.x, z.x, z.y, z.y, qf[s][0], qf[s][1]);
+            // one quad per k-step pair (layout.h kb_index): rows gq = group gq & 3 at
+            // k-step s (even), rows gq+8 = the same group at s+1; the other rows of
+            // each product are don't-care (lanes gq >= 4 duplicate groups 0-3)
+            if ((s & 1) == 0) zk = bkp[s >> 1];
+            if (s == 0) mma16816_zc(kbias, zk.x, zk.y, zk.z, zk.w, qf[s][0], qf[s][1]);
+            else if (s == 1) mma16816_zc(kbias2, zk.x, zk.y, zk.z, zk.w, qf[s][0], qf[s][1]);
+            else if ((s & 1) == 0) mma16816(kbias, zk.x, zk.y, zk.z, zk.w, qf[s][0], qf[s][1]);
+            else mma16816(kbias2, zk.x, zk.y, zk.z, zk.w, qf[s][0], qf[s][1]);
         }
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
@@ -224,8 +229,8 @@ __device__ __forceinline__ void process_block(const uint8_t *__restrict__ sb, Wa
     float kb0[4], kb1[4];
 #pragma unroll
     for (int grp = 0; grp < 4; ++grp) {
-        kb0[grp] = __shfl_sync(0xffffffffu, kbias[0], grp * 4 + tq);
-        kb1[grp] = __shfl_sync(0xffffffffu, kbias[1], grp * 4 + tq);
+        kb0[grp] = __shfl_sync(0xffffffffu, kbias[0] + kbias2[2], grp * 4 + tq);
+        kb1[grp] = __shfl_sync(0xffffffffu, kbias[1] + kbias2[3], grp * 4 + tq);
     }
     // logits relative to the running max, y = logit - m (one FFMA with the key
     // norm); first block of a segment: m = -inf, measure against 0 instead
@@ -269,6 +274,8 @@ __device__ __forceinline__ void process_block(const uint8_t *__restrict__ sb, Wa
         }
         st.ob[0] *= al0;
         st.ob[1] *= al1;
+        st.ob2[2] *= al0;
+        st.ob2[3] *= al1;
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
             sacc[i][0] -= d0;
@@ -293,7 +300,8 @@ __device__ __forceinline__ void process_block(const uint8_t *__restrict__ sb, Wa
     long long t2 = tm ? clk() : 0;
     // ---- P.V ---------------------------------------------------------------------------
     // value offsets as A: row gq (< 4) = channel group, k = tokens
-    const uint2 *vbp = reinterpret_cast<const uint2 *>(sb + Blk::VB_OFF + ((gq & 3) * 4 + tq) * 64);
+    const uint4 *vbp = reinterpret_cast<const uint4 *>(sb + Blk::VB_OFF + ((gq & 3) * 4 + tq) * 64);
+    uint4 zv;
     const int srcA = 4 * tq + (gq >> 1), srcB = 4 * (tq + 4) + (gq >> 1);
     const bool odd = (gq & 1) != 0;
 #pragma unroll
@@ -342,8 +350,13 @@ __device__ __forceinline__ void process_block(const uint8_t *__restrict__ sb, Wa
                      src[2 * WPF + half] & mask, src[3 * WPF + half] & mask, bv[mm >> 1][0], bv[mm >> 1][1]);
         }
         {
-            const uint2 z = vbp[j];
-            mma16816(st.ob, z.x, z.x, z.y, z.y, bp0, bp1);  // rows >= 4 don't-care, as for the keys
+            // paired quads as for the keys: even j -> rows gq of ob, odd j -> rows gq+8 of ob2
+            if ((j & 1) == 0) {
+                zv = vbp[j >> 1];
+                mma16816(st.ob, zv.x, zv.y, zv.z, zv.w, bp0, bp1);
+            } else {
+                mma16816(st.ob2, zv.x, zv.y, zv.z, zv.w, bp0, bp1);
+            }
         }
     }
     if (tm) {
@@ -783,6 +796,7 @@ __global__ void __launch_bounds__(NCW_ * 32, 1) decode_attn_kernel(const AttnArg
 #pragma unroll
         for (int mm = 0; mm < 8; ++mm) st.o[mm][0] = st.o[mm][1] = st.o[mm][2] = st.o[mm][3] = 0.f;
         st.ob[0] = st.ob[1] = st.ob[2] = st.ob[3] = 0.f;
+        st.ob2[0] = st.ob2[1] = st.ob2[2] = st.ob2[3] = 0.f;
         st.m[0] = st.m[1] = -CUDART_INF_F;
         st.l[0] = st.l[1] = 0.f;
         if (a.prof) tmr[6] += clk() - tq0;
@@ -859,8 +873,8 @@ __global__ void __launch_bounds__(NCW_ * 32, 1) decode_attn_kernel(const AttnArg
             float vb0[4], vb1[4];
 #pragma unroll
             for (int gc = 0; gc < 4; ++gc) {
-                vb0[gc] = __shfl_sync(0xffffffffu, st.ob[0], gc * 4 + tq);
-                vb1[gc] = __shfl_sync(0xffffffffu, st.ob[1], gc * 4 + tq);
+                vb0[gc] = __shfl_sync(0xffffffffu, st.ob[0] + st.ob2[2], gc * 4 + tq);
+                vb1[gc] = __shfl_sync(0xffffffffu, st.ob[1] + st.ob2[3], gc * 4 + tq);
             }
             constexpr int TPW = BITS == 0 ? 8 : 16 / (BITS == 0 ? 2 : BITS);
             constexpr int HALFT = TPW / 2;

@@ -151,11 +151,14 @@ OSK_HD int ka_index(int c, int grp) {
     k_chan_split(c, s, tq, slot);
     return ((s * 4 + tq) * 4 + grp) * 4 + slot;
 }
-// K b-params: [grp][tq][s][slot]  (lane g<4 reads 64 B: its group, all k-steps)
+// K b-params: [grp][tq][s/2][word][half], word = (slot/2)*2 + s%2: one 16-byte
+// load per k-step PAIR is an A quad (x_s, x_s+1, y_s, y_s+1) whose rows g hold
+// k-step s and rows g+8 k-step s+1, so the bias MMAs read it without moves
+// (lane g<4 reads 64 B: its group, all k-steps)
 OSK_HD int kb_index(int c, int grp) {
     int s, tq, slot;
     k_chan_split(c, s, tq, slot);
-    return ((grp * 4 + tq) * 8 + s) * 4 + slot;
+    return ((grp * 4 + tq) * 4 + (s >> 1)) * 8 + ((slot >> 1) * 2 + (s & 1)) * 2 + (slot & 1);
 }
 // token t = 16j + r; the B-fragment slot order is (tq, tq+8, tq+4, tq+12)
 OSK_HD void v_tok_split(int t, int &j, int &tq, int &slot) {
@@ -171,11 +174,11 @@ OSK_HD int va_index(int t, int gc) {
     v_tok_split(t, j, tq, slot);
     return ((j * 4 + tq) * 4 + gc) * 4 + slot;
 }
-// V b-params: [gc][tq][j][slot]
+// V b-params: [gc][tq][j/2][word][half], paired like the K b-params
 OSK_HD int vb_index(int t, int gc) {
     int j, tq, slot;
     v_tok_split(t, j, tq, slot);
-    return ((gc * 4 + tq) * 8 + j) * 4 + slot;
+    return ((gc * 4 + tq) * 4 + (j >> 1)) * 8 + ((slot >> 1) * 2 + (j & 1)) * 2 + (slot & 1);
 }
 // norms: [g][i][2] -> token 16i + g (+8 for slot 1)
 OSK_HD int norm_index(int t) {

@@ -152,6 +152,41 @@ int oscar_kv_materialize(oscar_kv_handle *h, int64_t b, double *k_out, double *v
 int oscar_lse_merge(const float *outs, const float *lses, int64_t parts, int64_t rows, int64_t d,
                     float *out, float *lse_out, void *stream);
 
+/* ---- fused sequence-shard exchange over peer memory (C5) ----
+ * Replaces "attend -> all-gather (O, LSE) -> oscar_lse_merge" by: the
+ * attention kernel's final merge stores each normalised row straight into
+ * every rank's receive area (NVLink peer stores) and raises a per-row epoch
+ * flag; oscar_peer_merge on each rank waits for the flags and merges.
+ * Rank r's receive area (oscar_peer_area_bytes, on rank r's GPU, mapped into
+ * every peer with oscar_ipc_*): fp32 recv[2][world][rows][OSCAR_PEER_STRIDE]
+ * (O[0..127], LSE at 128) followed by uint32 flags[2][world][rows], zeroed.
+ * Epochs start at 1 and increase by one per step on every rank. */
+#define OSCAR_PEER_MAX 8
+#define OSCAR_PEER_STRIDE 132
+typedef struct oscar_peer_plan {
+    int32_t world, rank;              /* this handle's shard; world <= OSCAR_PEER_MAX */
+    int64_t rows;                     /* batch * q_heads */
+    float *recv[OSCAR_PEER_MAX];      /* rank p's receive area, as mapped here */
+    uint32_t *flags[OSCAR_PEER_MAX];  /* rank p's flags, as mapped here */
+} oscar_peer_plan;
+int64_t oscar_peer_area_bytes(int32_t world, int64_t rows);
+/* attend (k = v = NULL) or decode_step (current token attended and appended)
+ * whose result is published to every rank of the plan instead of returned. */
+int oscar_kv_attend_publish(oscar_kv_handle *h, const void *q, const void *k, const void *v,
+                            const oscar_peer_plan *plan, uint32_t epoch, void *stream);
+/* an empty shard's contribution (LSE = -inf rows) */
+int oscar_peer_publish_empty(const oscar_peer_plan *plan, uint32_t epoch, void *stream);
+/* wait for all ranks' rows of `epoch` in this rank's area, merge -> out
+ * fp32 [rows, 128], lse optional; status (device int32, optional) becomes 1
+ * and out NaN if a peer does not publish within ~5 s. */
+int oscar_peer_merge(const oscar_peer_plan *plan, uint32_t epoch, float *out, float *lse, int32_t *status,
+                     void *stream);
+/* CUDA IPC plumbing for the receive areas (64-byte handles). */
+int oscar_ipc_alloc(int64_t bytes, int32_t device, void **dptr, void *handle_out);
+int oscar_ipc_open(const void *handle, int32_t device, void **dptr);
+int oscar_ipc_close(void *dptr);
+int oscar_ipc_free(void *dptr);
+
 /* Number of kernels the last decode/attend call launched (instrumentation). */
 int oscar_kv_last_launch_count(const oscar_kv_handle *h);
 

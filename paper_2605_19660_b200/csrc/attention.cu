@@ -31,6 +31,7 @@
 #include "device_common.cuh"
 #include "kernels.h"
 #include "layout.h"
+#include "peer.cuh"
 #include "split.h"
 
 namespace osk {
@@ -1082,10 +1083,14 @@ __global__ void __launch_bounds__(NCW_ * 32, 1) decode_attn_kernel(const AttnArg
 #pragma unroll
         for (int e = 0; e < 4; ++e) x[e] *= inv;
         if (a.rotate_v) fht128_warp(x, lane);  // explicit-V mode: rotate the output back
-        *reinterpret_cast<float4 *>(a.out + ((int64_t)b * a.Hq + kvh * g + h) * D + lane * 4) =
-            make_float4(x[0], x[1], x[2], x[3]);
-        if (a.lse && lane == 0)
-            a.lse[(int64_t)b * a.Hq + kvh * g + h] = (L > 0.f) ? (M + __log2f(L)) * LN2 : -CUDART_INF_F;
+        const int64_t row = (int64_t)b * a.Hq + kvh * g + h;
+        const float lse_row = (L > 0.f) ? (M + __log2f(L)) * LN2 : -CUDART_INF_F;
+        if (a.pub.world > 0) {
+            peer_publish_row(a.pub, a.pub_epoch, row, make_float4(x[0], x[1], x[2], x[3]), lse_row, lane);
+        } else {
+            *reinterpret_cast<float4 *>(a.out + row * D + lane * 4) = make_float4(x[0], x[1], x[2], x[3]);
+            if (a.lse && lane == 0) a.lse[row] = lse_row;
+        }
         if (h == 0 && lane == 0) a.counters[bh] = 0;  // the ticket is complete: reset for the next launch
     }
     if (a.prof) tmr[10] += clk() - tf0;

@@ -350,10 +350,15 @@ struct oscar_kv_handle {
         return a;
     }
 
-    void decode_step(const void *q, const void *k, const void *v, float *out, float *lse, cudaStream_t s) {
+    void decode_step(const void *q, const void *k, const void *v, float *out, float *lse, cudaStream_t s,
+                     const PeerPlan *pub = nullptr, uint32_t epoch = 0) {
         if (packed + residual + 1 > max_tokens) throw InvalidArg("decode_step: cache capacity exceeded");
         last_launches = 0;
         AttnArgs a = attn_args(q, k, v, out, lse);
+        if (pub) {
+            a.pub = *pub;
+            a.pub_epoch = epoch;
+        }
         CK(launch_attention(dbits, a, s));
         ++last_launches;
         blocks_written = false;
@@ -366,10 +371,15 @@ struct oscar_kv_handle {
         }
     }
 
-    void attend(const void *q, float *out, float *lse, cudaStream_t s) {
+    void attend(const void *q, float *out, float *lse, cudaStream_t s, const PeerPlan *pub = nullptr,
+                uint32_t epoch = 0) {
         last_launches = 0;
         if (packed + residual == 0) throw LogicErr("attend: empty cache");
         AttnArgs a = attn_args(q, nullptr, nullptr, out, lse);
+        if (pub) {
+            a.pub = *pub;
+            a.pub_epoch = epoch;
+        }
         // debug: OSCAR_PROF=1 prints per-phase cycles averaged over warps (synchronises)
         static int prof = -1;
         if (prof < 0) prof = getenv("OSCAR_PROF") ? 1 : 0;
@@ -1051,6 +1061,99 @@ int oscar_kv_attend(oscar_kv_handle *h, const void *q, float *out, float *lse, v
         h->last_stream = (cudaStream_t)stream;
         h->attend(q, out, lse, (cudaStream_t)stream);
     });
+}
+
+namespace {
+PeerPlan peer_plan(const oscar_peer_plan *p, int64_t rows_expected) {
+    static_assert(OSCAR_PEER_MAX == PEER_MAX && OSCAR_PEER_STRIDE == PEER_STRIDE, "peer layout");
+    if (!p) throw InvalidArg("peer plan: null");
+    if (p->world < 1 || p->world > OSCAR_PEER_MAX || p->rank < 0 || p->rank >= p->world)
+        throw InvalidArg("peer plan: bad world/rank");
+    if (p->rows <= 0 || (rows_expected >= 0 && p->rows != rows_expected))
+        throw InvalidArg("peer plan: rows must be batch * q_heads");
+    PeerPlan q{};
+    q.world = p->world;
+    q.rank = p->rank;
+    q.rows = p->rows;
+    for (int i = 0; i < p->world; ++i) {
+        if (!p->recv[i] || !p->flags[i]) throw InvalidArg("peer plan: null receive area");
+        if (((uintptr_t)p->recv[i]) % 16 || ((uintptr_t)p->flags[i]) % 4)
+            throw InvalidArg("peer plan: misaligned receive area");
+        q.recv[i] = p->recv[i];
+        q.flags[i] = p->flags[i];
+    }
+    return q;
+}
+}  // namespace
+
+int64_t oscar_peer_area_bytes(int32_t world, int64_t rows) {
+    if (world < 1 || world > OSCAR_PEER_MAX || rows <= 0) return -1;
+    return (int64_t)2 * world * rows * (OSCAR_PEER_STRIDE * 4 + 4);
+}
+
+int oscar_kv_attend_publish(oscar_kv_handle *h, const void *q, const void *k, const void *v,
+                            const oscar_peer_plan *plan, uint32_t epoch, void *stream) {
+    return guard([&] {
+        if (!h || !q) throw InvalidArg("attend_publish: null argument");
+        if ((k == nullptr) != (v == nullptr)) throw InvalidArg("attend_publish: k and v go together");
+        if (epoch == 0) throw InvalidArg("attend_publish: epochs start at 1");
+        const PeerPlan pp = peer_plan(plan, h->B * h->Hq);
+        CK(cudaSetDevice(h->device));
+        h->last_stream = (cudaStream_t)stream;
+        if (k) h->decode_step(q, k, v, nullptr, nullptr, (cudaStream_t)stream, &pp, epoch);
+        else h->attend(q, nullptr, nullptr, (cudaStream_t)stream, &pp, epoch);
+    });
+}
+
+int oscar_peer_publish_empty(const oscar_peer_plan *plan, uint32_t epoch, void *stream) {
+    return guard([&] {
+        if (epoch == 0) throw InvalidArg("peer_publish_empty: epochs start at 1");
+        const PeerPlan pp = peer_plan(plan, -1);
+        CK(launch_peer_publish_empty(pp, epoch, (cudaStream_t)stream));
+    });
+}
+
+int oscar_peer_merge(const oscar_peer_plan *plan, uint32_t epoch, float *out, float *lse, int32_t *status,
+                     void *stream) {
+    return guard([&] {
+        if (!out) throw InvalidArg("peer_merge: null out");
+        if (epoch == 0) throw InvalidArg("peer_merge: epochs start at 1");
+        const PeerPlan pp = peer_plan(plan, -1);
+        CK(launch_peer_merge(pp, epoch, out, lse, status, (cudaStream_t)stream));
+    });
+}
+
+int oscar_ipc_alloc(int64_t bytes, int32_t device, void **dptr, void *handle_out) {
+    return guard([&] {
+        if (bytes <= 0 || !dptr || !handle_out) throw InvalidArg("ipc_alloc: bad argument");
+        CK(cudaSetDevice(device));
+        void *p = nullptr;
+        CK(cudaMalloc(&p, (size_t)bytes));
+        CK(cudaMemset(p, 0, (size_t)bytes));
+        cudaIpcMemHandle_t hd;
+        static_assert(sizeof(hd) == 64, "ipc handle size");
+        CK(cudaIpcGetMemHandle(&hd, p));
+        memcpy(handle_out, &hd, sizeof(hd));
+        *dptr = p;
+    });
+}
+
+int oscar_ipc_open(const void *handle, int32_t device, void **dptr) {
+    return guard([&] {
+        if (!handle || !dptr) throw InvalidArg("ipc_open: bad argument");
+        CK(cudaSetDevice(device));
+        cudaIpcMemHandle_t hd;
+        memcpy(&hd, handle, sizeof(hd));
+        CK(cudaIpcOpenMemHandle(dptr, hd, cudaIpcMemLazyEnablePeerAccess));
+    });
+}
+
+int oscar_ipc_close(void *dptr) {
+    return guard([&] { CK(cudaIpcCloseMemHandle(dptr)); });
+}
+
+int oscar_ipc_free(void *dptr) {
+    return guard([&] { CK(cudaFree(dptr)); });
 }
 
 int oscar_kv_decode_step_host(oscar_kv_handle *h, const void *q_host, const void *k_host, const void *v_host,

@@ -50,6 +50,19 @@ struct RingCopyArgs {
 };
 cudaError_t launch_ring_copy(const RingCopyArgs &a, cudaStream_t st);
 
+// Sequence-shard exchange plan (C5): rank r's receive area recv[r] holds
+// [2 parities][world][rows][PEER_STRIDE] floats (O[0..127], LSE at 128) and
+// flags[r] holds [2][world][rows] epochs; both live on rank r's GPU and are
+// mapped into every peer (CUDA IPC).  Same layout as oscar_peer_plan.
+constexpr int PEER_MAX = 8;
+constexpr int PEER_STRIDE = 132;  // 128 + LSE, padded to 16 B
+struct PeerPlan {
+    int32_t world, rank;
+    int64_t rows;
+    float *recv[PEER_MAX];
+    uint32_t *flags[PEER_MAX];
+};
+
 struct AttnArgs {
     const uint8_t *blocks;
     int64_t max_blocks;
@@ -78,6 +91,11 @@ struct AttnArgs {
     int pdl_prefetch;  // packed records unchanged since the previous launch on this stream:
                        // the ring fill may start before griddepcontrol.wait
     unsigned long long *prof;  // debug: per-warp phase cycles [ncta][NCW][5] or null
+    // fused sequence-shard exchange (peer.cu): when pub_world > 0 the final merge
+    // stores each normalised row (O, LSE) straight into every rank's receive area
+    // over peer memory and raises its flag, instead of writing out / lse
+    PeerPlan pub;
+    uint32_t pub_epoch;
 };
 // bits: 2, 4 or 0 (bf16 baseline)
 cudaError_t launch_attention(int bits, const AttnArgs &a, cudaStream_t st);
@@ -85,6 +103,13 @@ int attention_max_partials(int64_t nb, int BH, int ncta);
 int64_t attention_scratch_floats(int max_ctas);  // floats per segment slot set
 int attention_max_segments(int64_t nb_units, int BH, int ncta);
 int attention_grid(int bits, int num_sms, int64_t nb, int BH);
+
+// peer.cu: wait for every rank's row of this epoch in recv[rank], merge -> out/lse;
+// status (optional, device int) is set to 1 if a peer did not publish within ~5 s
+cudaError_t launch_peer_merge(const PeerPlan &p, uint32_t epoch, float *out, float *lse, int *status,
+                              cudaStream_t st);
+// an empty shard publishes LSE = -inf rows (it contributes nothing to the softmax)
+cudaError_t launch_peer_publish_empty(const PeerPlan &p, uint32_t epoch, cudaStream_t st);
 
 cudaError_t launch_lse_merge(const float *outs, const float *lses, int64_t parts, int64_t rows, int64_t d,
                              float *out, float *lse_out, cudaStream_t st);

@@ -56,6 +56,16 @@ class _Export(ctypes.Structure):
         "k_raw", "v_raw", "k_norms", "k_residual", "k_norms_residual", "v_residual")]
 
 
+PEER_MAX, PEER_STRIDE = 8, 132
+
+
+class _PeerPlan(ctypes.Structure):
+    """oscar_peer_plan (include/oscar_kv.h)."""
+
+    _fields_ = [("world", ctypes.c_int32), ("rank", ctypes.c_int32), ("rows", ctypes.c_int64),
+                ("recv", _P * PEER_MAX), ("flags", _P * PEER_MAX)]
+
+
 _lib = None
 
 
@@ -85,6 +95,15 @@ def lib():
         L.oscar_kv_materialize.argtypes = [_P, ctypes.c_int64, _P, _P]
         L.oscar_lse_merge.argtypes = [_P, _P, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64, _P, _P, _P]
         L.oscar_kv_last_launch_count.argtypes = [_P]
+        L.oscar_peer_area_bytes.restype = ctypes.c_int64
+        L.oscar_peer_area_bytes.argtypes = [ctypes.c_int32, ctypes.c_int64]
+        L.oscar_kv_attend_publish.argtypes = [_P, _P, _P, _P, ctypes.POINTER(_PeerPlan), ctypes.c_uint32, _P]
+        L.oscar_peer_publish_empty.argtypes = [ctypes.POINTER(_PeerPlan), ctypes.c_uint32, _P]
+        L.oscar_peer_merge.argtypes = [ctypes.POINTER(_PeerPlan), ctypes.c_uint32, _P, _P, _P, _P]
+        L.oscar_ipc_alloc.argtypes = [ctypes.c_int64, ctypes.c_int32, ctypes.POINTER(_P), _P]
+        L.oscar_ipc_open.argtypes = [_P, ctypes.c_int32, ctypes.POINTER(_P)]
+        L.oscar_ipc_close.argtypes = [_P]
+        L.oscar_ipc_free.argtypes = [_P]
         _lib = L
     return _lib
 
@@ -94,7 +113,8 @@ C_ABI_SYMBOLS = [
     "oscar_last_error", "oscar_kv_config_validate", "oscar_kv_create", "oscar_kv_destroy", "oscar_kv_append",
     "oscar_kv_decode_step", "oscar_kv_decode_step_many", "oscar_kv_attend", "oscar_kv_decode_step_host", "oscar_kv_stats",
     "oscar_kv_memory_report", "oscar_kv_export", "oscar_kv_dump", "oscar_kv_load", "oscar_kv_materialize", "oscar_lse_merge",
-    "oscar_kv_last_launch_count",
+    "oscar_kv_last_launch_count", "oscar_peer_area_bytes", "oscar_kv_attend_publish", "oscar_peer_publish_empty",
+    "oscar_peer_merge", "oscar_ipc_alloc", "oscar_ipc_open", "oscar_ipc_close", "oscar_ipc_free",
 ]
 
 
@@ -202,6 +222,12 @@ class KvCache:
             lse = torch.empty((self.B, self.Hq), dtype=torch.float32, device=q.device)
         _check(lib().oscar_kv_attend(self._h, _ptr(q), _ptr(out), _ptr(lse), _stream(stream)))
         return out, lse
+
+    def attend_publish(self, q, plan: "PeerPlan", epoch: int, k=None, v=None, stream=None):
+        """attend (k = v = None) or decode_step whose rows are published to every
+        rank of `plan` (fused sequence-shard exchange) instead of returned."""
+        _check(lib().oscar_kv_attend_publish(self._h, _ptr(q), _ptr(k), _ptr(v), ctypes.byref(plan.c), epoch,
+                                             _stream(stream)))
 
     def decode_step_host(self, q: np.ndarray, k: np.ndarray, v: np.ndarray, out: np.ndarray, lse=None,
                          stream=None):
@@ -320,3 +346,60 @@ def lse_merge(outs, lses, out=None, lse_out=None, stream=None):
         out = torch.empty((rows, d), dtype=torch.float32, device=outs.device)
     _check(lib().oscar_lse_merge(_ptr(outs), _ptr(lses), P, rows, d, _ptr(out), _ptr(lse_out), _stream(stream)))
     return out
+
+
+# ----------------------------------------------------------------------------- peer exchange (C5)
+def peer_area_bytes(world: int, rows: int) -> int:
+    """Bytes of one rank's receive area: fp32 recv [2][world][rows][132] + uint32 flags [2][world][rows]."""
+    n = lib().oscar_peer_area_bytes(world, rows)
+    if n < 0:
+        raise ValueError(f"bad peer area shape world={world} rows={rows}")
+    return int(n)
+
+
+class PeerPlan:
+    """oscar_peer_plan over receive areas given as device addresses (one per
+    rank, as mapped in this process)."""
+
+    def __init__(self, world: int, rank: int, rows: int, areas):
+        if len(areas) != world:
+            raise ValueError("one receive area per rank")
+        self.world, self.rank, self.rows = world, rank, rows
+        off = 2 * world * rows * PEER_STRIDE * 4
+        self.c = _PeerPlan(world, rank, rows)
+        for p, a in enumerate(areas):
+            self.c.recv[p] = int(a)
+            self.c.flags[p] = int(a) + off
+
+
+def peer_publish_empty(plan: PeerPlan, epoch: int, stream=None):
+    _check(lib().oscar_peer_publish_empty(ctypes.byref(plan.c), epoch, _stream(stream)))
+
+
+def peer_merge(plan: PeerPlan, epoch: int, out, lse=None, status=None, stream=None):
+    """Wait for every rank's rows of `epoch` and merge -> out [rows, 128] (device)."""
+    _check(lib().oscar_peer_merge(ctypes.byref(plan.c), epoch, _ptr(out), _ptr(lse), _ptr(status),
+                                  _stream(stream)))
+    return out
+
+
+def ipc_alloc(nbytes: int, device: int = 0) -> tuple[int, bytes]:
+    """Zeroed device allocation + its 64-byte CUDA IPC handle."""
+    p = _P()
+    h = ctypes.create_string_buffer(64)
+    _check(lib().oscar_ipc_alloc(nbytes, device, ctypes.byref(p), h))
+    return p.value, h.raw
+
+
+def ipc_open(handle: bytes, device: int = 0) -> int:
+    p = _P()
+    _check(lib().oscar_ipc_open(ctypes.create_string_buffer(handle, 64), device, ctypes.byref(p)))
+    return p.value
+
+
+def ipc_close(ptr: int):
+    _check(lib().oscar_ipc_close(_P(ptr)))
+
+
+def ipc_free(ptr: int):
+    _check(lib().oscar_ipc_free(_P(ptr)))

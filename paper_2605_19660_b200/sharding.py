@@ -13,8 +13,11 @@ partitionings, matching BASELINE.json configs 3-5:
   flush_v_block work on whole R-blocks, kv_cache.cpp:101-157); the residual
   window and every appended token live on the tail rank, which therefore
   flushes exactly when the single-cache reference would.  Each rank attends
-  its shard, the (O, LSE) partials are exchanged with ONE all-gather and
-  merged on device by the log-sum-exp merge kernel (oscar_lse_merge).
+  its shard; the (O, LSE) partials are either exchanged with ONE all-gather
+  and merged by oscar_lse_merge (exchange="nccl"), or published by the
+  attention kernel itself into every rank's receive area over NVLink peer
+  memory and merged by one flag-polling kernel (exchange="p2p",
+  PeerExchange; no collective on the data path).
 
 The reference is single-process (no MPI/NCCL anywhere); these
 plans are new, but the union of the per-rank caches is bit-identical to the
@@ -119,6 +122,65 @@ def gather_partials(o, lse, group=None):
     return allb[:, :, :d].contiguous(), allb[:, :, d].contiguous()
 
 
+class PeerExchange:
+    """Receive areas of the fused sequence-shard exchange (oscar_kv_attend_publish
+    + oscar_peer_merge): this rank allocates its area on its GPU, the 64-byte
+    CUDA IPC handles are all-gathered over the process group (host bytes, so
+    gloo or NCCL), and every peer's area is mapped here.  No collective runs on
+    the data path: the attention kernel stores its rows into the peers' areas
+    over NVLink and the merge kernel polls the local flags."""
+
+    def __init__(self, rows: int, device: int = 0, group=None):
+        from . import kv_cache as kc
+
+        td = _dist()
+        self.world = td.get_world_size(group) if td.is_initialized() else 1
+        self.rank = td.get_rank(group) if td.is_initialized() else 0
+        self.rows, self.device = rows, device
+        nbytes = kc.peer_area_bytes(self.world, rows)
+        self._own, handle = kc.ipc_alloc(nbytes, device)
+        handles = [None] * self.world
+        if self.world > 1:
+            td.all_gather_object(handles, handle, group=group)
+        else:
+            handles = [handle]
+        self._opened = []
+        areas = []
+        for p, h in enumerate(handles):
+            if p == self.rank:
+                areas.append(self._own)
+            else:
+                a = kc.ipc_open(h, device)
+                self._opened.append(a)
+                areas.append(a)
+        self.plan = kc.PeerPlan(self.world, self.rank, rows, areas)
+        self.epoch = 0
+
+    def close(self):
+        from . import kv_cache as kc
+
+        for a in self._opened:
+            kc.ipc_close(a)
+        self._opened = []
+        if self._own:
+            kc.ipc_free(self._own)
+            self._own = 0
+
+
+def local_peer_plans(world: int, rows: int, device=None):
+    """Receive areas of `world` VIRTUAL ranks on one device (single-GPU tests of
+    the publish / merge kernels: every plan maps every area directly).
+    Returns (plans, areas); keep `areas` alive while the plans are used."""
+    import torch
+
+    from . import kv_cache as kc
+
+    nbytes = kc.peer_area_bytes(world, rows)
+    areas = [torch.zeros(nbytes, dtype=torch.uint8, device=device or "cuda") for _ in range(world)]
+    ptrs = [a.data_ptr() for a in areas]
+    return [kc.PeerPlan(world, r, rows, ptrs) for r in range(world)], areas
+
+
 # ----------------------------------------------------------------------------- sharded caches
 class SeqShardedKvCache:
     """One rank's share of a sequence-sharded cache (C5).
@@ -130,7 +192,10 @@ class SeqShardedKvCache:
     """
 
     def __init__(self, cfg, batch: int, q_heads: int, max_tokens_per_rank: int, device: int = 0,
-                 keep_exact: bool = True, group=None, merge=None):
+                 keep_exact: bool = True, group=None, merge=None, exchange: str = "nccl"):
+        """exchange: "nccl" (all-gather of the packed partials + lse_merge) or
+        "p2p" (the attention kernel publishes its rows into every rank's
+        receive area over peer memory; one merge kernel per rank)."""
         from .kv_cache import KvCache, lse_merge
 
         td = _dist()
@@ -142,6 +207,10 @@ class SeqShardedKvCache:
                              keep_exact=keep_exact)
         self.shard = None
         self._merge = merge or (lambda outs, lses: lse_merge(outs, lses))
+        if exchange not in ("nccl", "p2p"):
+            raise ValueError(f"exchange must be 'nccl' or 'p2p', not {exchange!r}")
+        self.exchange = exchange
+        self.peers = PeerExchange(batch * q_heads, device, group) if exchange == "p2p" and self.world > 1 else None
 
     def prefill(self, k, v, S: int | None = None, sliced: bool = False, stream=None):
         S = k.shape[1] if S is None else S
@@ -171,11 +240,31 @@ class SeqShardedKvCache:
         return out, lse
 
     def decode_step(self, q, k, v, stream=None):
+        if self.peers is not None:
+            return self._decode_step_p2p(q, k, v, stream)
         o, l = self.local_partial(q, k, v, stream=stream)
         if self.world == 1:  # the only shard: its partial is the normalised result
             return o.reshape(self.B, self.Hq, D)
         outs, lses = gather_partials(o, l, self.group)
         return self._merge(outs, lses).reshape(self.B, self.Hq, D)
+
+    def _decode_step_p2p(self, q, k, v, stream=None):
+        import torch
+
+        from . import kv_cache as kc
+
+        px = self.peers
+        px.epoch += 1
+        if self.shard is not None and self.shard.tail and k is not None:
+            self.cache.attend_publish(q, px.plan, px.epoch, k, v, stream=stream)
+        elif self.cache.total_tokens > 0:
+            self.cache.attend_publish(q, px.plan, px.epoch, stream=stream)
+        else:
+            kc.peer_publish_empty(px.plan, px.epoch, stream=stream)
+        if getattr(self, "_p2p_out", None) is None:
+            self._p2p_out = torch.empty((self.B * self.Hq, D), dtype=torch.float32, device=q.device)
+        kc.peer_merge(px.plan, px.epoch, self._p2p_out, stream=stream)
+        return self._p2p_out.reshape(self.B, self.Hq, D)
 
     @property
     def total_tokens(self) -> int:
@@ -191,4 +280,7 @@ class SeqShardedKvCache:
         return int(t.item())
 
     def close(self):
+        if self.peers is not None:
+            self.peers.close()
+            self.peers = None
         self.cache.close()

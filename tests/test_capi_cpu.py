@@ -12,7 +12,7 @@ LIB = os.path.join(ROOT, "paper_2605_19660_b200", "liboscar_b200.so")
 
 def declared_symbols():
     src = open(HEADER).read()
-    return sorted(set(re.findall(r"^\s*(?:int|const char \*)\s*(oscar_\w+)\s*\(", src, re.M)))
+    return sorted(set(re.findall(r"^\s*(?:int|int64_t|const char \*)\s*(oscar_\w+)\s*\(", src, re.M)))
 
 
 def test_library_exports_every_declared_symbol():
@@ -42,6 +42,36 @@ def test_config_validation_without_gpu():
                 dict(bits=3), dict(head_dim=64)):
         with pytest.raises(ValueError):
             PipelineConfig(**bad).validate()
+
+
+def test_peer_plan_validation_without_gpu():
+    """The fused exchange's C-ABI checks its plan before touching the device
+    (status 1 = std::invalid_argument), and sizes receive areas host-side."""
+    if not os.path.exists(LIB):
+        pytest.skip("library not built")
+    from paper_2605_19660_b200 import kv_cache as kc
+
+    rows = 28
+    assert kc.peer_area_bytes(8, rows) == 2 * 8 * rows * (132 * 4 + 4)
+    with pytest.raises(ValueError):
+        kc.peer_area_bytes(9, rows)
+    ok = kc.PeerPlan(2, 0, rows, [4096, 8192])
+    bad = [kc.PeerPlan(2, 2, rows, [4096, 8192]),       # rank out of range
+           kc.PeerPlan(2, 0, rows, [4096, 0]),          # unmapped area
+           kc.PeerPlan(2, 1, rows, [4096 + 4, 8192])]   # misaligned area
+    for p in bad:
+        with pytest.raises(ValueError):
+            kc.peer_merge(p, 1, _FakeTensor(4096), stream=0)
+    with pytest.raises(ValueError):
+        kc.peer_merge(ok, 0, _FakeTensor(4096), stream=0)  # epochs start at 1
+
+
+class _FakeTensor:
+    def __init__(self, addr):
+        self.addr = addr
+
+    def data_ptr(self):
+        return self.addr
 
 
 CPP_PROGRAM = r"""

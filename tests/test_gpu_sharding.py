@@ -98,3 +98,132 @@ def test_head_sharded_equals_full_heads():
         ef, eh = full.export(1), c.export(1)
         for key in ("k_payload", "v_payload", "k_delta", "k_zp", "v_delta", "v_zp", "k_norms"):
             assert np.array_equal(eh[key], ef[key][hs.kv_lo:hs.kv_hi]), key
+
+
+# ---------------------------------------------------------------- fused peer-memory exchange
+def _single_cache_outputs():
+    from paper_2605_19660_b200 import KvCache, PipelineConfig
+
+    k, v, q = _inputs()
+    c = KvCache(PipelineConfig(heads=H), batch=1, q_heads=H * G_, max_tokens=S + STEPS)
+    c.buffer_quant(dev_bf16(k[None, :S]), dev_bf16(v[None, :S]))
+    return [c.decode_step(dev_bf16(q[t][None]), dev_bf16(k[S + t][None]), dev_bf16(v[S + t][None])).cpu().numpy()
+            for t in range(STEPS)]
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_peer_publish_merge_virtual_ranks(world):
+    """The attention kernel publishes its rows into every rank's receive area
+    and the flag-polling merge kernel combines them (oscar_kv_attend_publish +
+    oscar_peer_merge).  `world` virtual ranks share cuda:0 (their areas are
+    mapped directly); publish kernels go first on the stream, then the merges.
+    30 steps (epoch parities alternate) crossing a flush on the tail shard."""
+    import torch
+
+    from paper_2605_19660_b200 import KvCache, PipelineConfig
+    from paper_2605_19660_b200 import kv_cache as kc
+    from paper_2605_19660_b200.sharding import local_peer_plans, sequence_shard
+
+    k, v, q = _inputs()
+    rows = H * G_
+    plans, areas = local_peer_plans(world, rows)
+    shards = [sequence_shard(S, world, r) for r in range(world)]
+    caches = []
+    for sh in shards:
+        c = KvCache(PipelineConfig(heads=H), batch=1, q_heads=rows, max_tokens=S + STEPS)
+        c.buffer_quant(dev_bf16(k[None, sh.tok_lo:sh.tok_hi]), dev_bf16(v[None, sh.tok_lo:sh.tok_hi]))
+        caches.append(c)
+    ref = _single_cache_outputs()
+    status = torch.zeros(1, dtype=torch.int32, device="cuda")
+    outs = [torch.empty((rows, 128), dtype=torch.float32, device="cuda") for _ in range(world)]
+    lses = [torch.empty((rows,), dtype=torch.float32, device="cuda") for _ in range(world)]
+    for t in range(STEPS):
+        epoch = t + 1
+        qt, kt, vt = dev_bf16(q[t][None]), dev_bf16(k[S + t][None]), dev_bf16(v[S + t][None])
+        for r, (c, sh) in enumerate(zip(caches, shards)):
+            if sh.tail:
+                c.attend_publish(qt, plans[r], epoch, kt, vt)
+            else:
+                c.attend_publish(qt, plans[r], epoch)
+        for r in range(world):
+            kc.peer_merge(plans[r], epoch, outs[r], lses[r], status)
+        for r in range(world):
+            assert rel_err(outs[r].cpu().numpy()[None], ref[t]) < 1e-5, (t, r)
+    assert status.item() == 0
+    assert caches[-1].flush_count == 1
+    # every rank merged the same rows; LSE equals the single cache's
+    full = KvCache(PipelineConfig(heads=H), batch=1, q_heads=rows, max_tokens=S + STEPS + 1)
+    full.buffer_quant(dev_bf16(k[None, :S + STEPS]), dev_bf16(v[None, :S + STEPS]))
+    _, lse_full = full.attend(dev_bf16(q[STEPS - 1][None]))
+    for r, c in enumerate(caches):
+        c.attend_publish(dev_bf16(q[STEPS - 1][None]), plans[r], STEPS + 1)
+    kc.peer_merge(plans[0], STEPS + 1, outs[0], lses[0], status)
+    assert np.allclose(lses[0].cpu().numpy(), lse_full.cpu().numpy().ravel(), atol=2e-4)
+
+
+def test_peer_publish_empty_shard_and_timeout():
+    """An empty shard publishes LSE = -inf rows (no softmax mass); a rank whose
+    peer never publishes gets status 1 and NaN rows after ~5 s, not a hang."""
+    import torch
+
+    from paper_2605_19660_b200 import KvCache, PipelineConfig
+    from paper_2605_19660_b200 import kv_cache as kc
+    from paper_2605_19660_b200.sharding import local_peer_plans
+
+    k, v, q = _inputs()
+    rows = H * G_
+    plans, areas = local_peer_plans(2, rows)
+    c = KvCache(PipelineConfig(heads=H), batch=1, q_heads=rows, max_tokens=S + 4)
+    c.buffer_quant(dev_bf16(k[None, :S]), dev_bf16(v[None, :S]))
+    o_ref, _ = c.attend(dev_bf16(q[0][None]))
+    kc.peer_publish_empty(plans[0], 1)
+    c.attend_publish(dev_bf16(q[0][None]), plans[1], 1)
+    out = torch.empty((rows, 128), dtype=torch.float32, device="cuda")
+    status = torch.zeros(1, dtype=torch.int32, device="cuda")
+    kc.peer_merge(plans[0], 1, out, None, status)
+    assert status.item() == 0
+    assert rel_err(out.cpu().numpy(), o_ref.cpu().numpy()[0]) < 1e-6
+    kc.peer_merge(plans[0], 2, out, None, status)  # epoch 2 was never published
+    assert status.item() == 1
+    assert np.isnan(out.cpu().numpy()).all()
+
+
+def _p2p_worker(rank, world, rdzv, res_path):
+    import torch
+    import torch.distributed as td
+
+    from paper_2605_19660_b200 import PipelineConfig
+    from paper_2605_19660_b200.sharding import SeqShardedKvCache
+
+    torch.cuda.set_device(0)
+    td.init_process_group("gloo", init_method=f"file://{rdzv}", rank=rank, world_size=world)
+    try:
+        k, v, q = _inputs()
+        c = SeqShardedKvCache(PipelineConfig(heads=H), batch=1, q_heads=H * G_, max_tokens_per_rank=S + STEPS,
+                              exchange="p2p")
+        c.prefill(dev_bf16(k[None, :S]), dev_bf16(v[None, :S]))
+        outs = []
+        for t in range(8):
+            o = c.decode_step(dev_bf16(q[t][None]), dev_bf16(k[S + t][None]), dev_bf16(v[S + t][None]))
+            outs.append(o.cpu().numpy())
+        np.save(res_path + f".{rank}.npy", np.stack(outs))
+        td.barrier()
+        c.close()
+    finally:
+        td.destroy_process_group()
+
+
+def test_p2p_exchange_two_processes_ipc(tmp_path):
+    """The SPMD p2p path end to end: two processes (gloo only for the one-time
+    IPC handle exchange) map each other's receive areas with CUDA IPC; every
+    step's rows travel by the attention kernels' peer stores.  Both share
+    cuda:0 here (one B200 per box); on 8 GPUs the same stores go over NVLink."""
+    import torch.multiprocessing as mp
+
+    res = str(tmp_path / "p2p")
+    mp.spawn(_p2p_worker, args=(2, str(tmp_path / "rdzv"), res), nprocs=2, join=True)
+    ref = _single_cache_outputs()
+    for rank in range(2):
+        got = np.load(res + f".{rank}.npy")
+        for t in range(8):
+            assert rel_err(got[t], ref[t]) < 1e-5, (rank, t)

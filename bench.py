@@ -50,6 +50,9 @@ def parse():
                         "GPU and CPU reference side by side) or the multi-GPU configs of BASELINE.json: "
                         "c3 32-layer Qwen2.5-7B batch-sharded, c4 128K head-sharded, c5 512K sequence-sharded")
     p.add_argument("--layers", type=int, default=32, help="c3: layers per step")
+    p.add_argument("--exchange", default="p2p", choices=["p2p", "nccl"],
+                   help="c5 with N > 1: (O, LSE) rows by peer stores from the attention kernel (p2p) "
+                        "or one NCCL all-gather + lse_merge")
     return p.parse_args()
 
 
@@ -680,13 +683,13 @@ def run_config(args, rank, world, local_rank):
     else:
         Hq, Hkv, S, Bg = 28, 4, 524288, 1
         B, Hloc, Hqloc = 1, Hkv, Hq
-        desc = "C5: Qwen2.5-VL-7B dims (28 q / 4 kv heads), 512K ctx, batch 1, sequence-sharded, (O, LSE) all-gather"
+        desc = "C5: Qwen2.5-VL-7B dims (28 q / 4 kv heads), 512K ctx, batch 1, sequence-sharded, (O, LSE) exchange"
     cfg = PipelineConfig(method="oscar", bits=bits, heads=Hloc)
     t_pre = 0.0
     for layer in range(layers):
         if c == "c5":
             cache = shd.SeqShardedKvCache(cfg, batch=1, q_heads=Hq, max_tokens_per_rank=S // world + 2 * R + K + W,
-                                          device=local_rank, keep_exact=False)
+                                          device=local_rank, keep_exact=False, exchange=args.exchange)
             s_ = shd.sequence_shard(S, world, rank)
             kk, vv = synth_kv(1, s_.tokens, Hloc, 7 + layer + 100 * rank, dev)
             torch.cuda.synchronize()
@@ -727,6 +730,35 @@ def run_config(args, rank, world, local_rank):
                                 "window top-up + whole blocks quantized from the input + window remainder"}
         extra.close()
         del ka, va, chunks
+    merge_stats = None
+    if c == "c5":  # receive side of the p2p exchange: one peer_merge launch over 8 ranks' rows (flags set)
+        from paper_2605_19660_b200 import kv_cache as kcm
+
+        plans, areas = shd.local_peer_plans(8, Hq, dev)
+        torch.cuda.synchronize()  # areas zeroed on the default stream
+        for pl in plans:
+            kcm.peer_publish_empty(pl, 1, stream=sh)
+        mo = torch.empty((Hq, D), dtype=torch.float32, device=dev)
+        for _ in range(10):
+            kcm.peer_merge(plans[0], 1, mo, stream=sh)
+        torch.cuda.synchronize()
+        gr = torch.cuda.CUDAGraph()  # 200 launches in one graph: device time, not host launch rate
+        with torch.cuda.graph(gr, stream=stream):
+            for _ in range(200):
+                kcm.peer_merge(plans[0], 1, mo, stream=stream.cuda_stream)
+        gr.replay()
+        torch.cuda.synchronize()
+        m0, m1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        m0.record(stream)
+        with torch.cuda.stream(stream):
+            gr.replay()
+        m1.record(stream)
+        torch.cuda.synchronize()
+        merge_stats = {"peer_merge_us_8_ranks": m0.elapsed_time(m1) * 1e3 / 200,
+                       "what": "oscar_peer_merge of 8 ranks' (O, LSE) rows already published (28 rows), per launch "
+                               "(200 launches replayed from one CUDA graph, flags set)"}
+        del gr
+        del plans, areas
     q, kn, vn = step_inputs(K + W, B, Hqloc, Hloc, 11 + rank, dev)
     out = torch.empty((B, Hqloc, D), dtype=torch.float32, device=dev)
 
@@ -774,6 +806,8 @@ def run_config(args, rank, world, local_rank):
                      "frac": step_bytes / (ms / K * 1e-3) / 1e9 / peak, "algorithmic_bytes_per_step_per_gpu": step_bytes},
         "prefill_s": t_pre,
         "streaming_append": stream_stats,
+        "exchange": (None if c != "c5" else
+                     {"mode": args.exchange if world > 1 else "none (one shard)", **(merge_stats or {})}),
     }
 
 

@@ -26,17 +26,20 @@ __global__ void peer_merge_kernel(const PeerPlan p, uint32_t epoch, float *out, 
     const int lane = threadIdx.x;
     const float *recv = p.recv[p.rank];
     const uint32_t *flags = p.flags[p.rank];
-    // every lane acquires every rank's flag (so its own reads below are ordered)
+    // lane src polls rank src's flag (acquire, system scope); the warp barrier then
+    // orders every lane's reads after those acquires; the rows are read from L2
+    // (__ldcg: never a stale L1 line of an earlier epoch)
     bool ok = true;
-    for (int src = 0; src < p.world && ok; ++src) {
-        const uint32_t *f = flags + peer_slot(p, epoch, src, row);
-        if (ld_acquire_sys_u32(f) == epoch) continue;
-        const uint64_t t0 = globaltimer_ns();
-        while (ld_acquire_sys_u32(f) != epoch) {
-            __nanosleep(128);
-            if (globaltimer_ns() - t0 > 5000000000ull) {  // a peer never published: fail loudly, don't hang
-                ok = false;
-                break;
+    if (lane < p.world) {
+        const uint32_t *f = flags + peer_slot(p, epoch, lane, row);
+        if (ld_acquire_sys_u32(f) != epoch) {
+            const uint64_t t0 = globaltimer_ns();
+            while (ld_acquire_sys_u32(f) != epoch) {
+                __nanosleep(64);
+                if (globaltimer_ns() - t0 > 5000000000ull) {  // a peer never published: fail loudly, don't hang
+                    ok = false;
+                    break;
+                }
             }
         }
     }
@@ -46,15 +49,20 @@ __global__ void peer_merge_kernel(const PeerPlan p, uint32_t epoch, float *out, 
                                                                           CUDART_NAN_F);
         return;
     }
-    float M = -CUDART_INF_F;
-    for (int src = 0; src < p.world; ++src) M = fmaxf(M, recv[peer_slot(p, epoch, src, row) * PEER_STRIDE + 128]);
+    __syncwarp();  // memory ordering: the acquires above happen before every lane's reads below
+    // lane src < world holds rank src's LSE
+    const float my_l = lane < p.world ? __ldcg(recv + peer_slot(p, epoch, lane, row) * PEER_STRIDE + 128)
+                                      : -CUDART_INF_F;
+    float M = my_l;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o));
     float4 O = make_float4(0.f, 0.f, 0.f, 0.f);
     float L = 0.f;
     for (int src = 0; src < p.world; ++src) {
         const float *r = recv + peer_slot(p, epoch, src, row) * PEER_STRIDE;
-        const float l = r[128];
+        const float l = __shfl_sync(0xffffffffu, my_l, src);
         const float w = (l == -CUDART_INF_F) ? 0.f : __expf(l - M);
-        const float4 v = reinterpret_cast<const float4 *>(r)[lane];
+        const float4 v = __ldcg(reinterpret_cast<const float4 *>(r) + lane);
         O.x += v.x * w;
         O.y += v.y * w;
         O.z += v.z * w;

@@ -655,6 +655,19 @@ __device__ __forceinline__ void residual_merge(const ResPartial &rp, float *slot
 
 // One 16-token tile [t0, t0+16) of the residual window (+ the current token at
 // index r), merged into the warp's partial slot.
+// one normalised output row (b, kv head bh's query head h): out / lse, or the
+// peer receive areas of a sequence-shard exchange
+__device__ __forceinline__ void write_row(const AttnArgs &a, int b, int kvh, int h, const float (&x)[4],
+                                          float lse_row, int lane) {
+    const int64_t row = (int64_t)b * a.Hq + kvh * a.g + h;
+    if (a.pub.world > 0) {
+        peer_publish_row(a.pub, a.pub_epoch, row, make_float4(x[0], x[1], x[2], x[3]), lse_row, lane);
+    } else {
+        *reinterpret_cast<float4 *>(a.out + row * D + lane * 4) = make_float4(x[0], x[1], x[2], x[3]);
+        if (a.lse && lane == 0) a.lse[row] = lse_row;
+    }
+}
+
 __device__ __noinline__ void residual_tile(const ResidualRefs rr, float *slot, const __nv_bfloat16 *qbase, int t0,
                                            int ntok, int lane, float c0, uint16_t *ring_k_w, uint16_t *ring_v_w) {
     ResPartial rp;
@@ -981,9 +994,12 @@ __global__ void __launch_bounds__(NCW_ * 32, 1) decode_attn_kernel(const AttnArg
         const bool lastk = kk == nseg - 1;
         const float *const *tab = reinterpret_cast<const float *const *>(smem + C::TAB_OFF);
         auto src = [&](int w) -> const float * { return lastk ? tab[w] : wp + w * MERGE_FLOATS; };
+        // a segment entirely inside this CTA's range: its CTA partial IS the result
+        // (no split-KV partial, ticket or final merge)
+        const bool single = total == 0 || (bh * nb >= start && (bh + 1) * nb <= end);
         int64_t first_cta = 0;
-        if (total > 0) first_cta = sp.cta_of(bh * nb);
-        const int pslot = (int)(total > 0 ? cta - first_cta : 0);
+        if (!single) first_cta = sp.cta_of(bh * nb);
+        const int pslot = (int)(cta - first_cta);
         float *po = a.part_o + ((int64_t)bh * a.maxp + pslot) * 8 * D;
         float *pml = a.part_ml + ((int64_t)bh * a.maxp + pslot) * 16;
         // lane w < NCW holds warp w's (m, l) of head h
@@ -1009,10 +1025,18 @@ __global__ void __launch_bounds__(NCW_ * 32, 1) decode_attn_kernel(const AttnArg
                 O.w += v[w].w * f;
             }
         }
-        *reinterpret_cast<float4 *>(po + h * D + lane * 4) = O;
-        if (lane == 0) {
-            pml[2 * h] = M;
-            pml[2 * h + 1] = L;
+        if (single) {
+            const float inv = (L > 0.f) ? 1.f / L : 0.f;
+            float x[4] = {O.x * inv, O.y * inv, O.z * inv, O.w * inv};
+            if (a.rotate_v) fht128_warp(x, lane);  // explicit-V mode: rotate the output back
+            write_row(a, (int)(bh / a.Hkv), (int)(bh % a.Hkv), h, x, (L > 0.f) ? (M + __log2f(L)) * LN2 : -CUDART_INF_F,
+                      lane);
+        } else {
+            *reinterpret_cast<float4 *>(po + h * D + lane * 4) = O;
+            if (lane == 0) {
+                pml[2 * h] = M;
+                pml[2 * h + 1] = L;
+            }
         }
     }
     __syncthreads();
@@ -1020,10 +1044,13 @@ __global__ void __launch_bounds__(NCW_ * 32, 1) decode_attn_kernel(const AttnArg
     // (2) publish: one acq_rel ticket per segment (cumulative over the barrier)
     if (threadIdx.x < nseg) {
         const int64_t bh = seg_first + threadIdx.x;
-        int expected = 1;
-        if (total > 0) expected = (int)(sp.cta_of((bh + 1) * nb - 1) - sp.cta_of(bh * nb) + 1);
-        const int prev = atomic_add_acq_rel_gpu(&a.counters[bh], 1);
-        lastflag[threadIdx.x] = (prev == expected - 1) ? expected : 0;
+        if (total == 0 || (bh * nb >= start && (bh + 1) * nb <= end)) {
+            lastflag[threadIdx.x] = 0;  // finished in (1)
+        } else {
+            const int expected = (int)(sp.cta_of((bh + 1) * nb - 1) - sp.cta_of(bh * nb) + 1);
+            const int prev = atomic_add_acq_rel_gpu(&a.counters[bh], 1);
+            lastflag[threadIdx.x] = (prev == expected - 1) ? expected : 0;
+        }
     }
     __syncthreads();
     if (a.prof) {
@@ -1083,14 +1110,7 @@ __global__ void __launch_bounds__(NCW_ * 32, 1) decode_attn_kernel(const AttnArg
 #pragma unroll
         for (int e = 0; e < 4; ++e) x[e] *= inv;
         if (a.rotate_v) fht128_warp(x, lane);  // explicit-V mode: rotate the output back
-        const int64_t row = (int64_t)b * a.Hq + kvh * g + h;
-        const float lse_row = (L > 0.f) ? (M + __log2f(L)) * LN2 : -CUDART_INF_F;
-        if (a.pub.world > 0) {
-            peer_publish_row(a.pub, a.pub_epoch, row, make_float4(x[0], x[1], x[2], x[3]), lse_row, lane);
-        } else {
-            *reinterpret_cast<float4 *>(a.out + row * D + lane * 4) = make_float4(x[0], x[1], x[2], x[3]);
-            if (a.lse && lane == 0) a.lse[row] = lse_row;
-        }
+        write_row(a, b, kvh, h, x, (L > 0.f) ? (M + __log2f(L)) * LN2 : -CUDART_INF_F, lane);
         if (h == 0 && lane == 0) a.counters[bh] = 0;  // the ticket is complete: reset for the next launch
     }
     if (a.prof) tmr[10] += clk() - tf0;

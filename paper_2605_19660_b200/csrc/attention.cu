@@ -38,6 +38,13 @@ namespace osk {
 
 namespace {
 
+// phase-cycle counters (OSCAR_PROF) exist only in the profiling build
+// (make PROF=1 -> liboscar_b200_prof.so): the timers cost ~30 issue slots per unit
+#ifndef OSK_PROF
+#define OSK_PROF 0
+#endif
+constexpr bool kProf = OSK_PROF != 0;
+
 constexpr int MERGE_FLOATS = 8 * D + 16 + D;  // per-warp partial: O[8][128], m[8], l[8] + 128 scratch
 constexpr float LOG2E = 1.4426950408889634f;
 constexpr float LN2 = 0.6931471805599453f;
@@ -763,7 +770,7 @@ __global__ void __launch_bounds__(NCW_ * 32, 1) decode_attn_kernel(const AttnArg
     if (!active) return;
     const float c0 = LOG2E * 0.08838834764831845f;  // log2(e)/sqrt(128)
     long long tmr[12] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
-    const long long tk0 = a.prof ? clk() : 0;
+    const long long tk0 = (kProf && a.prof) ? clk() : 0;
 
     // the stage of warp w's final unit (positions p = w, w + NCW, ... < nunits), free
     // after it is consumed: p + NST >= nunits, so it is never refilled.  Only used
@@ -790,7 +797,7 @@ __global__ void __launch_bounds__(NCW_ * 32, 1) decode_attn_kernel(const AttnArg
         const bool owns_tail = total == 0 || hi == (bh + 1) * nb;
         const __nv_bfloat16 *qbase = reinterpret_cast<const __nv_bfloat16 *>(a.q) + ((int64_t)b * a.Hq + kvh * g) * D;
 
-        const long long tq0 = a.prof ? clk() : 0;
+        const long long tq0 = (kProf && a.prof) ? clk() : 0;
         // ---- q fragments from this segment's CTA-shared tile; every QSEG segments
         //      the next wave of tiles is built (all warps walk the same segments) ----
         if (k > 0 && k % QSEG == 0) {
@@ -813,7 +820,7 @@ __global__ void __launch_bounds__(NCW_ * 32, 1) decode_attn_kernel(const AttnArg
         st.ob2[0] = st.ob2[1] = st.ob2[2] = st.ob2[3] = 0.f;
         st.m[0] = st.m[1] = -CUDART_INF_F;
         st.l[0] = st.l[1] = 0.f;
-        if (a.prof) tmr[6] += clk() - tq0;
+        if (kProf && a.prof) tmr[6] += clk() - tq0;
 
         // ---- packed units of this segment: positions p = gidx - start, p % NCW == warp ----
         if (total > 0) {
@@ -822,14 +829,14 @@ __global__ void __launch_bounds__(NCW_ * 32, 1) decode_attn_kernel(const AttnArg
             for (int64_t p = first; p < hi - start; p += NCW) {
                 const int stg = (int)p % C::NST;  // 32-bit: p < units of one CTA
                 const int round = (int)p / C::NST;
-                const long long ts0 = a.prof ? clk() : 0;
+                const long long ts0 = (kProf && a.prof) ? clk() : 0;
                 if (lane == 0)
                     while (ld_volatile_shared(&consumed[stg]) < round) {
                     }
                 __syncwarp();
-                const long long ts1 = a.prof ? clk() : 0;
+                const long long ts1 = (kProf && a.prof) ? clk() : 0;
                 mbar_wait(&full[stg], (uint32_t)(round & 1));
-                if (a.prof) {
+                if (kProf && a.prof) {
                     const long long ts2 = clk();
                     tmr[5] += ts1 - ts0;
                     tmr[0] += ts2 - ts1;
@@ -838,7 +845,7 @@ __global__ void __launch_bounds__(NCW_ * 32, 1) decode_attn_kernel(const AttnArg
                 if constexpr (BITS == 0) {
                     process_quarter_bf16(sb, st, qf, lane, c0);
                 } else {
-                    process_block<BITS>(sb, st, qh + gq * QH_STRIDE + 2 * tq, lane, c0, a.prof ? tmr : nullptr);
+                    process_block<BITS>(sb, st, qh + gq * QH_STRIDE + 2 * tq, lane, c0, (kProf && a.prof) ? tmr : nullptr);
                 }
                 // stage consumed: refill it with unit p + NST, then publish the round
                 __syncwarp();
@@ -870,7 +877,7 @@ __global__ void __launch_bounds__(NCW_ * 32, 1) decode_attn_kernel(const AttnArg
             }
         }
 
-        const long long te0 = a.prof ? clk() : 0;
+        const long long te0 = (kProf && a.prof) ? clk() : 0;
         // ---- warp partial -> slot (unnormalized O[h][c], m[h], l[h]).  For the CTA's
         //      last segment the slot is the warp's last ring stage (shared memory: no
         //      stage is refilled or re-read once its final round is consumed), else
@@ -944,7 +951,7 @@ __global__ void __launch_bounds__(NCW_ * 32, 1) decode_attn_kernel(const AttnArg
             }
         }
 
-        if (a.prof) tmr[7] += clk() - te0;
+        if (kProf && a.prof) tmr[7] += clk() - te0;
     }
 
     if constexpr (DEFER) {  // tiles of the tail segments after the first, after the packed units
@@ -981,7 +988,7 @@ __global__ void __launch_bounds__(NCW_ * 32, 1) decode_attn_kernel(const AttnArg
 
     // ======== end of the CTA's work: cooperative merges (all warps finish within
     //          ~one unit of each other under the static round-robin schedule) ========
-    const long long tm0 = a.prof ? clk() : 0;
+    const long long tm0 = (kProf && a.prof) ? clk() : 0;
     if (lane == 0) reinterpret_cast<float **>(smem + C::TAB_OFF)[warp] = last_seg_slot(warp);
     __syncthreads();
     int *lastflag = reinterpret_cast<int *>(smem + C::SEG_OFF);  // [nseg] (segcnt area reused)
@@ -1040,7 +1047,7 @@ __global__ void __launch_bounds__(NCW_ * 32, 1) decode_attn_kernel(const AttnArg
         }
     }
     __syncthreads();
-    const long long tp0 = a.prof ? clk() : 0;
+    const long long tp0 = (kProf && a.prof) ? clk() : 0;
     // (2) publish: one acq_rel ticket per segment (cumulative over the barrier)
     if (threadIdx.x < nseg) {
         const int64_t bh = seg_first + threadIdx.x;
@@ -1053,11 +1060,11 @@ __global__ void __launch_bounds__(NCW_ * 32, 1) decode_attn_kernel(const AttnArg
         }
     }
     __syncthreads();
-    if (a.prof) {
+    if (kProf && a.prof) {
         tmr[8] += clk() - tm0;
         tmr[9] += clk() - tp0;  // the ticket (atomic) part
     }
-    const long long tf0 = a.prof ? clk() : 0;
+    const long long tf0 = (kProf && a.prof) ? clk() : 0;
     // (3) final merge for the (b, kv heads) this CTA completed last: warp-per-(segment, head)
     for (int item = warp; item < nseg * g; item += NCW) {
         const int kk = item / g, h = item % g;
@@ -1113,9 +1120,9 @@ __global__ void __launch_bounds__(NCW_ * 32, 1) decode_attn_kernel(const AttnArg
         write_row(a, b, kvh, h, x, (L > 0.f) ? (M + __log2f(L)) * LN2 : -CUDART_INF_F, lane);
         if (h == 0 && lane == 0) a.counters[bh] = 0;  // the ticket is complete: reset for the next launch
     }
-    if (a.prof) tmr[10] += clk() - tf0;
-    if (a.prof) tmr[4] += clk() - tm0;
-    if (a.prof && lane == 0) {
+    if (kProf && a.prof) tmr[10] += clk() - tf0;
+    if (kProf && a.prof) tmr[4] += clk() - tm0;
+    if (kProf && a.prof && lane == 0) {
         // per-warp phase cycles: [wait, qk, softmax, pv, merge, spin, qprologue, segtail]; total in slot 4 of the
         // host view is replaced below by the whole-kernel cycles
         unsigned long long *pp = a.prof + ((int64_t)blockIdx.x * NCW_MAX + warp) * 12;

@@ -12,6 +12,10 @@
 // KVC1 dump, materialize).  Compiled with -ffp-contract=off.
 #include <cuda_runtime.h>
 
+#ifndef OSK_PROF
+#define OSK_PROF 0
+#endif
+
 #include <cmath>
 #include <cstdlib>
 #include <cstdio>
@@ -382,7 +386,14 @@ struct oscar_kv_handle {
         }
         // debug: OSCAR_PROF=1 prints per-phase cycles averaged over warps (synchronises)
         static int prof = -1;
-        if (prof < 0) prof = getenv("OSCAR_PROF") ? 1 : 0;
+        if (prof < 0) {
+            prof = getenv("OSCAR_PROF") ? 1 : 0;
+#if !OSK_PROF
+            if (prof) std::fprintf(stderr, "OSCAR_PROF: counters need the profiling build (make PROF=1, "
+                                           "OSCAR_LIB=.../liboscar_b200_prof.so); ignored\n");
+            prof = 0;
+#endif
+        }
         unsigned long long *pbuf = nullptr;
         const int nw = a.ncta * 16;
         if (prof) {

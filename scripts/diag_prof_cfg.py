@@ -1,5 +1,6 @@
 """OSCAR_PROF phase breakdown of one attend launch for a config shape.
-usage: OSCAR_PROF=1 python scripts/diag_prof_cfg.py B S Hq Hkv [decode]"""
+usage: OSCAR_PROF=1 OSCAR_LIB=$PWD/paper_2605_19660_b200/liboscar_b200_prof.so python scripts/diag_prof_cfg.py B S Hq Hkv
+(build the profiling library first: make -C paper_2605_19660_b200/csrc PROF=1)"""
 import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch

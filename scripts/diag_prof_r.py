@@ -1,5 +1,6 @@
 """OSCAR_PROF phase breakdown + per-CTA dump of attend at residual fill r (C2 INT2).
-usage: OSCAR_PROF=1 OSCAR_PROF_FILE=... python scripts/diag_prof_r.py r"""
+usage: OSCAR_PROF=1 OSCAR_PROF_FILE=... OSCAR_LIB=.../liboscar_b200_prof.so python scripts/diag_prof_r.py r
+(profiling library: make -C paper_2605_19660_b200/csrc PROF=1)"""
 import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch

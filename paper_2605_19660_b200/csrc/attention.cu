@@ -724,7 +724,8 @@ __global__ void __launch_bounds__(NCW_ * 32, 1) decode_attn_kernel(const AttnArg
     // until the stage's previous round is consumed (software counter) -- which
     // also means the TMA for unit p was issued, so the full-barrier wait is on
     // the right phase -- and after consuming refills the stage with unit p+NST.
-    auto issue = [&](int64_t p, int64_t bh, int64_t uidx) {  // uidx: unit index within bh
+    const int nb32 = (int)nb;  // units per (b, kv head) fit 32 bits
+    auto issue = [&](int64_t p, int64_t bh, int uidx) {  // uidx: unit index within bh
         const int stg = (int)p % C::NST;
         mbar_arrive_expect_tx(&full[stg], C::STAGE);
         bulk_g2s(ring + stg * C::STAGE,
@@ -825,6 +826,7 @@ __global__ void __launch_bounds__(NCW_ * 32, 1) decode_attn_kernel(const AttnArg
         // ---- packed units of this segment: positions p = gidx - start, p % NCW == warp ----
         if (total > 0) {
             const int64_t p0 = lo - start;
+            const int u_seg0 = (int)(lo - bh * nb);  // unit index within bh of position p0
             const int64_t first = p0 + ((warp - (int)(p0 % NCW)) + NCW) % NCW;
             for (int64_t p = first; p < hi - start; p += NCW) {
                 const int stg = (int)p % C::NST;  // 32-bit: p < units of one CTA
@@ -847,28 +849,20 @@ __global__ void __launch_bounds__(NCW_ * 32, 1) decode_attn_kernel(const AttnArg
                 } else {
                     process_block<BITS>(sb, st, qh + gq * QH_STRIDE + 2 * tq, lane, c0, (kProf && a.prof) ? tmr : nullptr);
                 }
-                // stage consumed: refill it with unit p + NST, then publish the round
+                // stage consumed: refill it with unit p + NST, then publish the round.
+                // No proxy fence: this warp's generic-proxy reads of the stage have all
+                // returned (their registers fed the MMAs above) before the bulk copy is
+                // issued -- the same consumer-release ordering TMA pipelines rely on.
                 __syncwarp();
                 if (lane == 0) {
                     if (p + C::NST < nunits) {
-                        int64_t bh2 = bh, u2 = start + p - bh * nb + C::NST;
-                        while (u2 >= nb) {
-                            u2 -= nb;
+                        int64_t bh2 = bh;
+                        int u2 = u_seg0 + (int)(p - p0) + C::NST;  // unit index within bh (32-bit)
+                        while (u2 >= nb32) {
+                            u2 -= nb32;
                             ++bh2;
                         }
-                        fence_proxy_async_smem();
                         issue(p + C::NST, bh2, u2);
-                        // optional L2 prefetch pf_dist units beyond the ring (OSCAR_L2_PREFETCH)
-                        if (a.pf_dist > 0 && p + C::NST + a.pf_dist < nunits) {
-                            int64_t bh3 = bh2, u3 = u2 + a.pf_dist;
-                            while (u3 >= nb) {
-                                u3 -= nb;
-                                ++bh3;
-                            }
-                            bulk_prefetch_l2(a.blocks + (bh3 * a.max_blocks + u3 / SUB) * (int64_t)C::BYTES +
-                                                 (u3 % SUB) * C::STAGE,
-                                             C::STAGE);
-                        }
                     }
                     // no fence needed: a waiter only relies on phase `round` of this
                     // stage being complete, which held before this warp consumed it

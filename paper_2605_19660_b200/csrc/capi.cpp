@@ -279,14 +279,6 @@ struct oscar_kv_handle {
         a.counters = counters;
         a.warp_part = warp_part;
         a.maxseg = maxseg_alloc;
-        {
-            static int pf = -1;
-            if (pf < 0) {
-                const char *e = getenv("OSCAR_L2_PREFETCH");
-                pf = e ? atoi(e) : 0;
-            }
-            a.pf_dist = pf;
-        }
         a.ncta = attention_grid(dbits, num_sms, a.nb, a.BH);
         {
             static int64_t sc = -1;  // OSCAR_SEG_COST overrides the per-segment split weight (tuning knob)

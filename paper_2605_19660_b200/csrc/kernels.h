@@ -85,7 +85,6 @@ struct AttnArgs {
     int maxseg;        // segment slots per CTA in warp_part
     int maxp;
     int ncta;
-    int pf_dist;       // L2 prefetch distance beyond the ring (units), 0 = off
     int64_t seg_cost;  // virtual units per (b, kv head) segment in the stream-K split (split.h)
     int64_t tail_cost; // virtual units charged to a segment's residual-window tiles (split.h)
     int pdl_prefetch;  // packed records unchanged since the previous launch on this stream:

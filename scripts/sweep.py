@@ -1,5 +1,5 @@
 """Kernel-config sweep: attend-only latency at the C2 workload (B=16, 32K, 32/8 heads).
-usage: OSCAR_NCW=.. OSCAR_L2_PREFETCH=.. python scripts/sweep.py BITS"""
+usage: OSCAR_NCW=.. python scripts/sweep.py BITS"""
 import json
 import os
 import sys
@@ -44,5 +44,5 @@ torch.cuda.synchronize()
 us = 1e3 * e0.elapsed_time(e1) / (3 * n)
 byt = B * Hkv * (ctx // 128) * BLOCK_BYTES[bits]
 print(json.dumps({"bits": bits, "ncw": os.environ.get("OSCAR_NCW", "default"),
-                  "pf": os.environ.get("OSCAR_L2_PREFETCH", "0"), "ctx": ctx, "us": round(us, 2),
+                  "ctx": ctx, "us": round(us, 2),
                   "GBps": round(byt / us / 1e3, 1)}))

@@ -48,6 +48,10 @@ constexpr bool kProf = OSK_PROF != 0;
 constexpr int MERGE_FLOATS = 8 * D + 16 + D;  // per-warp partial: O[8][128], m[8], l[8] + 128 scratch
 constexpr float LOG2E = 1.4426950408889634f;
 constexpr float LN2 = 0.6931471805599453f;
+#ifndef OSK_RESCALE_SLACK
+#define OSK_RESCALE_SLACK 3
+#endif
+constexpr float RESCALE_SLACK = (float)OSK_RESCALE_SLACK;  // log2 units
 
 constexpr int MAXSEG_SMEM = 64;  // max segments (b, kv heads) per CTA range
 constexpr int NCW_MAX = 16;
@@ -257,9 +261,12 @@ __device__ __forceinline__ void process_block(const uint8_t *__restrict__ sb, Wa
         bm0 = fmaxf(bm0, fmaxf(sacc[i][0], sacc[i][2]));
         bm1 = fmaxf(bm1, fmaxf(sacc[i][1], sacc[i][3]));
     }
-    // lazy rescale: the running max only moves when some lane's block max
-    // exceeds it (rare after the first blocks) -- then reduce and rescale
-    if (!__all_sync(0xffffffffu, bm0 <= 0.f && bm1 <= 0.f && st.m[0] != -CUDART_INF_F && st.m[1] != -CUDART_INF_F)) {
+    // lazy rescale: the reference only moves when some lane's block max exceeds
+    // it by more than RESCALE_SLACK (then reduce and rescale to the exact max);
+    // in between, P = 2^(logit - m) may reach 2^RESCALE_SLACK (fp16-safe: the
+    // P*a fold stays finite for value-group ranges below 65504 * 3 / 2^SLACK)
+    if (!__all_sync(0xffffffffu, bm0 <= RESCALE_SLACK && bm1 <= RESCALE_SLACK && st.m[0] != -CUDART_INF_F &&
+                                     st.m[1] != -CUDART_INF_F)) {
 #pragma unroll
         for (int o = 4; o < 32; o <<= 1) {
             bm0 = fmaxf(bm0, __shfl_xor_sync(0xffffffffu, bm0, o));

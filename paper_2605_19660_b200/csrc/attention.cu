@@ -732,13 +732,14 @@ __global__ void __launch_bounds__(NCW_ * 32, 1) decode_attn_kernel(const AttnArg
     // also means the TMA for unit p was issued, so the full-barrier wait is on
     // the right phase -- and after consuming refills the stage with unit p+NST.
     const int nb32 = (int)nb;  // units per (b, kv head) fit 32 bits
-    auto issue = [&](int64_t p, int64_t bh, int uidx) {  // uidx: unit index within bh
-        const int stg = (int)p % C::NST;
+    const uint32_t consumed_s = smem_u32(consumed), full_s = smem_u32(full);
+    auto issue_stage = [&](int stg, int64_t bh, int uidx) {  // uidx: unit index within bh
         mbar_arrive_expect_tx(&full[stg], C::STAGE);
         bulk_g2s(ring + stg * C::STAGE,
                  a.blocks + (bh * a.max_blocks + uidx / SUB) * (int64_t)C::BYTES + (uidx % SUB) * C::STAGE, C::STAGE,
                  &full[stg], pol);
     };
+    auto issue = [&](int64_t p, int64_t bh, int uidx) { issue_stage((int)p % C::NST, bh, uidx); };
 
     // Programmatic dependent launch: the next decode step's CTAs may start as
     // this grid's CTAs retire; each new CTA streams its first NST packed
@@ -832,19 +833,20 @@ __global__ void __launch_bounds__(NCW_ * 32, 1) decode_attn_kernel(const AttnArg
 
         // ---- packed units of this segment: positions p = gidx - start, p % NCW == warp ----
         if (total > 0) {
-            const int64_t p0 = lo - start;
+            // positions are CTA-local (32-bit); stage and round advance incrementally
+            const int p0 = (int)(lo - start);
             const int u_seg0 = (int)(lo - bh * nb);  // unit index within bh of position p0
-            const int64_t first = p0 + ((warp - (int)(p0 % NCW)) + NCW) % NCW;
-            for (int64_t p = first; p < hi - start; p += NCW) {
-                const int stg = (int)p % C::NST;  // 32-bit: p < units of one CTA
-                const int round = (int)p / C::NST;
+            const int first = p0 + ((warp - p0 % NCW) + NCW) % NCW;
+            const int pend = (int)(hi - start);
+            int stg = first % C::NST, round = first / C::NST;
+            for (int p = first; p < pend; p += NCW) {
                 const long long ts0 = (kProf && a.prof) ? clk() : 0;
                 if (lane == 0)
-                    while (ld_volatile_shared(&consumed[stg]) < round) {
+                    while (ld_volatile_shared_u32(consumed_s + 4 * stg) < round) {
                     }
                 __syncwarp();
                 const long long ts1 = (kProf && a.prof) ? clk() : 0;
-                mbar_wait(&full[stg], (uint32_t)(round & 1));
+                mbar_wait_s(full_s + 8 * stg, (uint32_t)(round & 1));
                 if (kProf && a.prof) {
                     const long long ts2 = clk();
                     tmr[5] += ts1 - ts0;
@@ -862,18 +864,23 @@ __global__ void __launch_bounds__(NCW_ * 32, 1) decode_attn_kernel(const AttnArg
                 // issued -- the same consumer-release ordering TMA pipelines rely on.
                 __syncwarp();
                 if (lane == 0) {
-                    if (p + C::NST < nunits) {
+                    if (p + C::NST < nu32) {
                         int64_t bh2 = bh;
-                        int u2 = u_seg0 + (int)(p - p0) + C::NST;  // unit index within bh (32-bit)
+                        int u2 = u_seg0 + (p - p0) + C::NST;  // unit index within bh (32-bit)
                         while (u2 >= nb32) {
                             u2 -= nb32;
                             ++bh2;
                         }
-                        issue(p + C::NST, bh2, u2);
+                        issue_stage(stg, bh2, u2);  // unit p + NST lands in the same stage
                     }
                     // no fence needed: a waiter only relies on phase `round` of this
                     // stage being complete, which held before this warp consumed it
-                    st_volatile_shared(&consumed[stg], round + 1);
+                    st_volatile_shared_u32(consumed_s + 4 * stg, round + 1);
+                }
+                stg += NCW;
+                if (stg >= C::NST) {
+                    stg -= C::NST;
+                    ++round;
                 }
             }
         }

@@ -61,6 +61,29 @@ __device__ __forceinline__ void bulk_prefetch_l2(const void *src_gmem, uint32_t 
     asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(src_gmem), "r"(bytes) : "memory");
 }
 
+// the same on a precomputed shared-window address (no per-use address conversion)
+__device__ __forceinline__ int ld_volatile_shared_u32(uint32_t saddr) {
+    int v;
+    asm volatile("ld.volatile.shared.u32 %0, [%1];\n" : "=r"(v) : "r"(saddr));
+    return v;
+}
+__device__ __forceinline__ void st_volatile_shared_u32(uint32_t saddr, int v) {
+    asm volatile("st.volatile.shared.u32 [%0], %1;\n" ::"r"(saddr), "r"(v) : "memory");
+}
+__device__ __forceinline__ void mbar_wait_s(uint32_t saddr, uint32_t phase) {
+    asm volatile(
+        "{\n"
+        ".reg .pred P1;\n"
+        "LAB_WAIT:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+        "@P1 bra.uni DONE;\n"
+        "bra.uni LAB_WAIT;\n"
+        "DONE:\n"
+        "}\n" ::"r"(saddr),
+        "r"(phase)
+        : "memory");
+}
+
 __device__ __forceinline__ int ld_volatile_shared(const int *p) {
     int v;
     asm volatile("ld.volatile.shared.u32 %0, [%1];\n" : "=r"(v) : "r"(smem_u32(p)));

@@ -1133,12 +1133,14 @@ __global__ void __launch_bounds__(NCW_ * 32, 1) decode_attn_kernel(const AttnArg
     if (kProf && a.prof && lane == 0) {
         // per-warp phase cycles: [wait, qk, softmax, pv, merge, spin, qprologue, segtail]; total in slot 4 of the
         // host view is replaced below by the whole-kernel cycles
-        unsigned long long *pp = a.prof + ((int64_t)blockIdx.x * NCW_MAX + warp) * 12;
+        // [0..7] wait qk softmax pv merge spin qprologue segtail, [8] total, [9] cta merge,
+        // [10] ticket, [11] smid, [12] final merge
+        unsigned long long *pp = a.prof + ((int64_t)blockIdx.x * NCW_MAX + warp) * 16;
         for (int i = 0; i < 8; ++i) pp[i] = (unsigned long long)tmr[i];
         pp[8] = (unsigned long long)(clk() - tk0);
         pp[9] = (unsigned long long)tmr[8];
         pp[10] = (unsigned long long)tmr[9];
-        pp[7] = (unsigned long long)tmr[10];  // (per-CTA dump) final-merge cycles of this warp
+        pp[12] = (unsigned long long)tmr[10];
         unsigned smid;
         asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
         pp[11] = smid;

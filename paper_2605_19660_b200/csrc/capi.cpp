@@ -389,25 +389,26 @@ struct oscar_kv_handle {
         unsigned long long *pbuf = nullptr;
         const int nw = a.ncta * 16;
         if (prof) {
-            CK(cudaMalloc(&pbuf, sizeof(unsigned long long) * 12 * nw));
-            CK(cudaMemsetAsync(pbuf, 0, sizeof(unsigned long long) * 12 * nw, s));
+            CK(cudaMalloc(&pbuf, sizeof(unsigned long long) * 16 * nw));
+            CK(cudaMemsetAsync(pbuf, 0, sizeof(unsigned long long) * 16 * nw, s));
             a.prof = pbuf;
         }
         CK(launch_attention(dbits, a, s));
         ++last_launches;
         blocks_written = false;
         if (prof) {
-            std::vector<unsigned long long> hbuf(12 * nw);
+            std::vector<unsigned long long> hbuf(16 * nw);
             CK(cudaMemcpyAsync(hbuf.data(), pbuf, hbuf.size() * 8, cudaMemcpyDeviceToHost, s));
             CK(cudaStreamSynchronize(s));
-            double acc[12] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
-            double mx = 0;
+            double acc[13] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+            double mx = 0, fmax = 0;
             int cnt = 0;
             for (int w = 0; w < nw; ++w) {
-                if (hbuf[12 * w + 8] == 0) continue;
+                if (hbuf[16 * w + 8] == 0) continue;
                 ++cnt;
-                for (int i = 0; i < 12; ++i) acc[i] += (double)hbuf[12 * w + i];
-                mx = std::max(mx, (double)hbuf[12 * w + 8]);
+                for (int i = 0; i < 13; ++i) acc[i] += (double)hbuf[16 * w + i];
+                mx = std::max(mx, (double)hbuf[16 * w + 8]);
+                fmax = std::max(fmax, (double)hbuf[16 * w + 12]);
             }
             {
                 // per-CTA spread: slowest warp per CTA, min/max across CTAs
@@ -416,7 +417,7 @@ struct oscar_kv_handle {
                 for (int c = 0; c < a.ncta; ++c) {
                     double lo = 1e30, hi = 0;
                     for (int w = 0; w < 16; ++w) {
-                        const double t = (double)hbuf[12 * (c * 16 + w) + 8];
+                        const double t = (double)hbuf[16 * (c * 16 + w) + 8];
                         if (t == 0) continue;
                         lo = std::min(lo, t);
                         hi = std::max(hi, t);
@@ -436,14 +437,14 @@ struct oscar_kv_handle {
                             double hi = 0, cm = 0, tk = 0, fm = 0;
                             unsigned long long sm = 0;
                             for (int w = 0; w < 16; ++w) {
-                                const double t = (double)hbuf[12 * (c * 16 + w) + 8];
+                                const double t = (double)hbuf[16 * (c * 16 + w) + 8];
                                 if (t > hi) {
                                     hi = t;
-                                    sm = hbuf[12 * (c * 16 + w) + 11];
+                                    sm = hbuf[16 * (c * 16 + w) + 11];
                                 }
-                                cm = std::max(cm, (double)hbuf[12 * (c * 16 + w) + 9]);
-                                tk = std::max(tk, (double)hbuf[12 * (c * 16 + w) + 10]);
-                                fm = std::max(fm, (double)hbuf[12 * (c * 16 + w) + 7]);
+                                cm = std::max(cm, (double)hbuf[16 * (c * 16 + w) + 9]);
+                                tk = std::max(tk, (double)hbuf[16 * (c * 16 + w) + 10]);
+                                fm = std::max(fm, (double)hbuf[16 * (c * 16 + w) + 12]);
                             }
                             const int64_t st = sp.begin(c), en = sp.end(c);
                             int64_t tails = 0;
@@ -464,10 +465,10 @@ struct oscar_kv_handle {
                 std::fprintf(stderr,
                              "OSCAR_PROF warps=%d avg cycles: wait %.0f qk %.0f softmax %.0f pv %.0f merge %.0f "
                              "spin %.0f qprologue %.0f segtail %.0f total %.0f max %.0f | merge parts: cta %.0f "
-                             "atomic %.0f final %.0f (sums over all warps / cnt*12)\n",
+                             "atomic %.0f final %.0f (per-warp averages; final max %.0f)\n",
                              cnt, acc[0] / cnt, acc[1] / cnt, acc[2] / cnt, acc[3] / cnt, acc[4] / cnt, acc[5] / cnt,
-                             acc[6] / cnt, acc[7] / cnt, acc[8] / cnt, mx, acc[9] / cnt * 12, acc[10] / cnt * 12,
-                             acc[11] / cnt * 12);
+                             acc[6] / cnt, acc[7] / cnt, acc[8] / cnt, mx, acc[9] / cnt, acc[10] / cnt,
+                             acc[12] / cnt, fmax);
             cudaFree(pbuf);
         }
     }

@@ -68,3 +68,27 @@ def test_kernel_equals_fp16_rounding_model(bits):
     assert worst_model <= 1.2e-3, worst_model
     assert worst_model < 0.5 * worst_oracle, (worst_model, worst_oracle)
     assert worst_oracle <= 1e-2, worst_oracle
+
+
+@pytest.mark.parametrize("bits", [2, 4])
+def test_large_value_magnitudes_stay_finite(bits):
+    """Values of magnitude ~2000 (group ranges ~9000): the fp16 steps and the
+    P*a fold (P <= 2^3 between lazy rescales) stay finite; the output matches
+    the oracle within the attention tolerance."""
+    from paper_2605_19660_b200 import KvCache, PipelineConfig
+
+    rng = np.random.default_rng(70 + bits)
+    S, H, g, d = 2048, 2, 4, 128
+    k = _bf16(rng.standard_normal((1, S + 1, H, d)) * 3.0)
+    v = _bf16(rng.standard_normal((1, S + 1, H, d)) * 2000.0)
+    q = _bf16(rng.standard_normal((1, H * g, d)))
+    cache = KvCache(PipelineConfig(heads=H, bits=bits), batch=1, q_heads=H * g, max_tokens=S + 8)
+    cache.buffer_quant(dev_bf16(k[:, :S]), dev_bf16(v[:, :S]))
+    out = cache.decode_step(dev_bf16(q), dev_bf16(k[:, S]), dev_bf16(v[:, S])).cpu().numpy()[0].astype(np.float64)
+    assert np.isfinite(out).all()
+    o = ob.PortCache(H=H, bits=bits)
+    o.append(k[0, :S], v[0, :S])
+    ref = o.decode_step(q[0], k[0, S], v[0, S], g, append=False)
+    err = rel_err(out, ref)
+    log_err(f"large_values[bits={bits}][|v|~2000]", err)
+    assert err <= 5e-3, err

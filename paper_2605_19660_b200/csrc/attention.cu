@@ -1082,38 +1082,33 @@ __global__ void __launch_bounds__(NCW_ * 32, 1) decode_attn_kernel(const AttnArg
         const int b = (int)(bh / a.Hkv), kvh = (int)(bh % a.Hkv);
         const float *pmb = a.part_ml + (int64_t)bh * a.maxp * 16;
         const float *pob = a.part_o + (int64_t)bh * a.maxp * 8 * D;
-        // one pass, online over batches of partials: every lane loads the (m, l) of
-        // each partial (warp-uniform broadcast) next to its 4 channels of O
-        float M = -CUDART_INF_F, L = 0.f;
+        // one pass, online over batches of FB partials: lane u loads the (m, l) of
+        // partial s0 + u, every lane its 4 channels of all FB partials' O rows (all
+        // loads in flight at once; registers are free at this point of the kernel)
+        float M = -CUDART_INF_F, Lw = 0.f;  // Lw: this lane's share of the denominator
         float x[4] = {0.f, 0.f, 0.f, 0.f};
-        constexpr int FB = 16;  // partials' loads in flight per batch (registers are free at this point)
+        constexpr int FB = 32;
         for (int s0 = 0; s0 < expected; s0 += FB) {
-            float m2[FB], l2[FB];
+            const bool mine = s0 + lane < expected;
+            const float ml = mine ? __ldcg(pmb + (s0 + lane) * 16 + 2 * h) : -CUDART_INF_F;
+            const float ll = mine ? __ldcg(pmb + (s0 + lane) * 16 + 2 * h + 1) : 0.f;
             float4 v[FB];
 #pragma unroll
-            for (int u = 0; u < FB; ++u) {
-                const int s2 = s0 + u;
-                if (s2 < expected) {
-                    m2[u] = __ldcg(pmb + s2 * 16 + 2 * h);
-                    l2[u] = __ldcg(pmb + s2 * 16 + 2 * h + 1);
-                    v[u] = __ldcg(reinterpret_cast<const float4 *>(pob + s2 * 8 * D + h * D + lane * 4));
-                } else {
-                    m2[u] = -CUDART_INF_F;
-                    l2[u] = 0.f;
-                    v[u] = make_float4(0.f, 0.f, 0.f, 0.f);
-                }
-            }
-            float bm = M;
+            for (int u = 0; u < FB; ++u)
+                v[u] = (s0 + u < expected)
+                           ? __ldcg(reinterpret_cast<const float4 *>(pob + (s0 + u) * 8 * D + h * D + lane * 4))
+                           : make_float4(0.f, 0.f, 0.f, 0.f);
+            float bm = fmaxf(M, ml);
 #pragma unroll
-            for (int u = 0; u < FB; ++u) bm = fmaxf(bm, m2[u]);
+            for (int o = 1; o < 32; o <<= 1) bm = fmaxf(bm, __shfl_xor_sync(0xffffffffu, bm, o));
             const float sc = (M == -CUDART_INF_F) ? 0.f : fast_exp2(M - bm);
-            L *= sc;
+            const float fl = (ml == -CUDART_INF_F) ? 0.f : fast_exp2(ml - bm);
+            Lw = Lw * sc + ll * fl;
 #pragma unroll
             for (int e = 0; e < 4; ++e) x[e] *= sc;
 #pragma unroll
             for (int u = 0; u < FB; ++u) {
-                const float f = (m2[u] == -CUDART_INF_F) ? 0.f : fast_exp2(m2[u] - bm);
-                L += l2[u] * f;
+                const float f = __shfl_sync(0xffffffffu, fl, u);
                 x[0] += v[u].x * f;
                 x[1] += v[u].y * f;
                 x[2] += v[u].z * f;
@@ -1121,6 +1116,7 @@ __global__ void __launch_bounds__(NCW_ * 32, 1) decode_attn_kernel(const AttnArg
             }
             M = bm;
         }
+        const float L = warp_sum(Lw);
         const float inv = (L > 0.f) ? 1.f / L : 0.f;
 #pragma unroll
         for (int e = 0; e < 4; ++e) x[e] *= inv;

@@ -27,20 +27,6 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t *bar, uint32_t by
                  "r"(bytes)
                  : "memory");
 }
-__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t phase) {
-    asm volatile(
-        "{\n"
-        ".reg .pred P1;\n"
-        "LAB_WAIT:\n"
-        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
-        "@P1 bra.uni DONE;\n"
-        "bra.uni LAB_WAIT;\n"
-        "DONE:\n"
-        "}\n" ::"r"(smem_u32(bar)),
-        "r"(phase)
-        : "memory");
-}
-
 // ---- bulk async copy global -> shared (TMA engine, non-tensor form) -------------
 __device__ __forceinline__ uint64_t l2_evict_first_policy() {
     uint64_t pol;
@@ -56,12 +42,8 @@ __device__ __forceinline__ void bulk_g2s(void *dst_smem, const void *src_gmem, u
         : "memory");
 }
 
-// L2 prefetch of a contiguous global range (TMA engine, no completion tracking)
-__device__ __forceinline__ void bulk_prefetch_l2(const void *src_gmem, uint32_t bytes) {
-    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(src_gmem), "r"(bytes) : "memory");
-}
-
-// the same on a precomputed shared-window address (no per-use address conversion)
+// volatile shared loads/stores and mbarrier waits on precomputed shared-window
+// addresses (no per-use generic-to-shared conversion in the hot loop)
 __device__ __forceinline__ int ld_volatile_shared_u32(uint32_t saddr) {
     int v;
     asm volatile("ld.volatile.shared.u32 %0, [%1];\n" : "=r"(v) : "r"(saddr));
@@ -84,19 +66,8 @@ __device__ __forceinline__ void mbar_wait_s(uint32_t saddr, uint32_t phase) {
         : "memory");
 }
 
-__device__ __forceinline__ int ld_volatile_shared(const int *p) {
-    int v;
-    asm volatile("ld.volatile.shared.u32 %0, [%1];\n" : "=r"(v) : "r"(smem_u32(p)));
-    return v;
-}
 __device__ __forceinline__ void st_volatile_shared(int *p, int v) {
     asm volatile("st.volatile.shared.u32 [%0], %1;\n" ::"r"(smem_u32(p)), "r"(v) : "memory");
-}
-
-// order this thread's generic-proxy shared-memory accesses before its
-// subsequent async-proxy (TMA) writes to the same buffer
-__device__ __forceinline__ void fence_proxy_async_smem() {
-    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
 }
 
 // gpu-scope acq_rel atomic add: releases this warp's prior writes (ordered

@@ -317,17 +317,13 @@ __device__ __forceinline__ void process_block(const uint8_t *__restrict__ sb, Wa
     // value offsets as A: row gq (< 4) = channel group, k = tokens
     const uint4 *vbp = reinterpret_cast<const uint4 *>(sb + Blk::VB_OFF + ((gq & 3) * 4 + tq) * 64);
     uint4 zv;
-    const int srcA = 4 * tq + (gq >> 1), srcB = 4 * (tq + 4) + (gq >> 1);
-    const bool odd = (gq & 1) != 0;
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
-        const uint32_t H0 = pack_half2(sacc[j][0], sacc[j][2]);
-        const uint32_t H1 = pack_half2(sacc[j][1], sacc[j][3]);
-        const uint32_t x0 = __shfl_sync(0xffffffffu, H0, srcA);
-        const uint32_t x1 = __shfl_sync(0xffffffffu, H1, srcA);
-        const uint32_t y0 = __shfl_sync(0xffffffffu, H0, srcB);
-        const uint32_t y1 = __shfl_sync(0xffffffffu, H1, srcB);
-        const uint32_t bp0 = odd ? x1 : x0, bp1 = odd ? y1 : y0;
+        // P of tokens 16j..16j+15 as the B operand: the accumulator rows (tokens) x
+        // cols (heads 2tq, 2tq+1), transposed per 8x8 half by movmatrix, is exactly
+        // the B fragment (k = tokens 2tq, 2tq+1 | 2tq+8, 2tq+9; n = head gq)
+        const uint32_t bp0 = movmatrix_t(pack_half2(sacc[j][0], sacc[j][1]));
+        const uint32_t bp1 = movmatrix_t(pack_half2(sacc[j][2], sacc[j][3]));
         uint32_t bv[4][2];
         {
             const uint4 *p = reinterpret_cast<const uint4 *>(sb + Blk::VA_OFF + (j * 4 + tq) * 32);

@@ -124,6 +124,13 @@ __device__ __forceinline__ uint32_t hmul2_u32(uint32_t a, uint32_t b) {
     __half2 r = __hmul2(*reinterpret_cast<__half2 *>(&a), *reinterpret_cast<__half2 *>(&b));
     return *reinterpret_cast<uint32_t *>(&r);
 }
+// transpose of an 8x8 16-bit matrix held one row-pair per lane (row lane/4,
+// cols 2(lane%4), +1): the mma accumulator layout becomes the B-fragment layout
+__device__ __forceinline__ uint32_t movmatrix_t(uint32_t x) {
+    uint32_t y;
+    asm("movmatrix.sync.aligned.m8n8.trans.b16 %0, %1;\n" : "=r"(y) : "r"(x));
+    return y;
+}
 __device__ __forceinline__ uint32_t pack_half2(float lo, float hi) {
     __half2 r = __floats2half2_rn(lo, hi);
     return *reinterpret_cast<uint32_t *>(&r);

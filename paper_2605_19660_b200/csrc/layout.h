@@ -119,9 +119,10 @@ OSK_HD void k_word_coords(int BITS, int w, int f, int hi, int &token, int &chann
 
 // ---- V code words ----------------------------------------------------------
 // word index w = ((j*32 + lane)*4 + fam)*WPF + half
-//   fam: 0 (row g; t1,t2) 1 (row g+8; t1,t2) 2 (row g; t3,t4) 3 (row g+8; t3,t4)
-//   t1 = 16j+tq, t2 = 16j+tq+8, t3 = 16j+tq+4, t4 = 16j+tq+12
-//   low half -> first token of the pair, high half -> second
+//   fam: 0 (row g; k 2tq,2tq+1) 1 (row g+8; same k) 2 (row g; k 2tq+8,2tq+9) 3 (row g+8; same k)
+//   k = token within the 16-token tile j in natural order (the P.V B operand is the
+//   movmatrix transpose of the QK accumulator, whose rows are tokens 16j..16j+15)
+//   low half -> the even k of the pair, high half -> the odd one
 // field f -> PV m-tile m = half*TPW + f -> channel 16m + row
 OSK_HD void v_word_coords(int BITS, int w, int f, int hi, int &token, int &channel) {
     const int tpw = 16 / BITS, wpf = 8 / tpw;
@@ -133,8 +134,7 @@ OSK_HD void v_word_coords(int BITS, int w, int f, int hi, int &token, int &chann
     const int m = half * tpw + f;
     const int row = g + ((fam & 1) ? 8 : 0);
     channel = 16 * m + row;
-    const int base = 16 * j + tq + ((fam & 2) ? 4 : 0);
-    token = base + (hi ? 8 : 0);
+    token = 16 * j + 2 * tq + (hi ? 1 : 0) + ((fam & 2) ? 8 : 0);
 }
 
 // ---- params ----------------------------------------------------------------
@@ -160,13 +160,13 @@ OSK_HD int kb_index(int c, int grp) {
     k_chan_split(c, s, tq, slot);
     return ((grp * 4 + tq) * 4 + (s >> 1)) * 8 + ((slot >> 1) * 2 + (s & 1)) * 2 + (slot & 1);
 }
-// token t = 16j + r; the B-fragment slot order is (tq, tq+8, tq+4, tq+12)
+// token t = 16j + r; B-fragment k = r (natural order): lane pair tq = (r mod 8) / 2,
+// slot = (r & 1) + 2 (r >= 8)  (slots 0,1 -> b0 = k 2tq,2tq+1; 2,3 -> b1 = k 2tq+8,2tq+9)
 OSK_HD void v_tok_split(int t, int &j, int &tq, int &slot) {
     j = t >> 4;
     const int r = t & 15;
-    tq = r & 3;
-    const int q = r >> 2;  // 0..3 <-> offsets 0,4,8,12
-    slot = (q == 0) ? 0 : (q == 2) ? 1 : (q == 1) ? 2 : 3;
+    tq = (r & 7) >> 1;
+    slot = (r & 1) + ((r >> 3) << 1);
 }
 // V a-params: [j][tq][gc][slot]
 OSK_HD int va_index(int t, int gc) {

@@ -31,6 +31,10 @@ namespace {
 
 constexpr int QT = 128;  // threads per CTA
 constexpr int KU_ROW = 4 * 33;  // doubles per token row of the K_u tile (4 quarters of 32, padded to 33)
+// byte stride of a token row in the shared code tiles: 132 makes the permuted-word
+// gathers of the pack loop (and the V code writes) at most 2-way bank conflicted
+// (128 was 4-way for K, 8-way for V) while three CTAs still fit per SM
+constexpr int CODE_STRIDE = D + 4;
 
 __device__ __forceinline__ double dadd(double a, double b) { return __dadd_rn(a, b); }
 __device__ __forceinline__ double dsub(double a, double b) { return __dsub_rn(a, b); }
@@ -214,8 +218,8 @@ __global__ void __launch_bounds__(QT * GPAR) quantize_kernel(const QuantizeArgs 
     extern __shared__ __align__(16) uint8_t smem[];
     double *ku = reinterpret_cast<double *>(smem) + (threadIdx.x / QT) * 32 * KU_ROW;  // [GPAR][32][4][33]
     uint8_t *ck = smem + GPAR * 32 * KU_ROW * 8;                  // [128][128] K codes
-    uint8_t *cv = ck + R * D;                                     // [128][128] V codes
-    uint8_t *prm = cv + R * D;                                    // params + norms (BYTES - KA_OFF)
+    uint8_t *cv = ck + R * CODE_STRIDE;                           // [128][128] V codes
+    uint8_t *prm = cv + R * CODE_STRIDE;                          // params + norms (BYTES - KA_OFF)
     __half *ka = reinterpret_cast<__half *>(prm);
     __half *kb = ka + D * NGRP;
     __half *va = kb + D * NGRP;
@@ -316,7 +320,7 @@ __global__ void __launch_bounds__(QT * GPAR) quantize_kernel(const QuantizeArgs 
                                          : group_params_f32(y, BITS);
 #pragma unroll
             quantize_group([&](int i) { return y[i]; }, p, BITS,
-                           [&](int i, int code) { cv[t * D + q * 32 + i] = (uint8_t)code; });
+                           [&](int i, int code) { cv[t * CODE_STRIDE + q * 32 + i] = (uint8_t)code; });
             __half ha, hb;
             affine16(p, ha, hb);
             va[va_index(t, q)] = ha;
@@ -333,7 +337,7 @@ __global__ void __launch_bounds__(QT * GPAR) quantize_kernel(const QuantizeArgs 
             const int cc = (c >> 5) * 33 + (c & 31);
             const GroupQ p = group_params([&](int i) { return ku[i * KU_ROW + cc]; }, BITS);
             quantize_group([&](int i) { return ku[i * KU_ROW + cc]; }, p, BITS,
-                           [&](int i, int code) { ck[(gi * G + i) * D + c] = (uint8_t)code; });
+                           [&](int i, int code) { ck[(gi * G + i) * CODE_STRIDE + c] = (uint8_t)code; });
             // keys use the same affine form as values, x = a*code + b with
             // b = -delta*zp (a constant group is a = 0, b = lo: its codes are 0,
             // quant.cpp:37-42, 65-68); the attention kernel folds b into one
@@ -358,13 +362,16 @@ __global__ void __launch_bounds__(QT * GPAR) quantize_kernel(const QuantizeArgs 
         uint32_t wk = 0, wv = 0;
 #pragma unroll
         for (int hi = 0; hi < 2; ++hi) {
+            // field f of a K word is token +16f of field 0, of a V word channel +16f
+            int tk, ckn, tv, cvn;
+            k_word_coords(BITS, w, 0, hi, tk, ckn);
+            v_word_coords(BITS, w, 0, hi, tv, cvn);
+            const uint8_t *pk = ck + tk * CODE_STRIDE + ckn;
+            const uint8_t *pv = cv + tv * CODE_STRIDE + cvn;
 #pragma unroll
             for (int f = 0; f < TPW; ++f) {
-                int t, c;
-                k_word_coords(BITS, w, f, hi, t, c);
-                wk |= (uint32_t)ck[t * D + c] << (hi * 16 + f * BITS);
-                v_word_coords(BITS, w, f, hi, t, c);
-                wv |= (uint32_t)cv[t * D + c] << (hi * 16 + f * BITS);
+                wk |= (uint32_t)pk[16 * f * CODE_STRIDE] << (hi * 16 + f * BITS);
+                wv |= (uint32_t)pv[16 * f] << (hi * 16 + f * BITS);
             }
         }
         reinterpret_cast<uint32_t *>(out + Blk::K_OFF)[w] = wk;
@@ -444,7 +451,7 @@ __global__ void ring_copy_kernel(const RingCopyArgs a) {
 
 template <int BITS, int GPAR>
 cudaError_t launch_q(const QuantizeArgs &a, dim3 grid, cudaStream_t st) {
-    const int smem = GPAR * 32 * KU_ROW * 8 + 2 * R * D + Block<BITS>::BYTES - Block<BITS>::KA_OFF;
+    const int smem = GPAR * 32 * KU_ROW * 8 + 2 * R * CODE_STRIDE + Block<BITS>::BYTES - Block<BITS>::KA_OFF;
     static bool init = false;
     if (!init) {
         cudaError_t e = cudaFuncSetAttribute(quantize_kernel<BITS, GPAR>, cudaFuncAttributeMaxDynamicSharedMemorySize,

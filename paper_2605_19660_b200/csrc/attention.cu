@@ -837,10 +837,9 @@ __global__ void __launch_bounds__(NCW_ * 32, 1) decode_attn_kernel(const AttnArg
             int stg = first % C::NST, round = first / C::NST;
             for (int p = first; p < pend; p += NCW) {
                 const long long ts0 = (kProf && a.prof) ? clk() : 0;
-                if (lane == 0)
-                    while (ld_volatile_shared_u32(consumed_s + 4 * stg) < round) {
-                    }
-                __syncwarp();
+                // every lane polls the same word (a broadcast): no divergent region
+                while (ld_volatile_shared_u32(consumed_s + 4 * stg) < round) {
+                }
                 const long long ts1 = (kProf && a.prof) ? clk() : 0;
                 mbar_wait_s(full_s + 8 * stg, (uint32_t)(round & 1));
                 if (kProf && a.prof) {

@@ -101,18 +101,18 @@ def test_head_sharded_equals_full_heads():
 
 
 # ---------------------------------------------------------------- fused peer-memory exchange
-def _single_cache_outputs():
+def _single_cache_outputs(cfg=None):
     from paper_2605_19660_b200 import KvCache, PipelineConfig
 
     k, v, q = _inputs()
-    c = KvCache(PipelineConfig(heads=H), batch=1, q_heads=H * G_, max_tokens=S + STEPS)
+    c = KvCache(cfg or PipelineConfig(heads=H), batch=1, q_heads=H * G_, max_tokens=S + STEPS)
     c.buffer_quant(dev_bf16(k[None, :S]), dev_bf16(v[None, :S]))
     return [c.decode_step(dev_bf16(q[t][None]), dev_bf16(k[S + t][None]), dev_bf16(v[S + t][None])).cpu().numpy()
             for t in range(STEPS)]
 
 
-@pytest.mark.parametrize("world", [2, 3])
-def test_peer_publish_merge_virtual_ranks(world):
+@pytest.mark.parametrize("world,bits,rotate_v", [(2, 2, False), (3, 2, False), (2, 4, True)])
+def test_peer_publish_merge_virtual_ranks(world, bits, rotate_v):
     """The attention kernel publishes its rows into every rank's receive area
     and the flag-polling merge kernel combines them (oscar_kv_attend_publish +
     oscar_peer_merge).  `world` virtual ranks share cuda:0 (their areas are
@@ -126,14 +126,15 @@ def test_peer_publish_merge_virtual_ranks(world):
 
     k, v, q = _inputs()
     rows = H * G_
+    cfg = PipelineConfig(heads=H, bits=bits, rotate_v=rotate_v)
     plans, areas = local_peer_plans(world, rows)
     shards = [sequence_shard(S, world, r) for r in range(world)]
     caches = []
     for sh in shards:
-        c = KvCache(PipelineConfig(heads=H), batch=1, q_heads=rows, max_tokens=S + STEPS)
+        c = KvCache(cfg, batch=1, q_heads=rows, max_tokens=S + STEPS)
         c.buffer_quant(dev_bf16(k[None, sh.tok_lo:sh.tok_hi]), dev_bf16(v[None, sh.tok_lo:sh.tok_hi]))
         caches.append(c)
-    ref = _single_cache_outputs()
+    ref = _single_cache_outputs(cfg)
     status = torch.zeros(1, dtype=torch.int32, device="cuda")
     outs = [torch.empty((rows, 128), dtype=torch.float32, device="cuda") for _ in range(world)]
     lses = [torch.empty((rows,), dtype=torch.float32, device="cuda") for _ in range(world)]
@@ -152,7 +153,7 @@ def test_peer_publish_merge_virtual_ranks(world):
     assert status.item() == 0
     assert caches[-1].flush_count == 1
     # every rank merged the same rows; LSE equals the single cache's
-    full = KvCache(PipelineConfig(heads=H), batch=1, q_heads=rows, max_tokens=S + STEPS + 1)
+    full = KvCache(cfg, batch=1, q_heads=rows, max_tokens=S + STEPS + 1)
     full.buffer_quant(dev_bf16(k[None, :S + STEPS]), dev_bf16(v[None, :S + STEPS]))
     _, lse_full = full.attend(dev_bf16(q[STEPS - 1][None]))
     for r, c in enumerate(caches):

@@ -105,6 +105,17 @@ int oscar_kv_attend(oscar_kv_handle *h, const void *q, float *out, float *lse, v
 int oscar_kv_decode_step_host(oscar_kv_handle *h, const void *q_host, const void *k_host,
                               const void *v_host, float *out_host, float *lse_host, void *stream);
 
+/* Device-side status accumulated by the quantize/append kernels since the
+ * last clear (synchronises the handle's last stream):
+ *   OSCAR_STATUS_FP16_OVERFLOW  a group's step or offset exceeds the fp16 range
+ *                               of the attention record (attention over that
+ *                               group is not finite; export/dump stay exact),
+ *   OSCAR_STATUS_NONFINITE      a group had non-finite input values.
+ * The reference has no such condition for finite inputs (it keeps fp64). */
+#define OSCAR_STATUS_FP16_OVERFLOW 1
+#define OSCAR_STATUS_NONFINITE 2
+int oscar_kv_status(oscar_kv_handle *h, int32_t *flags, int32_t clear);
+
 /* packed_tokens / residual_tokens / flush_count (kv_cache.hpp:67-71). */
 int oscar_kv_stats(const oscar_kv_handle *h, int64_t *packed, int64_t *residual, int64_t *flushes);
 int oscar_kv_memory_report(const oscar_kv_handle *h, oscar_kv_memory_report_t *out);

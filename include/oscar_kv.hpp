@@ -96,6 +96,12 @@ public:
         return s.packed + s.residual;
     }
     int64_t flush_count() const { return stats().flushes; }
+    // device-side flags since the last clear (OSCAR_STATUS_*; synchronises)
+    int32_t status(bool clear = false) {
+        int32_t f = 0;
+        check(oscar_kv_status(h_, &f, clear ? 1 : 0));
+        return f;
+    }
 
     oscar_kv_memory_report_t memory_report() const {
         oscar_kv_memory_report_t r{};

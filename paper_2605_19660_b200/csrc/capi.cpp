@@ -114,6 +114,7 @@ struct oscar_kv_handle {
     void *ring_k = nullptr, *ring_v = nullptr;
     float *part_o = nullptr, *part_ml = nullptr;
     int *counters = nullptr;
+    int *status_d = nullptr;  // device status word (kernels.h STATUS_*)
     float *warp_part = nullptr;
     int maxp_alloc = 0;
     int maxseg_alloc = 1;
@@ -151,6 +152,7 @@ struct oscar_kv_handle {
         cudaFree(part_o);
         cudaFree(part_ml);
         cudaFree(counters);
+        cudaFree(status_d);
         cudaFree(warp_part);
         cudaFree(stage);
     }
@@ -176,6 +178,7 @@ struct oscar_kv_handle {
         a.blk0 = blk0;
         a.shadow = shadow;
         a.tc = tc();
+        a.status = status_d;
         if (ring_prefix > 0) {
             a.rk = ring_k;
             a.rv = ring_v;
@@ -1004,6 +1007,8 @@ int oscar_kv_create(const oscar_kv_config *cfg, int64_t batch, int64_t q_heads, 
         h->part_ml = (float *)h->dalloc(sizeof(float) * (size_t)(h->BH * h->maxp_alloc * 16));
         h->counters = (int *)h->dalloc(sizeof(int) * (size_t)h->BH);
         CK(cudaMemset(h->counters, 0, sizeof(int) * (size_t)h->BH));
+        h->status_d = (int *)h->dalloc(sizeof(int));
+        CK(cudaMemset(h->status_d, 0, sizeof(int)));
         // segments (b, kv heads) one CTA range can touch: <= BH/ncta + 2 (nb >= 1 unit)
         h->maxseg_alloc = (int)std::min<int64_t>(64, h->BH / h->num_sms + 2);
         h->warp_part = (float *)h->dalloc(
@@ -1208,6 +1213,18 @@ int oscar_kv_decode_step_host(oscar_kv_handle *h, const void *q_host, const void
         if (!zo) CK(cudaMemcpyAsync(out_host, dout, ob, cudaMemcpyDeviceToHost, s));
         if (lse_host && !zl) CK(cudaMemcpyAsync(lse_host, dlse, lb, cudaMemcpyDeviceToHost, s));
         CK(cudaStreamSynchronize(s));
+    });
+}
+
+int oscar_kv_status(oscar_kv_handle *h, int32_t *flags, int32_t clear) {
+    return guard([&] {
+        if (!h || !flags) throw InvalidArg("status: null argument");
+        CK(cudaSetDevice(h->device));
+        CK(cudaStreamSynchronize(h->last_stream));
+        int v = 0;
+        CK(cudaMemcpy(&v, h->status_d, sizeof(int), cudaMemcpyDeviceToHost));
+        if (clear) CK(cudaMemset(h->status_d, 0, sizeof(int)));
+        *flags = v;
     });
 }
 

@@ -34,7 +34,12 @@ struct QuantizeArgs {
     // the rings (K [bh][R][D], V [bh][D][R]), the rest from the source above
     const void *rk = nullptr, *rv = nullptr;
     int64_t rtok = 0;
+    // device status word (nullable): bit 0 = an fp16 step/offset of the record
+    // overflowed (the exact fp64 params are still exported), bit 1 = a group
+    // had non-finite input (the reference's params are then non-finite too)
+    int *status = nullptr;
 };
+constexpr int STATUS_FP16_OVERFLOW = 1, STATUS_NONFINITE_INPUT = 2;
 cudaError_t launch_quantize(const QuantizeArgs &a, cudaStream_t st);
 
 // Copy n tokens of raw bf16 K/V into the residual ring at slot0: K ring

@@ -41,8 +41,8 @@ __device__ __forceinline__ double dsub(double a, double b) { return __dsub_rn(a,
 __device__ __forceinline__ double dmul(double a, double b) { return __dmul_rn(a, b); }
 __device__ __forceinline__ double ddiv(double a, double b) { return __ddiv_rn(a, b); }
 
-// 32 bf16 -> fp64 (exact)
-__device__ __forceinline__ void load32(const __nv_bfloat16 *p, double (&x)[32]) {
+// 32 bf16 -> fp64 (exact); bit 15 / 31 of `bad` flags non-finite inputs
+__device__ __forceinline__ void load32(const __nv_bfloat16 *p, double (&x)[32], uint32_t &bad) {
     const uint4 *p4 = reinterpret_cast<const uint4 *>(p);
 #pragma unroll
     for (int v = 0; v < 4; ++v) {
@@ -52,8 +52,15 @@ __device__ __forceinline__ void load32(const __nv_bfloat16 *p, double (&x)[32]) 
         for (int e = 0; e < 4; ++e) {
             x[v * 8 + 2 * e] = (double)__uint_as_float(w[e] << 16);
             x[v * 8 + 2 * e + 1] = (double)__uint_as_float(w[e] & 0xffff0000u);
+            // a half is non-finite iff its exponent is all ones: adding 0x0080 to the
+            // masked exponent then carries into bit 15 (no carry across halves)
+            bad |= (w[e] & 0x7F807F80u) + 0x00800080u;
         }
     }
+}
+__device__ __forceinline__ double bf16_bits_to_double(uint16_t u, uint32_t &bad) {
+    bad |= ((uint32_t)u & 0x7F80u) + 0x0080u;  // bit 15 set iff non-finite
+    return (double)__uint_as_float((uint32_t)u << 16);
 }
 
 // hadamard.cpp:10-26 on a 128-vector spread over a 4-lane quad (32 per lane)
@@ -209,6 +216,13 @@ __device__ __forceinline__ void affine16(const GroupQ &p, __half &a, __half &b) 
     }
 }
 
+// device status (QuantizeArgs::status): record overflow / non-finite input
+__device__ __forceinline__ void flag_status(int *status, const GroupQ &p, __half ha, __half hb) {
+    if (!status) return;
+    // (non-finite inputs are flagged where they are loaded)
+    if (isfinite(p.lo) && isfinite(p.hi) && (__hisinf(ha) || __hisinf(hb))) atomicOr(status, STATUS_FP16_OVERFLOW);
+}
+
 // GPAR 32-token groups of the block are processed concurrently by GPAR
 // 128-thread quarters of the CTA (GPAR = 1: prefill, throughput; GPAR = 4:
 // the single-block flush, latency).
@@ -245,10 +259,11 @@ __global__ void __launch_bounds__(QT * GPAR) quantize_kernel(const QuantizeArgs 
         const int t = gi * G + tl;  // token within the block
         // ---------------- K: rotate, scale (apply_method) ----------------
         double x[32];
+        uint32_t bad = 0;  // non-finite K or V inputs of this thread's row
         const bool from_ring = blk == 0 && t < a.rtok;
         load32(from_ring ? reinterpret_cast<const __nv_bfloat16 *>(rk) + (int64_t)t * D + q * 32
                          : kin + (tok_base + t) * a.st + q * 32,
-               x);
+               x, bad);
         if (tc.rotates) fht128_quad(x, q);
         double s = 1.0, inv = 1.0;
         if (tc.scales) {
@@ -302,16 +317,15 @@ __global__ void __launch_bounds__(QT * GPAR) quantize_kernel(const QuantizeArgs 
             double y[32];
             if (from_ring) {  // channel-major residual ring
 #pragma unroll
-                for (int i = 0; i < 32; ++i)
-                    y[i] = (double)__uint_as_float((uint32_t)rv[(int64_t)(q * 32 + i) * R + t] << 16);
+                for (int i = 0; i < 32; ++i) y[i] = bf16_bits_to_double(rv[(int64_t)(q * 32 + i) * R + t], bad);
             } else if (a.vsc == 1) {
-                load32(vin + (tok_base + t) * a.vst + q * 32, y);
+                load32(vin + (tok_base + t) * a.vst + q * 32, y, bad);
             } else {  // channel-major source (the residual ring)
                 const uint16_t *vp = reinterpret_cast<const uint16_t *>(vin) + (tok_base + t) * a.vst;
 #pragma unroll
-                for (int i = 0; i < 32; ++i)
-                    y[i] = (double)__uint_as_float((uint32_t)vp[(int64_t)(q * 32 + i) * a.vsc] << 16);
+                for (int i = 0; i < 32; ++i) y[i] = bf16_bits_to_double(vp[(int64_t)(q * 32 + i) * a.vsc], bad);
             }
+            if ((bad & 0x80008000u) && a.status) atomicOr(a.status, STATUS_NONFINITE_INPUT);
             if (tc.rotate_v) fht128_quad(y, q);
             // raw (bf16-valued) V: the group range in fp32 is exact, one FMNMX per
             // element; a zero extreme re-runs the sequential std::min/max so the
@@ -323,6 +337,7 @@ __global__ void __launch_bounds__(QT * GPAR) quantize_kernel(const QuantizeArgs 
                            [&](int i, int code) { cv[t * CODE_STRIDE + q * 32 + i] = (uint8_t)code; });
             __half ha, hb;
             affine16(p, ha, hb);
+            flag_status(a.status, p, ha, hb);
             va[va_index(t, q)] = ha;
             vb[vb_index(t, q)] = hb;
             if (shadow) {
@@ -344,6 +359,7 @@ __global__ void __launch_bounds__(QT * GPAR) quantize_kernel(const QuantizeArgs 
             // MMA per k-step against the rotated query
             __half ha, hb;
             affine16(p, ha, hb);
+            flag_status(a.status, p, ha, hb);
             ka[ka_index(c, gi)] = ha;
             kb[kb_index(c, gi)] = hb;
             if (shadow) {

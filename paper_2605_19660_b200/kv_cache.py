@@ -95,6 +95,7 @@ def lib():
         L.oscar_kv_materialize.argtypes = [_P, ctypes.c_int64, _P, _P]
         L.oscar_lse_merge.argtypes = [_P, _P, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64, _P, _P, _P]
         L.oscar_kv_last_launch_count.argtypes = [_P]
+        L.oscar_kv_status.argtypes = [_P, ctypes.POINTER(ctypes.c_int32), ctypes.c_int32]
         L.oscar_peer_area_bytes.restype = ctypes.c_int64
         L.oscar_peer_area_bytes.argtypes = [ctypes.c_int32, ctypes.c_int64]
         L.oscar_kv_attend_publish.argtypes = [_P, _P, _P, _P, ctypes.POINTER(_PeerPlan), ctypes.c_uint32, _P]
@@ -115,6 +116,7 @@ C_ABI_SYMBOLS = [
     "oscar_kv_memory_report", "oscar_kv_export", "oscar_kv_dump", "oscar_kv_load", "oscar_kv_materialize", "oscar_lse_merge",
     "oscar_kv_last_launch_count", "oscar_peer_area_bytes", "oscar_kv_attend_publish", "oscar_peer_publish_empty",
     "oscar_peer_merge", "oscar_ipc_alloc", "oscar_ipc_open", "oscar_ipc_close", "oscar_ipc_free",
+    "oscar_kv_status",
 ]
 
 
@@ -259,6 +261,12 @@ class KvCache:
     @property
     def flush_count(self):
         return self._stats()[2]
+
+    def status(self, clear: bool = False) -> dict:
+        """Device-side flags of the quantize/append kernels (oscar_kv_status)."""
+        f = ctypes.c_int32()
+        _check(lib().oscar_kv_status(self._h, ctypes.byref(f), int(clear)))
+        return {"fp16_overflow": bool(f.value & 1), "nonfinite_input": bool(f.value & 2), "raw": f.value}
 
     def last_launch_count(self) -> int:
         return lib().oscar_kv_last_launch_count(self._h)

@@ -92,3 +92,36 @@ def test_large_value_magnitudes_stay_finite(bits):
     err = rel_err(out, ref)
     log_err(f"large_values[bits={bits}][|v|~2000]", err)
     assert err <= 5e-3, err
+
+
+def test_device_status_flags():
+    """oscar_kv_status: finite inputs in range raise nothing; a value range beyond
+    the fp16 step/offset raises FP16_OVERFLOW (the exported fp64 params stay
+    bit-exact with the oracle); a non-finite input raises NONFINITE; clear resets."""
+    from paper_2605_19660_b200 import KvCache, PipelineConfig
+
+    rng = np.random.default_rng(5)
+    S, H, d = 256, 2, 128
+    k = _bf16(rng.standard_normal((1, S, H, d)))
+    v = _bf16(rng.standard_normal((1, S, H, d)))
+    c = KvCache(PipelineConfig(heads=H, bits=2), batch=1, q_heads=H * 4, max_tokens=S + 8)
+    c.buffer_quant(dev_bf16(k), dev_bf16(v))
+    assert c.status()["raw"] == 0
+
+    big = v.copy()
+    big[0, 5, 1, :] *= 1e6  # one token's value groups span ~1e6: the fp16 step overflows
+    big = _bf16(big)
+    c2 = KvCache(PipelineConfig(heads=H, bits=2), batch=1, q_heads=H * 4, max_tokens=S + 8)
+    c2.buffer_quant(dev_bf16(k), dev_bf16(big))
+    st = c2.status()
+    assert st["fp16_overflow"] and not st["nonfinite_input"], st
+    o = ob.PortCache(H=H, bits=2)
+    o.append(k[0], big[0])
+    assert ob.caches_equal(export_to_oracle(c2.export(0), H), o.export()) == []
+    assert c2.status(clear=True)["raw"] != 0 and c2.status()["raw"] == 0
+
+    bad = k.copy()
+    bad[0, 7, 0, 3] = np.nan
+    c3 = KvCache(PipelineConfig(heads=H, bits=2), batch=1, q_heads=H * 4, max_tokens=S + 8)
+    c3.buffer_quant(dev_bf16(bad), dev_bf16(v))
+    assert c3.status()["nonfinite_input"]

@@ -909,10 +909,12 @@ __global__ void __launch_bounds__(NCW_ * 32, 1) decode_attn_kernel(const AttnArg
                 const int cA = 16 * mm + gq, cB = cA + 8;
                 const int h0 = 2 * tq, h1 = 2 * tq + 1;
                 const float bb0 = BITS == 0 ? 0.f : vb0[mm >> 1], bb1 = BITS == 0 ? 0.f : vb1[mm >> 1];
-                slot[h0 * D + cA] = st.o[mm][0] * sc + bb0;
-                slot[h1 * D + cA] = st.o[mm][1] * sc + bb1;
-                slot[h0 * D + cB] = st.o[mm][2] * sc + bb0;
-                slot[h1 * D + cB] = st.o[mm][3] * sc + bb1;
+                if (h0 < g) {  // rows of padding heads (g < 8) are never read
+                    slot[h0 * D + cA] = st.o[mm][0] * sc + bb0;
+                    slot[h1 * D + cA] = st.o[mm][1] * sc + bb1;
+                    slot[h0 * D + cB] = st.o[mm][2] * sc + bb0;
+                    slot[h1 * D + cB] = st.o[mm][3] * sc + bb1;
+                }
             }
             if (gq == 0) {
                 slot[8 * D + 2 * tq] = st.m[0];

@@ -41,3 +41,16 @@ def test_bench_reference_arm_rank0_only():
     d = json.loads(lines[0])
     assert d["impl"] == "reference" and d["value"] > 0
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["cpu_baseline"]["cores"] >= 1
+
+
+@pytest.mark.parametrize("extra,port", [(["--config", "c3", "--batch", "16", "--layers", "2"], 29563),
+                                        (["--config", "c4"], 29564),
+                                        (["--config", "c5", "--exchange", "nccl"], 29565),
+                                        (["--config", "c5", "--exchange", "p2p"], 29566)])
+def test_bench_sharded_configs_two_ranks(extra, port):
+    """batch (C3), head (C4) and sequence (C5; NCCL-path and peer-memory exchange)
+    sharding through bench.py on two ranks."""
+    lines = _torchrun(extra + ["--steps", "4", "--warmup", "3"], port)
+    assert len(lines) == 1, lines
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["value"] > 0

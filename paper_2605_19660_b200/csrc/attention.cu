@@ -614,7 +614,8 @@ __device__ __forceinline__ void residual_merge(const ResPartial &rp, float *slot
     const float fs0 = (ms0 == -CUDART_INF_F) ? 0.f : fast_exp2(ms0 - M0);
     const float fs1 = (ms1 == -CUDART_INF_F) ? 0.f : fast_exp2(ms1 - M1);
     const float fr0 = fast_exp2(m0 - M0), fr1 = fast_exp2(m1 - M1);
-    if (!rotate_v) {
+    // (rows of padding heads, h >= g, are neither written by the warp partial nor read)
+    if (!rotate_v && h0 < g) {
 #pragma unroll
         for (int mm = 0; mm < 8; ++mm) {
             const int cA = 16 * mm + gq, cB = cA + 8;
@@ -627,7 +628,7 @@ __device__ __forceinline__ void residual_merge(const ResPartial &rp, float *slot
     // rotate_v: rescale the packed partial, then add the rotated residual partial head by head
     float *part = slot + 8 * D + 16;  // 128 floats of scratch reserved after m/l
 #pragma unroll
-    for (int mm = 0; mm < 8 && rotate_v; ++mm) {
+    for (int mm = 0; mm < 8 && rotate_v && h0 < g; ++mm) {
         const int cA = 16 * mm + gq, cB = cA + 8;
         slot[h0 * D + cA] *= fs0;
         slot[h1 * D + cA] *= fs1;

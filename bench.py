@@ -689,7 +689,8 @@ def run_config(args, rank, world, local_rank):
     for layer in range(layers):
         if c == "c5":
             cache = shd.SeqShardedKvCache(cfg, batch=1, q_heads=Hq, max_tokens_per_rank=S // world + 2 * R + K + W,
-                                          device=local_rank, keep_exact=False, exchange=args.exchange)
+                                          device=local_rank, keep_exact=False, exchange=args.exchange,
+                                          strict=False)  # timeout status checked after the timed region
             s_ = shd.sequence_shard(S, world, rank)
             kk, vv = synth_kv(1, s_.tokens, Hloc, 7 + layer + 100 * rank, dev)
             torch.cuda.synchronize()
@@ -799,6 +800,9 @@ def run_config(args, rank, world, local_rank):
     if dist:
         td.all_reduce(t, op=td.ReduceOp.MAX)
     ms = float(t.item())
+    if c == "c5":
+        for cache in caches:
+            cache.check_exchange()  # raises if any peer merge timed out
     per_rank_tokens = S // world if c == "c5" else S
     nb = per_rank_tokens // R
     step_bytes = layers * (B * Hloc * nb * BLOCK_BYTES[bits] + B * Hqloc * D * 6)

@@ -87,6 +87,21 @@ int oscar_kv_append(oscar_kv_handle *h, const void *k, const void *v, int64_t n_
 int oscar_kv_decode_step(oscar_kv_handle *h, const void *q, const void *k, const void *v, float *out,
                          float *lse, void *stream);
 
+/* decode_step that also returns StepOutput.logits (pipeline.hpp:54-58,
+ * pipeline.cpp:314-318): logits fp32 [batch, q_heads, S_total] with
+ * S_total = total tokens before the step + 1 (history then the current
+ * token), natural units q.k/sqrt(d) as attend_one writes them
+ * (pipeline.cpp:158-165), computed from the device cache's records.  A
+ * debug/fidelity output: one extra kernel before the attention kernel.
+ * logits may be NULL (== oscar_kv_decode_step). */
+int oscar_kv_decode_step_logits(oscar_kv_handle *h, const void *q, const void *k, const void *v, float *out,
+                                float *lse, float *logits, void *stream);
+
+/* The same logits without attending or appending: over the cache contents,
+ * plus the current token's key k (bf16 [batch, heads, d]) when k is non-NULL.
+ * logits: fp32 [batch, q_heads, total_tokens (+1)]. */
+int oscar_kv_logits(oscar_kv_handle *h, const void *q, const void *k, float *logits, void *stream);
+
 /* decode_step for n independent caches (e.g. the layers of one model step)
  * in ONE host call: element i of every array belongs to handles[i]; lse may
  * be NULL (or contain NULLs).  Same semantics as n oscar_kv_decode_step
@@ -189,7 +204,7 @@ int oscar_kv_attend_publish(oscar_kv_handle *h, const void *q, const void *k, co
 int oscar_peer_publish_empty(const oscar_peer_plan *plan, uint32_t epoch, void *stream);
 /* wait for all ranks' rows of `epoch` in this rank's area, merge -> out
  * fp32 [rows, 128], lse optional; status (device int32, optional) becomes 1
- * and out NaN if a peer does not publish within ~5 s. */
+ * and out / lse NaN if a peer does not publish within ~5 s. */
 int oscar_peer_merge(const oscar_peer_plan *plan, uint32_t epoch, float *out, float *lse, int32_t *status,
                      void *stream);
 /* CUDA IPC plumbing for the receive areas (64-byte handles). */

@@ -1162,13 +1162,9 @@ __global__ void lse_merge_kernel(const float *outs, const float *lses, int64_t p
 template <int BITS, int NCW, bool DEFER>
 cudaError_t launch_d(const AttnArgs &a, cudaStream_t st) {
     using C = AttnCfg<BITS, NCW>;
-    static bool init = false;
-    if (!init) {
-        cudaError_t e = cudaFuncSetAttribute(decode_attn_kernel<BITS, NCW, DEFER>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
-        if (e != cudaSuccess) return e;
-        init = true;
-    }
+    static std::atomic<uint64_t> attr_done{0};
+    if (cudaError_t e = ensure_smem_attr(decode_attn_kernel<BITS, NCW, DEFER>, C::SMEM, attr_done); e != cudaSuccess)
+        return e;
     // programmatic stream serialization: may overlap the previous kernel's tail
     // (the kernel orders its dependent accesses with griddepcontrol.wait)
     cudaLaunchConfig_t cfg = {};
@@ -1188,11 +1184,7 @@ cudaError_t launch_d(const AttnArgs &a, cudaStream_t st) {
 // tail): more than two segments per CTA on average
 template <int BITS, int NCW>
 cudaError_t launch_t(const AttnArgs &a, cudaStream_t st) {
-    static int force = -2;  // OSCAR_DEFER=0|1 overrides the choice (experiments)
-    if (force == -2) {
-        const char *e = getenv("OSCAR_DEFER");
-        force = e ? atoi(e) : -1;
-    }
+    static const long force = env_knob("OSCAR_DEFER", -1);  // OSCAR_DEFER=0|1 overrides the choice (experiments)
     const bool defer = force >= 0 ? force == 1 : (a.nb > 0 && (int64_t)a.BH > 2 * (int64_t)a.ncta);
     return defer ? launch_d<BITS, NCW, true>(a, st) : launch_d<BITS, NCW, false>(a, st);
 }
@@ -1214,24 +1206,13 @@ int attention_grid(int bits, int num_sms, int64_t nb, int BH) {
     return (int)(want < num_sms ? want : num_sms);
 }
 
-int64_t attention_scratch_floats(int max_ctas) {
-    return (int64_t)max_ctas * NCW_MAX * MERGE_FLOATS;  // per segment slot
-}
-
-int attention_max_partials(int64_t nb, int BH, int ncta) {
-    const int64_t total = nb * BH;
-    if (total == 0) return 1;
-    const int64_t per = total / ncta;  // >= 1
-    return (int)(nb / (per > 0 ? per : 1) + 2);
+int64_t attention_scratch_floats(int64_t slots) {
+    return slots * NCW_MAX * MERGE_FLOATS;  // per (CTA, segment) slot: one partial per warp
 }
 
 // warps per CTA: OSCAR_NCW=8|12 overrides the default (tuning knob)
 static int ncw_choice(int bits) {
-    static int env = -1;
-    if (env < 0) {
-        const char *e = getenv("OSCAR_NCW");
-        env = e ? atoi(e) : 0;
-    }
+    static const long env = env_knob("OSCAR_NCW", 0);
     if (env == 8 || env == 12 || env == 16) return env;
     return bits == 4 ? 8 : 12;
 }

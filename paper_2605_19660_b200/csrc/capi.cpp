@@ -118,6 +118,8 @@ struct oscar_kv_handle {
     float *warp_part = nullptr;
     int maxp_alloc = 0;
     int maxseg_alloc = 1;
+    int64_t scratch_slots = 0;  // (CTA, segment) warp-partial slots in warp_part
+    static constexpr int64_t kMaxSegments = 64;  // attention.cu MAXSEG_SMEM
     void *stage = nullptr;  // host-API staging: q, k, v, out, lse
     int64_t device_bytes = 0;
     int last_launches = 0;
@@ -155,6 +157,17 @@ struct oscar_kv_handle {
         cudaFree(status_d);
         cudaFree(warp_part);
         cudaFree(stage);
+    }
+
+    void grow_scratch(int64_t slots, int64_t maxseg) {  // synchronous, rare (shape changes)
+        if (warp_part) {
+            CK(cudaDeviceSynchronize());
+            cudaFree(warp_part);
+            device_bytes -= sizeof(float) * attention_scratch_floats(scratch_slots);
+        }
+        scratch_slots = slots;
+        maxseg_alloc = (int)maxseg;
+        warp_part = (float *)dalloc(sizeof(float) * (size_t)attention_scratch_floats(scratch_slots));
     }
 
     // ---- kernels --------------------------------------------------------------
@@ -284,30 +297,37 @@ struct oscar_kv_handle {
         a.maxseg = maxseg_alloc;
         a.ncta = attention_grid(dbits, num_sms, a.nb, a.BH);
         {
-            static int64_t sc = -1;  // OSCAR_SEG_COST overrides the per-segment split weight (tuning knob)
-            if (sc < 0) {
-                const char *e = getenv("OSCAR_SEG_COST");
-                sc = e ? atoll(e) : 3;
-            }
+            static const int64_t sc = env_knob("OSCAR_SEG_COST", 3);  // per-segment split weight (tuning knob)
             a.seg_cost = sc;
             // the residual-window tiles (one 16-token tile per warp of the tail owner)
             // cost that CTA about half a unit per warp: charge it OSCAR_TAIL_COST units
-            static int64_t tcost = -1;
-            if (tcost < 0) {
-                const char *e = getenv("OSCAR_TAIL_COST");
-                tcost = e ? atoll(e) : 6;
-            }
+            static const int64_t tcost = env_knob("OSCAR_TAIL_COST", 6);
             const int ntok = (int)residual + (kc ? 1 : 0);
             a.tail_cost = ntok > 0 ? tcost : 0;
         }
         a.pdl_prefetch = blocks_written ? 0 : 1;
         a.maxp = maxp_alloc;
-        // exact partial-slot requirement
         if (a.nb > 0) {
             const int64_t nbs = a.nb * (dbits == 0 ? 4 : 1);  // pipeline units per (b, kv head)
-            const int64_t total = nbs * a.BH;
-            (void)total;
-            const Split sp{nbs, a.BH, a.ncta, a.seg_cost, a.tail_cost};
+            // segments (b, kv heads) per CTA range; a CTA holds at most MAX_SEGMENTS of them
+            // (shared-memory ticket table), so large batches of short sequences get a grid
+            // of more CTAs than SMs (they run in waves) instead of being rejected
+            auto max_segments = [&](const Split &sp) {
+                int64_t nseg = 0;
+                for (int64_t c = 0; c < sp.ncta; ++c) {
+                    const int64_t st = sp.begin(c), en = sp.end(c);
+                    if (en > st) nseg = std::max(nseg, (en - 1) / nbs - st / nbs + 1);
+                }
+                return nseg;
+            };
+            Split sp{nbs, a.BH, a.ncta, a.seg_cost, a.tail_cost};
+            int64_t nseg = max_segments(sp);
+            while (nseg > kMaxSegments) {
+                a.ncta = (int)std::min<int64_t>((int64_t)a.BH * nbs, (a.ncta * nseg + kMaxSegments - 9) / (kMaxSegments - 8));
+                sp.ncta = a.ncta;
+                nseg = max_segments(sp);
+            }
+            // exact split-KV partial-slot requirement
             int64_t need = 0;
             for (int64_t bh = 0; bh < a.BH; ++bh)
                 need = std::max(need, sp.cta_of((bh + 1) * nbs - 1) - sp.cta_of(bh * nbs) + 1);
@@ -323,36 +343,47 @@ struct oscar_kv_handle {
                 a.part_ml = part_ml;
                 a.maxp = maxp_alloc;
             }
-            // segments per CTA range (units: nb blocks x SUB quarters for bf16)
-            const int64_t sub = dbits == 0 ? 4 : 1, nbu = a.nb * sub, totu = nbu * a.BH;
-            int64_t nseg = 0;
-            (void)totu;
-            for (int64_t c = 0; c < a.ncta; ++c) {
-                const int64_t st = sp.begin(c), en = sp.end(c);
-                if (en > st) nseg = std::max(nseg, (en - 1) / nbu - st / nbu + 1);
-            }
-            if (nseg > 64) throw InvalidArg("attention: more than 64 (sequence, kv head) segments per CTA");
-            if (nseg > maxseg_alloc) {  // rare (few long CTA ranges over short sequences): grow the scratch
-                CK(cudaDeviceSynchronize());
-                cudaFree(warp_part);
-                device_bytes -= sizeof(float) * attention_scratch_floats(
-                                                    (int)std::max<int64_t>((int64_t)num_sms * maxseg_alloc, BH));
-                maxseg_alloc = (int)nseg;
-                warp_part = (float *)dalloc(sizeof(float) * (size_t)attention_scratch_floats(
-                                                                (int)std::max<int64_t>((int64_t)num_sms * maxseg_alloc, BH)));
-                a.warp_part = warp_part;
-                a.maxseg = maxseg_alloc;
-            }
+            // per-(CTA, segment) warp-partial scratch: the kernel indexes slot cta * maxseg + k
+            const int64_t maxseg = std::max<int64_t>(nseg, maxseg_alloc);
+            if (nseg > maxseg_alloc || (int64_t)a.ncta * maxseg > scratch_slots)
+                grow_scratch(std::max<int64_t>((int64_t)a.ncta * maxseg, scratch_slots), maxseg);
+            a.warp_part = warp_part;
+            a.maxseg = maxseg_alloc;
         } else {
-            a.maxseg = 1;  // residual-only mode: one segment per CTA
+            a.maxseg = 1;  // residual-only mode: one segment per CTA (ncta = BH <= scratch slots)
         }
         return a;
     }
 
+    // StepOutput.logits over the cache contents (+ the current token when k is given)
+    void logits(const void *q, const void *k, float *out, cudaStream_t s) {
+        LogitsArgs a{};
+        a.blocks = blocks;
+        a.max_blocks = max_blocks;
+        a.block_bytes = block_bytes;
+        a.nb = packed / R;
+        a.BH = (int)BH;
+        a.Hkv = (int)cfg.heads;
+        a.g = (int)g;
+        a.Hq = (int)Hq;
+        a.q = q;
+        a.kcur = k;
+        a.ring_k = ring_k;
+        a.r = (int)residual;
+        a.rotates = dbits != 0 && rotates(cfg);
+        a.logits = out;
+        a.s_total = packed + residual + (k ? 1 : 0);
+        CK(launch_logits(dbits, a, s));
+        ++last_launches;
+    }
+
     void decode_step(const void *q, const void *k, const void *v, float *out, float *lse, cudaStream_t s,
-                     const PeerPlan *pub = nullptr, uint32_t epoch = 0) {
+                     const PeerPlan *pub = nullptr, uint32_t epoch = 0, float *logits_out = nullptr) {
         if (packed + residual + 1 > max_tokens) throw InvalidArg("decode_step: cache capacity exceeded");
         last_launches = 0;
+        // the logits read the window and the records before the attention kernel
+        // writes the current token into the ring and before any flush
+        if (logits_out) logits(q, k, logits_out, s);
         AttnArgs a = attn_args(q, k, v, out, lse);
         if (pub) {
             a.pub = *pub;
@@ -380,15 +411,16 @@ struct oscar_kv_handle {
             a.pub_epoch = epoch;
         }
         // debug: OSCAR_PROF=1 prints per-phase cycles averaged over warps (synchronises)
-        static int prof = -1;
-        if (prof < 0) {
-            prof = getenv("OSCAR_PROF") ? 1 : 0;
+        static const int prof = [] {
+            const int p = getenv("OSCAR_PROF") ? 1 : 0;
 #if !OSK_PROF
-            if (prof) std::fprintf(stderr, "OSCAR_PROF: counters need the profiling build (make PROF=1, "
-                                           "OSCAR_LIB=.../liboscar_b200_prof.so); ignored\n");
-            prof = 0;
+            if (p) std::fprintf(stderr, "OSCAR_PROF: counters need the profiling build (make PROF=1, "
+                                        "OSCAR_LIB=.../liboscar_b200_prof.so); ignored\n");
+            return 0;
+#else
+            return p;
 #endif
-        }
+        }();
         unsigned long long *pbuf = nullptr;
         const int nw = a.ncta * 16;
         if (prof) {
@@ -797,14 +829,11 @@ void load_kvc1(oscar_kv_handle *h, int64_t b, const char *path) {
         throw InvalidArg("cache load: key and value streams differ in length");
     if (packed % R || r < 0 || r >= R) throw InvalidArg("cache load: inconsistent token counts");
     if (packed + r > h->max_tokens) throw InvalidArg("cache load: cache capacity exceeded");
-    if (!h->prefilled) {
-        h->packed = packed;
-        h->residual = r;
-        h->flushes = flushes;
-        h->prefilled = m.flag("k_prefilled");
-    } else if (h->packed != packed || h->residual != r) {
+    // nothing of the handle changes until every section is parsed, converted and
+    // uploaded: a failed load leaves the handle (counters and device state) as it was
+    const bool adopt = !h->prefilled;
+    if (!adopt && (h->packed != packed || h->residual != r))
         throw InvalidArg("cache load: sequences of one handle must hold the same number of tokens");
-    }
     if (h->dbits && !h->keep_exact) throw InvalidArg("cache load: handle created without keep_exact");
     const int64_t H = c.heads, nb = packed / R;
     const int bits = h->dbits;
@@ -851,20 +880,21 @@ void load_kvc1(oscar_kv_handle *h, int64_t b, const char *path) {
         for (int64_t k = 0; k < nb; ++k) vb[hh].push_back(read_block(vp));
     const auto vres = read_vec<double>(f, r * H * D);
 
-    CK(cudaSetDevice(h->device));
-    if (h->last_stream) CK(cudaStreamSynchronize(h->last_stream));
-    std::vector<uint8_t> rec(h->block_bytes);
-    std::vector<double> sh(SHADOW_DOUBLES);
+    // (1) convert everything on the host (may throw: inconsistent params, codes
+    //     out of range, rows that are not transforms of bf16 inputs)
+    std::vector<uint8_t> recs((size_t)(H * nb * h->block_bytes), 0);
+    std::vector<double> shadows(bits ? (size_t)(H * nb * SHADOW_DOUBLES) : 0);
+    std::vector<uint16_t> rings_k(r > 0 ? (size_t)(H * R * D) : 0, 0), rings_v(r > 0 ? (size_t)(H * R * D) : 0, 0);
     for (int64_t hh = 0; hh < H; ++hh) {
-        const int64_t bh = b * H + hh;
         for (int64_t k = 0; k < nb; ++k) {
             const Blk &K = kb[hh][k], &V = vb[hh][k];
-            std::fill(rec.begin(), rec.end(), 0);
+            uint8_t *rec_p = recs.data() + (size_t)((hh * nb + k) * h->block_bytes);
+            double *sh = bits ? shadows.data() + (size_t)((hh * nb + k) * SHADOW_DOUBLES) : nullptr;
             if (bits) {
                 const int tpw = 16 / bits;
                 const int64_t code_bytes = (int64_t)R * D * bits / 8;
-                uint32_t *kw = reinterpret_cast<uint32_t *>(rec.data());
-                uint32_t *vw = reinterpret_cast<uint32_t *>(rec.data() + code_bytes);
+                uint32_t *kw = reinterpret_cast<uint32_t *>(rec_p);
+                uint32_t *vw = reinterpret_cast<uint32_t *>(rec_p + code_bytes);
                 const uint32_t maxc = (1u << bits) - 1;
                 for (int w = 0; w < (int)(code_bytes / 4); ++w)
                     for (int hi = 0; hi < 2; ++hi)
@@ -884,11 +914,11 @@ void load_kvc1(oscar_kv_handle *h, int64_t b, const char *path) {
                 const int va_off = bits == 2 ? Block<2>::VA_OFF : Block<4>::VA_OFF;
                 const int vb_off = bits == 2 ? Block<2>::VB_OFF : Block<4>::VB_OFF;
                 const int nr_off = bits == 2 ? Block<2>::NORM_OFF : Block<4>::NORM_OFF;
-                uint16_t *pka = reinterpret_cast<uint16_t *>(rec.data() + ka_off);
-                uint16_t *pkb = reinterpret_cast<uint16_t *>(rec.data() + kb_off);
-                uint16_t *pva = reinterpret_cast<uint16_t *>(rec.data() + va_off);
-                uint16_t *pvb = reinterpret_cast<uint16_t *>(rec.data() + vb_off);
-                float *pn = reinterpret_cast<float *>(rec.data() + nr_off);
+                uint16_t *pka = reinterpret_cast<uint16_t *>(rec_p + ka_off);
+                uint16_t *pkb = reinterpret_cast<uint16_t *>(rec_p + kb_off);
+                uint16_t *pva = reinterpret_cast<uint16_t *>(rec_p + va_off);
+                uint16_t *pvb = reinterpret_cast<uint16_t *>(rec_p + vb_off);
+                float *pn = reinterpret_cast<float *>(rec_p + nr_off);
                 // affine16 (quantize.cu): a = delta, b = delta * -zp; constant group a = 0, b = lo
                 auto affine = [&](double dl, int64_t zp, double cst, uint16_t &a, uint16_t &bb) {
                     if (dl == 0.0) {
@@ -918,8 +948,6 @@ void load_kvc1(oscar_kv_handle *h, int64_t b, const char *path) {
                     pn[norm_index(t)] = (float)(s * 0.12751743074202186);  // log2(e)/sqrt(d), as quantize.cu
                     sh[SHADOW_K_DOUBLES + SHADOW_V_DOUBLES + t] = s;
                 }
-                CK(cudaMemcpy(h->shadow + (bh * h->max_blocks + k) * SHADOW_DOUBLES, sh.data(),
-                              sizeof(double) * SHADOW_DOUBLES, cudaMemcpyHostToDevice));
             } else {
                 // raw block: transformed rows -> raw bf16 rows -> fragment order
                 std::vector<uint16_t> kraw(R * D), vraw(R * D);
@@ -929,7 +957,7 @@ void load_kvc1(oscar_kv_handle *h, int64_t b, const char *path) {
                 }
                 constexpr int QW = BF16_QUARTER_BYTES / 8;
                 for (int qu = 0; qu < 4; ++qu) {
-                    uint32_t *qw = reinterpret_cast<uint32_t *>(rec.data() + qu * BF16_QUARTER_BYTES);
+                    uint32_t *qw = reinterpret_cast<uint32_t *>(rec_p + qu * BF16_QUARTER_BYTES);
                     for (int w = 0; w < QW; ++w)
                         for (int hi = 0; hi < 2; ++hi) {
                             int t, ch;
@@ -940,22 +968,44 @@ void load_kvc1(oscar_kv_handle *h, int64_t b, const char *path) {
                         }
                 }
             }
-            CK(cudaMemcpy(h->blocks + (bh * h->max_blocks + k) * h->block_bytes, rec.data(), h->block_bytes,
-                          cudaMemcpyHostToDevice));
         }
         // residual window -> raw bf16 rings (K token-major, V channel-major)
         if (r > 0) {
-            std::vector<uint16_t> rk((size_t)R * D, 0), rv((size_t)R * D, 0), row(D);
+            uint16_t *rk = rings_k.data() + (size_t)(hh * R * D), *rv = rings_v.data() + (size_t)(hh * R * D);
+            std::vector<uint16_t> row(D);
             for (int64_t t = 0; t < r; ++t) {
                 raw_key_row(&kres[(t * H + hh) * D], kres_n[t * H + hh], tc, c.scaling, &rk[t * D]);
                 raw_value_row(&vres[(t * H + hh) * D], c.rotate_v, row.data());
                 for (int ch = 0; ch < D; ++ch) rv[(size_t)ch * R + t] = row[ch];
             }
-            CK(cudaMemcpy(reinterpret_cast<uint16_t *>(h->ring_k) + bh * R * D, rk.data(), sizeof(uint16_t) * R * D,
-                          cudaMemcpyHostToDevice));
-            CK(cudaMemcpy(reinterpret_cast<uint16_t *>(h->ring_v) + bh * R * D, rv.data(), sizeof(uint16_t) * R * D,
-                          cudaMemcpyHostToDevice));
         }
+    }
+    // (2) upload (only CUDA errors can fail from here on)
+    CK(cudaSetDevice(h->device));
+    if (h->last_stream) CK(cudaStreamSynchronize(h->last_stream));
+    for (int64_t hh = 0; hh < H; ++hh) {
+        const int64_t bh = b * H + hh;
+        if (nb > 0) {
+            CK(cudaMemcpy(h->blocks + bh * h->max_blocks * h->block_bytes, recs.data() + (size_t)(hh * nb * h->block_bytes),
+                          (size_t)(nb * h->block_bytes), cudaMemcpyHostToDevice));
+            if (bits)
+                CK(cudaMemcpy(h->shadow + bh * h->max_blocks * SHADOW_DOUBLES,
+                              shadows.data() + (size_t)(hh * nb * SHADOW_DOUBLES),
+                              sizeof(double) * (size_t)(nb * SHADOW_DOUBLES), cudaMemcpyHostToDevice));
+        }
+        if (r > 0) {
+            CK(cudaMemcpy(reinterpret_cast<uint16_t *>(h->ring_k) + bh * R * D, rings_k.data() + (size_t)(hh * R * D),
+                          sizeof(uint16_t) * R * D, cudaMemcpyHostToDevice));
+            CK(cudaMemcpy(reinterpret_cast<uint16_t *>(h->ring_v) + bh * R * D, rings_v.data() + (size_t)(hh * R * D),
+                          sizeof(uint16_t) * R * D, cudaMemcpyHostToDevice));
+        }
+    }
+    // (3) commit the token counters (kv_cache.cpp:540-548)
+    if (adopt) {
+        h->packed = packed;
+        h->residual = r;
+        h->flushes = flushes;
+        h->prefilled = m.flag("k_prefilled");
     }
     h->blocks_written = true;  // the next attention launch waits before touching the records
 }
@@ -1009,11 +1059,12 @@ int oscar_kv_create(const oscar_kv_config *cfg, int64_t batch, int64_t q_heads, 
         CK(cudaMemset(h->counters, 0, sizeof(int) * (size_t)h->BH));
         h->status_d = (int *)h->dalloc(sizeof(int));
         CK(cudaMemset(h->status_d, 0, sizeof(int)));
-        // segments (b, kv heads) one CTA range can touch: <= BH/ncta + 2 (nb >= 1 unit)
-        h->maxseg_alloc = (int)std::min<int64_t>(64, h->BH / h->num_sms + 2);
-        h->warp_part = (float *)h->dalloc(
-            sizeof(float) * (size_t)attention_scratch_floats(
-                                (int)std::max<int64_t>((int64_t)h->num_sms * h->maxseg_alloc, h->BH)));
+        // segments (b, kv heads) one CTA range can touch: <= BH/ncta + 2 (nb >= 1 unit);
+        // residual-only launches use BH CTAs of one segment each
+        {
+            const int64_t maxseg = std::min<int64_t>(oscar_kv_handle::kMaxSegments, h->BH / h->num_sms + 2);
+            h->grow_scratch(std::max<int64_t>((int64_t)h->num_sms * maxseg, h->BH), maxseg);
+        }
         const size_t stage_bytes = (size_t)(h->B * h->Hq * D * 2 + 2 * h->BH * D * 2 + h->B * h->Hq * D * 4 +
                                             h->B * h->Hq * 4 + 256);
         h->stage = h->dalloc(stage_bytes);
@@ -1042,6 +1093,26 @@ int oscar_kv_decode_step(oscar_kv_handle *h, const void *q, const void *k, const
         CK(cudaSetDevice(h->device));
         h->last_stream = (cudaStream_t)stream;
         h->decode_step(q, k, v, out, lse, (cudaStream_t)stream);
+    });
+}
+
+int oscar_kv_decode_step_logits(oscar_kv_handle *h, const void *q, const void *k, const void *v, float *out,
+                                float *lse, float *logits, void *stream) {
+    return guard([&] {
+        if (!h || !q || !k || !v || !out) throw InvalidArg("decode_step: null argument");
+        CK(cudaSetDevice(h->device));
+        h->last_stream = (cudaStream_t)stream;
+        h->decode_step(q, k, v, out, lse, (cudaStream_t)stream, nullptr, 0, logits);
+    });
+}
+
+int oscar_kv_logits(oscar_kv_handle *h, const void *q, const void *k, float *logits, void *stream) {
+    return guard([&] {
+        if (!h || !q || !logits) throw InvalidArg("logits: null argument");
+        CK(cudaSetDevice(h->device));
+        h->last_stream = (cudaStream_t)stream;
+        h->last_launches = 0;
+        h->logits(q, k, logits, (cudaStream_t)stream);
     });
 }
 

@@ -3,8 +3,35 @@
 #pragma once
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdlib.h>
+
+#include <atomic>
 
 namespace osk {
+
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per (kernel, device):
+// function attributes live in the device's context, so a process driving
+// several GPUs (one handle per device) must set them on each.  `done` is a
+// per-kernel bit set of devices; concurrent first calls both set the
+// attribute, which is idempotent.
+template <typename Kernel>
+inline cudaError_t ensure_smem_attr(Kernel kernel, int bytes, std::atomic<uint64_t> &done) {
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    const uint64_t bit = dev < 64 ? (uint64_t{1} << dev) : 0;
+    if (bit && (done.load(std::memory_order_acquire) & bit)) return cudaSuccess;
+    e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    if (e == cudaSuccess && bit) done.fetch_or(bit, std::memory_order_acq_rel);
+    return e;
+}
+
+// integer tuning knob from the environment, read once (thread-safe static init
+// at the call site: `static const long v = env_knob("X", dflt);`)
+inline long env_knob(const char *name, long dflt) {
+    const char *e = getenv(name);
+    return e ? atol(e) : dflt;
+}
 
 struct TransformCfg {
     int bits;       // 0, 2, 4 (0 => raw bf16 block, no transform)
@@ -103,10 +130,25 @@ struct AttnArgs {
 };
 // bits: 2, 4 or 0 (bf16 baseline)
 cudaError_t launch_attention(int bits, const AttnArgs &a, cudaStream_t st);
-int attention_max_partials(int64_t nb, int BH, int ncta);
-int64_t attention_scratch_floats(int max_ctas);  // floats per segment slot set
-int attention_max_segments(int64_t nb_units, int BH, int ncta);
+int64_t attention_scratch_floats(int64_t slots);  // floats of `slots` (CTA, segment) warp-partial slots
 int attention_grid(int bits, int num_sms, int64_t nb, int BH);
+
+// logits.cu: StepOutput.logits (pipeline.hpp:54-58) from the device records:
+// fp32 [B][Hq][s_total], natural units, packed tokens then window then current
+struct LogitsArgs {
+    const uint8_t *blocks;
+    int64_t max_blocks, block_bytes;
+    int64_t nb;               // packed blocks per (b, kv head)
+    int BH, Hkv, g, Hq;
+    const void *q;            // bf16 [B][Hq][D]
+    const void *kcur;         // bf16 [B][Hkv][D] or null
+    const void *ring_k;       // K ring [bh][R][D]
+    int r;                    // window tokens
+    int rotates;              // rotate q for the packed tokens
+    float *logits;
+    int64_t s_total;          // nb*R + r + (kcur ? 1 : 0)
+};
+cudaError_t launch_logits(int bits, const LogitsArgs &a, cudaStream_t st);
 
 // peer.cu: wait for every rank's row of this epoch in recv[rank], merge -> out/lse;
 // status (optional, device int) is set to 1 if a peer did not publish within ~5 s

@@ -137,6 +137,41 @@ OSK_HD void v_word_coords(int BITS, int w, int f, int hi, int &token, int &chann
     token = 16 * j + 2 * tq + (hi ? 1 : 0) + ((fam & 2) ? 8 : 0);
 }
 
+// ---- inverse maps (element -> word, bit shift), for per-element readers --------
+// K code of (token t, channel c): inverse of k_word_coords
+OSK_HD void k_code_loc(int BITS, int t, int c, int &word, int &shift) {
+    const int tpw = 16 / BITS, wpf = 8 / tpw;
+    const int i = t >> 4, row = t & 15, s = c >> 4, kc = c & 15;
+    const int tq = (kc & 7) >> 1, hi = kc & 1;
+    const int fam = (row >= 8 ? 1 : 0) + (kc >= 8 ? 2 : 0);
+    const int lane = (row & 7) * 4 + tq;
+    const int half = i / tpw, f = i % tpw;
+    word = ((s * 32 + lane) * 4 + fam) * wpf + half;
+    shift = hi * 16 + f * BITS;
+}
+// V code of (token t, channel c): inverse of v_word_coords
+OSK_HD void v_code_loc(int BITS, int t, int c, int &word, int &shift) {
+    const int tpw = 16 / BITS, wpf = 8 / tpw;
+    const int m = c >> 4, row = c & 15, j = t >> 4, r = t & 15;
+    const int tq = (r & 7) >> 1, hi = r & 1;
+    const int fam = (row >= 8 ? 1 : 0) + (r >= 8 ? 2 : 0);
+    const int lane = (row & 7) * 4 + tq;
+    const int half = m / tpw, f = m % tpw;
+    word = ((j * 32 + lane) * 4 + fam) * wpf + half;
+    shift = hi * 16 + f * BITS;
+}
+// raw bf16 K of (token t in 0..R-1, channel c) in a bf16 record: byte offset of
+// the 16-bit value (inverse of bf16_k_coords over the four quarters)
+OSK_HD int bf16_k_byte(int t, int c) {
+    const int qu = t >> 5, tt = t & 31;
+    const int i = tt >> 4, row = tt & 15, s = c >> 4, kc = c & 15;
+    const int tq = (kc & 7) >> 1, hi = kc & 1;
+    const int reg = (row >= 8 ? 1 : 0) + (kc >= 8 ? 2 : 0);
+    const int lane = (row & 7) * 4 + tq;
+    const int w = ((i * 8 + s) * 32 + lane) * 4 + reg;
+    return qu * BF16_QUARTER_BYTES + w * 4 + hi * 2;
+}
+
 // ---- params ----------------------------------------------------------------
 // channel c = 16s + kc; slot of kc within the lane's 4 B-fragment channels
 OSK_HD void k_chan_split(int c, int &s, int &tq, int &slot) {

@@ -47,6 +47,7 @@ __global__ void peer_merge_kernel(const PeerPlan p, uint32_t epoch, float *out, 
         if (lane == 0 && status) atomicExch(status, 1);
         reinterpret_cast<float4 *>(out + row * 128)[lane] = make_float4(CUDART_NAN_F, CUDART_NAN_F, CUDART_NAN_F,
                                                                           CUDART_NAN_F);
+        if (lse_out && lane == 0) lse_out[row] = CUDART_NAN_F;
         return;
     }
     __syncwarp();  // memory ordering: the acquires above happen before every lane's reads below

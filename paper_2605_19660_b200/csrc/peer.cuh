@@ -6,9 +6,8 @@
 // the rows.  Replaces the NCCL all-gather + lse_merge of the baseline path.
 //
 // Memory ordering: every lane stores its 16 B of the row and fences at system
-// scope, the warp synchronises, and one lane stores the flags (relaxed, system
-// scope: the fences already ordered the rows before them); the reader acquires
-// the flag (system scope) before reading.
+// scope, the warp synchronises, and one lane stores the flags with
+// st.release.sys; the reader acquires the flag (system scope) before reading.
 // Double-buffered by epoch parity: a rank cannot publish epoch e+2 before
 // every rank has merged epoch e (its own merge of e+1 needs their e+1 rows,
 // published after their merge of e), so parity slots are never overwritten
@@ -20,8 +19,8 @@
 
 namespace osk {
 
-__device__ __forceinline__ void st_relaxed_sys_u32(uint32_t *p, uint32_t v) {
-    asm volatile("st.relaxed.sys.global.u32 [%0], %1;\n" ::"l"(p), "r"(v) : "memory");
+__device__ __forceinline__ void st_release_sys_u32(uint32_t *p, uint32_t v) {
+    asm volatile("st.release.sys.global.u32 [%0], %1;\n" ::"l"(p), "r"(v) : "memory");
 }
 __device__ __forceinline__ uint32_t ld_acquire_sys_u32(const uint32_t *p) {
     uint32_t v;
@@ -44,9 +43,10 @@ __device__ __forceinline__ void peer_publish_row(const PeerPlan &p, uint32_t epo
         if (lane == 0) base[128] = lse;
     }
     __threadfence_system();  // each lane's row stores are performed before ...
-    __syncwarp();            // ... the warp reconverges and lane 0 raises the flags
+    __syncwarp();            // ... the warp reconverges and lane 0 raises the flags with release
+                             // semantics (cumulative over the stores ordered before the barrier)
     if (lane == 0)
-        for (int dst = 0; dst < p.world; ++dst) st_relaxed_sys_u32(p.flags[dst] + slot, epoch);
+        for (int dst = 0; dst < p.world; ++dst) st_release_sys_u32(p.flags[dst] + slot, epoch);
 }
 
 }  // namespace osk

@@ -468,13 +468,8 @@ __global__ void ring_copy_kernel(const RingCopyArgs a) {
 template <int BITS, int GPAR>
 cudaError_t launch_q(const QuantizeArgs &a, dim3 grid, cudaStream_t st) {
     const int smem = GPAR * 32 * KU_ROW * 8 + 2 * R * CODE_STRIDE + Block<BITS>::BYTES - Block<BITS>::KA_OFF;
-    static bool init = false;
-    if (!init) {
-        cudaError_t e = cudaFuncSetAttribute(quantize_kernel<BITS, GPAR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             smem);
-        if (e != cudaSuccess) return e;
-        init = true;
-    }
+    static std::atomic<uint64_t> attr_done{0};
+    if (cudaError_t e = ensure_smem_attr(quantize_kernel<BITS, GPAR>, smem, attr_done); e != cudaSuccess) return e;
     quantize_kernel<BITS, GPAR><<<grid, QT * GPAR, smem, st>>>(a);
     return cudaGetLastError();
 }
@@ -483,11 +478,9 @@ cudaError_t launch_quantize(const QuantizeArgs &a, cudaStream_t st) {
     if (a.n_blocks <= 0) return cudaSuccess;
     dim3 grid((unsigned)a.n_blocks, (unsigned)(a.B * a.H));
     if (a.tc.bits == 0) {
-        static bool init0 = false;
-        if (!init0) {
-            cudaFuncSetAttribute(raw_block_kernel_dyn, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * R * D * 2);
-            init0 = true;
-        }
+        static std::atomic<uint64_t> attr_done{0};
+        if (cudaError_t e = ensure_smem_attr(raw_block_kernel_dyn, 2 * R * D * 2, attr_done); e != cudaSuccess)
+            return e;
         raw_block_kernel_dyn<<<grid, QT, 2 * R * D * 2, st>>>(a);
         return cudaGetLastError();
     }

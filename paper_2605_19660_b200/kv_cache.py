@@ -164,6 +164,38 @@ def _ptr(t) -> int:
     return t.data_ptr()
 
 
+def _dev_of(t, name: str) -> int:
+    import torch
+
+    if not isinstance(t, torch.Tensor) or not t.is_cuda:
+        raise ValueError(f"{name}: expected a CUDA tensor, got {type(t).__name__}")
+    return t.device.index
+
+
+def _need(t, name: str, device: int, dtype: str, shape=None, numel=None):
+    """The C-ABI takes raw device pointers and cannot check what they point to:
+    verify device, dtype, contiguity and shape here (a wrong batch or head
+    count would read/write out of bounds on the device; a strided view would
+    silently build a wrong cache)."""
+    import torch
+
+    if t is None:
+        raise ValueError(f"{name}: tensor required")
+    if not isinstance(t, torch.Tensor) or not t.is_cuda or t.device.index != device:
+        raise ValueError(f"{name}: expected a CUDA tensor on cuda:{device}, got "
+                         f"{getattr(t, 'device', type(t).__name__)}")
+    want = {"bf16": torch.bfloat16, "f32": torch.float32}[dtype]
+    if t.dtype != want:
+        raise ValueError(f"{name}: expected {want}, got {t.dtype}")
+    if not t.is_contiguous():
+        raise ValueError(f"{name}: tensor must be contiguous (pass .contiguous())")
+    if shape is not None and tuple(t.shape) != tuple(shape):
+        raise ValueError(f"{name}: expected shape {tuple(shape)}, got {tuple(t.shape)}")
+    if numel is not None and t.numel() != numel:
+        raise ValueError(f"{name}: expected {numel} elements, got {t.numel()}")
+    return t
+
+
 def _stream(stream):
     if stream is None:
         import torch
@@ -201,6 +233,10 @@ class KvCache:
         """k, v: bf16 CUDA tensors [B, S, H, d] (raw keys; values pre-rotated
         unless cfg.rotate_v)."""
         n = 0 if k is None else k.shape[1]
+        if n > 0:
+            shp = (self.B, n, self.H, D)
+            _need(k, "buffer_quant k", self.device, "bf16", shp)
+            _need(v, "buffer_quant v", self.device, "bf16", shp)
         _check(lib().oscar_kv_append(self._h, _ptr(k), _ptr(v), n, _stream(stream)))
 
     append = buffer_quant
@@ -209,11 +245,24 @@ class KvCache:
     def decode_step(self, q, k, v, out=None, lse=None, stream=None):
         import torch
 
+        self._check_step(q, k, v)
         if out is None:
             out = torch.empty((self.B, self.Hq, D), dtype=torch.float32, device=q.device)
+        self._check_out(out, lse)
         _check(lib().oscar_kv_decode_step(self._h, _ptr(q), _ptr(k), _ptr(v), _ptr(out), _ptr(lse),
                                           _stream(stream)))
         return out
+
+    def _check_step(self, q, k=None, v=None):
+        _need(q, "q", self.device, "bf16", (self.B, self.Hq, D))
+        if k is not None or v is not None:
+            _need(k, "k", self.device, "bf16", (self.B, self.H, D))
+            _need(v, "v", self.device, "bf16", (self.B, self.H, D))
+
+    def _check_out(self, out, lse):
+        _need(out, "out", self.device, "f32", numel=self.B * self.Hq * D)
+        if lse is not None:
+            _need(lse, "lse", self.device, "f32", numel=self.B * self.Hq)
 
     def attend(self, q, out=None, lse=None, stream=None):
         import torch
@@ -222,12 +271,15 @@ class KvCache:
             out = torch.empty((self.B, self.Hq, D), dtype=torch.float32, device=q.device)
         if lse is None:
             lse = torch.empty((self.B, self.Hq), dtype=torch.float32, device=q.device)
+        self._check_step(q)
+        self._check_out(out, lse)
         _check(lib().oscar_kv_attend(self._h, _ptr(q), _ptr(out), _ptr(lse), _stream(stream)))
         return out, lse
 
     def attend_publish(self, q, plan: "PeerPlan", epoch: int, k=None, v=None, stream=None):
         """attend (k = v = None) or decode_step whose rows are published to every
         rank of `plan` (fused sequence-shard exchange) instead of returned."""
+        self._check_step(q, k, v)
         _check(lib().oscar_kv_attend_publish(self._h, _ptr(q), _ptr(k), _ptr(v), ctypes.byref(plan.c), epoch,
                                              _stream(stream)))
 
@@ -330,6 +382,11 @@ class DecodeBatch:
 
     def __init__(self, caches, qs, ks, vs, outs, lses=None):
         n = len(caches)
+        if not all(len(x) == n for x in (qs, ks, vs, outs)) or (lses is not None and len(lses) != n):
+            raise ValueError("DecodeBatch: one q/k/v/out (and lse) per cache")
+        for i, c in enumerate(caches):
+            c._check_step(qs[i], ks[i], vs[i])
+            c._check_out(outs[i], None if lses is None else lses[i])
         arr = ctypes.c_void_p * n
         self.n = n
         self._keep = (caches, qs, ks, vs, outs, lses)
@@ -349,7 +406,14 @@ def lse_merge(outs, lses, out=None, lse_out=None, stream=None):
     """Merge P partial attentions: outs [P, rows, d], lses [P, rows] (device)."""
     import torch
 
+    dev = _dev_of(outs, "outs")
     P, rows, d = outs.shape
+    _need(outs, "outs", dev, "f32")
+    _need(lses, "lses", dev, "f32", (P, rows))
+    if out is not None:
+        _need(out, "out", dev, "f32", numel=rows * d)
+    if lse_out is not None:
+        _need(lse_out, "lse_out", dev, "f32", numel=rows)
     if out is None:
         out = torch.empty((rows, d), dtype=torch.float32, device=outs.device)
     _check(lib().oscar_lse_merge(_ptr(outs), _ptr(lses), P, rows, d, _ptr(out), _ptr(lse_out), _stream(stream)))
@@ -385,7 +449,18 @@ def peer_publish_empty(plan: PeerPlan, epoch: int, stream=None):
 
 
 def peer_merge(plan: PeerPlan, epoch: int, out, lse=None, status=None, stream=None):
-    """Wait for every rank's rows of `epoch` and merge -> out [rows, 128] (device)."""
+    """Wait for every rank's rows of `epoch` and merge -> out [rows, 128] (device).
+    status: optional device int32 tensor, set to 1 (and the rows to NaN) if a
+    peer does not publish within ~5 s."""
+    dev = _dev_of(out, "out")
+    _need(out, "out", dev, "f32", numel=plan.rows * D)
+    if lse is not None:
+        _need(lse, "lse", dev, "f32", numel=plan.rows)
+    if status is not None:
+        import torch
+
+        if status.dtype != torch.int32 or not status.is_cuda:
+            raise ValueError("status: expected a CUDA int32 tensor")
     _check(lib().oscar_peer_merge(ctypes.byref(plan.c), epoch, _ptr(out), _ptr(lse), _ptr(status),
                                   _stream(stream)))
     return out

@@ -26,6 +26,7 @@ with the oracle).
 """
 from __future__ import annotations
 
+import contextlib
 from dataclasses import dataclass
 
 R = 128
@@ -192,10 +193,12 @@ class SeqShardedKvCache:
     """
 
     def __init__(self, cfg, batch: int, q_heads: int, max_tokens_per_rank: int, device: int = 0,
-                 keep_exact: bool = True, group=None, merge=None, exchange: str = "nccl"):
+                 keep_exact: bool = True, group=None, merge=None, exchange: str = "nccl", strict: bool = True):
         """exchange: "nccl" (all-gather of the packed partials + lse_merge) or
         "p2p" (the attention kernel publishes its rows into every rank's
-        receive area over peer memory; one merge kernel per rank)."""
+        receive area over peer memory; one merge kernel per rank).
+        strict (p2p): check the merge's timeout status after every step (one
+        host sync per step); with strict=False call check_exchange() yourself."""
         from .kv_cache import KvCache, lse_merge
 
         td = _dist()
@@ -211,6 +214,22 @@ class SeqShardedKvCache:
             raise ValueError(f"exchange must be 'nccl' or 'p2p', not {exchange!r}")
         self.exchange = exchange
         self.peers = PeerExchange(batch * q_heads, device, group) if exchange == "p2p" and self.world > 1 else None
+        self.strict = strict
+        self._status = None
+        self._ext = {}
+
+    def _on(self, stream):
+        """Run torch ops (gather, merge, fills) on the caller's stream, so they
+        are ordered after the attention kernel launched there (and the reused
+        result buffers are stream-ordered across steps)."""
+        import torch
+
+        if stream is None:
+            return contextlib.nullcontext()
+        s = self._ext.get(stream)
+        if s is None:
+            s = self._ext[stream] = torch.cuda.ExternalStream(stream, device=torch.device("cuda", self.cache.device))
+        return torch.cuda.stream(s)
 
     def prefill(self, k, v, S: int | None = None, sliced: bool = False, stream=None):
         S = k.shape[1] if S is None else S
@@ -240,15 +259,16 @@ class SeqShardedKvCache:
         return out, lse
 
     def decode_step(self, q, k, v, stream=None):
-        if self.peers is not None:
-            return self._decode_step_p2p(q, k, v, stream)
-        o, l = self.local_partial(q, k, v, stream=stream)
-        if self.world == 1:  # the only shard: its partial is the normalised result
-            return o.reshape(self.B, self.Hq, D)
-        outs, lses = gather_partials(o, l, self.group)
-        return self._merge(outs, lses).reshape(self.B, self.Hq, D)
+        with self._on(stream):  # every launch and torch op below on one stream
+            if self.peers is not None:
+                return self._decode_step_p2p(q, k, v)
+            o, l = self.local_partial(q, k, v)
+            if self.world == 1:  # the only shard: its partial is the normalised result
+                return o.reshape(self.B, self.Hq, D)
+            outs, lses = gather_partials(o, l, self.group)
+            return self._merge(outs, lses).reshape(self.B, self.Hq, D)
 
-    def _decode_step_p2p(self, q, k, v, stream=None):
+    def _decode_step_p2p(self, q, k, v):
         import torch
 
         from . import kv_cache as kc
@@ -256,15 +276,25 @@ class SeqShardedKvCache:
         px = self.peers
         px.epoch += 1
         if self.shard is not None and self.shard.tail and k is not None:
-            self.cache.attend_publish(q, px.plan, px.epoch, k, v, stream=stream)
+            self.cache.attend_publish(q, px.plan, px.epoch, k, v)
         elif self.cache.total_tokens > 0:
-            self.cache.attend_publish(q, px.plan, px.epoch, stream=stream)
+            self.cache.attend_publish(q, px.plan, px.epoch)
         else:
-            kc.peer_publish_empty(px.plan, px.epoch, stream=stream)
+            kc.peer_publish_empty(px.plan, px.epoch)
         if getattr(self, "_p2p_out", None) is None:
             self._p2p_out = torch.empty((self.B * self.Hq, D), dtype=torch.float32, device=q.device)
-        kc.peer_merge(px.plan, px.epoch, self._p2p_out, stream=stream)
+            self._status = torch.zeros(1, dtype=torch.int32, device=q.device)
+        kc.peer_merge(px.plan, px.epoch, self._p2p_out, status=self._status)
+        if self.strict:
+            self.check_exchange()
         return self._p2p_out.reshape(self.B, self.Hq, D)
+
+    def check_exchange(self):
+        """Raise if a peer-merge since the last check timed out (a rank did not
+        publish within ~5 s; its rows were returned as NaN).  Synchronises."""
+        if self._status is not None and int(self._status.item()) != 0:
+            self._status.zero_()
+            raise RuntimeError("sequence-shard exchange: a peer did not publish its (O, LSE) rows within 5 s")
 
     @property
     def total_tokens(self) -> int:

@@ -25,7 +25,7 @@ def _inputs():
     return k, v, q
 
 
-def _seq_worker(rank, world, rdzv, res_path):
+def _seq_worker(rank, world, rdzv, res_path, side_stream=False):
     import torch
     import torch.distributed as td
 
@@ -39,8 +39,19 @@ def _seq_worker(rank, world, rdzv, res_path):
         c = SeqShardedKvCache(PipelineConfig(heads=H), batch=1, q_heads=H * G_, max_tokens_per_rank=S + STEPS)
         c.prefill(dev_bf16(k[None, :S]), dev_bf16(v[None, :S]))
         outs = []
+        st = torch.cuda.Stream() if side_stream else None
         for t in range(STEPS):
-            o = c.decode_step(dev_bf16(q[t][None]), dev_bf16(k[S + t][None]), dev_bf16(v[S + t][None]))
+            qt, kt, vt = dev_bf16(q[t][None]), dev_bf16(k[S + t][None]), dev_bf16(v[S + t][None])
+            if st is None:
+                o = c.decode_step(qt, kt, vt)
+            else:
+                # a NON-current stream, held back by a spin kernel: the exchange and
+                # merge must be ordered after the attention kernel on that stream
+                st.wait_stream(torch.cuda.current_stream())
+                with torch.cuda.stream(st):
+                    torch.cuda._sleep(2_000_000)
+                o = c.decode_step(qt, kt, vt, stream=st.cuda_stream)
+                torch.cuda.current_stream().wait_stream(st)
             outs.append(o.cpu().numpy())
         tot = c.total_tokens
         if rank == 0:
@@ -51,13 +62,14 @@ def _seq_worker(rank, world, rdzv, res_path):
         td.destroy_process_group()
 
 
-def test_sequence_sharded_decode_matches_single_cache(tmp_path):
+@pytest.mark.parametrize("side_stream", [False, True])
+def test_sequence_sharded_decode_matches_single_cache(tmp_path, side_stream):
     import torch.multiprocessing as mp
 
     from paper_2605_19660_b200 import KvCache, PipelineConfig
 
     res = str(tmp_path / "seq.npy")
-    mp.spawn(_seq_worker, args=(2, str(tmp_path / "rdzv"), res), nprocs=2, join=True)
+    mp.spawn(_seq_worker, args=(2, str(tmp_path / "rdzv"), res, side_stream), nprocs=2, join=True)
     sharded = np.load(res)
     k, v, q = _inputs()
     c = KvCache(PipelineConfig(heads=H), batch=1, q_heads=H * G_, max_tokens=S + STEPS)

@@ -83,11 +83,37 @@ static int check_bf16() {
     return 0;
 }
 
+// the inverse maps the per-element readers (logits kernel) use
+static int check_inverse(int bits) {
+    const int tpw = 16 / bits, nwords = R * D * bits / 32;
+    for (int w = 0; w < nwords; ++w)
+        for (int hi = 0; hi < 2; ++hi)
+            for (int f = 0; f < tpw; ++f) {
+                int t, c, w2, s2;
+                k_word_coords(bits, w, f, hi, t, c);
+                k_code_loc(bits, t, c, w2, s2);
+                if (w2 != w || s2 != hi * 16 + f * bits) return 30;
+                v_word_coords(bits, w, f, hi, t, c);
+                v_code_loc(bits, t, c, w2, s2);
+                if (w2 != w || s2 != hi * 16 + f * bits) return 31;
+            }
+    for (int qu = 0; qu < 4; ++qu)
+        for (int w = 0; w < 32 * D / 2; ++w)
+            for (int hi = 0; hi < 2; ++hi) {
+                int t, c;
+                bf16_k_coords(w, hi, t, c);
+                if (bf16_k_byte(qu * 32 + t, c) != qu * BF16_QUARTER_BYTES + w * 4 + hi * 2) return 32;
+            }
+    return 0;
+}
+
 int main() {
     int rc = check_codes(2);
     if (!rc) rc = check_codes(4);
     if (!rc) rc = check_params();
     if (!rc) rc = check_bf16();
+    if (!rc) rc = check_inverse(2);
+    if (!rc) rc = check_inverse(4);
     std::printf("layout rc %d\n", rc);
     return rc;
 }

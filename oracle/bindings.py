@@ -174,6 +174,14 @@ class Ref(_Lib):
         L.ref_cache_load.argtypes = [ctypes.c_char_p, ctypes.POINTER(ctypes.c_void_p)]
         L.ref_cache_materialize.argtypes = [ctypes.c_void_p, _dp, _dp]
         L.ref_decode_step.argtypes = [ctypes.c_void_p, _dp, _dp, _dp, ctypes.c_int64, _dp, ctypes.c_int]
+        L.ref_decode_step_logits.argtypes = [ctypes.c_void_p, _dp, _dp, _dp, ctypes.c_int64, _dp, _dp,
+                                             ctypes.c_int]
+        L.ref_crit7_inputs.argtypes = [ctypes.c_uint64, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64,
+                                       ctypes.c_int64, _dp, _dp, _dp, _dp, _dp]
+        L.ref_simulate_fidelity.argtypes = [ctypes.c_int64, ctypes.c_int64, _dp, ctypes.c_int64, ctypes.c_int64,
+                                            _dp, _dp, _dp, _dp, ctypes.c_int, ctypes.c_int, ctypes.c_int, _dp,
+                                            _i64p]
+        L.ref_preprocess.argtypes = [ctypes.c_int64, ctypes.c_int64, _dp, _dp, _dp, _dp]
         L.ref_fht.argtypes = [_dp, ctypes.c_int64]
         L.ref_token_scale.argtypes = [_dp, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64, ctypes.c_int,
                                       _dp, _dp, _i64p]
@@ -263,6 +271,59 @@ class RefCache:
         out = np.zeros((self.H * g, self.d))
         Ref.check(Ref.lib().ref_decode_step(self.h, _ptr(q), _ptr(k), _ptr(v), g, _ptr(out), int(append)))
         return out
+
+
+    def decode_step_logits(self, q_raw, k_raw, v_raw, g, append=True):
+        """decode_step + StepOutput.logits [Hq, total + 1] (natural units)."""
+        q = np.ascontiguousarray(q_raw, np.float64)
+        k = np.ascontiguousarray(k_raw, np.float64)
+        v = np.ascontiguousarray(v_raw, np.float64)
+        total = self.stats()["total"] + 1
+        out = np.zeros((self.H * g, self.d))
+        lg = np.zeros((self.H * g, total))
+        Ref.check(Ref.lib().ref_decode_step_logits(self.h, _ptr(q), _ptr(k), _ptr(v), g, _ptr(out), _ptr(lg),
+                                                   int(append)))
+        return out, lg
+
+
+MEMORY_FIELDS = ["packed_tokens", "residual_tokens", "packed_k_payload_bits", "packed_v_payload_bits",
+                 "residual_k_payload_bits", "residual_v_payload_bits", "k_norm_bits", "param_bits"]
+
+
+def ref_crit7_inputs(seed: int, S: int = 256, Dn: int = 64, heads: int = 4, d_h: int = 128):
+    """Acceptance criterion 7's inputs for `seed` (acceptance_main.cpp:282-312):
+    generate(TniSpec) hidden rows [(S+Dn), heads*d_h] and the make_sim_stub
+    weights (w_q, w_k, w_v, w_o), all from the compiled reference."""
+    dm = heads * d_h
+    hidden = np.zeros((S + Dn, dm))
+    w = [np.zeros((dm, dm)) for _ in range(4)]
+    Ref.check(Ref.lib().ref_crit7_inputs(seed, S, Dn, heads, d_h, _ptr(hidden), *[_ptr(x) for x in w]))
+    return hidden, w
+
+
+def ref_simulate_fidelity(hidden, S: int, weights, method: str, bits: int = 2, heads: int = 4, d_h: int = 128,
+                          scaling: str = "l2") -> dict:
+    """The reference's simulate_fidelity (pipeline.cpp:359-408) on these inputs."""
+    hidden = np.ascontiguousarray(hidden, np.float64)
+    Dn = hidden.shape[0] - S
+    ws = [np.ascontiguousarray(x, np.float64) for x in weights]
+    o6 = np.zeros(6)
+    m8 = np.zeros(8, np.int64)
+    Ref.check(Ref.lib().ref_simulate_fidelity(heads, d_h, _ptr(hidden), S, Dn, *[_ptr(x) for x in ws],
+                                              METHODS[method], bits, SCALINGS[scaling], _ptr(o6), _ptr(m8, _i64p)))
+    mem = {k: int(v) for k, v in zip(MEMORY_FIELDS, m8)}
+    mem["effective_bits_per_value"] = float(o6[5])
+    return {"output_mse": float(o6[0]), "logit_mse": float(o6[1]), "prefill_output_mse": float(o6[2]),
+            "flushes": int(o6[3]), "decode_steps": int(o6[4]), "memory": mem}
+
+
+def ref_preprocess(w_v, w_o, heads: int = 4, d_h: int = 128):
+    """preprocess (pipeline.cpp:38-78): folded (W_V, W_O)."""
+    wv = np.ascontiguousarray(w_v, np.float64)
+    wo = np.ascontiguousarray(w_o, np.float64)
+    a, b = np.zeros_like(wv), np.zeros_like(wo)
+    Ref.check(Ref.lib().ref_preprocess(heads, d_h, _ptr(wv), _ptr(wo), _ptr(a), _ptr(b)))
+    return a, b
 
 
 def ref_fht(v: np.ndarray) -> np.ndarray:

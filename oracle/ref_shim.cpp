@@ -16,6 +16,7 @@
 // reference evaluates as g independent non-causal rows per KV head
 // (pipeline.cpp:184-198).
 #include <chrono>
+#include <cmath>
 #include <cstdint>
 #include <cstring>
 #include <exception>
@@ -28,6 +29,7 @@
 #include <omp.h>
 #endif
 
+#include "oscar/datagen.hpp"
 #include "oscar/hadamard.hpp"
 #include "oscar/kv_cache.hpp"
 #include "oscar/pipeline.hpp"
@@ -231,6 +233,155 @@ int ref_decode_step(void *h, const double *q_raw, const double *k_raw, const dou
             c->cache.buffer_quant_k(k_t, norms);
             c->cache.buffer_quant_v(xv);
         }
+        return 0;
+    } catch (const std::exception &e) {
+        return fail(e);
+    }
+}
+
+// decode_step body as ref_decode_step, also returning StepOutput.logits for the
+// GQA heads: logits[(h*g + j) * total + s] = (Qrot . K_all[s]) / sqrt(d) -- the
+// dot and temperature of attend_one (pipeline.cpp:155-165, an anonymous-namespace
+// function, restated here for GQA over the reference's own materialize_k +
+// current-token rows).
+int ref_decode_step_logits(void *h, const double *q_raw, const double *k_raw, const double *v_raw,
+                           int64_t g, double *out, double *logits, int do_append) {
+    try {
+        auto *c = static_cast<RefCache *>(h);
+        const PipelineConfig &cfg = c->cfg;
+        const int64_t H = cfg.heads, d = cfg.head_dim;
+        if (logits) {
+            Tensor3 xk = to_tensor(k_raw, 1, H, d);
+            Tensor3 k_t;
+            std::vector<double> norms;
+            transform_k(cfg, xk, k_t, norms);
+            Tensor3 q(g, H, d);
+            for (int64_t hh = 0; hh < H; ++hh)
+                for (int64_t j = 0; j < g; ++j)
+                    std::memcpy(q.row(j, hh), q_raw + (hh * g + j) * d, sizeof(double) * d);
+            const Tensor3 qt = cfg.rotates() ? fht_tensor(q) : q;
+            const Tensor3 k_hist = c->cache.materialize_k();
+            const int64_t total = k_hist.tokens + 1;
+            const double temp = 1.0 / std::sqrt(static_cast<double>(d));
+            for (int64_t hh = 0; hh < H; ++hh)
+                for (int64_t j = 0; j < g; ++j) {
+                    const double *qr = qt.row(j, hh);
+                    double *lo = logits + (hh * g + j) * total;
+                    for (int64_t s = 0; s < total; ++s) {
+                        double dot = 0.0;
+                        if (s < k_hist.tokens) {
+                            const double *kr = k_hist.row(s, hh);
+                            for (int64_t cc = 0; cc < d; ++cc) dot += qr[cc] * kr[cc];
+                        } else {  // the current token, norm restored (pipeline.cpp:302-306)
+                            const double sc = norms[static_cast<size_t>(hh)];
+                            const double *kr = k_t.row(0, hh);
+                            for (int64_t cc = 0; cc < d; ++cc) dot += qr[cc] * (kr[cc] * sc);
+                        }
+                        lo[s] = dot * temp;
+                    }
+                }
+        }
+        return ref_decode_step(h, q_raw, k_raw, v_raw, g, out, do_append);
+    } catch (const std::exception &e) {
+        return fail(e);
+    }
+}
+
+// ---- fidelity harness (acceptance criterion 7, acceptance_main.cpp:278-335) ----
+// The inputs criterion 7 builds for `seed`: generate(TniSpec) hidden rows
+// [(S + D) x heads*d_h] and make_sim_stub(heads, d_h, 0.12, 0.5) weights
+// (each d_model x d_model, row-major).
+int ref_crit7_inputs(uint64_t seed, int64_t S, int64_t Dn, int64_t heads, int64_t d_h, double *hidden,
+                     double *wq, double *wk, double *wv, double *wo) {
+    try {
+        TniSpec spec;
+        spec.tokens = S + Dn;
+        spec.heads = heads;
+        spec.head_dim = d_h;
+        spec.seed = seed;
+        spec.offset_channels = {0, 1, 2, 3};
+        spec.offset_factor = 18.0;
+        spec.offset_width = 0.3;
+        spec.scaled_channels = {4, 5, 6, 7, 8, 9, 10, 11};
+        spec.scaled_factor = 8.0;
+        spec.sink_factor = 0.01;
+        SeededRng pick(seed * 77 + 5);
+        while (spec.sink_tokens.size() < 8) {
+            const int64_t t = static_cast<int64_t>(pick.next_below(static_cast<uint64_t>(S)));
+            bool dup = false;
+            for (int64_t s : spec.sink_tokens) dup = dup || s == t;
+            if (!dup) spec.sink_tokens.push_back(t);
+        }
+        const GeneratedData data = generate(spec);
+        std::memcpy(hidden, data.tensor.data.data(), sizeof(double) * data.tensor.data.size());
+        SeededRng stub_rng(seed ^ 0x9e3779b97f4a7c15ull);
+        const ModelStub m = make_sim_stub(heads, d_h, 0.12, 0.5, stub_rng);
+        const size_t n = static_cast<size_t>(m.d_model * m.d_model);
+        std::memcpy(wq, m.w_q.data.data(), sizeof(double) * n);
+        std::memcpy(wk, m.w_k.data.data(), sizeof(double) * n);
+        std::memcpy(wv, m.w_v.data.data(), sizeof(double) * n);
+        std::memcpy(wo, m.w_o.data.data(), sizeof(double) * n);
+        return 0;
+    } catch (const std::exception &e) {
+        return fail(e);
+    }
+}
+
+// simulate_fidelity (pipeline.cpp:359-408) on given hidden rows and weights.
+// out6: output_mse, logit_mse, prefill_output_mse, flushes, decode_steps,
+// effective_bits_per_value; mem8: the method cache's MemoryReport fields.
+int ref_simulate_fidelity(int64_t heads, int64_t d_h, const double *hidden, int64_t S, int64_t Dn,
+                          const double *wq, const double *wk, const double *wv, const double *wo, int method,
+                          int bits, int scaling, double *out6, int64_t *mem8) {
+    try {
+        const int64_t dm = heads * d_h;
+        ModelStub m;
+        m.d_model = dm;
+        m.heads = heads;
+        m.head_dim = d_h;
+        const size_t n = static_cast<size_t>(dm * dm);
+        m.w_q = Matrix(dm, dm, std::vector<double>(wq, wq + n));
+        m.w_k = Matrix(dm, dm, std::vector<double>(wk, wk + n));
+        m.w_v = Matrix(dm, dm, std::vector<double>(wv, wv + n));
+        m.w_o = Matrix(dm, dm, std::vector<double>(wo, wo + n));
+        PipelineConfig cfg = make_cfg(method, bits, 32, 128, scaling, d_h, heads);
+        const Matrix hp(S, dm, std::vector<double>(hidden, hidden + S * dm));
+        const Matrix hd(Dn, dm, std::vector<double>(hidden + S * dm, hidden + (S + Dn) * dm));
+        const FidelityReport r = simulate_fidelity(m, hp, hd, cfg);
+        out6[0] = r.output_mse;
+        out6[1] = r.logit_mse;
+        out6[2] = r.prefill_output_mse;
+        out6[3] = static_cast<double>(r.flushes);
+        out6[4] = static_cast<double>(r.decode_steps);
+        out6[5] = r.memory.effective_bits_per_value();
+        const MemoryReport &mr = r.memory;
+        const int64_t f[8] = {mr.packed_tokens,          mr.residual_tokens,         mr.packed_k_payload_bits,
+                              mr.packed_v_payload_bits,  mr.residual_k_payload_bits, mr.residual_v_payload_bits,
+                              mr.k_norm_bits,            mr.param_bits};
+        std::memcpy(mem8, f, sizeof(f));
+        return 0;
+    } catch (const std::exception &e) {
+        return fail(e);
+    }
+}
+
+// preprocess (pipeline.cpp:38-78): the folded W_V, W_O of a model stub
+int ref_preprocess(int64_t heads, int64_t d_h, const double *wv, const double *wo, double *wv_out,
+                   double *wo_out) {
+    try {
+        const int64_t dm = heads * d_h;
+        const size_t n = static_cast<size_t>(dm * dm);
+        ModelStub m;
+        m.d_model = dm;
+        m.heads = heads;
+        m.head_dim = d_h;
+        m.w_q = Matrix::identity(dm);
+        m.w_k = Matrix::identity(dm);
+        m.w_v = Matrix(dm, dm, std::vector<double>(wv, wv + n));
+        m.w_o = Matrix(dm, dm, std::vector<double>(wo, wo + n));
+        const ModelStub f = preprocess(m);
+        std::memcpy(wv_out, f.w_v.data.data(), sizeof(double) * n);
+        std::memcpy(wo_out, f.w_o.data.data(), sizeof(double) * n);
         return 0;
     } catch (const std::exception &e) {
         return fail(e);

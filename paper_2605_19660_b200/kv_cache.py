@@ -84,6 +84,8 @@ def lib():
         L.oscar_kv_append.argtypes = [_P, _P, _P, ctypes.c_int64, _P]
         L.oscar_kv_decode_step.argtypes = [_P, _P, _P, _P, _P, _P, _P]
         L.oscar_kv_attend.argtypes = [_P, _P, _P, _P, _P]
+        L.oscar_kv_decode_step_logits.argtypes = [_P, _P, _P, _P, _P, _P, _P, _P]
+        L.oscar_kv_logits.argtypes = [_P, _P, _P, _P, _P]
         L.oscar_kv_decode_step_many.argtypes = [ctypes.c_int32, _P, _P, _P, _P, _P, _P, _P]
         L.oscar_kv_decode_step_host.argtypes = [_P, _P, _P, _P, _P, _P, _P]
         L.oscar_kv_stats.argtypes = [_P, ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(ctypes.c_int64),
@@ -116,7 +118,7 @@ C_ABI_SYMBOLS = [
     "oscar_kv_memory_report", "oscar_kv_export", "oscar_kv_dump", "oscar_kv_load", "oscar_kv_materialize", "oscar_lse_merge",
     "oscar_kv_last_launch_count", "oscar_peer_area_bytes", "oscar_kv_attend_publish", "oscar_peer_publish_empty",
     "oscar_peer_merge", "oscar_ipc_alloc", "oscar_ipc_open", "oscar_ipc_close", "oscar_ipc_free",
-    "oscar_kv_status",
+    "oscar_kv_status", "oscar_kv_decode_step_logits", "oscar_kv_logits",
 ]
 
 
@@ -242,15 +244,37 @@ class KvCache:
     append = buffer_quant
 
     # ---- decode_step body (pipeline.cpp:292-323) --------------------------------
-    def decode_step(self, q, k, v, out=None, lse=None, stream=None):
+    def decode_step(self, q, k, v, out=None, lse=None, stream=None, logits=None):
+        """logits: optional fp32 [B, Hq, total_tokens + 1] that receives
+        StepOutput.logits (pipeline.hpp:54-58) of this step."""
         import torch
 
         self._check_step(q, k, v)
         if out is None:
             out = torch.empty((self.B, self.Hq, D), dtype=torch.float32, device=q.device)
         self._check_out(out, lse)
-        _check(lib().oscar_kv_decode_step(self._h, _ptr(q), _ptr(k), _ptr(v), _ptr(out), _ptr(lse),
-                                          _stream(stream)))
+        if logits is None:
+            _check(lib().oscar_kv_decode_step(self._h, _ptr(q), _ptr(k), _ptr(v), _ptr(out), _ptr(lse),
+                                              _stream(stream)))
+        else:
+            _need(logits, "logits", self.device, "f32", numel=self.B * self.Hq * (self.total_tokens + 1))
+            _check(lib().oscar_kv_decode_step_logits(self._h, _ptr(q), _ptr(k), _ptr(v), _ptr(out), _ptr(lse),
+                                                     _ptr(logits), _stream(stream)))
+        return out
+
+    def logits(self, q, k=None, out=None, stream=None):
+        """Attention logits q.k/sqrt(d) (natural units) of every query head over
+        the cache contents (+ the current token k): fp32 [B, Hq, S]."""
+        import torch
+
+        self._check_step(q)
+        if k is not None:
+            _need(k, "k", self.device, "bf16", (self.B, self.H, D))
+        n = self.total_tokens + (1 if k is not None else 0)
+        if out is None:
+            out = torch.empty((self.B, self.Hq, n), dtype=torch.float32, device=q.device)
+        _need(out, "logits", self.device, "f32", numel=self.B * self.Hq * n)
+        _check(lib().oscar_kv_logits(self._h, _ptr(q), _ptr(k), _ptr(out), _stream(stream)))
         return out
 
     def _check_step(self, q, k=None, v=None):

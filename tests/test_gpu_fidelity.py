@@ -1,23 +1,112 @@
-"""Acceptance criterion 7 (acceptance_main.cpp:278-335) on the device path:
-oscar < rotate-only < kivi and scale-only > kivi in >= 18 of 20 seeds, with
-the output MSE of simulate_fidelity (pipeline.cpp:359-408) measured through
-the CUDA cache (paper_2605_19660_b200/fidelity.py)."""
+"""§8(f) #3/#4 on the device path, against the compiled reference:
+
+* StepOutput.logits (pipeline.hpp:54-58, pipeline.cpp:314-318) of the device
+  decode step vs the reference's logits (attend_one's q.k/sqrt(d) over
+  materialize_k + the current token), GQA, INT2 / INT4 / bf16 caches;
+* the fidelity harness on the REFERENCE'S criterion-7 inputs
+  (generate(TniSpec) + make_sim_stub, acceptance_main.cpp:282-312): the
+  device's output / logit MSE per method vs the reference's own
+  simulate_fidelity (pipeline.cpp:359-408) on the same rows, and criterion
+  7's orderings (>= 18 of 20 seeds);
+* MemoryReport of the device cache vs KvCache::memory_report
+  (kv_cache.cpp:383-402) at bits 0 / 2 / 4.
+"""
 import json
 import os
 
+import numpy as np
 import pytest
 
-pytestmark = pytest.mark.gpu
+from oracle import bindings as ob
+from paper_2605_19660_b200.synthetic import make_inputs, make_queries
+
+from gpu_util import dev_bf16, log_err
+
+pytestmark = [pytest.mark.gpu, pytest.mark.skipif(not ob.ref_available(), reason="oracle/_ref not built")]
+
+OUT_DIR = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "gpurun_out")
 
 
-def test_method_ordering_on_device():
+@pytest.mark.parametrize("bits,method", [(2, "oscar"), (4, "oscar"), (0, "oscar"), (2, "kivi")])
+def test_decode_step_logits_match_reference(bits, method):
+    """300-token cache (256 packed + 44 window) plus the current token; then a
+    step that flushes (window of 127 + current), checked the same way."""
+    from paper_2605_19660_b200 import KvCache, PipelineConfig
+
+    B, H, g = 2, 2, 4
+    for S in (300, 383):
+        data = [make_inputs(700 + b + S, S + 1, H) for b in range(B)]
+        k = np.stack([d[0] for d in data])
+        v = np.stack([d[1] for d in data])
+        q = make_queries(700 + S, B, H * g)
+        c = KvCache(PipelineConfig(method=method, heads=H, bits=bits), batch=B, q_heads=H * g, max_tokens=S + 8)
+        c.buffer_quant(dev_bf16(k[:, :S]), dev_bf16(v[:, :S]))
+        import torch
+
+        lg = torch.empty((B, H * g, S + 1), dtype=torch.float32, device="cuda")
+        c.decode_step(dev_bf16(q), dev_bf16(k[:, S]), dev_bf16(v[:, S]), logits=lg)
+        lg = lg.cpu().numpy().astype(np.float64)
+        for b in range(B):
+            ref = ob.RefCache(method=method, H=H, bits=bits)
+            ref.append(k[b, :S], v[b, :S])
+            _, rl = ref.decode_step_logits(q[b], k[b, S], v[b, S], g, append=False)
+            err = float(np.max(np.abs(lg[b] - rl)) / np.max(np.abs(rl)))
+            log_err(f"logits[{method},bits={bits},S={S}][b={b}]", err)
+            assert err <= (2e-3 if bits else 1e-5), (b, S, err)
+
+
+def test_fidelity_on_reference_inputs_matches_reference():
+    """Criterion 7's 20 seeds: every method's device output / logit MSE vs the
+    reference's simulate_fidelity on the same hidden rows and weights; the
+    orderings on the device."""
     from paper_2605_19660_b200 import fidelity as fd
 
-    cnt = fd.method_ordering(seeds=range(1, 21))
-    d = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "gpurun_out")
-    if os.path.isdir(d):
-        with open(os.path.join(d, "fidelity_ordering.json"), "w") as f:
-            json.dump(cnt, f)
-    assert cnt["oscar<rotate-only"] >= 18, cnt
-    assert cnt["rotate-only<kivi"] >= 18, cnt
-    assert cnt["scale-only>kivi"] >= 18, cnt
+    ob.ref_use_threads(os.cpu_count() or 1)
+    rows, inputs = [], []
+    for seed in range(1, 21):
+        hidden, (wq, wk, wv, wo) = ob.ref_crit7_inputs(seed)
+        inputs.append((hidden, fd.ModelStub(wq, wk, wv, wo, 4, 128), 256))
+    cnt = fd.method_ordering(inputs)
+    worst = {"output": 0.0, "logit": 0.0}
+    for seed, ((hidden, m, S), dev) in enumerate(zip(inputs, cnt["mse"]), start=1):
+        for method in ("kivi", "rotate-only", "scale-only", "oscar"):
+            ref = ob.ref_simulate_fidelity(hidden, S, [m.w_q, m.w_k, m.w_v, m.w_o], method)
+            rep = fd.simulate_fidelity(m, hidden, S, method) if seed <= 3 else None
+            row = {"seed": seed, "method": method, "device_output_mse": dev[method],
+                   "reference_output_mse": ref["output_mse"], "reference_logit_mse": ref["logit_mse"]}
+            if rep is not None:
+                row.update(device_logit_mse=rep.logit_mse, device_flushes=rep.flushes,
+                           device_memory=rep.memory)
+                worst["logit"] = max(worst["logit"], abs(rep.logit_mse / ref["logit_mse"] - 1))
+                assert rep.memory["effective_bits_per_value"] == ref["memory"]["effective_bits_per_value"]
+            worst["output"] = max(worst["output"], abs(dev[method] / ref["output_mse"] - 1))
+            rows.append(row)
+    summary = {k: v for k, v in cnt.items() if k != "mse"}
+    summary["worst_rel_dev_vs_ref"] = worst
+    if os.path.isdir(OUT_DIR):
+        with open(os.path.join(OUT_DIR, "fidelity_device_vs_reference.json"), "w") as f:
+            json.dump({"summary": summary, "rows": rows}, f, indent=1)
+    assert cnt["oscar<rotate-only"] >= 18, summary
+    assert cnt["rotate-only<kivi"] >= 18, summary
+    assert cnt["scale-only>kivi"] >= 18, summary
+    # the device path's MSEs are the reference's up to the bf16 input rounding and
+    # the fp16/fp32 attention arithmetic (the CPU harness shows ~2 % for the former)
+    assert worst["output"] < 0.1, summary
+    assert worst["logit"] < 0.1, summary
+
+
+@pytest.mark.parametrize("bits", [0, 2, 4])
+def test_memory_report_matches_reference(bits):
+    from paper_2605_19660_b200 import KvCache, PipelineConfig
+
+    H = 2
+    k, v = make_inputs(9, 700, H)
+    c = KvCache(PipelineConfig(heads=H, bits=bits), batch=3, q_heads=H, max_tokens=800)
+    ref = ob.RefCache(H=H, bits=bits)
+    for lo, hi in ((0, 300), (300, 301), (301, 520), (520, 700)):
+        c.buffer_quant(dev_bf16(np.stack([k[lo:hi]] * 3)), dev_bf16(np.stack([v[lo:hi]] * 3)))
+        ref.append(k[lo:hi], v[lo:hi])
+        mine, theirs = c.memory_report(), ref.memory_report()
+        for key, val in theirs.items():
+            assert mine[key] == val, (bits, hi, key, mine[key], val)
+        assert mine["device_hot_bytes"] > 0 and mine["device_total_bytes"] >= mine["device_hot_bytes"]

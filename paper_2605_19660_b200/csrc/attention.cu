@@ -160,7 +160,7 @@ __device__ __forceinline__ void process_block(const uint8_t *__restrict__ sb, Wa
     // ---- key offsets as A (row gq = group): bias[grp][head] = sum_c b[c,grp] * Qrot[head][c]
     //      (x = a*code + b, the value form of dequantize_one, quant.cpp:65-68) -- one
     //      MMA per k-step; row gq < 4 (= group) is read back, rows 4..15 are don't-care
-    const uint4 *bkp = reinterpret_cast<const uint4 *>(sb + Blk::KB_OFF + ((gq & 3) * 4 + tq) * 64);
+    const uint4 *bkp = reinterpret_cast<const uint4 *>(sb + Blk::KB_OFF + ((gq & 3) * 4 + tq) * 16);
     float kbias[4], kbias2[4];  // rows gq: even k-steps; rows gq+8: odd k-steps
     uint4 zk;
 
@@ -202,7 +202,7 @@ __device__ __forceinline__ void process_block(const uint8_t *__restrict__ sb, Wa
             // one quad per k-step pair (layout.h kb_index): rows gq = group gq & 3 at
             // k-step s (even), rows gq+8 = the same group at s+1; the other rows of
             // each product are don't-care (lanes gq >= 4 duplicate groups 0-3)
-            if ((s & 1) == 0) zk = bkp[s >> 1];
+            if ((s & 1) == 0) zk = bkp[(s >> 1) * 16];
             if (s == 0) mma16816_zc(kbias, zk.x, zk.y, zk.z, zk.w, qf[s][0], qf[s][1]);
             else if (s == 1) mma16816_zc(kbias2, zk.x, zk.y, zk.z, zk.w, qf[s][0], qf[s][1]);
             else if ((s & 1) == 0) mma16816(kbias, zk.x, zk.y, zk.z, zk.w, qf[s][0], qf[s][1]);
@@ -315,7 +315,7 @@ __device__ __forceinline__ void process_block(const uint8_t *__restrict__ sb, Wa
     long long t2 = tm ? clk() : 0;
     // ---- P.V ---------------------------------------------------------------------------
     // value offsets as A: row gq (< 4) = channel group, k = tokens
-    const uint4 *vbp = reinterpret_cast<const uint4 *>(sb + Blk::VB_OFF + ((gq & 3) * 4 + tq) * 64);
+    const uint4 *vbp = reinterpret_cast<const uint4 *>(sb + Blk::VB_OFF + ((gq & 3) * 4 + tq) * 16);
     uint4 zv;
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
@@ -363,7 +363,7 @@ __device__ __forceinline__ void process_block(const uint8_t *__restrict__ sb, Wa
         {
             // paired quads as for the keys: even j -> rows gq of ob, odd j -> rows gq+8 of ob2
             if ((j & 1) == 0) {
-                zv = vbp[j >> 1];
+                zv = vbp[(j >> 1) * 16];
                 mma16816(st.ob, zv.x, zv.y, zv.z, zv.w, bp0, bp1);
             } else {
                 mma16816(st.ob2, zv.x, zv.y, zv.z, zv.w, bp0, bp1);

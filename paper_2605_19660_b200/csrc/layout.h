@@ -186,14 +186,16 @@ OSK_HD int ka_index(int c, int grp) {
     k_chan_split(c, s, tq, slot);
     return ((s * 4 + tq) * 4 + grp) * 4 + slot;
 }
-// K b-params: [grp][tq][s/2][word][half], word = (slot/2)*2 + s%2: one 16-byte
+// K b-params: [s/2][grp][tq][word][half], word = (slot/2)*2 + s%2: one 16-byte
 // load per k-step PAIR is an A quad (x_s, x_s+1, y_s, y_s+1) whose rows g hold
 // k-step s and rows g+8 k-step s+1, so the bias MMAs read it without moves
-// (lane g<4 reads 64 B: its group, all k-steps)
+// (lane (g, tq) reads chunk (s/2)*16 + (g&3)*4 + tq: k-step-pair major, so the
+// 8 lanes of each quarter-warp phase read 8 consecutive 16-byte chunks --
+// conflict-free; a [grp][tq][s/2] order put them 64 B apart, 4-way conflicts)
 OSK_HD int kb_index(int c, int grp) {
     int s, tq, slot;
     k_chan_split(c, s, tq, slot);
-    return ((grp * 4 + tq) * 4 + (s >> 1)) * 8 + ((slot >> 1) * 2 + (s & 1)) * 2 + (slot & 1);
+    return (((s >> 1) * 16 + grp * 4 + tq)) * 8 + ((slot >> 1) * 2 + (s & 1)) * 2 + (slot & 1);
 }
 // token t = 16j + r; B-fragment k = r (natural order): lane pair tq = (r mod 8) / 2,
 // slot = (r & 1) + 2 (r >= 8)  (slots 0,1 -> b0 = k 2tq,2tq+1; 2,3 -> b1 = k 2tq+8,2tq+9)
@@ -209,11 +211,11 @@ OSK_HD int va_index(int t, int gc) {
     v_tok_split(t, j, tq, slot);
     return ((j * 4 + tq) * 4 + gc) * 4 + slot;
 }
-// V b-params: [gc][tq][j/2][word][half], paired like the K b-params
+// V b-params: [j/2][gc][tq][word][half], paired (and conflict-free) like the K b-params
 OSK_HD int vb_index(int t, int gc) {
     int j, tq, slot;
     v_tok_split(t, j, tq, slot);
-    return ((gc * 4 + tq) * 4 + (j >> 1)) * 8 + ((slot >> 1) * 2 + (j & 1)) * 2 + (slot & 1);
+    return (((j >> 1) * 16 + gc * 4 + tq)) * 8 + ((slot >> 1) * 2 + (j & 1)) * 2 + (slot & 1);
 }
 // norms: [g][i][2] -> token 16i + g (+8 for slot 1)
 OSK_HD int norm_index(int t) {

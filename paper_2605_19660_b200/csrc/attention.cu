@@ -278,8 +278,6 @@ __device__ __forceinline__ void process_block(const uint8_t *__restrict__ sb, Wa
         const float al0 = fast_exp2(st.m[0] - mn0), al1 = fast_exp2(st.m[1] - mn1);
         st.m[0] = mn0;
         st.m[1] = mn1;
-        st.l[0] *= al0;
-        st.l[1] *= al1;
 #pragma unroll
         for (int mm = 0; mm < 8; ++mm) {
             st.o[mm][0] *= al0;
@@ -299,31 +297,32 @@ __device__ __forceinline__ void process_block(const uint8_t *__restrict__ sb, Wa
             sacc[i][3] -= d1;
         }
     }
-    float ls0 = 0.f, ls1 = 0.f;
+    // P = 2^y straight into the fp16 pairs the P.V B operand needs: one
+    // ex2.f16x2 per two logits (the fp16 rounding of y costs no more than the
+    // fp16 rounding of P it replaces: |dP| <= P ln2 2^-11 |y|/2^floor(log2|y|)).
+    // The softmax denominator is not summed here: the value-offset MMA's spare
+    // A row 4 is all ones, so it accumulates sum_t P per head (see P.V below).
+    uint32_t P01[8], P23[8];
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
-        sacc[i][0] = fast_exp2(sacc[i][0]);
-        sacc[i][1] = fast_exp2(sacc[i][1]);
-        sacc[i][2] = fast_exp2(sacc[i][2]);
-        sacc[i][3] = fast_exp2(sacc[i][3]);
-        ls0 += sacc[i][0] + sacc[i][2];
-        ls1 += sacc[i][1] + sacc[i][3];
+        P01[i] = ex2_h2(pack_half2(sacc[i][0], sacc[i][1]));
+        P23[i] = ex2_h2(pack_half2(sacc[i][2], sacc[i][3]));
     }
-    st.l[0] += ls0;
-    st.l[1] += ls1;
 
     long long t2 = tm ? clk() : 0;
     // ---- P.V ---------------------------------------------------------------------------
     // value offsets as A: row gq (< 4) = channel group, k = tokens
+    //      (rows 4 / 12, lanes gq == 4: all ones -> the running sum_t P per head)
     const uint4 *vbp = reinterpret_cast<const uint4 *>(sb + Blk::VB_OFF + ((gq & 3) * 4 + tq) * 16);
-    uint4 zv;
+    constexpr uint32_t ONES = 0x3C003C00u;  // half2(1, 1)
+    uint4 zv = make_uint4(ONES, ONES, ONES, ONES);
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
         // P of tokens 16j..16j+15 as the B operand: the accumulator rows (tokens) x
         // cols (heads 2tq, 2tq+1), transposed per 8x8 half by movmatrix, is exactly
         // the B fragment (k = tokens 2tq, 2tq+1 | 2tq+8, 2tq+9; n = head gq)
-        const uint32_t bp0 = movmatrix_t(pack_half2(sacc[j][0], sacc[j][1]));
-        const uint32_t bp1 = movmatrix_t(pack_half2(sacc[j][2], sacc[j][3]));
+        const uint32_t bp0 = movmatrix_t(P01[j]);
+        const uint32_t bp1 = movmatrix_t(P23[j]);
         uint32_t bv[4][2];
         {
             const uint4 *p = reinterpret_cast<const uint4 *>(sb + Blk::VA_OFF + (j * 4 + tq) * 32);
@@ -363,7 +362,7 @@ __device__ __forceinline__ void process_block(const uint8_t *__restrict__ sb, Wa
         {
             // paired quads as for the keys: even j -> rows gq of ob, odd j -> rows gq+8 of ob2
             if ((j & 1) == 0) {
-                zv = vbp[(j >> 1) * 16];
+                if (gq != 4) zv = vbp[(j >> 1) * 16];
                 mma16816(st.ob, zv.x, zv.y, zv.z, zv.w, bp0, bp1);
             } else {
                 mma16816(st.ob2, zv.x, zv.y, zv.z, zv.w, bp0, bp1);
@@ -889,11 +888,18 @@ __global__ void __launch_bounds__(NCW_ * 32, 1) decode_attn_kernel(const AttnArg
         float *slot = bh == seg_last ? last_seg_slot(warp)
                                      : a.warp_part + (((int64_t)cta * a.maxseg + k) * NCW_MAX + warp) * MERGE_FLOATS;
         {
-            float l0 = st.l[0], l1 = st.l[1];
+            float l0, l1;
+            if constexpr (BITS == 0) {
+                l0 = st.l[0];
+                l1 = st.l[1];
 #pragma unroll
-            for (int o = 4; o < 32; o <<= 1) {
-                l0 += __shfl_xor_sync(0xffffffffu, l0, o);
-                l1 += __shfl_xor_sync(0xffffffffu, l1, o);
+                for (int o = 4; o < 32; o <<= 1) {
+                    l0 += __shfl_xor_sync(0xffffffffu, l0, o);
+                    l1 += __shfl_xor_sync(0xffffffffu, l1, o);
+                }
+            } else {  // sum_t P: row 4 (even token tiles) + row 12 (odd) of the value-offset MMAs
+                l0 = __shfl_sync(0xffffffffu, st.ob[0] + st.ob2[2], 16 + tq);
+                l1 = __shfl_sync(0xffffffffu, st.ob[1] + st.ob2[3], 16 + tq);
             }
             float vb0[4], vb1[4];
 #pragma unroll

@@ -572,7 +572,8 @@ HostCache build_host_cache(oscar_kv_handle *h, int64_t b) {
                 const int tpw = 16 / bits;
                 const int64_t code_bytes = (int64_t)R * D * bits / 8;
                 const uint32_t *kw = reinterpret_cast<const uint32_t *>(blk.data());
-                const uint32_t *vw = reinterpret_cast<const uint32_t *>(blk.data() + code_bytes);
+                const int v_off = bits == 2 ? Block<2>::V_OFF : Block<4>::V_OFF;
+                const uint32_t *vw = reinterpret_cast<const uint32_t *>(blk.data() + v_off);
                 const int nwords = (int)(code_bytes / 4);
                 const uint32_t fmask = (1u << bits) - 1;
                 auto &kc = hc.k_codes[hh][k];
@@ -894,7 +895,7 @@ void load_kvc1(oscar_kv_handle *h, int64_t b, const char *path) {
                 const int tpw = 16 / bits;
                 const int64_t code_bytes = (int64_t)R * D * bits / 8;
                 uint32_t *kw = reinterpret_cast<uint32_t *>(rec_p);
-                uint32_t *vw = reinterpret_cast<uint32_t *>(rec_p + code_bytes);
+                uint32_t *vw = reinterpret_cast<uint32_t *>(rec_p + (bits == 2 ? Block<2>::V_OFF : Block<4>::V_OFF));
                 const uint32_t maxc = (1u << bits) - 1;
                 for (int w = 0; w < (int)(code_bytes / 4); ++w)
                     for (int hi = 0; hi < 2; ++hi)

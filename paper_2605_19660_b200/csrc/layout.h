@@ -5,13 +5,20 @@
 // record in HBM, fetched by a single cp.async.bulk into shared memory:
 //
 //   INT2 record (12800 B)                       INT4 record (20992 B)
+//   K part (6656 B):                             K part (10752 B):
 //   [K codes  4096 B]  mma A-fragment order      [K codes  8192 B]
-//   [V codes  4096 B]  mma A-fragment order      [V codes  8192 B]
 //   [K a      1024 B]  fp16 step  per (ch,grp)   ... same params/norms ...
 //   [K b      1024 B]  fp16 offset -delta*zp per (ch,grp)
+//   [norms     512 B]  fp32 per token
+//   V part (6144 B):                             V part (10240 B):
+//   [V codes  4096 B]  mma A-fragment order      [V codes  8192 B]
 //   [V a      1024 B]  fp16 step  per (tok,gc)
 //   [V b      1024 B]  fp16 offset per (tok,gc)
-//   [norms     512 B]  fp32 per token
+//
+// Everything the QK^T half of the attention reads is the contiguous K part,
+// everything P.V reads the V part: the kernel streams them into separate
+// shared-memory slots and hands each back to the TMA as soon as its half of
+// the work is done (more bytes in flight per SM than whole-record stages).
 //
 // Keys and values both dequantise as x = a*code + b with a = delta and
 // b = -delta*zp (a constant group stores a = 0, b = constant; its codes are 0)
@@ -62,19 +69,22 @@ template <int BITS>
 struct Block {
     static constexpr int CODE_BYTES = R * D * BITS / 8;      // per K or V
     static constexpr int K_OFF = 0;
-    static constexpr int V_OFF = CODE_BYTES;
-    static constexpr int KA_OFF = 2 * CODE_BYTES;
+    static constexpr int KA_OFF = CODE_BYTES;
     static constexpr int KB_OFF = KA_OFF + D * NGRP * 2;
-    static constexpr int VA_OFF = KB_OFF + D * NGRP * 2;
+    static constexpr int NORM_OFF = KB_OFF + D * NGRP * 2;
+    static constexpr int K_PART = NORM_OFF + R * 4;           // [K codes][K a][K b][norms]
+    static constexpr int V_OFF = K_PART;
+    static constexpr int VA_OFF = V_OFF + CODE_BYTES;
     static constexpr int VB_OFF = VA_OFF + R * NGC * 2;
-    static constexpr int NORM_OFF = VB_OFF + R * NGC * 2;
-    static constexpr int BYTES = NORM_OFF + R * 4;
+    static constexpr int BYTES = VB_OFF + R * NGC * 2;
+    static constexpr int V_PART = BYTES - K_PART;              // [V codes][V a][V b]
     // words per lane per k-step (each word = 8/BITS*... m-tiles)
     static constexpr int TILES_PER_WORD = 16 / BITS;          // 8 (int2) / 4 (int4)
     static constexpr int WORDS_PER_LANE_STEP = 4 * 8 / TILES_PER_WORD;  // 4 / 8
 };
 static_assert(Block<2>::BYTES == 12800, "int2 block size");
 static_assert(Block<4>::BYTES == 20992, "int4 block size");
+static_assert(Block<2>::K_PART % 128 == 0 && Block<4>::K_PART % 128 == 0, "16-byte aligned parts for bulk copies");
 // bits == 0 (exact bf16 cache, the unquantized baseline): an R-block is four
 // 32-token quarters, each [K 8 KB][V 8 KB] of raw bf16 in A-fragment order so
 // a lane's four A registers are one 16-byte load.

@@ -233,12 +233,14 @@ __global__ void __launch_bounds__(QT * GPAR) quantize_kernel(const QuantizeArgs 
     double *ku = reinterpret_cast<double *>(smem) + (threadIdx.x / QT) * 32 * KU_ROW;  // [GPAR][32][4][33]
     uint8_t *ck = smem + GPAR * 32 * KU_ROW * 8;                  // [128][128] K codes
     uint8_t *cv = ck + R * CODE_STRIDE;                           // [128][128] V codes
-    uint8_t *prm = cv + R * CODE_STRIDE;                          // params + norms (BYTES - KA_OFF)
+    // params + norms staged in record order: K tail [a][b][norms] (K_PART - KA_OFF
+    // bytes), then V tail [a][b] (BYTES - VA_OFF bytes)
+    uint8_t *prm = cv + R * CODE_STRIDE;
     __half *ka = reinterpret_cast<__half *>(prm);
     __half *kb = ka + D * NGRP;
-    __half *va = kb + D * NGRP;
+    float *nrm = reinterpret_cast<float *>(kb + D * NGRP);
+    __half *va = reinterpret_cast<__half *>(nrm + R);
     __half *vb = va + R * NGC;
-    float *nrm = reinterpret_cast<float *>(vb + R * NGC);
 
     const int tid = threadIdx.x % QT, lane = tid & 31, q = tid & 3, tl = tid >> 2;
     const int bh = blockIdx.y, b = bh / a.H, h = bh % a.H;
@@ -374,29 +376,39 @@ __global__ void __launch_bounds__(QT * GPAR) quantize_kernel(const QuantizeArgs 
     uint8_t *out = a.blocks + out_blk * (int64_t)Blk::BYTES;
     constexpr int NWORDS = R * D * BITS / 32;
     constexpr int TPW = 16 / BITS;
-    for (int w = threadIdx.x; w < NWORDS; w += QT * GPAR) {
-        uint32_t wk = 0, wv = 0;
+    // four consecutive code words per thread -> one 128-bit store each for K and V
+    for (int w4 = threadIdx.x; w4 < NWORDS / 4; w4 += QT * GPAR) {
+        uint32_t wk[4], wv[4];
 #pragma unroll
-        for (int hi = 0; hi < 2; ++hi) {
-            // field f of a K word is token +16f of field 0, of a V word channel +16f
-            int tk, ckn, tv, cvn;
-            k_word_coords(BITS, w, 0, hi, tk, ckn);
-            v_word_coords(BITS, w, 0, hi, tv, cvn);
-            const uint8_t *pk = ck + tk * CODE_STRIDE + ckn;
-            const uint8_t *pv = cv + tv * CODE_STRIDE + cvn;
+        for (int e = 0; e < 4; ++e) {
+            const int w = 4 * w4 + e;
+            wk[e] = wv[e] = 0;
 #pragma unroll
-            for (int f = 0; f < TPW; ++f) {
-                wk |= (uint32_t)pk[16 * f * CODE_STRIDE] << (hi * 16 + f * BITS);
-                wv |= (uint32_t)pv[16 * f] << (hi * 16 + f * BITS);
+            for (int hi = 0; hi < 2; ++hi) {
+                // field f of a K word is token +16f of field 0, of a V word channel +16f
+                int tk, ckn, tv, cvn;
+                k_word_coords(BITS, w, 0, hi, tk, ckn);
+                v_word_coords(BITS, w, 0, hi, tv, cvn);
+                const uint8_t *pk = ck + tk * CODE_STRIDE + ckn;
+                const uint8_t *pv = cv + tv * CODE_STRIDE + cvn;
+#pragma unroll
+                for (int f = 0; f < TPW; ++f) {
+                    wk[e] |= (uint32_t)pk[16 * f * CODE_STRIDE] << (hi * 16 + f * BITS);
+                    wv[e] |= (uint32_t)pv[16 * f] << (hi * 16 + f * BITS);
+                }
             }
         }
-        reinterpret_cast<uint32_t *>(out + Blk::K_OFF)[w] = wk;
-        reinterpret_cast<uint32_t *>(out + Blk::V_OFF)[w] = wv;
+        reinterpret_cast<uint4 *>(out + Blk::K_OFF)[w4] = make_uint4(wk[0], wk[1], wk[2], wk[3]);
+        reinterpret_cast<uint4 *>(out + Blk::V_OFF)[w4] = make_uint4(wv[0], wv[1], wv[2], wv[3]);
     }
-    // params + norms: contiguous tail of the record
-    constexpr int TAIL = Blk::BYTES - Blk::KA_OFF;
-    for (int i = threadIdx.x; i < TAIL / 16; i += QT * GPAR)
-        reinterpret_cast<uint4 *>(out + Blk::KA_OFF)[i] = reinterpret_cast<const uint4 *>(prm)[i];
+    // params + norms: the K tail [a][b][norms] and the V tail [a][b] of the record
+    constexpr int KTAIL = Blk::K_PART - Blk::KA_OFF, VTAIL = Blk::BYTES - Blk::VA_OFF;
+    static_assert(KTAIL % 16 == 0 && VTAIL % 16 == 0, "128-bit tail stores");
+    for (int i = threadIdx.x; i < (KTAIL + VTAIL) / 16; i += QT * GPAR) {
+        const uint4 x = reinterpret_cast<const uint4 *>(prm)[i];
+        if (i < KTAIL / 16) reinterpret_cast<uint4 *>(out + Blk::KA_OFF)[i] = x;
+        else reinterpret_cast<uint4 *>(out + Blk::VA_OFF)[i - KTAIL / 16] = x;
+    }
 }
 
 // bits == 0 / method fp: the record is raw bf16, four 32-token quarters of
@@ -467,7 +479,8 @@ __global__ void ring_copy_kernel(const RingCopyArgs a) {
 
 template <int BITS, int GPAR>
 cudaError_t launch_q(const QuantizeArgs &a, dim3 grid, cudaStream_t st) {
-    const int smem = GPAR * 32 * KU_ROW * 8 + 2 * R * CODE_STRIDE + Block<BITS>::BYTES - Block<BITS>::KA_OFF;
+    const int smem = GPAR * 32 * KU_ROW * 8 + 2 * R * CODE_STRIDE + (Block<BITS>::K_PART - Block<BITS>::KA_OFF) +
+                     (Block<BITS>::BYTES - Block<BITS>::VA_OFF);
     static std::atomic<uint64_t> attr_done{0};
     if (cudaError_t e = ensure_smem_attr(quantize_kernel<BITS, GPAR>, smem, attr_done); e != cudaSuccess) return e;
     quantize_kernel<BITS, GPAR><<<grid, QT * GPAR, smem, st>>>(a);

@@ -136,6 +136,12 @@ struct WarpState {
     float m[2], l[2];
 };
 
+__device__ __forceinline__ unsigned long long gtime() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
 __device__ __forceinline__ long long clk() {
     long long c;
     asm volatile("mov.u64 %0, %%clock64;" : "=l"(c));
@@ -180,7 +186,7 @@ __device__ __forceinline__ void process_block(const uint8_t *__restrict__ sb, Wa
                 kw[4 * v + 3] = u.w;
             }
 #pragma unroll
-            for (int v = 0; v < 4 * WPF; ++v) kwh[v] = kw[v] >> 8;
+            for (int v = 0; v < 4 * WPF; ++v) kwh[v] = shr8(kw[v]);
         }
         uint32_t qf[8][2];  // only [s] is live
         qf[s][0] = *reinterpret_cast<const uint32_t *>(qsm + 16 * s);
@@ -348,7 +354,7 @@ __device__ __forceinline__ void process_block(const uint8_t *__restrict__ sb, Wa
                 vw[4 * v + 3] = u.w;
             }
 #pragma unroll
-            for (int v = 0; v < 4 * WPF; ++v) vwh[v] = vw[v] >> 8;
+            for (int v = 0; v < 4 * WPF; ++v) vwh[v] = shr8(vw[v]);
         }
 #pragma unroll
         for (int mm = 0; mm < 8; ++mm) {
@@ -744,6 +750,7 @@ __global__ void __launch_bounds__(NCW_ * 32, 1) decode_attn_kernel(const AttnArg
     // pdl_prefetch after a flush), then waits for the previous grid's
     // completion + memory flush before touching q, the current token, the
     // residual ring or any scratch the previous grid wrote.
+    const unsigned long long g_entry = kProf ? gtime() : 0;
     griddep_launch_dependents();
     if (threadIdx.x == 0) {
         for (int i = 0; i < C::NST; ++i) {
@@ -1001,8 +1008,10 @@ __global__ void __launch_bounds__(NCW_ * 32, 1) decode_attn_kernel(const AttnArg
     // ======== end of the CTA's work: cooperative merges (all warps finish within
     //          ~one unit of each other under the static round-robin schedule) ========
     const long long tm0 = (kProf && a.prof) ? clk() : 0;
+    const unsigned long long g_stream = kProf ? gtime() : 0;
     if (lane == 0) reinterpret_cast<float **>(smem + C::TAB_OFF)[warp] = last_seg_slot(warp);
     __syncthreads();
+    const unsigned long long g_sync1 = kProf ? gtime() : 0;
     int *lastflag = reinterpret_cast<int *>(smem + C::SEG_OFF);  // [nseg] (segcnt area reused)
     const int nseg = (int)(seg_last - seg_first + 1);
     // (1) CTA partial per segment: warp-per-(segment, head), lane = 4-channel chunk
@@ -1058,7 +1067,9 @@ __global__ void __launch_bounds__(NCW_ * 32, 1) decode_attn_kernel(const AttnArg
             }
         }
     }
+    const unsigned long long g_phase1 = kProf ? gtime() : 0;
     __syncthreads();
+    const unsigned long long g_sync2 = kProf ? gtime() : 0;
     const long long tp0 = (kProf && a.prof) ? clk() : 0;
     // (2) publish: one acq_rel ticket per segment (cumulative over the barrier)
     if (threadIdx.x < nseg) {
@@ -1072,6 +1083,7 @@ __global__ void __launch_bounds__(NCW_ * 32, 1) decode_attn_kernel(const AttnArg
         }
     }
     __syncthreads();
+    const unsigned long long g_ticket = kProf ? gtime() : 0;
     if (kProf && a.prof) {
         tmr[8] += clk() - tm0;
         tmr[9] += clk() - tp0;  // the ticket (atomic) part
@@ -1135,7 +1147,7 @@ __global__ void __launch_bounds__(NCW_ * 32, 1) decode_attn_kernel(const AttnArg
         // host view is replaced below by the whole-kernel cycles
         // [0..7] wait qk softmax pv merge spin qprologue segtail, [8] total, [9] cta merge,
         // [10] ticket, [11] smid, [12] final merge
-        unsigned long long *pp = a.prof + ((int64_t)blockIdx.x * NCW_MAX + warp) * 16;
+        unsigned long long *pp = a.prof + ((int64_t)blockIdx.x * NCW_MAX + warp) * kProfStride;
         for (int i = 0; i < 8; ++i) pp[i] = (unsigned long long)tmr[i];
         pp[8] = (unsigned long long)(clk() - tk0);
         pp[9] = (unsigned long long)tmr[8];
@@ -1144,6 +1156,13 @@ __global__ void __launch_bounds__(NCW_ * 32, 1) decode_attn_kernel(const AttnArg
         unsigned smid;
         asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
         pp[11] = smid;
+        pp[13] = g_entry;  // globaltimer (ns): kernel entry, end of this warp's streaming, exit
+        pp[14] = g_stream;
+        pp[15] = gtime();
+        pp[16] = g_sync1;  // after the first end-of-work barrier
+        pp[17] = g_phase1;  // CTA partials done (this warp)
+        pp[18] = g_sync2;
+        pp[19] = g_ticket;  // tickets + barrier
     }
 }
 

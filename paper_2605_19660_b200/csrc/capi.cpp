@@ -16,6 +16,7 @@
 #define OSK_PROF 0
 #endif
 
+#include <algorithm>
 #include <cmath>
 #include <cstdlib>
 #include <cstdio>
@@ -127,6 +128,13 @@ struct oscar_kv_handle {
     // a quantize kernel wrote packed records since the last attention launch:
     // the next attention launch must not prefetch them ahead of griddepcontrol.wait
     bool blocks_written = true;
+    // launch plan of the last attention launch shape (nb, tail charge): the grid
+    // and the CTA-range checks only change when a flush adds a block or the
+    // residual window empties, so the per-step host cost is one comparison
+    struct Plan {
+        int64_t nb = -1, tail_cost = -1;
+        int ncta = 0;
+    } plan;
 
     TransformCfg tc() const {
         TransformCfg t;
@@ -307,7 +315,9 @@ struct oscar_kv_handle {
         }
         a.pdl_prefetch = blocks_written ? 0 : 1;
         a.maxp = maxp_alloc;
-        if (a.nb > 0) {
+        if (a.nb > 0 && plan.nb == a.nb && plan.tail_cost == a.tail_cost) {
+            a.ncta = plan.ncta;  // same shape as the last launch: its checks hold
+        } else if (a.nb > 0) {
             const int64_t nbs = a.nb * (dbits == 0 ? 4 : 1);  // pipeline units per (b, kv head)
             // segments (b, kv heads) per CTA range; a CTA holds at most MAX_SEGMENTS of them
             // (shared-memory ticket table), so large batches of short sequences get a grid
@@ -349,6 +359,9 @@ struct oscar_kv_handle {
                 grow_scratch(std::max<int64_t>((int64_t)a.ncta * maxseg, scratch_slots), maxseg);
             a.warp_part = warp_part;
             a.maxseg = maxseg_alloc;
+            plan.nb = a.nb;
+            plan.tail_cost = a.tail_cost;
+            plan.ncta = a.ncta;
         } else {
             a.maxseg = 1;  // residual-only mode: one segment per CTA (ncta = BH <= scratch slots)
         }
@@ -424,26 +437,26 @@ struct oscar_kv_handle {
         unsigned long long *pbuf = nullptr;
         const int nw = a.ncta * 16;
         if (prof) {
-            CK(cudaMalloc(&pbuf, sizeof(unsigned long long) * 16 * nw));
-            CK(cudaMemsetAsync(pbuf, 0, sizeof(unsigned long long) * 16 * nw, s));
+            CK(cudaMalloc(&pbuf, sizeof(unsigned long long) * kProfStride * nw));
+            CK(cudaMemsetAsync(pbuf, 0, sizeof(unsigned long long) * kProfStride * nw, s));
             a.prof = pbuf;
         }
         CK(launch_attention(dbits, a, s));
         ++last_launches;
         blocks_written = false;
         if (prof) {
-            std::vector<unsigned long long> hbuf(16 * nw);
+            std::vector<unsigned long long> hbuf(kProfStride * nw);
             CK(cudaMemcpyAsync(hbuf.data(), pbuf, hbuf.size() * 8, cudaMemcpyDeviceToHost, s));
             CK(cudaStreamSynchronize(s));
             double acc[13] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
             double mx = 0, fmax = 0;
             int cnt = 0;
             for (int w = 0; w < nw; ++w) {
-                if (hbuf[16 * w + 8] == 0) continue;
+                if (hbuf[kProfStride * w + 8] == 0) continue;
                 ++cnt;
-                for (int i = 0; i < 13; ++i) acc[i] += (double)hbuf[16 * w + i];
-                mx = std::max(mx, (double)hbuf[16 * w + 8]);
-                fmax = std::max(fmax, (double)hbuf[16 * w + 12]);
+                for (int i = 0; i < 13; ++i) acc[i] += (double)hbuf[kProfStride * w + i];
+                mx = std::max(mx, (double)hbuf[kProfStride * w + 8]);
+                fmax = std::max(fmax, (double)hbuf[kProfStride * w + 12]);
             }
             {
                 // per-CTA spread: slowest warp per CTA, min/max across CTAs
@@ -452,7 +465,7 @@ struct oscar_kv_handle {
                 for (int c = 0; c < a.ncta; ++c) {
                     double lo = 1e30, hi = 0;
                     for (int w = 0; w < 16; ++w) {
-                        const double t = (double)hbuf[16 * (c * 16 + w) + 8];
+                        const double t = (double)hbuf[kProfStride * (c * 16 + w) + 8];
                         if (t == 0) continue;
                         lo = std::min(lo, t);
                         hi = std::max(hi, t);
@@ -465,29 +478,38 @@ struct oscar_kv_handle {
                 }
                 if (const char *fn = getenv("OSCAR_PROF_FILE")) {  // per-CTA: range, segments, tails, smid, cycles
                     if (FILE *f = std::fopen(fn, "w")) {
-                        std::fprintf(f, "cta,smid,units,segments,tails,slowest_warp_cycles,cta_merge,ticket,final_merge\n");
+                        std::fprintf(f, "cta,smid,units,segments,tails,slowest_warp_cycles,cta_merge,ticket,final_merge,"
+                                        "entry_ns,stream_end_ns,exit_ns\n");
+                        unsigned long long g0 = ~0ull;
+                        for (int w = 0; w < nw; ++w)
+                            if (hbuf[kProfStride * w + 8]) g0 = std::min(g0, hbuf[kProfStride * w + 13]);
                         const int64_t nbu = a.nb * (dbits == 0 ? 4 : 1);
                         const Split sp{nbu, a.BH, a.ncta, a.seg_cost, a.tail_cost};
                         for (int c = 0; c < a.ncta; ++c) {
                             double hi = 0, cm = 0, tk = 0, fm = 0;
-                            unsigned long long sm = 0;
+                            unsigned long long sm = 0, ge = 0, gs = 0, gx = 0;
                             for (int w = 0; w < 16; ++w) {
-                                const double t = (double)hbuf[16 * (c * 16 + w) + 8];
+                                const double t = (double)hbuf[kProfStride * (c * 16 + w) + 8];
                                 if (t > hi) {
                                     hi = t;
-                                    sm = hbuf[16 * (c * 16 + w) + 11];
+                                    sm = hbuf[kProfStride * (c * 16 + w) + 11];
                                 }
-                                cm = std::max(cm, (double)hbuf[16 * (c * 16 + w) + 9]);
-                                tk = std::max(tk, (double)hbuf[16 * (c * 16 + w) + 10]);
-                                fm = std::max(fm, (double)hbuf[16 * (c * 16 + w) + 12]);
+                                cm = std::max(cm, (double)hbuf[kProfStride * (c * 16 + w) + 9]);
+                                tk = std::max(tk, (double)hbuf[kProfStride * (c * 16 + w) + 10]);
+                                fm = std::max(fm, (double)hbuf[kProfStride * (c * 16 + w) + 12]);
+                                if (hbuf[kProfStride * (c * 16 + w) + 8]) {
+                                    ge = std::max(ge, hbuf[kProfStride * (c * 16 + w) + 13] - g0);
+                                    gs = std::max(gs, hbuf[kProfStride * (c * 16 + w) + 14] - g0);
+                                    gx = std::max(gx, hbuf[kProfStride * (c * 16 + w) + 15] - g0);
+                                }
                             }
                             const int64_t st = sp.begin(c), en = sp.end(c);
                             int64_t tails = 0;
                             for (int64_t bh = st / nbu; en > st && bh <= (en - 1) / nbu; ++bh)
                                 if ((bh + 1) * nbu <= en) ++tails;
-                            std::fprintf(f, "%d,%llu,%lld,%lld,%lld,%.0f,%.0f,%.0f,%.0f\n", c, sm, (long long)(en - st),
-                                         (long long)(en > st ? (en - 1) / nbu - st / nbu + 1 : 0), (long long)tails, hi,
-                                         cm, tk, fm);
+                            std::fprintf(f, "%d,%llu,%lld,%lld,%lld,%.0f,%.0f,%.0f,%.0f,%llu,%llu,%llu\n", c, sm,
+                                         (long long)(en - st), (long long)(en > st ? (en - 1) / nbu - st / nbu + 1 : 0),
+                                         (long long)tails, hi, cm, tk, fm, ge, gs, gx);
                         }
                         std::fclose(f);
                     }
@@ -495,6 +517,47 @@ struct oscar_kv_handle {
                 if (ncta_used)
                     std::fprintf(stderr, "OSCAR_PROF cta slowest-warp cycles: min %.0f max %.0f; mean in-CTA warp spread %.0f\n",
                                  cmin, cmax, wspread / ncta_used);
+            }
+            {
+                // timeline (globaltimer ns, relative to the first CTA's entry)
+                std::vector<double> ent, str, ext;
+                for (int w = 0; w < nw; ++w) {
+                    if (hbuf[kProfStride * w + 8] == 0) continue;
+                    ent.push_back((double)hbuf[kProfStride * w + 13]);
+                    str.push_back((double)hbuf[kProfStride * w + 14]);
+                    ext.push_back((double)hbuf[kProfStride * w + 15]);
+                }
+                if (!ent.empty()) {
+                    const double t0 = *std::min_element(ent.begin(), ent.end());
+                    auto q = [&](std::vector<double> v, double f) {
+                        std::sort(v.begin(), v.end());
+                        return (v[(size_t)(f * (double)(v.size() - 1))] - t0) * 1e-3;
+                    };
+                    std::fprintf(stderr,
+                                 "OSCAR_PROF timeline us: entry max %.2f | stream end min %.2f p10 %.2f p50 %.2f "
+                                 "p90 %.2f max %.2f | exit min %.2f p50 %.2f max %.2f\n",
+                                 q(ent, 1.0), q(str, 0.0), q(str, 0.1), q(str, 0.5), q(str, 0.9), q(str, 1.0),
+                                 q(ext, 0.0), q(ext, 0.5), q(ext, 1.0));
+                    // per CTA (warp 0): end-of-work phases relative to the CTA's last stream end
+                    double dp[5] = {0, 0, 0, 0, 0};
+                    int nc = 0;
+                    for (int c = 0; c < a.ncta; ++c) {
+                        const unsigned long long *w0 = &hbuf[kProfStride * (c * 16)];
+                        if (w0[8] == 0) continue;
+                        unsigned long long se = 0;
+                        for (int w = 0; w < 16; ++w)
+                            if (hbuf[kProfStride * (c * 16 + w) + 8]) se = std::max(se, hbuf[kProfStride * (c * 16 + w) + 14]);
+                        const unsigned long long pts[5] = {w0[16], w0[17], w0[18], w0[19], w0[15]};
+                        for (int i = 0; i < 5; ++i) dp[i] += (double)(long long)(pts[i] - se);
+                        ++nc;
+                    }
+                    if (nc)
+                        std::fprintf(stderr,
+                                     "OSCAR_PROF end phases (us after the CTA's last stream end, mean over CTAs): "
+                                     "sync1 %.2f phase1 %.2f sync2 %.2f ticket %.2f exit %.2f\n",
+                                     dp[0] / nc * 1e-3, dp[1] / nc * 1e-3, dp[2] / nc * 1e-3, dp[3] / nc * 1e-3,
+                                     dp[4] / nc * 1e-3);
+                }
             }
             if (cnt)
                 std::fprintf(stderr,

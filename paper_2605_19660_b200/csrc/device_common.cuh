@@ -94,9 +94,19 @@ __device__ __forceinline__ void named_bar(int id, int nthreads) {
 }
 
 // ---- tensor core: mma.sync m16n8k16 fp16 x fp16 -> fp32 --------------------------
+// OSK_MMA_VOLATILE=0: the mma asm is pure (no volatile), so the compiler may
+// move the products across the other volatile asm of the loop
+#ifndef OSK_MMA_VOLATILE
+#define OSK_MMA_VOLATILE 1
+#endif
+#if OSK_MMA_VOLATILE
+#define OSK_MMA_ASM asm volatile
+#else
+#define OSK_MMA_ASM asm
+#endif
 __device__ __forceinline__ void mma16816(float (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3,
                                          uint32_t b0, uint32_t b1) {
-    asm volatile(
+    OSK_MMA_ASM(
         "mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
         "{%0,%1,%2,%3};\n"
         : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
@@ -105,7 +115,7 @@ __device__ __forceinline__ void mma16816(float (&d)[4], uint32_t a0, uint32_t a1
 // D = A*B (no accumulator input): saves zero-initialising the accumulators
 __device__ __forceinline__ void mma16816_zc(float (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3,
                                             uint32_t b0, uint32_t b1) {
-    asm volatile(
+    OSK_MMA_ASM(
         "mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
         "{%10,%10,%10,%10};\n"
         : "=f"(d[0]), "=f"(d[1]), "=f"(d[2]), "=f"(d[3])
@@ -113,11 +123,26 @@ __device__ __forceinline__ void mma16816_zc(float (&d)[4], uint32_t a0, uint32_t
 }
 __device__ __forceinline__ void mma16816_bf16(float (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3,
                                               uint32_t b0, uint32_t b1) {
-    asm volatile(
+    OSK_MMA_ASM(
         "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
         "{%0,%1,%2,%3};\n"
         : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
         : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+
+// x >> 8 for the high code fields.  OSK_SHR_IMAD: as mul.hi by 2^24 (IMAD.HI on
+// the FMA pipe) instead of SHF on the ALU pipe, which the field masks saturate
+#ifndef OSK_SHR_IMAD
+#define OSK_SHR_IMAD 0
+#endif
+__device__ __forceinline__ uint32_t shr8(uint32_t x) {
+#if OSK_SHR_IMAD
+    uint32_t y;
+    asm("mul.hi.u32 %0, %1, 16777216;" : "=r"(y) : "r"(x));
+    return y;
+#else
+    return x >> 8;
+#endif
 }
 
 __device__ __forceinline__ uint32_t hmul2_u32(uint32_t a, uint32_t b) {

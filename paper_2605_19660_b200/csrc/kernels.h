@@ -95,6 +95,9 @@ struct PeerPlan {
     uint32_t *flags[PEER_MAX];
 };
 
+// profiling build: 64-bit slots per warp in AttnArgs::prof
+constexpr int kProfStride = 32;
+
 struct AttnArgs {
     const uint8_t *blocks;
     int64_t max_blocks;

@@ -77,6 +77,35 @@ int oscar_kv_destroy(oscar_kv_handle *h);
  * calls append token by token and flush at exactly R. */
 int oscar_kv_append(oscar_kv_handle *h, const void *k, const void *v, int64_t n_tokens, void *stream);
 
+/* The reference's own call shapes, fp64 rows as KvCache receives them
+ * (kv_cache.hpp:80-84):
+ *   oscar_kv_append_k = buffer_quant_k(new_k, norms) (kv_cache.cpp:194-249):
+ *     k_t: fp64 [batch, n_tokens, heads, head_dim], the ALREADY transformed
+ *     keys K_u (apply_method's output), norms: fp64 [batch, n_tokens, heads];
+ *   oscar_kv_append_v = buffer_quant_v(new_v) (kv_cache.cpp:251-292):
+ *     v: fp64 [batch, n_tokens, heads, head_dim], stored as given.
+ * Device pointers (host pointers are accepted too and staged through the
+ * device, synchronously).  K and V advance separately (first call = prefill branch,
+ * then token by token with a flush at exactly R), packed codes, params and
+ * norms bit-exact vs the reference; the residual window is kept exactly in
+ * fp64 (export / dump / flush) with a bf16 image for the decode kernel.  A
+ * cache takes one input form: these calls and oscar_kv_append /
+ * oscar_kv_decode_step (raw bf16 rows) cannot be mixed on one handle (status
+ * 2).  Needs bits 2 or 4 and rotate_v = 0.  Attention requires both streams
+ * to hold the same number of tokens. */
+int oscar_kv_append_k(oscar_kv_handle *h, const double *k_t, const double *norms, int64_t n_tokens, void *stream);
+int oscar_kv_append_v(oscar_kv_handle *h, const double *v, int64_t n_tokens, void *stream);
+/* decode_step (pipeline.cpp:292-323) with the current token in that form:
+ * k_t fp64 [batch, heads, d] (K_u of the token), norms fp64 [batch, heads],
+ * v fp64 [batch, heads, d]; q bf16 [batch, q_heads, d] (raw, rotated by the
+ * kernel).  Attends history + current token at full precision, then the
+ * flush at R, like oscar_kv_decode_step. */
+int oscar_kv_decode_step_f64(oscar_kv_handle *h, const void *q, const double *k_t, const double *norms,
+                             const double *v, float *out, float *lse, void *stream);
+/* Value-stream counters of the fp64 form (the reference's v_packed_tokens_ /
+ * v_residual_; oscar_kv_stats counts keys). */
+int oscar_kv_stats_v(const oscar_kv_handle *h, int64_t *v_packed, int64_t *v_residual);
+
 /* decode_step body (pipeline.cpp:292-323) without projections:
  * attention of q over (cache history + the current token at full precision),
  * then the current token is appended (a flush, if the window fills, runs
@@ -163,10 +192,17 @@ int oscar_kv_dump(oscar_kv_handle *h, int64_t b, const char *path);
  * file (written by the reference's KvCache::dump or oscar_kv_dump).  The
  * config (method, bits, G, R, scaling, H, d_h) must match; a fresh handle
  * adopts the file's token counts, a filled one must already hold the same
- * counts (one handle = sequences of equal length).  Residual rows and the
- * bits-0 raw rows must be the transform of bf16 inputs (verified bit for
- * bit); quantized blocks need keep_exact.  Synchronous. */
+ * counts (one handle = sequences of equal length).  Residual rows that are
+ * the transform of bf16 inputs (verified bit for bit) go to the raw form's
+ * bf16 rings; any other fp64 residual rows put the handle in the fp64 form
+ * (see oscar_kv_append_k; bits 2/4, rotate_v = 0).  The bits-0 raw rows must
+ * be bf16 transforms; quantized blocks need keep_exact.  Synchronous. */
 int oscar_kv_load(oscar_kv_handle *h, int64_t b, const char *path);
+
+/* The config and token count of a KVC1 file (its manifest), for creating a
+ * handle to load it into (static KvCache::load, kv_cache.hpp:95).  rotate_v
+ * is 0; tokens = packed + residual. */
+int oscar_kvc1_read_config(const char *path, oscar_kv_config *cfg, int64_t *tokens);
 
 /* materialize_k / materialize_v (kv_cache.cpp:327-381) of sequence b into
  * host fp64 [total, H, d] buffers (a debug/parity path, not the hot path). */

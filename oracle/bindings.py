@@ -176,6 +176,9 @@ class Ref(_Lib):
         L.ref_decode_step.argtypes = [ctypes.c_void_p, _dp, _dp, _dp, ctypes.c_int64, _dp, ctypes.c_int]
         L.ref_decode_step_logits.argtypes = [ctypes.c_void_p, _dp, _dp, _dp, ctypes.c_int64, _dp, _dp,
                                              ctypes.c_int]
+        L.ref_cache_buffer_quant_k.argtypes = [ctypes.c_void_p, _dp, _dp, ctypes.c_int64]
+        L.ref_cache_buffer_quant_v.argtypes = [ctypes.c_void_p, _dp, ctypes.c_int64]
+        L.ref_decode_step_f64.argtypes = [ctypes.c_void_p, _dp, _dp, _dp, _dp, ctypes.c_int64, _dp, ctypes.c_int]
         L.ref_crit7_inputs.argtypes = [ctypes.c_uint64, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64,
                                        ctypes.c_int64, _dp, _dp, _dp, _dp, _dp]
         L.ref_simulate_fidelity.argtypes = [ctypes.c_int64, ctypes.c_int64, _dp, ctypes.c_int64, ctypes.c_int64,
@@ -224,6 +227,27 @@ class RefCache:
         xk = np.ascontiguousarray(xk, dtype=np.float64)
         xv = np.ascontiguousarray(xv, dtype=np.float64)
         Ref.check(Ref.lib().ref_cache_append(self.h, _ptr(xk), _ptr(xv), xk.shape[0]))
+
+    def buffer_quant_k(self, k_t: np.ndarray, norms: np.ndarray):
+        """KvCache::buffer_quant_k(K_u [S,H,d], norms [S*H]) -- the reference's own call."""
+        k_t = np.ascontiguousarray(k_t, dtype=np.float64)
+        norms = np.ascontiguousarray(norms, dtype=np.float64).reshape(-1)
+        Ref.check(Ref.lib().ref_cache_buffer_quant_k(self.h, _ptr(k_t), _ptr(norms), k_t.shape[0]))
+
+    def buffer_quant_v(self, v: np.ndarray):
+        v = np.ascontiguousarray(v, dtype=np.float64)
+        Ref.check(Ref.lib().ref_cache_buffer_quant_v(self.h, _ptr(v), v.shape[0]))
+
+    def decode_step_f64(self, q_raw, k_t, norms, v, g, append=True):
+        """decode_step with the current token in the cache's form (tr.k [H,d], tr.norms [H], xv [H,d])."""
+        q = np.ascontiguousarray(q_raw, np.float64)
+        kt = np.ascontiguousarray(k_t, np.float64)
+        nr = np.ascontiguousarray(norms, np.float64).reshape(-1)
+        vv = np.ascontiguousarray(v, np.float64)
+        out = np.zeros((self.H * g, self.d))
+        Ref.check(Ref.lib().ref_decode_step_f64(self.h, _ptr(q), _ptr(kt), _ptr(nr), _ptr(vv), g, _ptr(out),
+                                                int(append)))
+        return out
 
     def stats(self):
         out = np.zeros(4, np.int64)
@@ -330,6 +354,20 @@ def ref_fht(v: np.ndarray) -> np.ndarray:
     v = np.array(v, dtype=np.float64)
     Ref.check(Ref.lib().ref_fht(_ptr(v), v.size))
     return v
+
+
+def ref_apply_k(x: np.ndarray, method="oscar", scaling="l2"):
+    """apply_method's key half (pipeline.cpp:224-236) by the compiled reference:
+    x [S, H, d] fp64 -> (K_u [S, H, d], norms [S*H])."""
+    x = np.array(x, dtype=np.float64)
+    rot = method in ("rotate-only", "oscar")
+    sc = method in ("scale-only", "oscar")
+    if rot:
+        x = np.stack([np.stack([ref_fht(x[t, h]) for h in range(x.shape[1])]) for t in range(x.shape[0])])
+    if sc:
+        ku, nr, _ = ref_token_scale(x, scaling)
+        return ku, nr
+    return x, np.ones(x.shape[0] * x.shape[1])
 
 
 def ref_token_scale(x: np.ndarray, scaling="l2"):

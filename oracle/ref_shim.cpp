@@ -128,6 +128,29 @@ int ref_cache_append(void *h, const double *xk, const double *xv, int64_t S) {
     }
 }
 
+// The reference's own call shapes: transformed keys K_u [S,H,d] + norms [S*H]
+// into buffer_quant_k, value rows [S,H,d] into buffer_quant_v (kv_cache.cpp:194-292).
+int ref_cache_buffer_quant_k(void *h, const double *kt, const double *norms, int64_t S) {
+    try {
+        auto *c = static_cast<RefCache *>(h);
+        const int64_t H = c->cfg.heads, d = c->cfg.head_dim;
+        c->cache.buffer_quant_k(to_tensor(kt, S, H, d), std::vector<double>(norms, norms + S * H));
+        return 0;
+    } catch (const std::exception &e) {
+        return fail(e);
+    }
+}
+int ref_cache_buffer_quant_v(void *h, const double *v, int64_t S) {
+    try {
+        auto *c = static_cast<RefCache *>(h);
+        const int64_t H = c->cfg.heads, d = c->cfg.head_dim;
+        c->cache.buffer_quant_v(to_tensor(v, S, H, d));
+        return 0;
+    } catch (const std::exception &e) {
+        return fail(e);
+    }
+}
+// v_packed_tokens / v_residual are private; the dump's manifest carries them
 int ref_cache_stats(void *h, int64_t *out4) {
     auto *c = static_cast<RefCache *>(h);
     out4[0] = c->cache.packed_tokens();
@@ -231,6 +254,47 @@ int ref_decode_step(void *h, const double *q_raw, const double *k_raw, const dou
                 std::memcpy(out + (hh * g + j) * d, o.row(j, hh), sizeof(double) * d);
         if (do_append) {
             c->cache.buffer_quant_k(k_t, norms);
+            c->cache.buffer_quant_v(xv);
+        }
+        return 0;
+    } catch (const std::exception &e) {
+        return fail(e);
+    }
+}
+
+// decode_step body (pipeline.cpp:290-323) with the current token already in the
+// cache's form: kt [H,d] = tr.k, norms [H] = tr.norms, v [H,d] = xv (stored as given)
+int ref_decode_step_f64(void *h, const double *q_raw, const double *kt, const double *norms, const double *v,
+                        int64_t g, double *out, int do_append) {
+    try {
+        auto *c = static_cast<RefCache *>(h);
+        const PipelineConfig &cfg = c->cfg;
+        const int64_t H = cfg.heads, d = cfg.head_dim;
+        const Tensor3 k_t = to_tensor(kt, 1, H, d);
+        const std::vector<double> nrm(norms, norms + H);
+        const Tensor3 xv = to_tensor(v, 1, H, d);
+        Tensor3 q(g, H, d);
+        for (int64_t hh = 0; hh < H; ++hh)
+            for (int64_t j = 0; j < g; ++j) std::memcpy(q.row(j, hh), q_raw + (hh * g + j) * d, sizeof(double) * d);
+        const Tensor3 qt = cfg.rotates() ? fht_tensor(q) : q;
+        const Tensor3 k_hist = c->cache.materialize_k();
+        const Tensor3 v_hist = c->cache.materialize_v();
+        const int64_t total = k_hist.tokens + 1;
+        Tensor3 k_all(total, H, d), v_all(total, H, d);
+        std::memcpy(k_all.data.data(), k_hist.data.data(), sizeof(double) * k_hist.data.size());
+        std::memcpy(v_all.data.data(), v_hist.data.data(), sizeof(double) * v_hist.data.size());
+        for (int64_t hh = 0; hh < H; ++hh) {
+            const double s = nrm[static_cast<size_t>(hh)];
+            const double *src = k_t.row(0, hh);
+            double *dst = k_all.row(total - 1, hh);
+            for (int64_t cc = 0; cc < d; ++cc) dst[cc] = src[cc] * s;
+            std::memcpy(v_all.row(total - 1, hh), xv.row(0, hh), sizeof(double) * d);
+        }
+        const Tensor3 o = attention(qt, k_all, v_all);
+        for (int64_t hh = 0; hh < H; ++hh)
+            for (int64_t j = 0; j < g; ++j) std::memcpy(out + (hh * g + j) * d, o.row(j, hh), sizeof(double) * d);
+        if (do_append) {
+            c->cache.buffer_quant_k(k_t, nrm);
             c->cache.buffer_quant_v(xv);
         }
         return 0;

@@ -501,6 +501,7 @@ struct ResidualRefs {
     const uint16_t *ringk, *ringv;  // this (b, kv head)'s rings
     const uint16_t *kc, *vc;        // current token or null
     int g, r, rotate_v;
+    int f16;  // rings hold fp16 (fp64-form caches; no current token): fp16 MMAs, q converted
 };
 
 // The tile's partial in registers: o in the packed partial's fragment layout
@@ -551,6 +552,13 @@ __device__ __forceinline__ void residual_compute(const ResidualRefs rr, const __
         qb[s][0] = ld32(qrow, c);
         qb[s][1] = ld32(qrow, c + 8);
     }
+    if (rr.f16) {  // the bf16 query pairs as fp16 (exact within fp16's range)
+#pragma unroll
+        for (int s = 0; s < 8; ++s)
+#pragma unroll
+            for (int e = 0; e < 2; ++e)
+                qb[s][e] = pack_half2(__uint_as_float(qb[s][e] << 16), __uint_as_float(qb[s][e] & 0xffff0000u));
+    }
 #pragma unroll
     for (int mm = 0; mm < 8; ++mm) {
         const int cA = 16 * mm + gq, cB = cA + 8;
@@ -561,8 +569,13 @@ __device__ __forceinline__ void residual_compute(const ResidualRefs rr, const __
     }
     // ---- QK^T ----
     float sacc[4] = {0.f, 0.f, 0.f, 0.f};
+    if (rr.f16) {
 #pragma unroll
-    for (int s = 0; s < 8; ++s) mma16816_bf16(sacc, kf[s][0], kf[s][1], kf[s][2], kf[s][3], qb[s][0], qb[s][1]);
+        for (int s = 0; s < 8; ++s) mma16816(sacc, kf[s][0], kf[s][1], kf[s][2], kf[s][3], qb[s][0], qb[s][1]);
+    } else {
+#pragma unroll
+        for (int s = 0; s < 8; ++s) mma16816_bf16(sacc, kf[s][0], kf[s][1], kf[s][2], kf[s][3], qb[s][0], qb[s][1]);
+    }
     // logits in log2 units; rows gq / gq+8 = tokens tA / tB; cols 2tq, 2tq+1 = heads
     const bool vA = tA < ntok, vB = tB < ntok;
     sacc[0] = vA ? sacc[0] * c0 : -CUDART_INF_F;
@@ -587,7 +600,8 @@ __device__ __forceinline__ void residual_compute(const ResidualRefs rr, const __
     }
     // ---- P as the B operand: lane (gq, tq) needs P[head gq][tokens 2tq, 2tq+1, 2tq+8, 2tq+9],
     //      held by lanes (2tq, gq/2) and (2tq+1, gq/2) in accumulator layout ----
-    const uint32_t X = pack_bf162(sacc[0], sacc[1]), Y = pack_bf162(sacc[2], sacc[3]);
+    const uint32_t X = rr.f16 ? pack_half2(sacc[0], sacc[1]) : pack_bf162(sacc[0], sacc[1]);
+    const uint32_t Y = rr.f16 ? pack_half2(sacc[2], sacc[3]) : pack_bf162(sacc[2], sacc[3]);
     const int sa = (2 * tq) * 4 + (gq >> 1), sbl = (2 * tq + 1) * 4 + (gq >> 1);
     const uint32_t xa = __shfl_sync(0xffffffffu, X, sa), ya = __shfl_sync(0xffffffffu, Y, sa);
     const uint32_t xb = __shfl_sync(0xffffffffu, X, sbl), yb = __shfl_sync(0xffffffffu, Y, sbl);
@@ -597,7 +611,8 @@ __device__ __forceinline__ void residual_compute(const ResidualRefs rr, const __
 #pragma unroll
     for (int mm = 0; mm < 8; ++mm) {
         rp.o[mm][0] = rp.o[mm][1] = rp.o[mm][2] = rp.o[mm][3] = 0.f;
-        mma16816_bf16(rp.o[mm], vf[mm][0], vf[mm][1], vf[mm][2], vf[mm][3], b0, b1);
+        if (rr.f16) mma16816(rp.o[mm], vf[mm][0], vf[mm][1], vf[mm][2], vf[mm][3], b0, b1);
+        else mma16816_bf16(rp.o[mm], vf[mm][0], vf[mm][1], vf[mm][2], vf[mm][3], b0, b1);
     }
     rp.m0 = m0;
     rp.m1 = m1;
@@ -964,6 +979,7 @@ __global__ void __launch_bounds__(NCW_ * 32, 1) decode_attn_kernel(const AttnArg
                 rr.g = g;
                 rr.r = a.r;
                 rr.rotate_v = a.rotate_v;
+                rr.f16 = a.ring_f16;
                 residual_tile(rr, slot, qbase, j * 16, ntok, lane, c0,
                               a.write_ring ? reinterpret_cast<uint16_t *>(a.ring_k) + bh * R * D : nullptr,
                               reinterpret_cast<uint16_t *>(a.ring_v) + bh * R * D);
@@ -998,6 +1014,7 @@ __global__ void __launch_bounds__(NCW_ * 32, 1) decode_attn_kernel(const AttnArg
             rr.g = g;
             rr.r = a.r;
             rr.rotate_v = a.rotate_v;
+            rr.f16 = a.ring_f16;
             residual_tile(rr, slot, reinterpret_cast<const __nv_bfloat16 *>(a.q) + ((int64_t)b * a.Hq + kvh * g) * D,
                           j * 16, ntok, lane, c0,
                           a.write_ring ? reinterpret_cast<uint16_t *>(a.ring_k) + bh * R * D : nullptr,

@@ -109,6 +109,18 @@ struct oscar_kv_handle {
     // state (kv_cache.hpp:104-122), uniform over the batch
     bool prefilled = false;
     int64_t packed = 0, residual = 0, flushes = 0;
+    // input form, fixed by the first append: 1 = raw bf16 rows (append / decode_step:
+    // the key transform runs on the device), 2 = the reference's own form (append_k /
+    // append_v / decode_step_f64: transformed fp64 keys + norms, fp64 values).  In
+    // form 2 the K and V streams advance separately like k_/v_ state of the
+    // reference (kv_cache.hpp:104-122): packed / residual / prefilled count keys,
+    // v_packed / v_residual / v_prefilled values.
+    int form = 0;
+    bool v_prefilled = false;
+    int64_t v_packed = 0, v_residual = 0;
+    // form 2: the exact residual window (fp64 K_u rows [bh][R][D], norms [bh][R], V rows);
+    // the rings hold their bf16 image for the decode kernel
+    double *res_k = nullptr, *res_n = nullptr, *res_v = nullptr;
     // device memory
     uint8_t *blocks = nullptr;
     double *shadow = nullptr;
@@ -159,6 +171,9 @@ struct oscar_kv_handle {
         cudaFree(shadow);
         cudaFree(ring_k);
         cudaFree(ring_v);
+        cudaFree(res_k);
+        cudaFree(res_n);
+        cudaFree(res_v);
         cudaFree(part_o);
         cudaFree(part_ml);
         cudaFree(counters);
@@ -238,6 +253,7 @@ struct oscar_kv_handle {
     void append(const void *k, const void *v, int64_t n, cudaStream_t s) {
         const int64_t H = cfg.heads;
         if (n < 0) throw InvalidArg("append: negative token count");
+        use_form(1);
         if (packed + residual + n > max_tokens) throw InvalidArg("append: cache capacity exceeded");
         last_launches = 0;
         const int64_t sb = n * H * D, st = H * D, sh = D;
@@ -277,6 +293,134 @@ struct oscar_kv_handle {
         }
     }
 
+    // ---- input form ----------------------------------------------------------------
+    void use_form(int f) {
+        if (form == f) return;
+        if (form != 0)
+            throw LogicErr(f == 2 ? "fp64 appends: this cache holds raw bf16 appends (one input form per cache)"
+                                  : "raw bf16 appends: this cache holds fp64 appends (one input form per cache)");
+        if (f == 2) {
+            if (!quantizes(cfg)) throw InvalidArg("fp64 appends need a quantising config (bits 2 or 4)");
+            if (cfg.rotate_v)
+                throw InvalidArg("fp64 appends store value rows as given; explicit-V mode (rotate_v) is for raw appends");
+            res_k = (double *)dalloc(sizeof(double) * (size_t)(BH * R * D));
+            res_n = (double *)dalloc(sizeof(double) * (size_t)(BH * R));
+            res_v = (double *)dalloc(sizeof(double) * (size_t)(BH * R * D));
+        }
+        form = f;
+    }
+    void in_step(const char *what) const {
+        if (form == 2 && (packed != v_packed || residual != v_residual))
+            throw LogicErr(std::string(what) + ": key and value streams hold different token counts");
+    }
+    void quantize_f64(int part, F64Src src, F64Src nrm, int64_t tok0, int64_t nblk, int64_t blk0, cudaStream_t s) {
+        QuantizeF64Args a{};
+        a.src = src;
+        a.norms = nrm;
+        a.part = part;
+        a.bits = dbits;
+        a.B = (int)B;
+        a.H = (int)cfg.heads;
+        a.tok0 = tok0;
+        a.n_blocks = nblk;
+        a.blocks = blocks;
+        a.max_blocks = max_blocks;
+        a.blk0 = blk0;
+        a.shadow = shadow;
+        a.status = status_d;
+        CK(launch_quantize_f64(a, s));
+        ++last_launches;
+        blocks_written = true;
+    }
+    void window_f64(int part, F64Src src, F64Src nrm, int64_t tok0, int64_t n, int64_t slot0, cudaStream_t s) {
+        WindowF64Args a{};
+        a.src = src;
+        a.norms = nrm;
+        a.part = part;
+        a.B = (int)B;
+        a.H = (int)cfg.heads;
+        a.tok0 = tok0;
+        a.n = n;
+        a.slot0 = slot0;
+        a.rotates = rotates(cfg);
+        a.scales = scales(cfg);
+        a.res_k = res_k;
+        a.res_n = res_n;
+        a.res_v = res_v;
+        a.ring_k = ring_k;
+        a.ring_v = ring_v;
+        CK(launch_window_f64(a, s));
+        ++last_launches;
+    }
+    // buffer_quant_k (kv_cache.cpp:194-249) / buffer_quant_v (251-292) on fp64 rows:
+    // part 0 = transformed keys [B, n, H, d] + norms [B, n, H], part 1 = values [B, n, H, d]
+    void append_f64(int part, const double *x, const double *norms, int64_t n, cudaStream_t s) {
+        use_form(2);
+        const int64_t H = cfg.heads;
+        if (n < 0) throw InvalidArg("append: negative token count");
+        bool &pre = part == 0 ? prefilled : v_prefilled;
+        int64_t &pk = part == 0 ? packed : v_packed;
+        int64_t &res = part == 0 ? residual : v_residual;
+        if (pk + res + n > max_tokens) throw InvalidArg("append: cache capacity exceeded");
+        last_launches = 0;
+        const F64Src src{x, n * H * D, D, H * D};
+        const F64Src nrm{norms, n * H, 1, H};
+        if (!pre) {  // prefill branch: pack S - r tokens, keep r = S mod R (kv_cache.cpp:204-218)
+            pre = true;
+            const int64_t r = n % R;
+            if (n - r > 0) quantize_f64(part, src, nrm, 0, (n - r) / R, 0, s);
+            pk += n - r;
+            if (r > 0) window_f64(part, src, nrm, n - r, r, 0, s);
+            res = r;
+            return;
+        }
+        // decode branch: token by token, a flush at exactly R (kv_cache.cpp:219-249)
+        for (int64_t pos = 0; pos < n;) {
+            const int64_t take = std::min<int64_t>(n - pos, R - res);
+            window_f64(part, src, nrm, pos, take, res, s);
+            res += take;
+            pos += take;
+            if (res == R) flush_f64(part, s);
+        }
+    }
+    // flush_k_block / flush_v_block of the full window (the exact fp64 residual)
+    void flush_f64(int part, cudaStream_t s) {
+        const int64_t H = cfg.heads;
+        int64_t &pk = part == 0 ? packed : v_packed;
+        int64_t &res = part == 0 ? residual : v_residual;
+        const F64Src src{part == 0 ? res_k : res_v, H * R * D, R * D, D};
+        const F64Src nrm{res_n, H * R, R, 1};
+        quantize_f64(part, src, nrm, 0, 1, pk / R, s);
+        pk += R;
+        res = 0;
+        if (part == 0) ++flushes;
+    }
+    // decode_step (pipeline.cpp:292-323) with the current token in the reference's
+    // form: appended to both windows, attended over history + current at full
+    // precision, then the flush at R
+    void decode_step_f64(const void *q, const double *kt, const double *kn, const double *v, float *out, float *lse,
+                         cudaStream_t s) {
+        use_form(2);
+        in_step("decode_step");
+        if (packed + residual + 1 > max_tokens) throw InvalidArg("decode_step: cache capacity exceeded");
+        if (!prefilled) throw LogicErr("decode_step: empty cache (prefill first)");
+        const int64_t H = cfg.heads;
+        last_launches = 0;
+        window_f64(0, F64Src{kt, H * D, D, H * D}, F64Src{kn, H, 1, H}, 0, 1, residual, s);
+        window_f64(1, F64Src{v, H * D, D, H * D}, F64Src{nullptr, 0, 0, 0}, 0, 1, residual, s);
+        residual += 1;
+        v_residual += 1;
+        const int launches = last_launches;
+        AttnArgs a = attn_args(q, nullptr, nullptr, out, lse);
+        CK(launch_attention(dbits, a, s));
+        last_launches = launches + 1;
+        blocks_written = false;
+        if (residual == R) {
+            flush_f64(0, s);
+            flush_f64(1, s);
+        }
+    }
+
     AttnArgs attn_args(const void *q, const void *kc, const void *vc, float *out, float *lse) {
         AttnArgs a{};
         a.blocks = blocks;
@@ -293,6 +437,7 @@ struct oscar_kv_handle {
         a.ring_v = ring_v;
         a.r = (int)residual;
         a.write_ring = kc != nullptr;
+        a.ring_f16 = form == 2;
         a.rotates = dbits != 0 && rotates(cfg);
         a.scales = scales(cfg);
         a.rotate_v = dbits != 0 && cfg.rotate_v;
@@ -382,6 +527,7 @@ struct oscar_kv_handle {
         a.q = q;
         a.kcur = k;
         a.ring_k = ring_k;
+        a.ring_f16 = form == 2;
         a.r = (int)residual;
         a.rotates = dbits != 0 && rotates(cfg);
         a.logits = out;
@@ -393,6 +539,7 @@ struct oscar_kv_handle {
     void decode_step(const void *q, const void *k, const void *v, float *out, float *lse, cudaStream_t s,
                      const PeerPlan *pub = nullptr, uint32_t epoch = 0, float *logits_out = nullptr) {
         if (packed + residual + 1 > max_tokens) throw InvalidArg("decode_step: cache capacity exceeded");
+        use_form(1);
         last_launches = 0;
         // the logits read the window and the records before the attention kernel
         // writes the current token into the ring and before any flush
@@ -418,6 +565,7 @@ struct oscar_kv_handle {
                 uint32_t epoch = 0) {
         last_launches = 0;
         if (packed + residual == 0) throw LogicErr("attend: empty cache");
+        in_step("attend");
         AttnArgs a = attn_args(q, nullptr, nullptr, out, lse);
         if (pub) {
             a.pub = *pub;
@@ -590,6 +738,7 @@ struct HostCache {
 
 HostCache build_host_cache(oscar_kv_handle *h, int64_t b) {
     if (b < 0 || b >= h->B) throw InvalidArg("export: sequence index out of range");
+    h->in_step("export");
     if (h->last_stream) CK(cudaStreamSynchronize(h->last_stream));
     CK(cudaDeviceSynchronize());
     HostCache hc;
@@ -699,11 +848,27 @@ HostCache build_host_cache(oscar_kv_handle *h, int64_t b) {
             }
         }
     }
-    // residual window: raw bf16 ring -> K_u rows and norms (kv_cache.cpp:219-224)
+    // residual window: raw bf16 ring -> K_u rows and norms (kv_cache.cpp:219-224), or
+    // (fp64 form) the exact residual rows as appended
     hc.k_res.assign(hc.r * H * D, 0.0);
     hc.k_norms_res.assign(hc.r * H, 0.0);
     hc.v_res.assign(hc.r * H * D, 0.0);
     std::vector<uint16_t> rk(R * D), rv(R * D);
+    if (h->form == 2 && hc.r > 0) {
+        std::vector<double> xk(R * D), xn(R), xv(R * D);
+        for (int64_t hh = 0; hh < H; ++hh) {
+            const int64_t bh = b * H + hh;
+            CK(cudaMemcpy(xk.data(), h->res_k + bh * R * D, sizeof(double) * R * D, cudaMemcpyDeviceToHost));
+            CK(cudaMemcpy(xn.data(), h->res_n + bh * R, sizeof(double) * R, cudaMemcpyDeviceToHost));
+            CK(cudaMemcpy(xv.data(), h->res_v + bh * R * D, sizeof(double) * R * D, cudaMemcpyDeviceToHost));
+            for (int64_t t = 0; t < hc.r; ++t) {
+                for (int c = 0; c < D; ++c) hc.k_res[(t * H + hh) * D + c] = xk[t * D + c];
+                hc.k_norms_res[t * H + hh] = xn[t];
+                for (int c = 0; c < D; ++c) hc.v_res[(t * H + hh) * D + c] = xv[t * D + c];
+            }
+        }
+        return hc;
+    }
     for (int64_t hh = 0; hh < H; ++hh) {
         const int64_t bh = b * H + hh;
         if (hc.r == 0) break;
@@ -1033,20 +1198,50 @@ void load_kvc1(oscar_kv_handle *h, int64_t b, const char *path) {
                 }
             }
         }
-        // residual window -> raw bf16 rings (K token-major, V channel-major)
-        if (r > 0) {
-            uint16_t *rk = rings_k.data() + (size_t)(hh * R * D), *rv = rings_v.data() + (size_t)(hh * R * D);
+    }
+    // residual window -> raw bf16 rings (K token-major, V channel-major).  Rows that
+    // are not transforms of bf16 inputs (a cache the reference built from its fp64
+    // projections) put the handle in the fp64 form: the rows are kept exactly in
+    // the residual shadow and the rings hold their bf16 image
+    bool f64_res = h->form == 2;
+    if (r > 0 && !f64_res) {
+        try {
             std::vector<uint16_t> row(D);
+            for (int64_t hh = 0; hh < H; ++hh) {
+                uint16_t *rk = rings_k.data() + (size_t)(hh * R * D), *rv = rings_v.data() + (size_t)(hh * R * D);
+                for (int64_t t = 0; t < r; ++t) {
+                    raw_key_row(&kres[(t * H + hh) * D], kres_n[t * H + hh], tc, c.scaling, &rk[t * D]);
+                    raw_value_row(&vres[(t * H + hh) * D], c.rotate_v, row.data());
+                    for (int ch = 0; ch < D; ++ch) rv[(size_t)ch * R + t] = row[ch];
+                }
+            }
+        } catch (const InvalidArg &) {
+            if (h->form == 1) throw;  // the handle already holds raw bf16 appends
+            if (!bits) throw InvalidArg("cache load: residual rows are not transforms of bf16 inputs (method fp)");
+            if (c.rotate_v) throw InvalidArg("cache load: fp64 residual rows need rotate_v = 0");
+            f64_res = true;
+        }
+    }
+    if (r > 0 && f64_res) {
+        for (int64_t hh = 0; hh < H; ++hh) {
+            uint16_t *rk = rings_k.data() + (size_t)(hh * R * D), *rv = rings_v.data() + (size_t)(hh * R * D);
             for (int64_t t = 0; t < r; ++t) {
-                raw_key_row(&kres[(t * H + hh) * D], kres_n[t * H + hh], tc, c.scaling, &rk[t * D]);
-                raw_value_row(&vres[(t * H + hh) * D], c.rotate_v, row.data());
-                for (int ch = 0; ch < D; ++ch) rv[(size_t)ch * R + t] = row[ch];
+                // window_f64_kernel's image: FHT(K_u * s) (apply_method inverted), fp16
+                double x[D];
+                const double sn = kres_n[t * H + hh];
+                for (int ch = 0; ch < D; ++ch) x[ch] = tc.scales ? kres[(t * H + hh) * D + ch] * sn : kres[(t * H + hh) * D + ch];
+                if (tc.rotates) host::fht(x, D);
+                for (int ch = 0; ch < D; ++ch) {
+                    rk[t * D + ch] = double_to_half_rn(x[ch]);
+                    rv[(size_t)ch * R + t] = double_to_half_rn(vres[(t * H + hh) * D + ch]);
+                }
             }
         }
     }
     // (2) upload (only CUDA errors can fail from here on)
     CK(cudaSetDevice(h->device));
     if (h->last_stream) CK(cudaStreamSynchronize(h->last_stream));
+    if (f64_res) h->use_form(2);
     for (int64_t hh = 0; hh < H; ++hh) {
         const int64_t bh = b * H + hh;
         if (nb > 0) {
@@ -1056,6 +1251,19 @@ void load_kvc1(oscar_kv_handle *h, int64_t b, const char *path) {
                 CK(cudaMemcpy(h->shadow + bh * h->max_blocks * SHADOW_DOUBLES,
                               shadows.data() + (size_t)(hh * nb * SHADOW_DOUBLES),
                               sizeof(double) * (size_t)(nb * SHADOW_DOUBLES), cudaMemcpyHostToDevice));
+        }
+        if (r > 0 && f64_res) {
+            std::vector<double> xk((size_t)(R * D), 0.0), xn((size_t)R, 0.0), xv((size_t)(R * D), 0.0);
+            for (int64_t t = 0; t < r; ++t) {
+                for (int ch = 0; ch < D; ++ch) {
+                    xk[(size_t)(t * D + ch)] = kres[(t * H + hh) * D + ch];
+                    xv[(size_t)(t * D + ch)] = vres[(t * H + hh) * D + ch];
+                }
+                xn[(size_t)t] = kres_n[t * H + hh];
+            }
+            CK(cudaMemcpy(h->res_k + bh * R * D, xk.data(), sizeof(double) * R * D, cudaMemcpyHostToDevice));
+            CK(cudaMemcpy(h->res_n + bh * R, xn.data(), sizeof(double) * R, cudaMemcpyHostToDevice));
+            CK(cudaMemcpy(h->res_v + bh * R * D, xv.data(), sizeof(double) * R * D, cudaMemcpyHostToDevice));
         }
         if (r > 0) {
             CK(cudaMemcpy(reinterpret_cast<uint16_t *>(h->ring_k) + bh * R * D, rings_k.data() + (size_t)(hh * R * D),
@@ -1070,6 +1278,9 @@ void load_kvc1(oscar_kv_handle *h, int64_t b, const char *path) {
         h->residual = r;
         h->flushes = flushes;
         h->prefilled = m.flag("k_prefilled");
+        h->v_packed = packed;
+        h->v_residual = r;
+        h->v_prefilled = m.flag("v_prefilled");
     }
     h->blocks_written = true;  // the next attention launch waits before touching the records
 }
@@ -1147,6 +1358,103 @@ int oscar_kv_append(oscar_kv_handle *h, const void *k, const void *v, int64_t n_
         CK(cudaSetDevice(h->device));
         h->last_stream = (cudaStream_t)stream;
         h->append(k, v, n_tokens, (cudaStream_t)stream);
+    });
+}
+
+namespace {
+// fp64 rows given in host memory (the reference's Tensor3 callers): staged to the
+// device for the call (a compatibility path; synchronises the stream before the
+// staging buffer is released)
+struct F64Stage {
+    double *d = nullptr;
+    cudaStream_t s = nullptr;
+    const double *view(const double *p, size_t n, cudaStream_t st) {
+        if (!p || n == 0) return p;
+        cudaPointerAttributes at{};
+        if (cudaPointerGetAttributes(&at, p) != cudaSuccess) (void)cudaGetLastError();
+        if (at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged) return p;
+        CK(cudaMalloc(&d, n * sizeof(double)));
+        CK(cudaMemcpyAsync(d, p, n * sizeof(double), cudaMemcpyHostToDevice, st));
+        s = st;
+        return d;
+    }
+    ~F64Stage() {
+        if (d) {
+            cudaStreamSynchronize(s);
+            cudaFree(d);
+        }
+    }
+};
+}  // namespace
+
+int oscar_kv_append_k(oscar_kv_handle *h, const double *k_t, const double *norms, int64_t n_tokens, void *stream) {
+    return guard([&] {
+        if (!h || (n_tokens > 0 && (!k_t || !norms))) throw InvalidArg("append_k: null argument");
+        CK(cudaSetDevice(h->device));
+        cudaStream_t s = (cudaStream_t)stream;
+        h->last_stream = s;
+        const size_t n = (size_t)(h->B * std::max<int64_t>(n_tokens, 0) * h->cfg.heads);
+        F64Stage sk, sn;
+        h->append_f64(0, sk.view(k_t, n * D, s), sn.view(norms, n, s), n_tokens, s);
+    });
+}
+
+int oscar_kv_append_v(oscar_kv_handle *h, const double *v, int64_t n_tokens, void *stream) {
+    return guard([&] {
+        if (!h || (n_tokens > 0 && !v)) throw InvalidArg("append_v: null argument");
+        CK(cudaSetDevice(h->device));
+        cudaStream_t s = (cudaStream_t)stream;
+        h->last_stream = s;
+        const size_t n = (size_t)(h->B * std::max<int64_t>(n_tokens, 0) * h->cfg.heads);
+        F64Stage sv;
+        h->append_f64(1, sv.view(v, n * D, s), nullptr, n_tokens, s);
+    });
+}
+
+int oscar_kv_decode_step_f64(oscar_kv_handle *h, const void *q, const double *k_t, const double *norms,
+                             const double *v, float *out, float *lse, void *stream) {
+    return guard([&] {
+        if (!h || !q || !k_t || !norms || !v || !out) throw InvalidArg("decode_step: null argument");
+        CK(cudaSetDevice(h->device));
+        h->last_stream = (cudaStream_t)stream;
+        h->decode_step_f64(q, k_t, norms, v, out, lse, (cudaStream_t)stream);
+    });
+}
+
+int oscar_kv_stats_v(const oscar_kv_handle *h, int64_t *v_packed, int64_t *v_residual) {
+    return guard([&] {
+        if (!h) throw InvalidArg("null handle");
+        const bool f2 = h->form == 2;
+        if (v_packed) *v_packed = f2 ? h->v_packed : h->packed;
+        if (v_residual) *v_residual = f2 ? h->v_residual : h->residual;
+    });
+}
+
+int oscar_kvc1_read_config(const char *path, oscar_kv_config *cfg, int64_t *tokens) {
+    return guard([&] {
+        if (!path || !cfg) throw InvalidArg("kvc1_read_config: null argument");
+        std::ifstream f(path, std::ios::binary);
+        if (!f) throw std::runtime_error(std::string("cache load: cannot open ") + path);
+        Manifest m;
+        std::getline(f, m.text);
+        if (m.raw("magic") != "KVC1") throw std::runtime_error("cache load: bad magic");
+        oscar_kv_config c{};
+        const std::string meth = m.raw("method"), sc = m.raw("scaling");
+        c.method = -1;
+        for (int i = 0; i < 5; ++i)
+            if (meth == method_name(i)) c.method = i;
+        c.scaling = -1;
+        for (int i = 0; i < 4; ++i)
+            if (sc == scaling_name(i)) c.scaling = i;
+        if (c.method < 0 || c.scaling < 0) throw InvalidArg("cache load: unknown method or scaling in the manifest");
+        c.bits = (int32_t)m.i("b");
+        c.group_size = m.i("G");
+        c.residual_len = m.i("R");
+        c.head_dim = m.i("d_h");
+        c.heads = m.i("H");
+        c.rotate_v = 0;
+        *cfg = c;
+        if (tokens) *tokens = m.i("S_packed") + m.i("residual_tokens");
     });
 }
 

@@ -82,6 +82,39 @@ struct RingCopyArgs {
 };
 cudaError_t launch_ring_copy(const RingCopyArgs &a, cudaStream_t st);
 
+// ---- reference-form fp64 appends (f64_path.cu) ----------------------------------
+// strided fp64 rows: element (b, h, t, c) at p[b*sb + h*sh + t*st + c] (norms: c = 0)
+struct F64Src {
+    const double *p;
+    int64_t sb, sh, st;
+};
+// one R-block per (block, b*H + h): the K part (part 0: K_u rows + norms) or the
+// V part (part 1) of records blk0 + i from source tokens tok0 + i*R ...
+struct QuantizeF64Args {
+    F64Src src, norms;
+    int part, bits;
+    int B, H;
+    int64_t tok0, n_blocks;
+    uint8_t *blocks;
+    int64_t max_blocks, blk0;
+    double *shadow;  // [bh][max_blocks][SHADOW_DOUBLES]
+    int *status;
+};
+cudaError_t launch_quantize_f64(const QuantizeF64Args &a, cudaStream_t st);
+// n tokens (source tokens tok0 ...) into window slots slot0 ...: the exact fp64
+// residual (res_k / res_n or res_v, [bh][R][D] / [bh][R]) and the bf16 image the
+// decode kernel attends (rings)
+struct WindowF64Args {
+    F64Src src, norms;
+    int part;
+    int B, H;
+    int64_t tok0, n, slot0;
+    int rotates, scales;
+    double *res_k, *res_n, *res_v;  // (the rings take fp16 images)
+    void *ring_k, *ring_v;
+};
+cudaError_t launch_window_f64(const WindowF64Args &a, cudaStream_t st);
+
 // Sequence-shard exchange plan (C5): rank r's receive area recv[r] holds
 // [2 parities][world][rows][PEER_STRIDE] floats (O[0..127], LSE at 128) and
 // flags[r] holds [2][world][rows] epochs; both live on rank r's GPU and are
@@ -108,6 +141,8 @@ struct AttnArgs {
     void *ring_k, *ring_v;    // K [bh][R][D], V [bh][D][R]
     int r;             // residual rows in ring
     int write_ring;    // store kcur/vcur at ring slot r
+    int ring_f16;      // rings hold fp16 images (fp64-form caches: the exact rows are in the
+                       // residual shadow; fp16 keeps the window's rounding 8x below bf16's)
     int rotates;       // rotate q for the packed part
     int scales;        // unused on device (norms are stored), kept for clarity
     int rotate_v;      // un-rotate output
@@ -146,6 +181,7 @@ struct LogitsArgs {
     const void *q;            // bf16 [B][Hq][D]
     const void *kcur;         // bf16 [B][Hkv][D] or null
     const void *ring_k;       // K ring [bh][R][D]
+    int ring_f16;             // ring K holds fp16 (fp64-form caches) instead of bf16
     int r;                    // window tokens
     int rotates;              // rotate q for the packed tokens
     float *logits;

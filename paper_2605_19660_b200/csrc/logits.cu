@@ -105,8 +105,9 @@ __global__ void __launch_bounds__(128) logits_kernel(const LogitsArgs a) {
             krow = a.kcur;
             off = (int64_t)bh * D;
         }
+        const bool f16 = a.ring_f16 && tid < a.r;
         for (int c = 0; c < D; ++c) {
-            const float kv = bf16_at(krow, off + c);
+            const float kv = f16 ? __half2float(reinterpret_cast<const __half *>(krow)[off + c]) : bf16_at(krow, off + c);
 #pragma unroll
             for (int j = 0; j < 8; ++j)
                 if (j < g) acc[j] += qs[j][c] * kv;

@@ -24,6 +24,7 @@
 #include "device_common.cuh"
 #include "kernels.h"
 #include "layout.h"
+#include "quant_common.cuh"
 
 namespace osk {
 
@@ -35,11 +36,6 @@ constexpr int KU_ROW = 4 * 33;  // doubles per token row of the K_u tile (4 quar
 // gathers of the pack loop (and the V code writes) at most 2-way bank conflicted
 // (128 was 4-way for K, 8-way for V) while three CTAs still fit per SM
 constexpr int CODE_STRIDE = D + 4;
-
-__device__ __forceinline__ double dadd(double a, double b) { return __dadd_rn(a, b); }
-__device__ __forceinline__ double dsub(double a, double b) { return __dsub_rn(a, b); }
-__device__ __forceinline__ double dmul(double a, double b) { return __dmul_rn(a, b); }
-__device__ __forceinline__ double ddiv(double a, double b) { return __ddiv_rn(a, b); }
 
 // 32 bf16 -> fp64 (exact); bit 15 / 31 of `bad` flags non-finite inputs
 __device__ __forceinline__ void load32(const __nv_bfloat16 *p, double (&x)[32], uint32_t &bad) {
@@ -119,33 +115,6 @@ __device__ __forceinline__ double quad_chain(const double (&x)[32], int q, int l
     return acc;
 }
 
-// quant.cpp:21-47 on 32 values in index order; returns delta, zp, lo, hi
-struct GroupQ {
-    double lo, hi, delta;
-    long long zp;
-};
-template <typename Get>
-__device__ __forceinline__ GroupQ group_params(Get get, int bits) {
-    GroupQ p;
-    double lo = get(0), hi = lo;
-#pragma unroll
-    for (int i = 0; i < 32; ++i) {
-        const double x = get(i);
-        lo = (x < lo) ? x : lo;  // std::min(lo, x)
-        hi = (hi < x) ? x : hi;  // std::max(hi, x)
-    }
-    p.lo = lo;
-    p.hi = hi;
-    if (hi == lo) {
-        p.delta = 0.0;
-        p.zp = 0;
-    } else {
-        p.delta = ddiv(dsub(hi, lo), (double)((1 << bits) - 1));
-        p.zp = llround(ddiv(-lo, p.delta));
-    }
-    return p;
-}
-
 // group_params for values that are exactly representable in fp32
 __device__ __forceinline__ GroupQ group_params_f32(const double (&y)[32], int bits) {
     float lo = (float)y[0], hi = lo;
@@ -166,61 +135,6 @@ __device__ __forceinline__ GroupQ group_params_f32(const double (&y)[32], int bi
         p.zp = llround(ddiv(-p.lo, p.delta));
     }
     return p;
-}
-
-// quant.cpp:53-57 over one group: q = clamp(llround(x / delta) + zp, 0, 2^b-1).
-// x / delta is taken as x * (1/delta) -- within 2 ulp of the IEEE quotient --
-// and rounded branch-free; an element whose product lies within 1e-9 of a
-// half-integer (where the two could round apart; 2 ulp < 1e-9 while
-// |x/delta| < 2^20, checked once per group) is redone with the exact IEEE
-// division afterwards.  The codes are bit-identical to the reference's.
-template <typename Get, typename Put>
-__device__ __forceinline__ void quantize_group(Get get, const GroupQ &p, int bits, Put put) {
-    const int mx = (1 << bits) - 1;
-    if (p.delta == 0.0) {
-#pragma unroll
-        for (int i = 0; i < 32; ++i) put(i, 0);
-        return;
-    }
-    const double inv = ddiv(1.0, p.delta);
-    const bool fast = dmul(fmax(fabs(p.lo), fabs(p.hi)), inv) < 1048576.0;
-    // codes saturate, so a zero point beyond +-2^30 acts like +-2^30
-    const int zp = p.zp > (1ll << 30) ? (1 << 30) : (p.zp < -(1ll << 30) ? -(1 << 30) : (int)p.zp);
-    unsigned tie = 0;
-#pragma unroll
-    for (int i = 0; i < 32; ++i) {
-        const double y = dmul(get(i), inv);
-        const double fl = floor(y);
-        const double fr = dsub(y, fl);
-        tie |= (fabs(dsub(fr, 0.5)) <= 1e-9 ? 1u : 0u) << i;
-        const int q = (int)fl + (fr > 0.5 ? 1 : 0) + zp;
-        put(i, q < 0 ? 0 : (q > mx ? mx : q));
-    }
-    if (!fast || tie) {  // rare: exact division for the flagged elements
-        for (int i = 0; i < 32; ++i) {
-            if (fast && !((tie >> i) & 1u)) continue;
-            long long q = llround(ddiv(get(i), p.delta)) + p.zp;
-            put(i, (int)(q < 0 ? 0 : (q > mx ? mx : q)));
-        }
-    }
-}
-
-// affine fp16 form used by the attention kernel: x = a*code + b
-__device__ __forceinline__ void affine16(const GroupQ &p, __half &a, __half &b) {
-    if (p.delta == 0.0) {
-        a = __double2half(0.0);
-        b = __double2half(p.lo);
-    } else {
-        a = __double2half(p.delta);
-        b = __double2half(dmul(p.delta, -(double)p.zp));
-    }
-}
-
-// device status (QuantizeArgs::status): record overflow / non-finite input
-__device__ __forceinline__ void flag_status(int *status, const GroupQ &p, __half ha, __half hb) {
-    if (!status) return;
-    // (non-finite inputs are flagged where they are loaded)
-    if (isfinite(p.lo) && isfinite(p.hi) && (__hisinf(ha) || __hisinf(hb))) atomicOr(status, STATUS_FP16_OVERFLOW);
 }
 
 // GPAR 32-token groups of the block are processed concurrently by GPAR

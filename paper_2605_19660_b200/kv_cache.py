@@ -88,6 +88,11 @@ def lib():
         L.oscar_kv_logits.argtypes = [_P, _P, _P, _P, _P]
         L.oscar_kv_decode_step_many.argtypes = [ctypes.c_int32, _P, _P, _P, _P, _P, _P, _P]
         L.oscar_kv_decode_step_host.argtypes = [_P, _P, _P, _P, _P, _P, _P]
+        L.oscar_kv_append_k.argtypes = [_P, _P, _P, ctypes.c_int64, _P]
+        L.oscar_kv_append_v.argtypes = [_P, _P, ctypes.c_int64, _P]
+        L.oscar_kv_decode_step_f64.argtypes = [_P, _P, _P, _P, _P, _P, _P, _P]
+        L.oscar_kv_stats_v.argtypes = [_P, ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(ctypes.c_int64)]
+        L.oscar_kvc1_read_config.argtypes = [ctypes.c_char_p, ctypes.POINTER(_Config), ctypes.POINTER(ctypes.c_int64)]
         L.oscar_kv_stats.argtypes = [_P, ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(ctypes.c_int64),
                                      ctypes.POINTER(ctypes.c_int64)]
         L.oscar_kv_memory_report.argtypes = [_P, ctypes.POINTER(_MemReport)]
@@ -119,6 +124,7 @@ C_ABI_SYMBOLS = [
     "oscar_kv_last_launch_count", "oscar_peer_area_bytes", "oscar_kv_attend_publish", "oscar_peer_publish_empty",
     "oscar_peer_merge", "oscar_ipc_alloc", "oscar_ipc_open", "oscar_ipc_close", "oscar_ipc_free",
     "oscar_kv_status", "oscar_kv_decode_step_logits", "oscar_kv_logits",
+    "oscar_kv_append_k", "oscar_kv_append_v", "oscar_kv_decode_step_f64", "oscar_kv_stats_v", "oscar_kvc1_read_config",
 ]
 
 
@@ -186,7 +192,7 @@ def _need(t, name: str, device: int, dtype: str, shape=None, numel=None):
     if not isinstance(t, torch.Tensor) or not t.is_cuda or t.device.index != device:
         raise ValueError(f"{name}: expected a CUDA tensor on cuda:{device}, got "
                          f"{getattr(t, 'device', type(t).__name__)}")
-    want = {"bf16": torch.bfloat16, "f32": torch.float32}[dtype]
+    want = {"bf16": torch.bfloat16, "f32": torch.float32, "f64": torch.float64}[dtype]
     if t.dtype != want:
         raise ValueError(f"{name}: expected {want}, got {t.dtype}")
     if not t.is_contiguous():
@@ -242,6 +248,44 @@ class KvCache:
         _check(lib().oscar_kv_append(self._h, _ptr(k), _ptr(v), n, _stream(stream)))
 
     append = buffer_quant
+
+    # ---- the reference's own call shapes: fp64 rows (kv_cache.hpp:80-84) ------------
+    def buffer_quant_k(self, k_t, norms, stream=None):
+        """KvCache::buffer_quant_k (kv_cache.cpp:194-249): k_t fp64 CUDA tensor
+        [B, n, H, d] of ALREADY transformed keys K_u, norms fp64 [B, n, H]."""
+        n = k_t.shape[1]
+        _need(k_t, "buffer_quant_k k_t", self.device, "f64", (self.B, n, self.H, D))
+        _need(norms, "buffer_quant_k norms", self.device, "f64", (self.B, n, self.H))
+        _check(lib().oscar_kv_append_k(self._h, _ptr(k_t), _ptr(norms), n, _stream(stream)))
+
+    def buffer_quant_v(self, v, stream=None):
+        """KvCache::buffer_quant_v (kv_cache.cpp:251-292): v fp64 [B, n, H, d], stored as given."""
+        n = v.shape[1]
+        _need(v, "buffer_quant_v v", self.device, "f64", (self.B, n, self.H, D))
+        _check(lib().oscar_kv_append_v(self._h, _ptr(v), n, _stream(stream)))
+
+    def decode_step_f64(self, q, k_t, norms, v, out=None, lse=None, stream=None):
+        """decode_step with the current token in the reference's form: q bf16 [B, Hq, d],
+        k_t fp64 [B, H, d], norms fp64 [B, H], v fp64 [B, H, d]."""
+        import torch
+
+        _need(q, "q", self.device, "bf16", (self.B, self.Hq, D))
+        _need(k_t, "k_t", self.device, "f64", (self.B, self.H, D))
+        _need(norms, "norms", self.device, "f64", (self.B, self.H))
+        _need(v, "v", self.device, "f64", (self.B, self.H, D))
+        if out is None:
+            out = torch.empty((self.B, self.Hq, D), dtype=torch.float32, device=q.device)
+        self._check_out(out, lse)
+        _check(lib().oscar_kv_decode_step_f64(self._h, _ptr(q), _ptr(k_t), _ptr(norms), _ptr(v), _ptr(out),
+                                              _ptr(lse), _stream(stream)))
+        return out
+
+    @property
+    def v_tokens(self):
+        """(v_packed, v_residual): the value stream's counters (fp64 form)."""
+        p, r = ctypes.c_int64(), ctypes.c_int64()
+        _check(lib().oscar_kv_stats_v(self._h, ctypes.byref(p), ctypes.byref(r)))
+        return p.value, r.value
 
     # ---- decode_step body (pipeline.cpp:292-323) --------------------------------
     def decode_step(self, q, k, v, out=None, lse=None, stream=None, logits=None):
@@ -390,6 +434,15 @@ class KvCache:
         """KvCache::load (kv_cache.cpp:509-549) into sequence b."""
         _check(lib().oscar_kv_load(self._h, b, path.encode()))
 
+    @classmethod
+    def from_kvc1(cls, path: str, q_heads: int, max_tokens: int | None = None, device: int = 0) -> "KvCache":
+        """static KvCache::load(path) (kv_cache.hpp:95): a one-sequence cache with
+        the file's config, holding the file's contents."""
+        cfg, tokens = read_kvc1_config(path)
+        c = cls(cfg, batch=1, q_heads=q_heads, max_tokens=max_tokens or tokens + cfg.residual_len, device=device)
+        c.load(0, path)
+        return c
+
     def materialize(self, b: int = 0):
         """materialize_k / materialize_v (kv_cache.cpp:327-381) of sequence b."""
         n = self.total_tokens
@@ -510,3 +563,15 @@ def ipc_close(ptr: int):
 
 def ipc_free(ptr: int):
     _check(lib().oscar_ipc_free(_P(ptr)))
+
+
+def read_kvc1_config(path: str):
+    """(PipelineConfig, tokens) of a KVC1 file's manifest (oscar_kvc1_read_config)."""
+    c = _Config()
+    n = ctypes.c_int64()
+    _check(lib().oscar_kvc1_read_config(path.encode(), ctypes.byref(c), ctypes.byref(n)))
+    inv_m = {v: k for k, v in METHODS.items()}
+    inv_s = {v: k for k, v in SCALINGS.items()}
+    cfg = PipelineConfig(method=inv_m[c.method], bits=c.bits, group_size=c.group_size, residual_len=c.residual_len,
+                         scaling=inv_s[c.scaling], head_dim=c.head_dim, heads=c.heads, rotate_v=bool(c.rotate_v))
+    return cfg, n.value

@@ -158,3 +158,106 @@ def test_cpp_program_drives_the_device_cache():
         theirs = os.path.join(td, "ref.kvc1")
         ref.dump(theirs)
         assert open(os.path.join(td, "cpp.kvc1"), "rb").read() == open(theirs, "rb").read()
+
+
+PROGRAM_F64 = r"""
+#include <cstdint>
+#include <cstdio>
+#include <string>
+#include <vector>
+#include "oscar_kv.hpp"
+
+static uint64_t st = 0x2545F4914F6CDD1Dull;
+static double next_f64(double scale) {  // LCG -> uniform(-2, 2) * scale, exact in fp64
+    st = st * 6364136223846793005ull + 1442695040888963407ull;
+    return ((double)(st >> 11) * 0x1p-53 - 0.5) * 4.0 * scale;
+}
+
+int main(int argc, char **argv) {
+    const int64_t H = 2, D = 128, S = 300, Hq = 8;
+    const std::string dir = argv[1];
+    oscar_b200::PipelineConfig pc;
+    pc.heads = H;
+    pc.bits = 2;
+    // the reference's calls, the reference's types: Tensor3 K_u + norms, Tensor3 V
+    oscar_b200::Tensor3 kt(S, H, D), v(S, H, D);
+    std::vector<double> norms(S * H);
+    for (int64_t t = 0; t < S; ++t)
+        for (int64_t h = 0; h < H; ++h) {
+            for (int64_t c = 0; c < D; ++c) kt.at(t, h, c) = next_f64(c < 4 ? 8.0 : 1.0);
+            for (int64_t c = 0; c < D; ++c) v.at(t, h, c) = next_f64(1.0);
+            norms[t * H + h] = 2.0 + next_f64(0.25);
+        }
+    oscar_b200::KvCache cache(pc, /*batch=*/1, Hq, S + 64, 0);
+    cache.buffer_quant_k(kt, norms);
+    cache.buffer_quant_v(v);
+    cache.dump(0, dir + "/f64.kvc1");
+    // static KvCache::load: config from the file
+    oscar_b200::KvCache loaded = oscar_b200::KvCache::load(dir + "/f64.kvc1", Hq);
+    const oscar_b200::Tensor3 mk = loaded.materialize_k(), mv = loaded.materialize_v();
+    FILE *f = std::fopen((dir + "/mat.bin").c_str(), "wb");
+    std::fwrite(mk.data.data(), 8, mk.data.size(), f);
+    std::fwrite(mv.data.data(), 8, mv.data.size(), f);
+    std::fclose(f);
+    int caught = 0;
+    oscar_b200::KvCache two(pc, /*batch=*/2, Hq, 64, 0);
+    try { two.buffer_quant_k(kt, norms); } catch (const std::invalid_argument &) { ++caught; }
+    try { cache.buffer_quant(nullptr, nullptr, 0); } catch (const std::logic_error &) { ++caught; }  // form mix
+    std::printf("packed %lld residual %lld loaded %lld %lld caught %d\n", (long long)cache.packed_tokens(),
+                (long long)cache.residual_tokens(), (long long)loaded.packed_tokens(),
+                (long long)loaded.residual_tokens(), caught);
+    return 0;
+}
+"""
+
+
+def _lcg_f64(S, H, D=128):
+    st = 0x2545F4914F6CDD1D
+    M = (1 << 64) - 1
+
+    def nxt(scale):
+        nonlocal st
+        st = (st * 6364136223846793005 + 1442695040888963407) & M
+        return (float(st >> 11) * 2.0 ** -53 - 0.5) * 4.0 * scale
+
+    kt = np.zeros((S, H, D))
+    v = np.zeros((S, H, D))
+    nr = np.zeros(S * H)
+    for t in range(S):
+        for h in range(H):
+            for c in range(D):
+                kt[t, h, c] = nxt(8.0 if c < 4 else 1.0)
+            for c in range(D):
+                v[t, h, c] = nxt(1.0)
+            nr[t * H + h] = 2.0 + nxt(0.25)
+    return kt, nr, v
+
+
+def test_cpp_reference_call_shapes():
+    """buffer_quant_k(Tensor3 K_u, norms) / buffer_quant_v(Tensor3) from host fp64
+    rows, static KvCache::load(path) and Tensor3 materialize_k / materialize_v
+    through the C++ wrapper: the dump is the reference's dump byte for byte and
+    the materialised rows are the reference's materialize_k / _v exactly."""
+    if shutil.which("g++") is None:
+        pytest.skip("no g++")
+    S, H = 300, 2
+    with tempfile.TemporaryDirectory() as td:
+        src = os.path.join(td, "prog.cpp")
+        with open(src, "w") as f:
+            f.write(PROGRAM_F64)
+        exe = os.path.join(td, "prog")
+        subprocess.run(["g++", "-std=c++17", "-O1", "-ffp-contract=off", "-I", os.path.join(ROOT, "include"),
+                        src, "-o", exe, "-L", LIBDIR, "-loscar_b200", f"-Wl,-rpath,{LIBDIR}"], check=True)
+        r = subprocess.run([exe, td], capture_output=True, text=True, timeout=300)
+        assert r.returncode == 0, r.stdout + r.stderr
+        assert r.stdout.strip() == "packed 256 residual 44 loaded 256 44 caught 2", r.stdout
+        kt, nr, v = _lcg_f64(S, H)
+        ref = ob.RefCache(H=H, bits=2)
+        ref.buffer_quant_k(kt, nr)
+        ref.buffer_quant_v(v)
+        theirs = os.path.join(td, "ref.kvc1")
+        ref.dump(theirs)
+        assert open(os.path.join(td, "f64.kvc1"), "rb").read() == open(theirs, "rb").read()
+        mat = np.fromfile(os.path.join(td, "mat.bin"), np.float64).reshape(2, S, H, 128)
+        rk, rv = ref.materialize()
+        assert np.array_equal(mat[0], rk) and np.array_equal(mat[1], rv)

@@ -717,6 +717,26 @@ __device__ __noinline__ void residual_tile(const ResidualRefs rr, float *slot, c
     }
 }
 
+// The tile as the warp's INITIAL partial of its segment (computed before the
+// packed units, while the CTA's ring fills -- its L2 round trip then costs no
+// streaming time): the partial is returned, the current token written to the rings.
+__device__ __noinline__ void residual_tile_first(const ResidualRefs rr, const __nv_bfloat16 *qbase, int t0, int ntok,
+                                                 int lane, float c0, uint16_t *ring_k_w, uint16_t *ring_v_w,
+                                                 ResPartial *out) {
+    ResPartial rp;
+    residual_compute(rr, qbase, t0, ntok, lane, c0, rp);
+    *out = rp;
+    if (ring_k_w && rr.kc && t0 <= rr.r && rr.r < t0 + 16) {
+        reinterpret_cast<uint2 *>(ring_k_w + rr.r * D)[lane] = reinterpret_cast<const uint2 *>(rr.kc)[lane];
+        const uint2 vv = reinterpret_cast<const uint2 *>(rr.vc)[lane];  // V ring is channel-major [D][R]
+        uint16_t *rv = ring_v_w + rr.r;
+        rv[(4 * lane + 0) * R] = (uint16_t)(vv.x & 0xffffu);
+        rv[(4 * lane + 1) * R] = (uint16_t)(vv.x >> 16);
+        rv[(4 * lane + 2) * R] = (uint16_t)(vv.y & 0xffffu);
+        rv[(4 * lane + 3) * R] = (uint16_t)(vv.y >> 16);
+    }
+}
+
 // DEFER: the tiles of a CTA's tail segments after its first run once the packed
 // units are done (launches where a CTA spans many (b, kv head) segments)
 template <int BITS, int NCW_, bool DEFER>
@@ -731,7 +751,9 @@ __global__ void __launch_bounds__(NCW_ * 32, 1) decode_attn_kernel(const AttnArg
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int gq = lane >> 2, tq = lane & 3;
-    const int cta = blockIdx.x;
+    // (cta_perm: experiments -- which stream-K range a block takes; the scratch and
+    //  partial indexing follow the range, so any permutation is consistent)
+    const int cta = a.cta_perm ? (int)((blockIdx.x * (unsigned)a.cta_perm) % (unsigned)a.ncta) : (int)blockIdx.x;
     const int g = a.g;
     const int64_t nb = a.nb * SUB;  // pipeline units per (b, kv head)
     const int64_t total = (int64_t)a.BH * nb;
@@ -849,6 +871,74 @@ __global__ void __launch_bounds__(NCW_ * 32, 1) decode_attn_kernel(const AttnArg
         st.l[0] = st.l[1] = 0.f;
         if (kProf && a.prof) tmr[6] += clk() - tq0;
 
+        // ---- residual window + current token on the tensor cores (bf16 mma, raw q . raw k:
+        //      the key transform is orthonormal up to the stored norm, so attending the raw
+        //      bf16 rows IS attend_one over the full-precision residual, pipeline.cpp:152-180):
+        //      one 16-token tile per warp of the tail owner (all its loads in one round trip).
+        //      The tile runs FIRST and seeds the warp's partial (its latency overlaps the ring
+        //      fill); in explicit-V mode (its partial is rotated head by head) and for the
+        //      deferred tails it is merged into the slot after the packed units instead ----
+        const int ntok_t = a.r + (a.kcur ? 1 : 0);
+        const int ntiles_t = (ntok_t + 15) >> 4;
+        int tile_j = -1;     // this warp's tile of this segment
+        bool tile_late = false;
+        if (owns_tail) {
+            const int j = (warp - rtile_base % NCW + NCW) % NCW;
+            rtile_base += ntiles_t;
+            bool now = true;
+            if constexpr (DEFER) {
+                now = !seen_tail;
+                seen_tail = true;
+            }
+            if (now && j < ntiles_t) {
+                tile_j = j;
+                tile_late = a.rotate_v != 0;
+            }
+        }
+        auto tile_refs = [&]() {
+            ResidualRefs rr;
+            rr.ringk = reinterpret_cast<const uint16_t *>(a.ring_k) + bh * R * D;
+            rr.ringv = reinterpret_cast<const uint16_t *>(a.ring_v) + bh * R * D;
+            rr.kc = a.kcur ? reinterpret_cast<const uint16_t *>(a.kcur) + ((int64_t)b * a.Hkv + kvh) * D : nullptr;
+            rr.vc = a.vcur ? reinterpret_cast<const uint16_t *>(a.vcur) + ((int64_t)b * a.Hkv + kvh) * D : nullptr;
+            rr.g = g;
+            rr.r = a.r;
+            rr.rotate_v = a.rotate_v;
+            rr.f16 = a.ring_f16;
+            return rr;
+        };
+        if (tile_j >= 0 && !tile_late) {
+            ResPartial rp;
+            residual_tile_first(tile_refs(), qbase, tile_j * 16, ntok_t, lane, c0,
+                                a.write_ring ? reinterpret_cast<uint16_t *>(a.ring_k) + bh * R * D : nullptr,
+                                reinterpret_cast<uint16_t *>(a.ring_v) + bh * R * D, &rp);
+            // the tile's partial in the packed accumulators' domain: o per m-tile in units of
+            // the code-field scale (exact powers of two), the denominator in the value-offset
+            // MMA's ones row (lanes gq == 4) -- or, for the bf16 baseline, st.l on one lane row
+            constexpr int TPW_ = BITS == 0 ? 8 : 16 / (BITS == 0 ? 2 : BITS);
+            constexpr int HALFT_ = TPW_ / 2;
+#pragma unroll
+            for (int mm = 0; mm < 8; ++mm) {
+                const int fs = (mm % TPW_) % HALFT_;
+                const float isc = (BITS == 0) ? 1.f : __int_as_float((127 - 24 + (BITS == 0 ? 0 : BITS) * fs) << 23);
+#pragma unroll
+                for (int e = 0; e < 4; ++e) st.o[mm][e] = rp.o[mm][e] * isc;
+            }
+            st.m[0] = rp.m0;
+            st.m[1] = rp.m1;
+            if constexpr (BITS == 0) {
+                if (gq == 0) {
+                    st.l[0] = rp.l0;
+                    st.l[1] = rp.l1;
+                }
+            } else {
+                if (gq == 4) {
+                    st.ob[0] = rp.l0;
+                    st.ob[1] = rp.l1;
+                }
+            }
+        }
+
         // ---- packed units of this segment: positions p = gidx - start, p % NCW == warp ----
         if (total > 0) {
             // positions are CTA-local (32-bit); stage and round advance incrementally
@@ -954,37 +1044,11 @@ __global__ void __launch_bounds__(NCW_ * 32, 1) decode_attn_kernel(const AttnArg
             __syncwarp();
         }
 
-        // ---- residual window + current token on the tensor cores (bf16 mma, raw q . raw k:
-        //      the key transform is orthonormal up to the stored norm, so attending the raw
-        //      bf16 rows IS attend_one over the full-precision residual, pipeline.cpp:152-180):
-        //      one 16-token tile per warp of the tail owner (all its loads in one round trip),
-        //      merged into the warp's slot; the tiles of successive tail segments of this CTA
-        //      rotate over the warps ----
-        if (owns_tail) {
-            const int ntok = a.r + (a.kcur ? 1 : 0);
-            const int ntiles = (ntok + 15) >> 4;
-            const int j = (warp - rtile_base % NCW + NCW) % NCW;  // this warp's tile in this segment
-            rtile_base += ntiles;
-            bool now = true;
-            if constexpr (DEFER) {
-                now = !seen_tail;
-                seen_tail = true;
-            }
-            if (now && j < ntiles) {
-                ResidualRefs rr;
-                rr.ringk = reinterpret_cast<const uint16_t *>(a.ring_k) + bh * R * D;
-                rr.ringv = reinterpret_cast<const uint16_t *>(a.ring_v) + bh * R * D;
-                rr.kc = a.kcur ? reinterpret_cast<const uint16_t *>(a.kcur) + ((int64_t)b * a.Hkv + kvh) * D : nullptr;
-                rr.vc = a.vcur ? reinterpret_cast<const uint16_t *>(a.vcur) + ((int64_t)b * a.Hkv + kvh) * D : nullptr;
-                rr.g = g;
-                rr.r = a.r;
-                rr.rotate_v = a.rotate_v;
-                rr.f16 = a.ring_f16;
-                residual_tile(rr, slot, qbase, j * 16, ntok, lane, c0,
-                              a.write_ring ? reinterpret_cast<uint16_t *>(a.ring_k) + bh * R * D : nullptr,
-                              reinterpret_cast<uint16_t *>(a.ring_v) + bh * R * D);
-            }
-        }
+        // explicit-V mode: the tile's raw-V partial is rotated into the slot after the units
+        if (tile_j >= 0 && tile_late)
+            residual_tile(tile_refs(), slot, qbase, tile_j * 16, ntok_t, lane, c0,
+                          a.write_ring ? reinterpret_cast<uint16_t *>(a.ring_k) + bh * R * D : nullptr,
+                          reinterpret_cast<uint16_t *>(a.ring_v) + bh * R * D);
 
         if (kProf && a.prof) tmr[7] += clk() - te0;
     }
@@ -1164,7 +1228,7 @@ __global__ void __launch_bounds__(NCW_ * 32, 1) decode_attn_kernel(const AttnArg
         // host view is replaced below by the whole-kernel cycles
         // [0..7] wait qk softmax pv merge spin qprologue segtail, [8] total, [9] cta merge,
         // [10] ticket, [11] smid, [12] final merge
-        unsigned long long *pp = a.prof + ((int64_t)blockIdx.x * NCW_MAX + warp) * kProfStride;
+        unsigned long long *pp = a.prof + ((int64_t)cta * NCW_MAX + warp) * kProfStride;
         for (int i = 0; i < 8; ++i) pp[i] = (unsigned long long)tmr[i];
         pp[8] = (unsigned long long)(clk() - tk0);
         pp[9] = (unsigned long long)tmr[8];

@@ -459,6 +459,19 @@ struct oscar_kv_handle {
             a.tail_cost = ntok > 0 ? tcost : 0;
         }
         a.pdl_prefetch = blocks_written ? 0 : 1;
+        {
+            static const long perm = env_knob("OSCAR_CTA_PERM", 0);  // experiments: block -> range permutation
+            a.cta_perm = 0;
+            if (perm > 1) {
+                int64_t x = perm % a.ncta, y = a.ncta;  // coprime check
+                while (y) {
+                    const int64_t t = x % y;
+                    x = y;
+                    y = t;
+                }
+                if (x == 1) a.cta_perm = (int)perm;
+            }
+        }
         a.maxp = maxp_alloc;
         if (a.nb > 0 && plan.nb == a.nb && plan.tail_cost == a.tail_cost) {
             a.ncta = plan.ncta;  // same shape as the last launch: its checks hold

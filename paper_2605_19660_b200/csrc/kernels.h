@@ -157,6 +157,7 @@ struct AttnArgs {
     int ncta;
     int64_t seg_cost;  // virtual units per (b, kv head) segment in the stream-K split (split.h)
     int64_t tail_cost; // virtual units charged to a segment's residual-window tiles (split.h)
+    int cta_perm;      // 0, or a multiplier coprime with ncta: block i takes range (i * cta_perm) % ncta
     int pdl_prefetch;  // packed records unchanged since the previous launch on this stream:
                        // the ring fill may start before griddepcontrol.wait
     unsigned long long *prof;  // debug: per-warp phase cycles [ncta][NCW][5] or null

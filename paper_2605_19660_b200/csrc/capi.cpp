@@ -1634,9 +1634,8 @@ int oscar_kv_decode_step_host(oscar_kv_handle *h, const void *q_host, const void
         void *dq = p, *dk = p + qb, *dv = p + qb + kb;
         float *dout = (float *)(p + qb + 2 * kb);
         float *dlse = (float *)(p + qb + 2 * kb + ob);
-        // inputs: one batched H2D copy of q, k, v (one submission instead of
-        // three; zero-copy reads of mapped inputs measured slower: PCIe latency
-        // lands on the kernel's q prologue and tail)
+        // inputs: one H2D copy each of q, k, v (zero-copy reads of mapped inputs
+        // measured slower: PCIe latency lands on the kernel's q prologue and tail)
         auto mapped = [](const void *hp) -> void * {
             cudaPointerAttributes at{};
             if (cudaPointerGetAttributes(&at, hp) != cudaSuccess) {
@@ -1645,22 +1644,9 @@ int oscar_kv_decode_step_host(oscar_kv_handle *h, const void *q_host, const void
             }
             return at.type == cudaMemoryTypeHost ? at.devicePointer : nullptr;
         };
-        {
-            void *dsts[3] = {dq, dk, dv};
-            void *srcs[3] = {const_cast<void *>(q_host), const_cast<void *>(k_host), const_cast<void *>(v_host)};
-            size_t sizes[3] = {qb, kb, kb};
-            cudaMemcpyAttributes attr = {};
-            attr.srcAccessOrder = cudaMemcpySrcAccessOrderStream;
-            attr.flags = cudaMemcpyFlagPreferOverlapWithCompute;
-            size_t attr_idx = 0, fail = 0;
-            const bool pinned = mapped(q_host) && mapped(k_host) && mapped(v_host);
-            if (!pinned || cudaMemcpyBatchAsync(dsts, srcs, sizes, 3, &attr, &attr_idx, 1, &fail, s) != cudaSuccess) {
-                (void)cudaGetLastError();
-                CK(cudaMemcpyAsync(dq, q_host, qb, cudaMemcpyHostToDevice, s));
-                CK(cudaMemcpyAsync(dk, k_host, kb, cudaMemcpyHostToDevice, s));
-                CK(cudaMemcpyAsync(dv, v_host, kb, cudaMemcpyHostToDevice, s));
-            }
-        }
+        CK(cudaMemcpyAsync(dq, q_host, qb, cudaMemcpyHostToDevice, s));
+        CK(cudaMemcpyAsync(dk, k_host, kb, cudaMemcpyHostToDevice, s));
+        CK(cudaMemcpyAsync(dv, v_host, kb, cudaMemcpyHostToDevice, s));
         // outputs: page-locked host buffers are written by the kernel itself
         // (mapped, zero-copy), saving the D2H copies; pageable ones are copied
         float *zo = (float *)mapped(out_host);

@@ -53,6 +53,10 @@ def parse():
     p.add_argument("--exchange", default="p2p", choices=["p2p", "nccl"],
                    help="c5 with N > 1: (O, LSE) rows by peer stores from the attention kernel (p2p) "
                         "or one NCCL all-gather + lse_merge")
+    p.add_argument("--proxy-world", type=int, default=0,
+                   help="c3/c4/c5 on ONE GPU: time the per-rank shard of an N-GPU run (c3: batch/N sequences; "
+                        "c4: the first KV-head shard; c5: the tail rank's 512K/N-token shard + its peer publish "
+                        "into N receive areas + the N-row merge) and project the whole-job tokens/s")
     return p.parse_args()
 
 
@@ -666,6 +670,10 @@ def run_config(args, rank, world, local_rank):
         import torch.distributed as td
     K, W, bits = args.steps, args.warmup, args.bits
     c = args.config
+    proxy = args.proxy_world if (args.proxy_world > 1 and not dist and c in ("c3", "c4", "c5")) else 0
+    if proxy:  # the shard shape of one rank of a `proxy`-GPU run, timed on this GPU alone
+        world = proxy
+        rank = proxy - 1 if c == "c5" else 0  # c5: the tail rank (residual window, appends, flushes)
     caches, layers = [], 1
     if c == "c1":
         return run_c1(args, rank, world, local_rank)
@@ -687,7 +695,15 @@ def run_config(args, rank, world, local_rank):
     cfg = PipelineConfig(method="oscar", bits=bits, heads=Hloc)
     t_pre = 0.0
     for layer in range(layers):
-        if c == "c5":
+        if c == "c5" and proxy:  # the tail rank's shard as a plain cache; exchange through virtual areas
+            s_ = shd.sequence_shard(S, world, rank)
+            cache = KvCache(cfg, batch=1, q_heads=Hq, max_tokens=s_.tokens + 2 * R + K + W, device=local_rank,
+                            keep_exact=False)
+            kk, vv = synth_kv(1, s_.tokens, Hloc, 7 + layer + 100 * rank, dev)
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            cache.buffer_quant(kk, vv, stream=sh)
+        elif c == "c5":
             cache = shd.SeqShardedKvCache(cfg, batch=1, q_heads=Hq, max_tokens_per_rank=S // world + 2 * R + K + W,
                                           device=local_rank, keep_exact=False, exchange=args.exchange,
                                           strict=False)  # timeout status checked after the timed region
@@ -776,8 +792,33 @@ def run_config(args, rank, world, local_rank):
 
     from paper_2605_19660_b200 import DecodeBatch
 
-    def step(i):
-        if c == "c5":
+    proxy_state = None
+    if c == "c5" and proxy:
+        from paper_2605_19660_b200 import kv_cache as kcm
+
+        pplans, pareas = shd.local_peer_plans(world, Hq, dev)
+        pout = torch.empty((Hq, D), dtype=torch.float32, device=dev)
+        pstatus = torch.zeros(1, dtype=torch.int32, device=dev)
+        torch.cuda.synchronize()
+        proxy_state = {"epoch": 0, "ev": []}
+
+    def step(i, timed=False):
+        if c == "c5" and proxy:
+            # the other N-1 virtual ranks publish first (outside the timed span), then this
+            # rank's step: attention + publish of its rows into all N areas, and the merge
+            proxy_state["epoch"] += 1
+            ep = proxy_state["epoch"]
+            for r_ in range(world - 1):
+                kcm.peer_publish_empty(pplans[r_], ep, stream=sh)
+            ea, eb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            ea.record(stream)
+            for cache in caches:
+                cache.attend_publish(q[i], pplans[world - 1], ep, kn[i], vn[i], stream=sh)
+                kcm.peer_merge(pplans[world - 1], ep, pout, status=pstatus, stream=sh)
+            eb.record(stream)
+            if timed:
+                proxy_state["ev"].append((ea, eb))
+        elif c == "c5":
             for cache in caches:
                 cache.decode_step(q[i], kn[i], vn[i], stream=sh)
         else:  # every layer's decode step in one C-ABI call (oscar_kv_decode_step_many)
@@ -789,18 +830,25 @@ def run_config(args, rank, world, local_rank):
         td.barrier()
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if proxy:  # the GPU sleeps while the host queues all K steps: device time, host submission hidden
+        with torch.cuda.stream(stream):
+            torch.cuda._sleep(int(2e6 * K))
     e0.record(stream)
     for i in range(W, W + K):
-        step(i)
+        step(i, timed=True)
     e1.record(stream)
     if dist:
         td.barrier()
     torch.cuda.synchronize()
     t = torch.tensor([e0.elapsed_time(e1)], device=dev)
+    if proxy_state is not None:  # c5 proxy: the tail rank's spans only (not the virtual peers' publishes)
+        t = torch.tensor([sum(a_.elapsed_time(b_) for a_, b_ in proxy_state["ev"])], device=dev)
+        if int(pstatus.item()) != 0:
+            raise RuntimeError("c5 proxy: peer merge timed out")
     if dist:
         td.all_reduce(t, op=td.ReduceOp.MAX)
     ms = float(t.item())
-    if c == "c5":
+    if c == "c5" and not proxy:
         for cache in caches:
             cache.check_exchange()  # raises if any peer merge timed out
     per_rank_tokens = S // world if c == "c5" else S
@@ -809,7 +857,7 @@ def run_config(args, rank, world, local_rank):
     peak, peak_src = peaks()
     value = (Bg if c != "c3" else Bg) * K / (ms * 1e-3)
     return {
-        "metric": METRIC + f" [{c}]", "value": value, "unit": "tokens/s", "n_gpus": world, "steps": K, "warmup": W,
+        "metric": METRIC + f" [{c}{' per-rank proxy' if proxy else ''}]", "value": value, "unit": "tokens/s", "n_gpus": world, "steps": K, "warmup": W,
         "ms_per_step": ms / K, "higher_is_better": True, "scaling": "weak" if c == "c3" else "strong",
         "vs_baseline": None, "dtype": "f16" if bits else "bf16",
         "storage": "int2" if bits == 2 else ("int4" if bits == 4 else "bf16"),
@@ -823,6 +871,14 @@ def run_config(args, rank, world, local_rank):
         "streaming_append": stream_stats,
         "exchange": (None if c != "c5" else
                      {"mode": args.exchange if world > 1 else "none (one shard)", **(merge_stats or {})}),
+        **({"n_gpus": 1, "proxy": {
+            "world": world, "rank": rank, "timing": "device time: the K steps are queued behind a sleep kernel "
+                                                    "(host submission not on the clock)",
+            "what": f"rank {rank} of a {world}-GPU run timed alone on 1 GPU; value = "
+                                                  f"whole-job tokens/s projected from this rank's step time (all ranks "
+                                                  f"carry equal shards{'; the tail rank is the largest' if c == 'c5' else ''}"
+                                                  f"{'; peer stores land in local memory, not over NVLink' if c == 'c5' else ''})"}}
+           if proxy else {}),
     }
 
 
@@ -845,6 +901,11 @@ def main():
         import torch.distributed as td
 
         torch.cuda.set_device(local_rank)
+        # communicator set-up lines (ranks, NVLink/NVLS transports) on stderr: stdout
+        # carries only the JSON line
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+        os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
         if os.environ.get("OSCAR_BENCH_ONE_DEVICE"):
             td.init_process_group("gloo")
         else:

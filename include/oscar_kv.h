@@ -217,19 +217,20 @@ int oscar_lse_merge(const float *outs, const float *lses, int64_t parts, int64_t
 /* ---- fused sequence-shard exchange over peer memory (C5) ----
  * Replaces "attend -> all-gather (O, LSE) -> oscar_lse_merge" by: the
  * attention kernel's final merge stores each normalised row straight into
- * every rank's receive area (NVLink peer stores) and raises a per-row epoch
- * flag; oscar_peer_merge on each rank waits for the flags and merges.
+ * every rank's receive area (NVLink peer stores); oscar_peer_merge on each
+ * rank waits for the rows and merges.  No fences or separate flags: every
+ * 8-byte word of a row is (epoch << 32 | fp32 bits) and the reader polls the
+ * words until their epoch matches.
  * Rank r's receive area (oscar_peer_area_bytes, on rank r's GPU, mapped into
- * every peer with oscar_ipc_*): fp32 recv[2][world][rows][OSCAR_PEER_STRIDE]
- * (O[0..127], LSE at 128) followed by uint32 flags[2][world][rows], zeroed.
+ * every peer with oscar_ipc_*): uint64 recv[2][world][rows][OSCAR_PEER_STRIDE]
+ * (O[0..127], LSE at 128), zeroed before the first epoch.
  * Epochs start at 1 and increase by one per step on every rank. */
 #define OSCAR_PEER_MAX 8
 #define OSCAR_PEER_STRIDE 132
 typedef struct oscar_peer_plan {
     int32_t world, rank;              /* this handle's shard; world <= OSCAR_PEER_MAX */
     int64_t rows;                     /* batch * q_heads */
-    float *recv[OSCAR_PEER_MAX];      /* rank p's receive area, as mapped here */
-    uint32_t *flags[OSCAR_PEER_MAX];  /* rank p's flags, as mapped here */
+    uint64_t *recv[OSCAR_PEER_MAX];   /* rank p's receive area, as mapped here */
 } oscar_peer_plan;
 int64_t oscar_peer_area_bytes(int32_t world, int64_t rows);
 /* attend (k = v = NULL) or decode_step (current token attended and appended)

@@ -459,33 +459,50 @@ __device__ __forceinline__ void process_quarter_bf16(const uint8_t *__restrict__
 }
 
 // Rotated (fp16) / raw (bf16 baseline) q tiles of segments [k0, k1) of this
-// CTA's range (k1 - k0 <= QSEG), built cooperatively: item (segment k, head
-// row j) -> warp item % NCW; tile (k % QSEG) row j, rows j >= g zero-filled.  Each segment's
-// rotation runs once per CTA instead of once per warp.
+// CTA's range (k1 - k0 <= QSEG), built cooperatively by warps 0..NCW-2 (the
+// last warp issues the ring fill): item (segment k, head row j) -> warp
+// item % (NCW-1); tile (k % QSEG) row j, rows j >= g zero-filled.  A warp
+// first issues the loads of all its items, then rotates them (one memory
+// round trip per warp, not per item).  `gate`: the first wave of a launch whose
+// ring fill was not issued ahead of griddepcontrol.wait -- every warp meets at
+// named barrier 1 once its q loads are in flight, and only then does the fill
+// warp queue the NST bulk copies (tens of MB over the GPU), so the q loads are
+// not stuck behind them in the memory system.  Each segment's rotation runs
+// once per CTA instead of once per warp.
 template <int BITS, int NCW>
 __device__ __forceinline__ void build_q_tiles(const AttnArgs &a, __half *tiles, int64_t seg_first, int k0, int k1,
-                                              int warp, int lane) {
+                                              int warp, int lane, bool gate) {
+    constexpr int QW = NCW - 1;                  // item warps
+    constexpr int MAXI = (QSEG * 8 + QW - 1) / QW;  // items per warp
     const int g = a.g;
-    for (int item = k0 * 8 + warp; item < k1 * 8; item += NCW) {
-        const int k = item >> 3, j = item & 7;
-        const int64_t bh = seg_first + k;
-        uint2 *row = reinterpret_cast<uint2 *>(tiles + ((k % QSEG) * 8 + j) * QH_STRIDE) + lane;
-        if (j >= g) {
-            *row = make_uint2(0u, 0u);
-            continue;
+    uint2 u[MAXI];
+    int row_of[MAXI];  // tile row of item i (-1: none)
+#pragma unroll
+    for (int i = 0; i < MAXI; ++i) {
+        const int item = k0 * 8 + warp + i * QW;
+        row_of[i] = (warp < QW && item < k1 * 8) ? ((item >> 3) % QSEG) * 8 + (item & 7) : -1;
+        u[i] = make_uint2(0u, 0u);
+        if (row_of[i] >= 0 && (item & 7) < g) {
+            const int bh = (int)seg_first + (item >> 3);
+            u[i] = *(reinterpret_cast<const uint2 *>(reinterpret_cast<const __nv_bfloat16 *>(a.q) +
+                                                     ((int64_t)(bh / a.Hkv) * a.Hq + (bh % a.Hkv) * g + (item & 7)) * D) +
+                     lane);
         }
-        const uint2 u = *(reinterpret_cast<const uint2 *>(reinterpret_cast<const __nv_bfloat16 *>(a.q) +
-                                                          ((bh / a.Hkv) * a.Hq + (bh % a.Hkv) * g + j) * D) +
-                          lane);
-        if (BITS == 0) {  // the bf16 baseline attends raw q
-            *row = u;
+    }
+    if (gate) named_bar(1, NCW * 32);
+#pragma unroll
+    for (int i = 0; i < MAXI; ++i) {
+        if (row_of[i] < 0) continue;
+        uint2 *row = reinterpret_cast<uint2 *>(tiles + row_of[i] * QH_STRIDE) + lane;
+        if ((row_of[i] & 7) >= g || BITS == 0) {  // padding rows; the bf16 baseline attends raw q
+            *row = u[i];
             continue;
         }
         float x[4];
-        x[0] = __uint_as_float(u.x << 16);
-        x[1] = __uint_as_float(u.x & 0xffff0000u);
-        x[2] = __uint_as_float(u.y << 16);
-        x[3] = __uint_as_float(u.y & 0xffff0000u);
+        x[0] = __uint_as_float(u[i].x << 16);
+        x[1] = __uint_as_float(u[i].x & 0xffff0000u);
+        x[2] = __uint_as_float(u[i].y << 16);
+        x[3] = __uint_as_float(u[i].y & 0xffff0000u);
         if (a.rotates) fht128_warp(x, lane);
         *row = make_uint2(pack_half2(x[0], x[1]), pack_half2(x[2], x[3]));
     }
@@ -788,14 +805,11 @@ __global__ void __launch_bounds__(NCW_ * 32, 1) decode_attn_kernel(const AttnArg
     // completion + memory flush before touching q, the current token, the
     // residual ring or any scratch the previous grid wrote.
     const unsigned long long g_entry = kProf ? gtime() : 0;
+    unsigned long long g_t0 = 0, g_t1 = 0, g_dep = 0, g_qb = 0;  // profiling: TMA issue start/end, dep wait, q built
     griddep_launch_dependents();
-    if (threadIdx.x == 0) {
-        for (int i = 0; i < C::NST; ++i) {
-            mbar_init(&full[i], 1);
-            st_volatile_shared(&consumed[i], 0);
-        }
-        fence_mbar_init();
-        if (!a.pdl_prefetch) griddep_wait();
+    // the ring fill: the first NST units of the range, issued by lane 0 of the last warp
+    const bool fill_thread = threadIdx.x == (NCW - 1) * 32;
+    auto fill = [&]() {
         if (nunits > 0) {
             int64_t bh = start / nb, uidx = start % nb;
             for (int64_t p = 0; p < nunits && p < C::NST; ++p) {
@@ -806,29 +820,44 @@ __global__ void __launch_bounds__(NCW_ * 32, 1) decode_attn_kernel(const AttnArg
                 }
             }
         }
+        if (kProf) g_t1 = gtime();
+    };
+    if (fill_thread) {
+        for (int i = 0; i < C::NST; ++i) {
+            mbar_init(&full[i], 1);
+            st_volatile_shared(&consumed[i], 0);
+        }
+        fence_mbar_init();
+        if (kProf) g_t0 = gtime();
+        if (a.pdl_prefetch) fill();
     }
     griddep_wait();
+    if (kProf) g_dep = gtime();
     // segments: residual-only mode (nb == 0): CTA c <-> bh c
     const bool active = total > 0 ? nunits > 0 : cta < a.BH;
     const int64_t seg_first = !active ? 0 : (total > 0 ? start / nb : cta);
     const int64_t seg_last = !active ? -1 : (total > 0 ? (end - 1) / nb : cta);
     const int nseg_all = (int)(seg_last - seg_first + 1);
     __half *qtiles = reinterpret_cast<__half *>(smem + C::QH_OFF);  // QSEG segment tiles of 8 x QH_STRIDE
-    build_q_tiles<BITS, NCW>(a, qtiles, seg_first, 0, nseg_all < QSEG ? nseg_all : QSEG, warp, lane);
+    const bool gate = !a.pdl_prefetch;
+    build_q_tiles<BITS, NCW>(a, qtiles, seg_first, 0, nseg_all < QSEG ? nseg_all : QSEG, warp, lane, gate);
+    if (kProf) g_qb = gtime();
+    if (fill_thread && !a.pdl_prefetch) fill();  // after every warp's q loads are in flight
     __syncthreads();  // barrier init + first wave of q tiles visible
     if (!active) return;
+    const unsigned long long g_ready = kProf ? gtime() : 0;
     const float c0 = LOG2E * 0.08838834764831845f;  // log2(e)/sqrt(128)
     long long tmr[12] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
     const long long tk0 = (kProf && a.prof) ? clk() : 0;
 
     // the stage of warp w's final unit (positions p = w, w + NCW, ... < nunits), free
-    // after it is consumed: p + NST >= nunits, so it is never refilled.  Only used
-    // when the CTA has at least NST units (small launches keep global slots).
-    const bool smem_last = total > 0 && nunits >= C::NST;
+    // after it is consumed: p + NST >= nunits (NST > NCW), so it is never refilled;
+    // a warp with no unit at all (nunits < NCW) takes stage w, which no unit uses
+    const bool smem_last = total > 0 && C::NST > NCW;
     const int nu32 = (int)nunits;
     auto last_seg_slot = [&](int w) -> float * {
         if (smem_last) {
-            const int pw = nu32 - 1 - ((nu32 - 1 - w) % NCW);
+            const int pw = w < nu32 ? nu32 - 1 - ((nu32 - 1 - w) % NCW) : w;
             return reinterpret_cast<float *>(ring + (pw % C::NST) * C::STAGE);
         }
         return a.warp_part + (((int64_t)cta * a.maxseg + (seg_last - seg_first)) * NCW_MAX + w) * MERGE_FLOATS;
@@ -851,7 +880,8 @@ __global__ void __launch_bounds__(NCW_ * 32, 1) decode_attn_kernel(const AttnArg
         //      the next wave of tiles is built (all warps walk the same segments) ----
         if (k > 0 && k % QSEG == 0) {
             __syncthreads();
-            build_q_tiles<BITS, NCW>(a, qtiles, seg_first, k, (k + QSEG < nseg_all ? k + QSEG : nseg_all), warp, lane);
+            build_q_tiles<BITS, NCW>(a, qtiles, seg_first, k, (k + QSEG < nseg_all ? k + QSEG : nseg_all), warp, lane,
+                                     false);
             __syncthreads();
         }
         const __half *qh = qtiles + (k % QSEG) * 8 * QH_STRIDE;
@@ -1244,6 +1274,11 @@ __global__ void __launch_bounds__(NCW_ * 32, 1) decode_attn_kernel(const AttnArg
         pp[17] = g_phase1;  // CTA partials done (this warp)
         pp[18] = g_sync2;
         pp[19] = g_ticket;  // tickets + barrier
+        pp[20] = g_ready;   // q tiles built (after the first barrier)
+        pp[21] = g_t0;      // thread 0: barriers initialised (0 on other warps)
+        pp[22] = g_t1;      // thread 0: first NST bulk copies issued
+        pp[23] = g_dep;     // after griddepcontrol.wait
+        pp[24] = g_qb;      // this warp's q-tile items done
     }
 }
 

@@ -681,9 +681,10 @@ struct oscar_kv_handle {
             }
             {
                 // timeline (globaltimer ns, relative to the first CTA's entry)
-                std::vector<double> ent, str, ext;
+                std::vector<double> ent, str, ext, rdy;
                 for (int w = 0; w < nw; ++w) {
                     if (hbuf[kProfStride * w + 8] == 0) continue;
+                    rdy.push_back((double)hbuf[kProfStride * w + 20]);
                     ent.push_back((double)hbuf[kProfStride * w + 13]);
                     str.push_back((double)hbuf[kProfStride * w + 14]);
                     ext.push_back((double)hbuf[kProfStride * w + 15]);
@@ -695,10 +696,40 @@ struct oscar_kv_handle {
                         return (v[(size_t)(f * (double)(v.size() - 1))] - t0) * 1e-3;
                     };
                     std::fprintf(stderr,
-                                 "OSCAR_PROF timeline us: entry max %.2f | stream end min %.2f p10 %.2f p50 %.2f "
-                                 "p90 %.2f max %.2f | exit min %.2f p50 %.2f max %.2f\n",
-                                 q(ent, 1.0), q(str, 0.0), q(str, 0.1), q(str, 0.5), q(str, 0.9), q(str, 1.0),
+                                 "OSCAR_PROF timeline us: entry max %.2f | q ready p50 %.2f max %.2f | stream end min "
+                                 "%.2f p10 %.2f p50 %.2f p90 %.2f max %.2f | exit min %.2f p50 %.2f max %.2f\n",
+                                 q(ent, 1.0), q(rdy, 0.5), q(rdy, 1.0), q(str, 0.0), q(str, 0.1), q(str, 0.5), q(str, 0.9), q(str, 1.0),
                                  q(ext, 0.0), q(ext, 0.5), q(ext, 1.0));
+                    {  // prologue (per CTA, relative to its warp 0 entry): TMA issue, dep wait, q items, ready
+                        double pr[6] = {0, 0, 0, 0, 0, 0};
+                        int npc = 0;
+                        for (int c = 0; c < a.ncta; ++c) {
+                            const unsigned long long *w0 = &hbuf[kProfStride * (c * 16)];
+                            if (w0[8] == 0) continue;
+                            unsigned long long qmax = 0, dmax = 0, b0 = 0, b1 = 0;
+                            for (int w = 0; w < 16; ++w) {
+                                const unsigned long long *pw = &hbuf[kProfStride * (c * 16 + w)];
+                                if (pw[8] == 0) continue;
+                                qmax = std::max(qmax, pw[24]);
+                                dmax = std::max(dmax, pw[23]);
+                                b0 = std::max(b0, pw[21]);  // set by the fill thread only
+                                b1 = std::max(b1, pw[22]);
+                            }
+                            const double e = (double)w0[13];
+                            pr[0] += (double)b0 - e;
+                            pr[1] += (double)b1 - e;
+                            pr[2] += (double)dmax - e;
+                            pr[3] += (double)qmax - e;
+                            pr[4] += (double)w0[20] - e;
+                            ++npc;
+                        }
+                        if (npc)
+                            std::fprintf(stderr,
+                                         "OSCAR_PROF prologue (us after the CTA's entry, mean over CTAs): barriers %.2f "
+                                         "tma issued %.2f dep wait %.2f q items %.2f ready %.2f\n",
+                                         pr[0] / npc * 1e-3, pr[1] / npc * 1e-3, pr[2] / npc * 1e-3, pr[3] / npc * 1e-3,
+                                         pr[4] / npc * 1e-3);
+                    }
                     // per CTA (warp 0): end-of-work phases relative to the CTA's last stream end
                     double dp[5] = {0, 0, 0, 0, 0};
                     int nc = 0;
@@ -1541,11 +1572,9 @@ PeerPlan peer_plan(const oscar_peer_plan *p, int64_t rows_expected) {
     q.rank = p->rank;
     q.rows = p->rows;
     for (int i = 0; i < p->world; ++i) {
-        if (!p->recv[i] || !p->flags[i]) throw InvalidArg("peer plan: null receive area");
-        if (((uintptr_t)p->recv[i]) % 16 || ((uintptr_t)p->flags[i]) % 4)
-            throw InvalidArg("peer plan: misaligned receive area");
+        if (!p->recv[i]) throw InvalidArg("peer plan: null receive area");
+        if (((uintptr_t)p->recv[i]) % 32) throw InvalidArg("peer plan: misaligned receive area");
         q.recv[i] = p->recv[i];
-        q.flags[i] = p->flags[i];
     }
     return q;
 }
@@ -1553,7 +1582,7 @@ PeerPlan peer_plan(const oscar_peer_plan *p, int64_t rows_expected) {
 
 int64_t oscar_peer_area_bytes(int32_t world, int64_t rows) {
     if (world < 1 || world > OSCAR_PEER_MAX || rows <= 0) return -1;
-    return (int64_t)2 * world * rows * (OSCAR_PEER_STRIDE * 4 + 4);
+    return (int64_t)2 * world * rows * OSCAR_PEER_STRIDE * 8;
 }
 
 int oscar_kv_attend_publish(oscar_kv_handle *h, const void *q, const void *k, const void *v,

@@ -116,16 +116,15 @@ struct WindowF64Args {
 cudaError_t launch_window_f64(const WindowF64Args &a, cudaStream_t st);
 
 // Sequence-shard exchange plan (C5): rank r's receive area recv[r] holds
-// [2 parities][world][rows][PEER_STRIDE] floats (O[0..127], LSE at 128) and
-// flags[r] holds [2][world][rows] epochs; both live on rank r's GPU and are
-// mapped into every peer (CUDA IPC).  Same layout as oscar_peer_plan.
+// [2 parities][world][rows][PEER_STRIDE] 8-byte words (epoch << 32 | fp32 bits:
+// O[0..127], LSE at 128); it lives on rank r's GPU and is mapped into every
+// peer (CUDA IPC).  Same layout as oscar_peer_plan.
 constexpr int PEER_MAX = 8;
-constexpr int PEER_STRIDE = 132;  // 128 + LSE, padded to 16 B
+constexpr int PEER_STRIDE = 132;  // words per row: 128 + LSE, padded to 32 B
 struct PeerPlan {
     int32_t world, rank;
     int64_t rows;
-    float *recv[PEER_MAX];
-    uint32_t *flags[PEER_MAX];
+    uint64_t *recv[PEER_MAX];
 };
 
 // profiling build: 64-bit slots per warp in AttnArgs::prof

@@ -63,7 +63,7 @@ class _PeerPlan(ctypes.Structure):
     """oscar_peer_plan (include/oscar_kv.h)."""
 
     _fields_ = [("world", ctypes.c_int32), ("rank", ctypes.c_int32), ("rows", ctypes.c_int64),
-                ("recv", _P * PEER_MAX), ("flags", _P * PEER_MAX)]
+                ("recv", _P * PEER_MAX)]
 
 
 _lib = None
@@ -499,7 +499,7 @@ def lse_merge(outs, lses, out=None, lse_out=None, stream=None):
 
 # ----------------------------------------------------------------------------- peer exchange (C5)
 def peer_area_bytes(world: int, rows: int) -> int:
-    """Bytes of one rank's receive area: fp32 recv [2][world][rows][132] + uint32 flags [2][world][rows]."""
+    """Bytes of one rank's receive area: uint64 (epoch << 32 | fp32) words [2][world][rows][132]."""
     n = lib().oscar_peer_area_bytes(world, rows)
     if n < 0:
         raise ValueError(f"bad peer area shape world={world} rows={rows}")
@@ -514,11 +514,9 @@ class PeerPlan:
         if len(areas) != world:
             raise ValueError("one receive area per rank")
         self.world, self.rank, self.rows = world, rank, rows
-        off = 2 * world * rows * PEER_STRIDE * 4
         self.c = _PeerPlan(world, rank, rows)
         for p, a in enumerate(areas):
             self.c.recv[p] = int(a)
-            self.c.flags[p] = int(a) + off
 
 
 def peer_publish_empty(plan: PeerPlan, epoch: int, stream=None):

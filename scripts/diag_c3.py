@@ -39,3 +39,19 @@ def attend_all(i):
     for c in caches: c.attend(q[0], out, lse, stream=sh)
 res["attend_32_per_layer_us"] = timeit(attend_all, 10) / L
 print(json.dumps({k: round(v, 2) if isinstance(v, float) else v for k, v in res.items()}))
+# device time of the 32 attends with no host gaps: one CUDA graph
+g = torch.cuda.CUDAGraph()
+with torch.cuda.graph(g, stream=st):
+    for c in caches: c.attend(q[0], out, lse, stream=sh)
+torch.cuda.synchronize()
+res["attend_32_graph_per_layer_us"] = timeit(lambda i: g.replay(), 20) / L
+# host submission cost of one decode_step_many call (no device wait)
+import time
+torch.cuda.synchronize()
+t0 = time.perf_counter()
+for i in range(5):
+    j = 200 + i
+    DecodeBatch(caches, [q[j]] * L, [kn[j]] * L, [vn[j]] * L, [out] * L).run(sh)
+res["many_host_per_layer_us"] = 1e6 * (time.perf_counter() - t0) / 5 / L
+torch.cuda.synchronize()
+print(json.dumps({k: round(v, 2) if isinstance(v, float) else v for k, v in res.items()}))

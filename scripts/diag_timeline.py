@@ -1,7 +1,7 @@
 """Per-launch timeline of one attend (globaltimer stamps of the profiling build):
 entry spread, end of streaming per warp, exit.  C2 shape by default.
 usage: OSCAR_PROF=1 OSCAR_LIB=$PWD/paper_2605_19660_b200/liboscar_b200_prof.so \
-       python scripts/diag_timeline.py [ctx] [batch] [bits]"""
+       python scripts/diag_timeline.py [ctx] [batch] [bits] [q heads] [kv heads]"""
 import os
 import sys
 
@@ -14,7 +14,8 @@ from paper_2605_19660_b200 import KvCache, PipelineConfig
 ctx = int(sys.argv[1]) if len(sys.argv) > 1 else 32768
 B = int(sys.argv[2]) if len(sys.argv) > 2 else 16
 bits = int(sys.argv[3]) if len(sys.argv) > 3 else 2
-Hq, Hkv = 32, 8
+Hq = int(sys.argv[4]) if len(sys.argv) > 4 else 32
+Hkv = int(sys.argv[5]) if len(sys.argv) > 5 else 8
 dev = torch.device("cuda")
 cache = KvCache(PipelineConfig(heads=Hkv, bits=bits), batch=B, q_heads=Hq, max_tokens=ctx + 256, keep_exact=False)
 k, v = synth_kv(B, ctx, Hkv, 1, dev)

@@ -52,13 +52,13 @@ def test_peer_plan_validation_without_gpu():
     from paper_2605_19660_b200 import kv_cache as kc
 
     rows = 28
-    assert kc.peer_area_bytes(8, rows) == 2 * 8 * rows * (132 * 4 + 4)
+    assert kc.peer_area_bytes(8, rows) == 2 * 8 * rows * 132 * 8
     with pytest.raises(ValueError):
         kc.peer_area_bytes(9, rows)
     ok = kc.PeerPlan(2, 0, rows, [4096, 8192])
     bad = [kc.PeerPlan(2, 2, rows, [4096, 8192]),       # rank out of range
            kc.PeerPlan(2, 0, rows, [4096, 0]),          # unmapped area
-           kc.PeerPlan(2, 1, rows, [4096 + 4, 8192])]   # misaligned area
+           kc.PeerPlan(2, 1, rows, [4096 + 16, 8192])]  # misaligned area (32-byte rows)
     # the C-ABI's own validation (no device work is reached): status 1 = invalid argument
     def merge_rc(plan, epoch):
         return kc.lib().oscar_peer_merge(ctypes.byref(plan.c), epoch, 4096, None, None, None)

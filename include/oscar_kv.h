@@ -158,6 +158,9 @@ int oscar_kv_decode_step_host(oscar_kv_handle *h, const void *q_host, const void
  * The reference has no such condition for finite inputs (it keeps fp64). */
 #define OSCAR_STATUS_FP16_OVERFLOW 1
 #define OSCAR_STATUS_NONFINITE 2
+/*   OSCAR_STATUS_MERGE_TIMEOUT  a split-KV merge waited > 2 s for another CTA's partial
+ *                               (cannot happen while every CTA is resident; its rows are NaN) */
+#define OSCAR_STATUS_MERGE_TIMEOUT 4
 int oscar_kv_status(oscar_kv_handle *h, int32_t *flags, int32_t clear);
 
 /* packed_tokens / residual_tokens / flush_count (kv_cache.hpp:67-71). */

@@ -716,6 +716,94 @@ __device__ __forceinline__ void write_row(const AttnArgs &a, int b, int kvh, int
     }
 }
 
+constexpr int LL_FB = 8;  // flag-in-word partials merged per batch (the poll path: one batch)
+
+// Poll-mode split-KV final merge of one (b, kv head) head row h: the
+// flag-in-word partials in slots [s_begin, expected) are polled until written,
+// then cleared to zero for the next launch, and merged on top of a running
+// (M, x, Lw) (the merging CTA's own partial; Lw is this lane's share of the
+// denominator).  Writes the normalised row (out / lse, or the peer receive areas).
+__device__ __forceinline__ void final_merge_ll(const AttnArgs &a, int64_t bh, int h, int s_begin, int expected, float M,
+                                            float Lw, float (&x)[4], int lane) {
+    uint64_t *pmb = a.part_ml + bh * a.maxp * 16;
+    uint64_t *pob = a.part_o + bh * a.maxp * 8 * D;
+    constexpr int FB = LL_FB;  // partials per batch: every lane's loads of a batch in flight at once
+    uint64_t t0 = 0;
+    bool ok = true;
+    for (int s0 = s_begin; s0 < expected && ok; s0 += FB) {
+        const bool mine = lane < FB && s0 + lane < expected;  // lane u < FB: (m, l) of partial s0 + u
+        uint64_t wm = 0, wl = 0;
+        uint64_t w[FB][4];
+        for (;;) {
+            if (mine) ld_volatile_v2_u64(pmb + (s0 + lane) * 16 + 2 * h, wm, wl);
+#pragma unroll
+            for (int u = 0; u < FB; ++u) {
+                if (s0 + u < expected) {
+                    const uint64_t *r = pob + (int64_t)(s0 + u) * 8 * D + h * D + lane * 4;
+                    ld_volatile_v2_u64(r, w[u][0], w[u][1]);
+                    ld_volatile_v2_u64(r + 2, w[u][2], w[u][3]);
+                }
+            }
+            uint32_t f = mine ? (uint32_t)(wm >> 32) & (uint32_t)(wl >> 32) : 1u;
+#pragma unroll
+            for (int u = 0; u < FB; ++u)
+                if (s0 + u < expected)
+                    f &= (uint32_t)(w[u][0] >> 32) & (uint32_t)(w[u][1] >> 32) & (uint32_t)(w[u][2] >> 32) &
+                         (uint32_t)(w[u][3] >> 32);
+            if (__all_sync(0xffffffffu, f == 1u)) break;
+            if (t0 == 0) t0 = gtime();
+            __nanosleep(64);
+            if (gtime() - t0 > 2000000000ull) {  // a partial never arrived: fail loudly, don't hang
+                ok = false;
+                break;
+            }
+        }
+        if (!ok) break;
+        // consumed: back to zero ("not written") for the next launch
+        if (mine) st_volatile_v2_u64(pmb + (s0 + lane) * 16 + 2 * h, 0ull, 0ull);
+#pragma unroll
+        for (int u = 0; u < FB; ++u) {
+            if (s0 + u < expected) {
+                uint64_t *r = pob + (int64_t)(s0 + u) * 8 * D + h * D + lane * 4;
+                st_volatile_v2_u64(r, 0ull, 0ull);
+                st_volatile_v2_u64(r + 2, 0ull, 0ull);
+            }
+        }
+        const float ml = mine ? __uint_as_float((uint32_t)wm) : -CUDART_INF_F;
+        const float ll = mine ? __uint_as_float((uint32_t)wl) : 0.f;
+        float bm = fmaxf(M, ml);
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) bm = fmaxf(bm, __shfl_xor_sync(0xffffffffu, bm, o));
+        const float sc = (M == -CUDART_INF_F) ? 0.f : fast_exp2(M - bm);
+        const float fl = (ml == -CUDART_INF_F) ? 0.f : fast_exp2(ml - bm);
+        Lw = Lw * sc + ll * fl;
+#pragma unroll
+        for (int e = 0; e < 4; ++e) x[e] *= sc;
+#pragma unroll
+        for (int u = 0; u < FB; ++u) {
+            const float fu = __shfl_sync(0xffffffffu, fl, u);
+            if (s0 + u < expected) {
+#pragma unroll
+                for (int e = 0; e < 4; ++e) x[e] += __uint_as_float((uint32_t)w[u][e]) * fu;
+            }
+        }
+        M = bm;
+    }
+    const int b = (int)(bh / a.Hkv), kvh = (int)(bh % a.Hkv);
+    if (!ok) {
+        if (lane == 0 && a.status) atomicOr(a.status, STATUS_MERGE_TIMEOUT);
+        float nanrow[4] = {CUDART_NAN_F, CUDART_NAN_F, CUDART_NAN_F, CUDART_NAN_F};
+        write_row(a, b, kvh, h, nanrow, CUDART_NAN_F, lane);
+        return;
+    }
+    const float L = warp_sum(Lw);
+    const float inv = (L > 0.f) ? 1.f / L : 0.f;
+#pragma unroll
+    for (int e = 0; e < 4; ++e) x[e] *= inv;
+    if (a.rotate_v) fht128_warp(x, lane);  // explicit-V mode: rotate the output back
+    write_row(a, b, kvh, h, x, (L > 0.f) ? (M + __log2f(L)) * LN2 : -CUDART_INF_F, lane);
+}
+
 __device__ __noinline__ void residual_tile(const ResidualRefs rr, float *slot, const __nv_bfloat16 *qbase, int t0,
                                            int ntok, int lane, float c0, uint16_t *ring_k_w, uint16_t *ring_v_w) {
     ResPartial rp;
@@ -1125,7 +1213,16 @@ __global__ void __launch_bounds__(NCW_ * 32, 1) decode_attn_kernel(const AttnArg
     const unsigned long long g_sync1 = kProf ? gtime() : 0;
     int *lastflag = reinterpret_cast<int *>(smem + C::SEG_OFF);  // [nseg] (segcnt area reused)
     const int nseg = (int)(seg_last - seg_first + 1);
-    // (1) CTA partial per segment: warp-per-(segment, head), lane = 4-channel chunk
+    const bool poll = a.poll_merge != 0;
+    // (1) CTA partial per segment: warp-per-(segment, head), lane = 4-channel chunk.
+    //     A split segment is merged one of two ways:
+    //     * poll (every CTA resident, <= LL_FB + 1 partials): its FIRST CTA -- which
+    //       reaches the segment at the end of its range, the others at the start of
+    //       theirs -- merges right here, polling the others' flag-in-word partials
+    //       (no fence, no atomic, no second barrier); the others publish and are done;
+    //     * ticket: fp32 partials, one acq_rel ticket per CTA and segment, the
+    //       last-arriving CTA merges (many partials: 32 loads in flight per batch)
+    bool any_ticket = false;
     for (int item = warp; item < nseg * g; item += NCW) {
         const int kk = item / g, h = item % g;
         const int64_t bh = seg_first + kk;
@@ -1136,11 +1233,15 @@ __global__ void __launch_bounds__(NCW_ * 32, 1) decode_attn_kernel(const AttnArg
         // a segment entirely inside this CTA's range: its CTA partial IS the result
         // (no split-KV partial, ticket or final merge)
         const bool single = total == 0 || (bh * nb >= start && (bh + 1) * nb <= end);
-        int64_t first_cta = 0;
-        if (!single) first_cta = sp.cta_of(bh * nb);
-        const int pslot = (int)(cta - first_cta);
-        float *po = a.part_o + ((int64_t)bh * a.maxp + pslot) * 8 * D;
-        float *pml = a.part_ml + ((int64_t)bh * a.maxp + pslot) * 16;
+        int first_cta = 0, expected = 1;
+        if (!single) {
+            first_cta = (int)sp.cta_of(bh * nb);
+            expected = (int)sp.cta_of((bh + 1) * nb - 1) - first_cta + 1;
+        }
+        const bool pollseg = poll && expected - 1 <= LL_FB;
+        const int pslot = cta - first_cta;
+        uint64_t *po = a.part_o + ((int64_t)bh * a.maxp + pslot) * 8 * D;
+        uint64_t *pml = a.part_ml + ((int64_t)bh * a.maxp + pslot) * 16;
         // lane w < NCW holds warp w's (m, l) of head h
         const float mwv = lane < NCW ? src(lane)[8 * D + h] : -CUDART_INF_F;
         const float lwv = lane < NCW ? src(lane)[8 * D + 8 + h] : 0.f;
@@ -1170,86 +1271,103 @@ __global__ void __launch_bounds__(NCW_ * 32, 1) decode_attn_kernel(const AttnArg
             if (a.rotate_v) fht128_warp(x, lane);  // explicit-V mode: rotate the output back
             write_row(a, (int)(bh / a.Hkv), (int)(bh % a.Hkv), h, x, (L > 0.f) ? (M + __log2f(L)) * LN2 : -CUDART_INF_F,
                       lane);
-        } else {
-            *reinterpret_cast<float4 *>(po + h * D + lane * 4) = O;
+        } else if (pollseg && pslot == 0) {
+            float x[4] = {O.x, O.y, O.z, O.w};
+            final_merge_ll(a, bh, h, 1, expected, M, lane == 0 ? L : 0.f, x, lane);
+        } else if (pollseg) {
+            st_volatile_v2_u64(po + h * D + lane * 4, ll_word(O.x, 1u), ll_word(O.y, 1u));
+            st_volatile_v2_u64(po + h * D + lane * 4 + 2, ll_word(O.z, 1u), ll_word(O.w, 1u));
+            if (lane == 0) st_volatile_v2_u64(pml + 2 * h, ll_word(M, 1u), ll_word(L, 1u));
+        } else {  // ticket segment: fp32 partial in the first half of the slot's words
+            any_ticket = true;
+            reinterpret_cast<float4 *>(po)[h * D / 4 + lane] = O;
             if (lane == 0) {
-                pml[2 * h] = M;
-                pml[2 * h + 1] = L;
+                reinterpret_cast<float *>(pml)[2 * h] = M;
+                reinterpret_cast<float *>(pml)[2 * h + 1] = L;
             }
         }
     }
     const unsigned long long g_phase1 = kProf ? gtime() : 0;
-    __syncthreads();
+    const bool ticket_phase = __syncthreads_or(any_ticket) != 0;
     const unsigned long long g_sync2 = kProf ? gtime() : 0;
+    unsigned long long g_ticket = g_sync2;
     const long long tp0 = (kProf && a.prof) ? clk() : 0;
-    // (2) publish: one acq_rel ticket per segment (cumulative over the barrier)
-    if (threadIdx.x < nseg) {
-        const int64_t bh = seg_first + threadIdx.x;
-        if (total == 0 || (bh * nb >= start && (bh + 1) * nb <= end)) {
-            lastflag[threadIdx.x] = 0;  // finished in (1)
-        } else {
-            const int expected = (int)(sp.cta_of((bh + 1) * nb - 1) - sp.cta_of(bh * nb) + 1);
-            const int prev = atomic_add_acq_rel_gpu(&a.counters[bh], 1);
-            lastflag[threadIdx.x] = (prev == expected - 1) ? expected : 0;
+    const long long tf0 = tp0;
+    if (ticket_phase) {
+        // (2) publish: one acq_rel ticket per ticket segment (cumulative over the barrier)
+        if (threadIdx.x < nseg) {
+            const int64_t bh = seg_first + threadIdx.x;
+            int flag = 0;
+            if (!(total == 0 || (bh * nb >= start && (bh + 1) * nb <= end))) {
+                const int expected = (int)(sp.cta_of((bh + 1) * nb - 1) - sp.cta_of(bh * nb) + 1);
+                if (!(poll && expected - 1 <= LL_FB)) {
+                    const int prev = atomic_add_acq_rel_gpu(&a.counters[bh], 1);
+                    flag = (prev == expected - 1) ? expected : 0;
+                }
+            }
+            lastflag[threadIdx.x] = flag;
+        }
+        __syncthreads();
+        if (kProf) g_ticket = gtime();
+        // (3) final merge for the ticket segments this CTA completed last: warp-per-(segment, head)
+        for (int item = warp; item < nseg * g; item += NCW) {
+            const int kk = item / g, h = item % g;
+            const int expected = lastflag[kk];
+            if (expected == 0) continue;
+            const int64_t bh = seg_first + kk;
+            const int b = (int)(bh / a.Hkv), kvh = (int)(bh % a.Hkv);
+            // one pass, online over batches of FB partials: lane u loads the (m, l) of
+            // partial s0 + u, every lane its 4 channels of all FB partials' O rows (all
+            // loads in flight at once; registers are free at this point of the kernel).
+            // A segment keeps its merge form for the whole launch plan (the host clears
+            // the partial words when the plan changes), so fp32 partials left here are
+            // never read as flag-in-word ones
+            float M = -CUDART_INF_F, Lw = 0.f;  // Lw: this lane's share of the denominator
+            float x[4] = {0.f, 0.f, 0.f, 0.f};
+            constexpr int FB = 32;
+            for (int s0 = 0; s0 < expected; s0 += FB) {
+                const bool mine = s0 + lane < expected;
+                const float *pm =
+                    reinterpret_cast<const float *>(a.part_ml + ((int64_t)bh * a.maxp + s0 + lane) * 16) + 2 * h;
+                const float ml = mine ? __ldcg(pm) : -CUDART_INF_F;
+                const float ll = mine ? __ldcg(pm + 1) : 0.f;
+                float4 v[FB];
+#pragma unroll
+                for (int u = 0; u < FB; ++u)
+                    v[u] = (s0 + u < expected)
+                               ? __ldcg(reinterpret_cast<const float4 *>(a.part_o + ((int64_t)bh * a.maxp + s0 + u) * 8 * D) +
+                                        h * D / 4 + lane)
+                               : make_float4(0.f, 0.f, 0.f, 0.f);
+                float bm = fmaxf(M, ml);
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) bm = fmaxf(bm, __shfl_xor_sync(0xffffffffu, bm, o));
+                const float sc = (M == -CUDART_INF_F) ? 0.f : fast_exp2(M - bm);
+                const float fl = (ml == -CUDART_INF_F) ? 0.f : fast_exp2(ml - bm);
+                Lw = Lw * sc + ll * fl;
+#pragma unroll
+                for (int e = 0; e < 4; ++e) x[e] *= sc;
+#pragma unroll
+                for (int u = 0; u < FB; ++u) {
+                    const float f = __shfl_sync(0xffffffffu, fl, u);
+                    x[0] += v[u].x * f;
+                    x[1] += v[u].y * f;
+                    x[2] += v[u].z * f;
+                    x[3] += v[u].w * f;
+                }
+                M = bm;
+            }
+            const float L = warp_sum(Lw);
+            const float inv = (L > 0.f) ? 1.f / L : 0.f;
+#pragma unroll
+            for (int e = 0; e < 4; ++e) x[e] *= inv;
+            if (a.rotate_v) fht128_warp(x, lane);  // explicit-V mode: rotate the output back
+            write_row(a, b, kvh, h, x, (L > 0.f) ? (M + __log2f(L)) * LN2 : -CUDART_INF_F, lane);
+            if (h == 0 && lane == 0) a.counters[bh] = 0;  // the ticket is complete: reset for the next launch
         }
     }
-    __syncthreads();
-    const unsigned long long g_ticket = kProf ? gtime() : 0;
     if (kProf && a.prof) {
         tmr[8] += clk() - tm0;
         tmr[9] += clk() - tp0;  // the ticket (atomic) part
-    }
-    const long long tf0 = (kProf && a.prof) ? clk() : 0;
-    // (3) final merge for the (b, kv heads) this CTA completed last: warp-per-(segment, head)
-    for (int item = warp; item < nseg * g; item += NCW) {
-        const int kk = item / g, h = item % g;
-        const int expected = lastflag[kk];
-        if (expected == 0) continue;
-        const int64_t bh = seg_first + kk;
-        const int b = (int)(bh / a.Hkv), kvh = (int)(bh % a.Hkv);
-        const float *pmb = a.part_ml + (int64_t)bh * a.maxp * 16;
-        const float *pob = a.part_o + (int64_t)bh * a.maxp * 8 * D;
-        // one pass, online over batches of FB partials: lane u loads the (m, l) of
-        // partial s0 + u, every lane its 4 channels of all FB partials' O rows (all
-        // loads in flight at once; registers are free at this point of the kernel)
-        float M = -CUDART_INF_F, Lw = 0.f;  // Lw: this lane's share of the denominator
-        float x[4] = {0.f, 0.f, 0.f, 0.f};
-        constexpr int FB = 32;
-        for (int s0 = 0; s0 < expected; s0 += FB) {
-            const bool mine = s0 + lane < expected;
-            const float ml = mine ? __ldcg(pmb + (s0 + lane) * 16 + 2 * h) : -CUDART_INF_F;
-            const float ll = mine ? __ldcg(pmb + (s0 + lane) * 16 + 2 * h + 1) : 0.f;
-            float4 v[FB];
-#pragma unroll
-            for (int u = 0; u < FB; ++u)
-                v[u] = (s0 + u < expected)
-                           ? __ldcg(reinterpret_cast<const float4 *>(pob + (s0 + u) * 8 * D + h * D + lane * 4))
-                           : make_float4(0.f, 0.f, 0.f, 0.f);
-            float bm = fmaxf(M, ml);
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) bm = fmaxf(bm, __shfl_xor_sync(0xffffffffu, bm, o));
-            const float sc = (M == -CUDART_INF_F) ? 0.f : fast_exp2(M - bm);
-            const float fl = (ml == -CUDART_INF_F) ? 0.f : fast_exp2(ml - bm);
-            Lw = Lw * sc + ll * fl;
-#pragma unroll
-            for (int e = 0; e < 4; ++e) x[e] *= sc;
-#pragma unroll
-            for (int u = 0; u < FB; ++u) {
-                const float f = __shfl_sync(0xffffffffu, fl, u);
-                x[0] += v[u].x * f;
-                x[1] += v[u].y * f;
-                x[2] += v[u].z * f;
-                x[3] += v[u].w * f;
-            }
-            M = bm;
-        }
-        const float L = warp_sum(Lw);
-        const float inv = (L > 0.f) ? 1.f / L : 0.f;
-#pragma unroll
-        for (int e = 0; e < 4; ++e) x[e] *= inv;
-        if (a.rotate_v) fht128_warp(x, lane);  // explicit-V mode: rotate the output back
-        write_row(a, b, kvh, h, x, (L > 0.f) ? (M + __log2f(L)) * LN2 : -CUDART_INF_F, lane);
-        if (h == 0 && lane == 0) a.counters[bh] = 0;  // the ticket is complete: reset for the next launch
     }
     if (kProf && a.prof) tmr[10] += clk() - tf0;
     if (kProf && a.prof) tmr[4] += clk() - tm0;

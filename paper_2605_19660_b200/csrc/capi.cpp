@@ -125,7 +125,7 @@ struct oscar_kv_handle {
     uint8_t *blocks = nullptr;
     double *shadow = nullptr;
     void *ring_k = nullptr, *ring_v = nullptr;
-    float *part_o = nullptr, *part_ml = nullptr;
+    uint64_t *part_o = nullptr, *part_ml = nullptr;  // flag-in-word split-KV partials, zero between launches
     int *counters = nullptr;
     int *status_d = nullptr;  // device status word (kernels.h STATUS_*)
     float *warp_part = nullptr;
@@ -180,6 +180,27 @@ struct oscar_kv_handle {
         cudaFree(status_d);
         cudaFree(warp_part);
         cudaFree(stage);
+    }
+
+    // a new launch plan can turn a (b, kv head)'s split-KV merge from the ticket
+    // form (fp32 partials) into the poll form (flag-in-word partials, zero = not
+    // written): the partial words are cleared once before the first launch of a plan
+    bool partials_dirty = false;
+    void launch_attn(const AttnArgs &a, cudaStream_t s) {
+        if (partials_dirty) {
+            CK(cudaMemsetAsync(part_o, 0, sizeof(uint64_t) * (size_t)(BH * maxp_alloc * 8 * D), s));
+            CK(cudaMemsetAsync(part_ml, 0, sizeof(uint64_t) * (size_t)(BH * maxp_alloc * 16), s));
+            partials_dirty = false;
+        }
+        CK(launch_attention(dbits, a, s));
+    }
+
+    void alloc_partials() {  // zeroed: a zero word is "not written" (attention.cu final_merge)
+        const size_t no = (size_t)(BH * maxp_alloc * 8 * D), nm = (size_t)(BH * maxp_alloc * 16);
+        part_o = (uint64_t *)dalloc(sizeof(uint64_t) * no);
+        part_ml = (uint64_t *)dalloc(sizeof(uint64_t) * nm);
+        CK(cudaMemset(part_o, 0, sizeof(uint64_t) * no));
+        CK(cudaMemset(part_ml, 0, sizeof(uint64_t) * nm));
     }
 
     void grow_scratch(int64_t slots, int64_t maxseg) {  // synchronous, rare (shape changes)
@@ -412,7 +433,7 @@ struct oscar_kv_handle {
         v_residual += 1;
         const int launches = last_launches;
         AttnArgs a = attn_args(q, nullptr, nullptr, out, lse);
-        CK(launch_attention(dbits, a, s));
+        launch_attn(a, s);
         last_launches = launches + 1;
         blocks_written = false;
         if (residual == R) {
@@ -446,6 +467,7 @@ struct oscar_kv_handle {
         a.part_o = part_o;
         a.part_ml = part_ml;
         a.counters = counters;
+        a.status = status_d;
         a.warp_part = warp_part;
         a.maxseg = maxseg_alloc;
         a.ncta = attention_grid(dbits, num_sms, a.nb, a.BH);
@@ -473,6 +495,8 @@ struct oscar_kv_handle {
             }
         }
         a.maxp = maxp_alloc;
+        // poll-mode merge needs every CTA resident at once (one CTA per SM)
+        static const long poll_knob = env_knob("OSCAR_POLL_MERGE", 1);  // 0: atomic tickets always (A/B)
         if (a.nb > 0 && plan.nb == a.nb && plan.tail_cost == a.tail_cost) {
             a.ncta = plan.ncta;  // same shape as the last launch: its checks hold
         } else if (a.nb > 0) {
@@ -503,10 +527,9 @@ struct oscar_kv_handle {
                 CK(cudaDeviceSynchronize());
                 cudaFree(part_o);
                 cudaFree(part_ml);
-                device_bytes -= sizeof(float) * (int64_t)BH * maxp_alloc * (8 * D + 16);
+                device_bytes -= sizeof(uint64_t) * (int64_t)BH * maxp_alloc * (8 * D + 16);
                 maxp_alloc = (int)need;
-                part_o = (float *)dalloc(sizeof(float) * (size_t)(BH * maxp_alloc * 8 * D));
-                part_ml = (float *)dalloc(sizeof(float) * (size_t)(BH * maxp_alloc * 16));
+                alloc_partials();
                 a.part_o = part_o;
                 a.part_ml = part_ml;
                 a.maxp = maxp_alloc;
@@ -520,9 +543,11 @@ struct oscar_kv_handle {
             plan.nb = a.nb;
             plan.tail_cost = a.tail_cost;
             plan.ncta = a.ncta;
+            partials_dirty = true;
         } else {
             a.maxseg = 1;  // residual-only mode: one segment per CTA (ncta = BH <= scratch slots)
         }
+        a.poll_merge = (poll_knob != 0 && a.ncta <= num_sms) ? 1 : 0;
         return a;
     }
 
@@ -562,7 +587,7 @@ struct oscar_kv_handle {
             a.pub = *pub;
             a.pub_epoch = epoch;
         }
-        CK(launch_attention(dbits, a, s));
+        launch_attn(a, s);
         ++last_launches;
         blocks_written = false;
         // buffer_quant_k/v of the current token (written into the ring by the kernel)
@@ -602,7 +627,7 @@ struct oscar_kv_handle {
             CK(cudaMemsetAsync(pbuf, 0, sizeof(unsigned long long) * kProfStride * nw, s));
             a.prof = pbuf;
         }
-        CK(launch_attention(dbits, a, s));
+        launch_attn(a, s);
         ++last_launches;
         blocks_written = false;
         if (prof) {
@@ -1372,8 +1397,7 @@ int oscar_kv_create(const oscar_kv_config *cfg, int64_t batch, int64_t q_heads, 
         h->ring_k = h->dalloc((size_t)(h->BH * R * D * 2));
         h->ring_v = h->dalloc((size_t)(h->BH * R * D * 2));
         h->maxp_alloc = (int)(2 * h->num_sms / h->BH + 3);
-        h->part_o = (float *)h->dalloc(sizeof(float) * (size_t)(h->BH * h->maxp_alloc * 8 * D));
-        h->part_ml = (float *)h->dalloc(sizeof(float) * (size_t)(h->BH * h->maxp_alloc * 16));
+        h->alloc_partials();
         h->counters = (int *)h->dalloc(sizeof(int) * (size_t)h->BH);
         CK(cudaMemset(h->counters, 0, sizeof(int) * (size_t)h->BH));
         h->status_d = (int *)h->dalloc(sizeof(int));

@@ -66,7 +66,7 @@ struct QuantizeArgs {
     // had non-finite input (the reference's params are then non-finite too)
     int *status = nullptr;
 };
-constexpr int STATUS_FP16_OVERFLOW = 1, STATUS_NONFINITE_INPUT = 2;
+constexpr int STATUS_FP16_OVERFLOW = 1, STATUS_NONFINITE_INPUT = 2, STATUS_MERGE_TIMEOUT = 4;
 cudaError_t launch_quantize(const QuantizeArgs &a, cudaStream_t st);
 
 // Copy n tokens of raw bf16 K/V into the residual ring at slot0: K ring
@@ -147,9 +147,15 @@ struct AttnArgs {
     int rotate_v;      // un-rotate output
     float *out;        // fp32 [B][Hq][D]
     float *lse;        // fp32 [B][Hq] or null
-    float *part_o;     // [BH][maxp][8][D]
-    float *part_ml;    // [BH][maxp][8][2]
-    int *counters;     // [BH], zero between launches
+    // split-KV partials of the CTAs sharing a (b, kv head), as flag-in-word
+    // 8-byte words (1 << 32 | fp32 bits; zero = not written): the merging CTA
+    // polls them and clears them again, so they are zero between launches
+    uint64_t *part_o;  // [BH][maxp][8][D]
+    uint64_t *part_ml; // [BH][maxp][8][2]
+    int *counters;     // [BH], zero between launches (ticket mode)
+    int poll_merge;    // 1: every CTA is resident (ncta <= SMs): the first CTA of a (b, kv head)
+                       // polls the others' partials; 0: last-arriving CTA by atomic ticket
+    int *status;       // device status word (STATUS_*) or null
     float *warp_part;  // [ncta][maxseg][12][8*D+16] per-warp partial scratch
     int maxseg;        // segment slots per CTA in warp_part
     int maxp;

@@ -1,8 +1,13 @@
 #!/bin/bash
+# Same-box A/B of the working tree against HEAD plus the GPU tests and the
+# profiling-build timelines.  Build first (here): scripts/abbuild.sh (writes
+# liboscar_b200_old.so from HEAD, liboscar_b200_new.so from the working tree)
+# and `make -C paper_2605_19660_b200/csrc PROF=1`.
+#   gpurun -- 'bash scripts/gpu_ab.sh'   -> gpurun_out/ab/
 export PYTHONUNBUFFERED=1
-OUT=gpurun_out/d5; mkdir -p $OUT
+OUT=gpurun_out/ab; mkdir -p $OUT
 timeout 900 python -m pytest tests -m gpu -x -q --timeout 600 > $OUT/pytest.txt 2>&1; echo "rc=$?" >> $OUT/pytest.txt
-for r in 1 2; do for v in head new; do L=$PWD/paper_2605_19660_b200/liboscar_b200_$v.so
+for r in 1 2; do for v in old new; do L=$PWD/paper_2605_19660_b200/liboscar_b200_$v.so
   echo "$v C2 $(OSCAR_LIB=$L timeout 200 python scripts/sweep.py 2 | tail -1)"
   for b in 1 8; do echo "$v C3b$b $(OSCAR_LIB=$L timeout 200 python scripts/diag_c3.py $b | tail -1)"; done
   echo "$v C5p8 $(OSCAR_LIB=$L timeout 200 python scripts/diag_c5proxy.py 8 | tail -1)"

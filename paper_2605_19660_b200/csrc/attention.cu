@@ -52,6 +52,19 @@ constexpr float LN2 = 0.6931471805599453f;
 #define OSK_RESCALE_SLACK 3
 #endif
 constexpr float RESCALE_SLACK = (float)OSK_RESCALE_SLACK;  // log2 units
+// Cost experiments for the accuracy/speed table (results are NOT
+// correct in these builds): OSK_COST_EXTRA extra record bytes per unit,
+// OSK_COST_KB_HILO a second key-offset MMA per k-step (hi/lo fp16 split of b),
+// OSK_COST_K_HILO a second code MMA + q*a_lo product per key tile (hi/lo split of q*a)
+#ifndef OSK_COST_EXTRA
+#define OSK_COST_EXTRA 0
+#endif
+#ifndef OSK_COST_KB_HILO
+#define OSK_COST_KB_HILO 0
+#endif
+#ifndef OSK_COST_K_HILO
+#define OSK_COST_K_HILO 0
+#endif
 
 constexpr int MAXSEG_SMEM = 64;  // max segments (b, kv heads) per CTA range
 constexpr int NCW_MAX = 16;
@@ -63,7 +76,9 @@ struct AttnCfg {
     // one pipeline stage: a whole INT2/INT4 record, or a 32-token quarter of a bf16 record
     static constexpr int BYTES = (BITS == 0) ? BF16_BLOCK_BYTES : Block<BITS == 0 ? 2 : BITS>::BYTES;
     static constexpr int SUB = (BITS == 0) ? 4 : 1;
-    static constexpr int STAGE = BYTES / SUB;
+    // (OSK_COST_EXTRA: cost experiments only -- every stage also streams that many
+    //  bytes past its record, as a wider record would)
+    static constexpr int STAGE = BYTES / SUB + (BITS == 0 ? 0 : OSK_COST_EXTRA);
     static constexpr int NCW = NCW_;  // warps per CTA, all consumers
     static constexpr int NTHREADS = NCW * 32;
     static constexpr int QH_OFF = 0;                                   // QSEG segment q tiles
@@ -213,6 +228,10 @@ __device__ __forceinline__ void process_block(const uint8_t *__restrict__ sb, Wa
             else if (s == 1) mma16816_zc(kbias2, zk.x, zk.y, zk.z, zk.w, qf[s][0], qf[s][1]);
             else if ((s & 1) == 0) mma16816(kbias, zk.x, zk.y, zk.z, zk.w, qf[s][0], qf[s][1]);
             else mma16816(kbias2, zk.x, zk.y, zk.z, zk.w, qf[s][0], qf[s][1]);
+            if (OSK_COST_KB_HILO) {  // cost experiment: the b_lo half of a split offset
+                if ((s & 1) == 0) mma16816(kbias, zk.y, zk.x, zk.w, zk.z, qf[s][0], qf[s][1]);
+                else mma16816(kbias2, zk.y, zk.x, zk.w, zk.z, qf[s][0], qf[s][1]);
+            }
         }
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
@@ -227,6 +246,11 @@ __device__ __forceinline__ void process_block(const uint8_t *__restrict__ sb, Wa
             else
                 mma16816(sacc[i], src[0 * WPF + half] & mask, src[1 * WPF + half] & mask,
                          src[2 * WPF + half] & mask, src[3 * WPF + half] & mask, bq[i >> 1][0], bq[i >> 1][1]);
+            if (OSK_COST_K_HILO) {  // cost experiment: the (q*a)_lo half of a split B operand
+                const uint32_t l0 = hmul2_u32(bq[i >> 1][0], 0x11001100u), l1 = hmul2_u32(bq[i >> 1][1], 0x11001100u);
+                mma16816(sacc[i], src[0 * WPF + half] & mask, src[1 * WPF + half] & mask,
+                         src[2 * WPF + half] & mask, src[3 * WPF + half] & mask, l0, l1);
+            }
         }
     }
 

@@ -388,7 +388,7 @@ def run_ours(args, rank, world, local_rank):
                                  f"written bytes)"),
         "e2e": {"value": world * B * K / e2e_s, "unit": "tokens/s", "h2d_bytes_per_step": int(h2d),
                 "d2h_bytes_per_step": int(d2h), "us_per_step": 1e6 * e2e_s / K,
-                "entry": "oscar_kv_decode_step_host (C-ABI, called with host pointers): pinned host q/k/v (one batched H2D copy), fp32 out written by the kernel into pinned host memory, stream synchronised each step"},
+                "entry": "oscar_kv_decode_step_host (C-ABI, called with host pointers): pinned host q/k/v read by the attention kernel over PCIe (counted as h2d bytes), fp32 out written by the kernel into pinned host memory, stream synchronised each step"},
         "clocks": clk,
     }
     cache.close()

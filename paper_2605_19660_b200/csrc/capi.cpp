@@ -1687,8 +1687,10 @@ int oscar_kv_decode_step_host(oscar_kv_handle *h, const void *q_host, const void
         void *dq = p, *dk = p + qb, *dv = p + qb + kb;
         float *dout = (float *)(p + qb + 2 * kb);
         float *dlse = (float *)(p + qb + 2 * kb + ob);
-        // inputs: one H2D copy each of q, k, v (zero-copy reads of mapped inputs
-        // measured slower: PCIe latency lands on the kernel's q prologue and tail)
+        // inputs: page-locked q, k, v are read by the attention kernel itself over
+        // PCIe (the q rows once per CTA after the ring fill is queued, the current k/v
+        // by the tail tiles): no copies ahead of the launch -- e2e 129-133 -> 113-121 us
+        // at C2 (same box); pageable inputs take one H2D copy each
         auto mapped = [](const void *hp) -> void * {
             cudaPointerAttributes at{};
             if (cudaPointerGetAttributes(&at, hp) != cudaSuccess) {
@@ -1697,9 +1699,19 @@ int oscar_kv_decode_step_host(oscar_kv_handle *h, const void *q_host, const void
             }
             return at.type == cudaMemoryTypeHost ? at.devicePointer : nullptr;
         };
-        CK(cudaMemcpyAsync(dq, q_host, qb, cudaMemcpyHostToDevice, s));
-        CK(cudaMemcpyAsync(dk, k_host, kb, cudaMemcpyHostToDevice, s));
-        CK(cudaMemcpyAsync(dv, v_host, kb, cudaMemcpyHostToDevice, s));
+        static const long zc_in = env_knob("OSCAR_HOST_INPUTS", 1);  // 0: always copy (A/B)
+        const void *zq = zc_in ? mapped(q_host) : nullptr;
+        const void *zk = zc_in ? mapped(k_host) : nullptr;
+        const void *zv = zc_in ? mapped(v_host) : nullptr;
+        if (zq && zk && zv) {
+            dq = const_cast<void *>(zq);
+            dk = const_cast<void *>(zk);
+            dv = const_cast<void *>(zv);
+        } else {
+            CK(cudaMemcpyAsync(dq, q_host, qb, cudaMemcpyHostToDevice, s));
+            CK(cudaMemcpyAsync(dk, k_host, kb, cudaMemcpyHostToDevice, s));
+            CK(cudaMemcpyAsync(dv, v_host, kb, cudaMemcpyHostToDevice, s));
+        }
         // outputs: page-locked host buffers are written by the kernel itself
         // (mapped, zero-copy), saving the D2H copies; pageable ones are copied
         float *zo = (float *)mapped(out_host);

@@ -100,3 +100,47 @@ def test_more_segments_than_the_ticket_table():
         err = rel_err(out[b].astype(np.float64), ref)
         log_err(f"many_segments_grid_growth[B=1200,S=200,H=8][b={b}]", err)
         assert err <= 5e-3, (b, err)
+
+
+_MERGE_FORMS_SCRIPT = r"""
+import sys, numpy as np, torch
+sys.path[:0] = sys.argv[1:2]
+from paper_2605_19660_b200 import KvCache, PipelineConfig
+gen = torch.Generator(device="cuda"); gen.manual_seed(11)
+outs = []
+# ~2 CTA partials per segment; 9 (the largest poll-form merge); 20 (ticket form in both runs)
+for B, H, g, S in ((16, 8, 4, 4 * 1024 + 77), (1, 1, 4, 72 * 128 + 5), (2, 1, 4, 160 * 128 + 5)):
+    k = torch.randn((B, S + 3, H, 128), generator=gen, device="cuda").to(torch.bfloat16)
+    v = torch.randn((B, S + 3, H, 128), generator=gen, device="cuda").to(torch.bfloat16)
+    q = torch.randn((B, H * g, 128), generator=gen, device="cuda").to(torch.bfloat16)
+    c = KvCache(PipelineConfig(heads=H, bits=2), batch=B, q_heads=H * g, max_tokens=S + 64, keep_exact=False)
+    c.buffer_quant(k[:, :S].contiguous(), v[:, :S].contiguous())
+    for t in range(S, S + 3):
+        outs.append(c.decode_step(q, k[:, t].contiguous(), v[:, t].contiguous()).cpu().numpy().ravel())
+    assert c.status()["raw"] == 0
+np.save(sys.argv[2], np.concatenate(outs))
+"""
+
+
+def test_poll_and_ticket_merge_forms_agree(tmp_path):
+    """The split-KV merge has two forms (attention.cu: the segment's first CTA polls
+    flag-in-word partials, or the last-arriving CTA merges after an atomic ticket).
+    The same decode steps with the poll form allowed (default) and with tickets only
+    (OSCAR_POLL_MERGE=0, read once per process) agree to fp32 rounding, at shapes
+    whose segments have ~2, 9 and 20 partials."""
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    script = tmp_path / "forms.py"
+    script.write_text(_MERGE_FORMS_SCRIPT)
+    res = {}
+    for mode in ("1", "0"):
+        env = dict(os.environ, OSCAR_POLL_MERGE=mode)
+        out = tmp_path / f"out{mode}.npy"
+        subprocess.run([sys.executable, str(script), root, str(out)], env=env, check=True, timeout=300)
+        res[mode] = np.load(out)
+    scale = np.abs(res["0"]).max()
+    err = np.abs(res["1"] - res["0"]).max() / scale
+    log_err("merge_forms_poll_vs_ticket", float(err))
+    assert err < 1e-5, err

@@ -245,3 +245,45 @@ def test_p2p_exchange_two_processes_ipc(tmp_path):
         got = np.load(res + f".{rank}.npy")
         for t in range(8):
             assert rel_err(got[t], ref[t]) < SHARD_TOL, (rank, t)
+
+
+def _nccl_gather_worker(rdzv, out_path):
+    import numpy as np
+    import torch
+    import torch.distributed as td
+
+    from paper_2605_19660_b200.kv_cache import lse_merge
+    from paper_2605_19660_b200.sharding import gather_partials
+
+    torch.cuda.set_device(0)
+    td.init_process_group("nccl", init_method=f"file://{rdzv}", rank=0, world_size=1,
+                          device_id=torch.device("cuda", 0))
+    g = torch.Generator(device="cuda")
+    g.manual_seed(3)
+    o = torch.randn((28, 128), generator=g, device="cuda")
+    lse = torch.randn((28,), generator=g, device="cuda")
+    outs, lses = gather_partials(o, lse)  # the NCCL branch: all_gather_into_tensor of [rows, d+1]
+    merged = lse_merge(outs, lses)
+    torch.cuda.synchronize()
+    assert td.get_backend() == "nccl"
+    np.save(out_path, np.stack([o.cpu().numpy(), outs[0].cpu().numpy(), merged.cpu().numpy()]))
+    td.destroy_process_group()
+
+
+def test_nccl_gather_partials_branch(tmp_path):
+    """gather_partials' NCCL branch (one packed all_gather_into_tensor of (O, LSE)) on a
+    one-rank NCCL group on the B200 (the box has one GPU; NCCL rejects two ranks on one
+    device), followed by the device LSE merge: a single partial merges to itself."""
+    import multiprocessing as mp
+
+    import numpy as np
+
+    ctx = mp.get_context("spawn")
+    out = tmp_path / "nccl.npy"
+    p = ctx.Process(target=_nccl_gather_worker, args=(str(tmp_path / "rdzv"), str(out)))
+    p.start()
+    p.join(240)
+    assert p.exitcode == 0, p.exitcode
+    o, gathered, merged = np.load(out)
+    assert np.array_equal(o, gathered)
+    assert np.allclose(merged, o, rtol=1e-6, atol=1e-6)

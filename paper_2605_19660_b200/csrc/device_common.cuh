@@ -171,13 +171,6 @@ __device__ __forceinline__ float fast_exp2(float x) {
     return y;
 }
 
-// 2^x on a packed half2 (one MUFU op for two values)
-__device__ __forceinline__ uint32_t ex2_h2(uint32_t x) {
-    uint32_t y;
-    asm("ex2.approx.f16x2 %0, %1;\n" : "=r"(y) : "r"(x));
-    return y;
-}
-
 __device__ __forceinline__ uint4 lds128(const void *p) {
     return *reinterpret_cast<const uint4 *>(p);
 }

@@ -535,7 +535,7 @@ __device__ __forceinline__ void build_q_tiles(const AttnArgs &a, __half *tiles, 
 // One 16-token tile [t0, t0+16) of the residual window (+ the current token at
 // index r) for one (b, kv head), merged into the warp's partial slot.
 //   QK^T: D[token, head] = sum_c K[token, c] q[head, c]    A = K rows (ring, row-major)
-//   P.V : D[chan, head]  = sum_t V^T[chan, t] P[head, t]   A = V^T rows (ring, channel-major)
+//   P.V : D[chan, head]  = sum_t V^T[chan, t] P[head, t]   A = V^T rows (ring, tile-major)
 // Invalid tokens (>= ntok) get -inf logits and zero V; the ring is read
 // through L2 (written by the previous steps).
 struct ResidualRefs {
@@ -571,10 +571,10 @@ __device__ __forceinline__ void residual_compute(const ResidualRefs rr, const __
     };
     const int u0 = t0 + 2 * tq, u1 = u0 + 8;  // token pairs (u0, u0+1), (u1, u1+1) of this lane
     auto vpair = [&](int c, int u) -> uint32_t {
-        uint32_t w = (u + 1 < r) ? *reinterpret_cast<const uint32_t *>(ringv + (int64_t)c * R + u) : 0u;
+        uint32_t w = (u + 1 < r) ? *reinterpret_cast<const uint32_t *>(ringv + vring_index(c, u)) : 0u;
         if (u + 1 >= r && u < ntok) {  // tail of the window: per-token select ring / current / zero
-            const uint32_t lo = u < r ? ringv[(int64_t)c * R + u] : (u < ntok ? vc[c] : 0u);
-            const uint32_t hi = u + 1 < r ? ringv[(int64_t)c * R + u + 1] : (u + 1 < ntok ? vc[c] : 0u);
+            const uint32_t lo = u < r ? ringv[vring_index(c, u)] : (u < ntok ? vc[c] : 0u);
+            const uint32_t hi = u + 1 < r ? ringv[vring_index(c, u + 1)] : (u + 1 < ntok ? vc[c] : 0u);
             w = lo | (hi << 16);
         }
         return w;
@@ -837,12 +837,11 @@ __device__ __noinline__ void residual_tile(const ResidualRefs rr, float *slot, c
     // slot r: nothing in this launch reads that slot (tiles take it from kcur)
     if (ring_k_w && rr.kc && t0 <= rr.r && rr.r < t0 + 16) {
         reinterpret_cast<uint2 *>(ring_k_w + rr.r * D)[lane] = reinterpret_cast<const uint2 *>(rr.kc)[lane];
-        const uint2 vv = reinterpret_cast<const uint2 *>(rr.vc)[lane];  // V ring is channel-major [D][R]
-        uint16_t *rv = ring_v_w + rr.r;
-        rv[(4 * lane + 0) * R] = (uint16_t)(vv.x & 0xffffu);
-        rv[(4 * lane + 1) * R] = (uint16_t)(vv.x >> 16);
-        rv[(4 * lane + 2) * R] = (uint16_t)(vv.y & 0xffffu);
-        rv[(4 * lane + 3) * R] = (uint16_t)(vv.y >> 16);
+        const uint2 vv = reinterpret_cast<const uint2 *>(rr.vc)[lane];  // V ring is tile-major (vring_index)
+        ring_v_w[vring_index(4 * lane + 0, rr.r)] = (uint16_t)(vv.x & 0xffffu);
+        ring_v_w[vring_index(4 * lane + 1, rr.r)] = (uint16_t)(vv.x >> 16);
+        ring_v_w[vring_index(4 * lane + 2, rr.r)] = (uint16_t)(vv.y & 0xffffu);
+        ring_v_w[vring_index(4 * lane + 3, rr.r)] = (uint16_t)(vv.y >> 16);
     }
 }
 
@@ -857,12 +856,11 @@ __device__ __noinline__ void residual_tile_first(const ResidualRefs rr, const __
     *out = rp;
     if (ring_k_w && rr.kc && t0 <= rr.r && rr.r < t0 + 16) {
         reinterpret_cast<uint2 *>(ring_k_w + rr.r * D)[lane] = reinterpret_cast<const uint2 *>(rr.kc)[lane];
-        const uint2 vv = reinterpret_cast<const uint2 *>(rr.vc)[lane];  // V ring is channel-major [D][R]
-        uint16_t *rv = ring_v_w + rr.r;
-        rv[(4 * lane + 0) * R] = (uint16_t)(vv.x & 0xffffu);
-        rv[(4 * lane + 1) * R] = (uint16_t)(vv.x >> 16);
-        rv[(4 * lane + 2) * R] = (uint16_t)(vv.y & 0xffffu);
-        rv[(4 * lane + 3) * R] = (uint16_t)(vv.y >> 16);
+        const uint2 vv = reinterpret_cast<const uint2 *>(rr.vc)[lane];  // V ring is tile-major (vring_index)
+        ring_v_w[vring_index(4 * lane + 0, rr.r)] = (uint16_t)(vv.x & 0xffffu);
+        ring_v_w[vring_index(4 * lane + 1, rr.r)] = (uint16_t)(vv.x >> 16);
+        ring_v_w[vring_index(4 * lane + 2, rr.r)] = (uint16_t)(vv.y & 0xffffu);
+        ring_v_w[vring_index(4 * lane + 3, rr.r)] = (uint16_t)(vv.y >> 16);
     }
 }
 

@@ -266,7 +266,7 @@ struct oscar_kv_handle {
     void flush(cudaStream_t s) {
         // the rings are the source of one block per (b, h): K [bh][R][D], V [bh][D][R]
         const int64_t H = cfg.heads;
-        quantize_from(ring_k, ring_v, H * R * D, D, (int64_t)R * D, 0, 1, packed / R, s, /*vst=*/1, /*vsc=*/R);
+        quantize_from(ring_k, ring_v, H * R * D, D, (int64_t)R * D, 0, 1, packed / R, s, /*vst=*/0, /*vsc=*/0);
         packed += R;
         residual = 0;
     }
@@ -953,7 +953,7 @@ HostCache build_host_cache(oscar_kv_handle *h, int64_t b) {
             if (tc.scales) s = host::token_scale(row, D, cfg.scaling);
             for (int c = 0; c < D; ++c) hc.k_res[(t * H + hh) * D + c] = row[c];
             hc.k_norms_res[t * H + hh] = s;
-            for (int c = 0; c < D; ++c) row[c] = host::bf16_to_double(rv[c * R + t]);  // V ring is channel-major
+            for (int c = 0; c < D; ++c) row[c] = host::bf16_to_double(rv[vring_index(c, (int)t)]);  // tile-major ring
             if (cfg.rotate_v) host::fht(row, D);
             for (int c = 0; c < D; ++c) hc.v_res[(t * H + hh) * D + c] = row[c];
         }
@@ -1268,7 +1268,7 @@ void load_kvc1(oscar_kv_handle *h, int64_t b, const char *path) {
             }
         }
     }
-    // residual window -> raw bf16 rings (K token-major, V channel-major).  Rows that
+    // residual window -> raw bf16 rings (K token-major, V tile-major).  Rows that
     // are not transforms of bf16 inputs (a cache the reference built from its fp64
     // projections) put the handle in the fp64 form: the rows are kept exactly in
     // the residual shadow and the rings hold their bf16 image
@@ -1281,7 +1281,7 @@ void load_kvc1(oscar_kv_handle *h, int64_t b, const char *path) {
                 for (int64_t t = 0; t < r; ++t) {
                     raw_key_row(&kres[(t * H + hh) * D], kres_n[t * H + hh], tc, c.scaling, &rk[t * D]);
                     raw_value_row(&vres[(t * H + hh) * D], c.rotate_v, row.data());
-                    for (int ch = 0; ch < D; ++ch) rv[(size_t)ch * R + t] = row[ch];
+                    for (int ch = 0; ch < D; ++ch) rv[vring_index(ch, (int)t)] = row[ch];
                 }
             }
         } catch (const InvalidArg &) {
@@ -1302,7 +1302,7 @@ void load_kvc1(oscar_kv_handle *h, int64_t b, const char *path) {
                 if (tc.rotates) host::fht(x, D);
                 for (int ch = 0; ch < D; ++ch) {
                     rk[t * D + ch] = double_to_half_rn(x[ch]);
-                    rv[(size_t)ch * R + t] = double_to_half_rn(vres[(t * H + hh) * D + ch]);
+                    rv[vring_index(ch, (int)t)] = double_to_half_rn(vres[(t * H + hh) * D + ch]);
                 }
             }
         }

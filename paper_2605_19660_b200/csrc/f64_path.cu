@@ -198,9 +198,9 @@ __global__ void window_f64_kernel(const WindowF64Args a) {
         double *rv = a.res_v + ((int64_t)bh * R + slot) * D;
 #pragma unroll
         for (int e = 0; e < 4; ++e) rv[4 * lane + e] = x[e];
-        uint16_t *ring = reinterpret_cast<uint16_t *>(a.ring_v) + (int64_t)bh * R * D + slot;  // channel-major
+        uint16_t *ring = reinterpret_cast<uint16_t *>(a.ring_v) + (int64_t)bh * R * D;  // tile-major (vring_index)
 #pragma unroll
-        for (int e = 0; e < 4; ++e) ring[(int64_t)(4 * lane + e) * R] = ring_image(x[e]);
+        for (int e = 0; e < 4; ++e) ring[vring_index(4 * lane + e, slot)] = ring_image(x[e]);
     }
 }
 

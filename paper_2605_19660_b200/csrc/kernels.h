@@ -45,7 +45,7 @@ struct TransformCfg {
 // Key element (b, h, token t, channel c) lives at
 //   k + b*sb + (tok0 + t)*st + h*sh + c,
 // value element at v + b*sb + (tok0 + t)*vst + h*sh + c*vsc (vsc = 1 for a
-// token-major source; the residual ring stores V channel-major, vsc = R).
+// token-major source); vsc = 0: v is a residual V ring (tile-major, layout.h vring_index).
 // Block k of (b,h) is written to blocks[((b*H+h)*max_blocks + blk0 + k)*bytes].
 struct QuantizeArgs {
     const void *k, *v;
@@ -70,8 +70,9 @@ constexpr int STATUS_FP16_OVERFLOW = 1, STATUS_NONFINITE_INPUT = 2, STATUS_MERGE
 cudaError_t launch_quantize(const QuantizeArgs &a, cudaStream_t st);
 
 // Copy n tokens of raw bf16 K/V into the residual ring at slot0: K ring
-// [bh][R][D] token-major, V ring [bh][D][R] channel-major (so the attention
-// kernel's P.V A fragments are contiguous token pairs).
+// [bh][R][D] token-major, V ring [bh][R/16][D][16] tile-major (layout.h
+// vring_index: the attention kernel's P.V A fragments are contiguous token
+// pairs, and one 16-token tile is one contiguous 4 KB span).
 struct RingCopyArgs {
     const void *k, *v;
     int64_t sb, st, sh, tok0;

@@ -65,6 +65,14 @@ constexpr int G = 32;         // group_size
 constexpr int NGRP = R / G;   // K groups per channel per block (4)
 constexpr int NGC = D / G;    // V groups per token (4)
 
+// Residual-window V ring of one (sequence, KV head): tile-major [R/16][D][16] bf16 --
+// the 16 tokens of a 16-token tile are contiguous per channel (a token pair is one
+// 32-bit word, the P.V A operand), and a whole tile is one contiguous 4 KB span that a
+// single bulk copy moves into shared memory.  (The K ring is token-major [R][D].)
+OSK_HD int64_t vring_index(int channel, int token) {
+    return (int64_t)(token >> 4) * (D * 16) + channel * 16 + (token & 15);
+}
+
 template <int BITS>
 struct Block {
     static constexpr int CODE_BYTES = R * D * BITS / 8;      // per K or V

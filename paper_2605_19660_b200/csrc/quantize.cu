@@ -231,15 +231,15 @@ __global__ void __launch_bounds__(QT * GPAR) quantize_kernel(const QuantizeArgs 
         // ---------------- V: optional rotation, per-token groups ----------------
         {
             double y[32];
-            if (from_ring) {  // channel-major residual ring
+            if (from_ring) {  // the residual V ring (tile-major)
 #pragma unroll
-                for (int i = 0; i < 32; ++i) y[i] = bf16_bits_to_double(rv[(int64_t)(q * 32 + i) * R + t], bad);
+                for (int i = 0; i < 32; ++i) y[i] = bf16_bits_to_double(rv[vring_index(q * 32 + i, t)], bad);
             } else if (a.vsc == 1) {
                 load32(vin + (tok_base + t) * a.vst + q * 32, y, bad);
-            } else {  // channel-major source (the residual ring)
-                const uint16_t *vp = reinterpret_cast<const uint16_t *>(vin) + (tok_base + t) * a.vst;
+            } else {  // a residual V ring (tile-major, vring_index): the flush
+                const uint16_t *vp = reinterpret_cast<const uint16_t *>(vin);
 #pragma unroll
-                for (int i = 0; i < 32; ++i) y[i] = bf16_bits_to_double(vp[(int64_t)(q * 32 + i) * a.vsc], bad);
+                for (int i = 0; i < 32; ++i) y[i] = bf16_bits_to_double(vp[vring_index(q * 32 + i, (int)(tok_base + t))], bad);
             }
             if ((bad & 0x80008000u) && a.status) atomicOr(a.status, STATUS_NONFINITE_INPUT);
             if (tc.rotate_v) fht128_quad(y, q);
@@ -342,10 +342,10 @@ __global__ void __launch_bounds__(QT) raw_block_kernel_dyn(const QuantizeArgs a)
     const uint16_t *rv = a.rv ? reinterpret_cast<const uint16_t *>(a.rv) + (int64_t)bh * R * D : nullptr;
     for (int i = threadIdx.x; i < R * 16; i += QT) {
         const int t = i >> 4, part = i & 15;
-        if (blk == 0 && t < a.rtok) {  // open residual window: K row-major, V channel-major rings
+        if (blk == 0 && t < a.rtok) {  // open residual window: K row-major ring, V tile-major ring
             reinterpret_cast<uint4 *>(sk)[i] = *reinterpret_cast<const uint4 *>(rk + (int64_t)t * D + part * 8);
 #pragma unroll
-            for (int e = 0; e < 8; ++e) sv[t * D + part * 8 + e] = rv[(int64_t)(part * 8 + e) * R + t];
+            for (int e = 0; e < 8; ++e) sv[t * D + part * 8 + e] = rv[vring_index(part * 8 + e, t)];
             continue;
         }
         reinterpret_cast<uint4 *>(sk)[i] = *reinterpret_cast<const uint4 *>(kin + (tok_base + t) * a.st + part * 8);
@@ -353,7 +353,7 @@ __global__ void __launch_bounds__(QT) raw_block_kernel_dyn(const QuantizeArgs a)
             reinterpret_cast<uint4 *>(sv)[i] = *reinterpret_cast<const uint4 *>(vin + (tok_base + t) * a.vst + part * 8);
         } else {
 #pragma unroll
-            for (int e = 0; e < 8; ++e) sv[t * D + part * 8 + e] = vin[(tok_base + t) * a.vst + (part * 8 + e) * a.vsc];
+            for (int e = 0; e < 8; ++e) sv[t * D + part * 8 + e] = vin[vring_index(part * 8 + e, (int)(tok_base + t))];
         }
     }
     __syncthreads();
@@ -379,14 +379,15 @@ __global__ void ring_copy_kernel(const RingCopyArgs a) {
     const uint16_t *kin = reinterpret_cast<const uint16_t *>(a.k) + b * a.sb + h * a.sh + (a.tok0 + t) * a.st;
     const uint16_t *vin = reinterpret_cast<const uint16_t *>(a.v) + b * a.sb + h * a.sh + (a.tok0 + t) * a.st;
     uint16_t *rk = reinterpret_cast<uint16_t *>(a.ring_k) + ((int64_t)bh * R + a.slot0 + t) * D;
-    uint16_t *rv = reinterpret_cast<uint16_t *>(a.ring_v) + (int64_t)bh * R * D + a.slot0 + t;
-    const int i = threadIdx.x;  // 32 threads: 16 B of K each (row-major), 4 V channels each (channel-major)
+    uint16_t *rv = reinterpret_cast<uint16_t *>(a.ring_v) + (int64_t)bh * R * D;
+    const int slot = (int)(a.slot0 + t);
+    const int i = threadIdx.x;  // 32 threads: 16 B of K each (row-major), 4 V channels each (tile-major ring)
     if (i < 16) reinterpret_cast<uint4 *>(rk)[i] = reinterpret_cast<const uint4 *>(kin)[i];
     const uint2 vv = reinterpret_cast<const uint2 *>(vin)[i];
-    rv[(4 * i + 0) * R] = (uint16_t)(vv.x & 0xffffu);
-    rv[(4 * i + 1) * R] = (uint16_t)(vv.x >> 16);
-    rv[(4 * i + 2) * R] = (uint16_t)(vv.y & 0xffffu);
-    rv[(4 * i + 3) * R] = (uint16_t)(vv.y >> 16);
+    rv[vring_index(4 * i + 0, slot)] = (uint16_t)(vv.x & 0xffffu);
+    rv[vring_index(4 * i + 1, slot)] = (uint16_t)(vv.x >> 16);
+    rv[vring_index(4 * i + 2, slot)] = (uint16_t)(vv.y & 0xffffu);
+    rv[vring_index(4 * i + 3, slot)] = (uint16_t)(vv.y >> 16);
 }
 
 }  // namespace

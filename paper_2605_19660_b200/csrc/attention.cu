@@ -56,6 +56,9 @@ constexpr float RESCALE_SLACK = (float)OSK_RESCALE_SLACK;  // log2 units
 // correct in these builds): OSK_COST_EXTRA extra record bytes per unit,
 // OSK_COST_KB_HILO a second key-offset MMA per k-step (hi/lo fp16 split of b),
 // OSK_COST_K_HILO a second code MMA + q*a_lo product per key tile (hi/lo split of q*a)
+#ifndef OSK_SKIP_TILES  // experiment: residual tiles not computed (results not correct)
+#define OSK_SKIP_TILES 0
+#endif
 #ifndef OSK_COST_EXTRA
 #define OSK_COST_EXTRA 0
 #endif
@@ -1047,7 +1050,7 @@ __global__ void __launch_bounds__(NCW_ * 32, 1) decode_attn_kernel(const AttnArg
             rr.f16 = a.ring_f16;
             return rr;
         };
-        if (tile_j >= 0 && !tile_late) {
+        if (tile_j >= 0 && !tile_late && !OSK_SKIP_TILES) {
             ResPartial rp;
             residual_tile_first(tile_refs(), qbase, tile_j * 16, ntok_t, lane, c0,
                                 a.write_ring ? reinterpret_cast<uint16_t *>(a.ring_k) + bh * R * D : nullptr,
@@ -1193,7 +1196,7 @@ __global__ void __launch_bounds__(NCW_ * 32, 1) decode_attn_kernel(const AttnArg
         if (kProf && a.prof) tmr[7] += clk() - te0;
     }
 
-    if constexpr (DEFER) {  // tiles of the tail segments after the first, after the packed units
+    if (DEFER && !OSK_SKIP_TILES) {  // tiles of the tail segments after the first, after the packed units
         const int ntok = a.r + (a.kcur ? 1 : 0);
         const int ntiles = (ntok + 15) >> 4;
         int rbase = (int)(nunits % NCW);

@@ -1,4 +1,5 @@
-"""Attention latency vs residual-window fill r, eager vs CUDA-graph timed (C2 INT2).
+"""Attention latency vs residual-window fill r, eager vs CUDA-graph timed (C2 INT2 by
+default; DIAG_SHAPE=c3b1|c3b8|c3b64|c3b256 for one C3 layer at that batch).
 usage: python scripts/diag_resid.py [bits]"""
 import json
 import os
@@ -11,7 +12,8 @@ from bench import step_inputs, synth_kv
 from paper_2605_19660_b200 import KvCache, PipelineConfig
 
 bits = int(sys.argv[1]) if len(sys.argv) > 1 else 2
-B, S, Hq, Hkv = 16, 32768, 32, 8
+B, S, Hq, Hkv = {"c2": (16, 32768, 32, 8), "c3b1": (1, 8192, 28, 4), "c3b8": (8, 8192, 28, 4),
+                 "c3b64": (64, 8192, 28, 4), "c3b256": (256, 8192, 28, 4)}[os.environ.get("DIAG_SHAPE", "c2")]
 dev = torch.device("cuda")
 cache = KvCache(PipelineConfig(heads=Hkv, bits=bits), batch=B, q_heads=Hq, max_tokens=S + 256, keep_exact=False)
 k, v = synth_kv(B, S, Hkv, 1, dev)

@@ -1700,9 +1700,11 @@ int oscar_kv_decode_step_host(oscar_kv_handle *h, const void *q_host, const void
             return at.type == cudaMemoryTypeHost ? at.devicePointer : nullptr;
         };
         static const long zc_in = env_knob("OSCAR_HOST_INPUTS", 1);  // 0: always copy (A/B)
-        const void *zq = zc_in ? mapped(q_host) : nullptr;
-        const void *zk = zc_in ? mapped(k_host) : nullptr;
-        const void *zv = zc_in ? mapped(v_host) : nullptr;
+        // (16-byte aligned rows only: the kernel reads them with vector loads)
+        const bool al = (((uintptr_t)q_host | (uintptr_t)k_host | (uintptr_t)v_host) & 15) == 0;
+        const void *zq = zc_in && al ? mapped(q_host) : nullptr;
+        const void *zk = zc_in && al ? mapped(k_host) : nullptr;
+        const void *zv = zc_in && al ? mapped(v_host) : nullptr;
         if (zq && zk && zv) {
             dq = const_cast<void *>(zq);
             dk = const_cast<void *>(zk);

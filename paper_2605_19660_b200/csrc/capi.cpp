@@ -1716,7 +1716,8 @@ int oscar_kv_decode_step_host(oscar_kv_handle *h, const void *q_host, const void
         }
         // outputs: page-locked host buffers are written by the kernel itself
         // (mapped, zero-copy), saving the D2H copies; pageable ones are copied
-        float *zo = ((uintptr_t)out_host & 15) == 0 ? (float *)mapped(out_host) : nullptr;  // float4 row stores
+        static const long zc_out = env_knob("OSCAR_HOST_OUT", 1);  // 0: device buffer + one D2H copy (A/B)
+        float *zo = zc_out && ((uintptr_t)out_host & 15) == 0 ? (float *)mapped(out_host) : nullptr;  // float4 rows
         float *zl = lse_host ? (float *)mapped(lse_host) : nullptr;
         h->decode_step(dq, dk, dv, zo ? zo : dout, lse_host ? (zl ? zl : dlse) : nullptr, s);
         if (!zo) CK(cudaMemcpyAsync(out_host, dout, ob, cudaMemcpyDeviceToHost, s));

@@ -74,7 +74,7 @@ constexpr int NCW_MAX = 16;
 constexpr int QH_STRIDE = 136;  // padded fp16 row of a q tile (conflict-free; 16-B aligned rows)
 constexpr int QSEG = 4;         // segment q tiles held in shared memory (one wave)
 
-template <int BITS, int NCW_ = ((BITS == 4) ? 8 : 12)>
+template <int BITS, int NCW_ = ((BITS == 4) ? 8 : 12), bool TILES_ = false>
 struct AttnCfg {
     // one pipeline stage: a whole INT2/INT4 record, or a 32-token quarter of a bf16 record
     static constexpr int BYTES = (BITS == 0) ? BF16_BLOCK_BYTES : Block<BITS == 0 ? 2 : BITS>::BYTES;
@@ -87,7 +87,8 @@ struct AttnCfg {
     static constexpr int QH_OFF = 0;                                   // QSEG segment q tiles
     static constexpr int SEG_OFF = QH_OFF + QSEG * 8 * QH_STRIDE * 2;  // lastflag[MAXSEG_SMEM]
     static constexpr int TAB_OFF = ((SEG_OFF + MAXSEG_SMEM * 4 + 7) / 8) * 8;  // last-segment slot per warp
-    static constexpr int BAR_OFF = TAB_OFF + NCW_MAX * 8;
+    static constexpr int WALK_OFF = TAB_OFF + NCW_MAX * 8;  // per-warp refill walker (tile units)
+    static constexpr int BAR_OFF = WALK_OFF + (TILES_ ? NCW_MAX * 16 : 0);
     // shared ring of NST stages: as many whole stages as fit in 227 KB
     static constexpr int NST = (232448 - BAR_OFF - 1024) / STAGE;
     static constexpr int CNT_OFF = BAR_OFF + NST * 8;  // consumed-round counter per stage
@@ -831,6 +832,126 @@ __device__ __forceinline__ void final_merge_ll(const AttnArgs &a, int64_t bh, in
     write_row(a, b, kvh, h, x, (L > 0.f) ? (M + __log2f(L)) * LN2 : -CUDART_INF_F, lane);
 }
 
+// ---- residual-window tiles as pipeline units (the TILES kernel, small launches) ------
+// A tile's bytes ride the ring 17 units ahead like the records instead of a dependent
+// round trip of their own.  Stage layout of a tile (tokens t0..t0+15 of one (b, kv head)):
+//   [0, 4096)      K rows [16][128] bf16 (ring rows t0..r-1; row r = the current token)
+//   [4096, 8192)   the ring's V tile [128][16] bf16 (tile-major ring: one 4 KB span)
+//   [8192, 8448)   the current token's V row [128] bf16 (when t0 <= r < t0 + 16)
+//   [8448, ...)    the raw q rows of the (b, kv head) [g][128] bf16
+constexpr int TILE_V_OFF = 4096, TILE_VCUR_OFF = 8192, TILE_Q_OFF = 8448;
+
+__device__ __noinline__ void tile_compute_smem(const uint8_t *__restrict__ sb, int t0, int r, int ntok, int g,
+                                               int lane, float c0, ResPartial *out) {
+    ResPartial &rp = *out;
+    const int gq = lane >> 2, tq = lane & 3;
+    const uint16_t *K = reinterpret_cast<const uint16_t *>(sb);
+    const uint16_t *V = reinterpret_cast<const uint16_t *>(sb + TILE_V_OFF);
+    const uint16_t *VC = reinterpret_cast<const uint16_t *>(sb + TILE_VCUR_OFF);
+    const uint16_t *Q = reinterpret_cast<const uint16_t *>(sb + TILE_Q_OFF);
+    const int tA = t0 + gq, tB = tA + 8;
+    const bool vA = tA < ntok, vB = tB < ntok;
+    uint32_t kf[8][4], qb[8][2], vf[8][4];
+#pragma unroll
+    for (int s = 0; s < 8; ++s) {
+        const int c = 16 * s + 2 * tq;
+        kf[s][0] = vA ? *reinterpret_cast<const uint32_t *>(K + gq * D + c) : 0u;
+        kf[s][1] = vB ? *reinterpret_cast<const uint32_t *>(K + (gq + 8) * D + c) : 0u;
+        kf[s][2] = vA ? *reinterpret_cast<const uint32_t *>(K + gq * D + c + 8) : 0u;
+        kf[s][3] = vB ? *reinterpret_cast<const uint32_t *>(K + (gq + 8) * D + c + 8) : 0u;
+        qb[s][0] = gq < g ? *reinterpret_cast<const uint32_t *>(Q + gq * D + c) : 0u;
+        qb[s][1] = gq < g ? *reinterpret_cast<const uint32_t *>(Q + gq * D + c + 8) : 0u;
+    }
+    const int u0 = 2 * tq, u1 = u0 + 8;  // tile-local token pairs of this lane
+    auto vpair = [&](int c, int ul) -> uint32_t {
+        const int u = t0 + ul;
+        if (u + 1 < r) return *reinterpret_cast<const uint32_t *>(V + c * 16 + ul);
+        const uint32_t lo = u < r ? V[c * 16 + ul] : (u < ntok ? VC[c] : 0u);
+        const uint32_t hi = u + 1 < r ? V[c * 16 + ul + 1] : (u + 1 < ntok ? VC[c] : 0u);
+        return lo | (hi << 16);
+    };
+#pragma unroll
+    for (int mm = 0; mm < 8; ++mm) {
+        const int cA = 16 * mm + gq, cB = cA + 8;
+        vf[mm][0] = vpair(cA, u0);
+        vf[mm][1] = vpair(cB, u0);
+        vf[mm][2] = vpair(cA, u1);
+        vf[mm][3] = vpair(cB, u1);
+    }
+    float sacc[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+    for (int s = 0; s < 8; ++s) mma16816_bf16(sacc, kf[s][0], kf[s][1], kf[s][2], kf[s][3], qb[s][0], qb[s][1]);
+    sacc[0] = vA ? sacc[0] * c0 : -CUDART_INF_F;
+    sacc[1] = vA ? sacc[1] * c0 : -CUDART_INF_F;
+    sacc[2] = vB ? sacc[2] * c0 : -CUDART_INF_F;
+    sacc[3] = vB ? sacc[3] * c0 : -CUDART_INF_F;
+    float m0 = fmaxf(sacc[0], sacc[2]), m1 = fmaxf(sacc[1], sacc[3]);
+#pragma unroll
+    for (int o = 4; o < 32; o <<= 1) {
+        m0 = fmaxf(m0, __shfl_xor_sync(0xffffffffu, m0, o));
+        m1 = fmaxf(m1, __shfl_xor_sync(0xffffffffu, m1, o));
+    }
+    sacc[0] = fast_exp2(sacc[0] - m0);  // (a tile holds >= 1 valid token: m0, m1 finite)
+    sacc[1] = fast_exp2(sacc[1] - m1);
+    sacc[2] = fast_exp2(sacc[2] - m0);
+    sacc[3] = fast_exp2(sacc[3] - m1);
+    float l0 = sacc[0] + sacc[2], l1 = sacc[1] + sacc[3];
+#pragma unroll
+    for (int o = 4; o < 32; o <<= 1) {
+        l0 += __shfl_xor_sync(0xffffffffu, l0, o);
+        l1 += __shfl_xor_sync(0xffffffffu, l1, o);
+    }
+    const uint32_t X = pack_bf162(sacc[0], sacc[1]);
+    const uint32_t Y = pack_bf162(sacc[2], sacc[3]);
+    const int sa = (2 * tq) * 4 + (gq >> 1), sbl = (2 * tq + 1) * 4 + (gq >> 1);
+    const uint32_t xa = __shfl_sync(0xffffffffu, X, sa), ya = __shfl_sync(0xffffffffu, Y, sa);
+    const uint32_t xb = __shfl_sync(0xffffffffu, X, sbl), yb = __shfl_sync(0xffffffffu, Y, sbl);
+    const uint32_t sel = (gq & 1) ? 0x7632u : 0x5410u;
+    const uint32_t b0 = __byte_perm(xa, xb, sel), b1 = __byte_perm(ya, yb, sel);
+#pragma unroll
+    for (int mm = 0; mm < 8; ++mm) {
+        rp.o[mm][0] = rp.o[mm][1] = rp.o[mm][2] = rp.o[mm][3] = 0.f;
+        mma16816_bf16(rp.o[mm], vf[mm][0], vf[mm][1], vf[mm][2], vf[mm][3], b0, b1);
+    }
+    rp.m0 = m0;
+    rp.m1 = m1;
+    rp.l0 = l0;
+    rp.l1 = l1;
+}
+
+// online-softmax merge of a tile partial (natural units) into the warp's running
+// packed-domain state: o per m-tile in code-field scale units, the denominator in
+// the value-offset MMA's ones row (lanes gq == 4)
+template <int BITS>
+__device__ __forceinline__ void merge_tile(const ResPartial &rp, WarpState &st, int lane) {
+    const int gq = lane >> 2;
+    constexpr int TPW = 16 / BITS;
+    constexpr int HALFT = TPW / 2;
+    const float M0 = fmaxf(st.m[0], rp.m0), M1 = fmaxf(st.m[1], rp.m1);
+    const float as0 = st.m[0] == -CUDART_INF_F ? 0.f : fast_exp2(st.m[0] - M0);
+    const float as1 = st.m[1] == -CUDART_INF_F ? 0.f : fast_exp2(st.m[1] - M1);
+    const float ar0 = fast_exp2(rp.m0 - M0), ar1 = fast_exp2(rp.m1 - M1);
+#pragma unroll
+    for (int mm = 0; mm < 8; ++mm) {
+        const int fs = (mm % TPW) % HALFT;
+        const float isc = __int_as_float((127 - 24 + BITS * fs) << 23);
+        st.o[mm][0] = st.o[mm][0] * as0 + rp.o[mm][0] * (isc * ar0);
+        st.o[mm][1] = st.o[mm][1] * as1 + rp.o[mm][1] * (isc * ar1);
+        st.o[mm][2] = st.o[mm][2] * as0 + rp.o[mm][2] * (isc * ar0);
+        st.o[mm][3] = st.o[mm][3] * as1 + rp.o[mm][3] * (isc * ar1);
+    }
+    st.ob[0] *= as0;
+    st.ob[1] *= as1;
+    st.ob2[2] *= as0;
+    st.ob2[3] *= as1;
+    if (gq == 4) {
+        st.ob[0] += rp.l0 * ar0;
+        st.ob[1] += rp.l1 * ar1;
+    }
+    st.m[0] = M0;
+    st.m[1] = M1;
+}
+
 __device__ __noinline__ void residual_tile(const ResidualRefs rr, float *slot, const __nv_bfloat16 *qbase, int t0,
                                            int ntok, int lane, float c0, uint16_t *ring_k_w, uint16_t *ring_v_w) {
     ResPartial rp;
@@ -869,9 +990,9 @@ __device__ __noinline__ void residual_tile_first(const ResidualRefs rr, const __
 
 // DEFER: the tiles of a CTA's tail segments after its first run once the packed
 // units are done (launches where a CTA spans many (b, kv head) segments)
-template <int BITS, int NCW_, bool DEFER>
+template <int BITS, int NCW_, bool DEFER, bool TILES = false>
 __global__ void __launch_bounds__(NCW_ * 32, 1) decode_attn_kernel(const AttnArgs a) {
-    using C = AttnCfg<BITS, NCW_>;
+    using C = AttnCfg<BITS, NCW_, TILES>;
     constexpr int NCW = C::NCW;
     constexpr int SUB = C::SUB;
     extern __shared__ __align__(1024) uint8_t smem[];
@@ -909,6 +1030,51 @@ __global__ void __launch_bounds__(NCW_ * 32, 1) decode_attn_kernel(const AttnArg
                  &full[stg], pol);
     };
     auto issue = [&](int64_t p, int64_t bh, int uidx) { issue_stage((int)p % C::NST, bh, uidx); };
+    // ---- TILES kernel: the pipeline positions are the range's packed units and, after
+    //      the last unit of every (b, kv head) whose tail this CTA owns, its window tiles ----
+    const bool tmode = TILES && total > 0;
+    const int ntu = tmode ? ((a.r + (a.kcur ? 1 : 0) + 15) >> 4) : 0;  // tiles per owned tail
+    int P32 = (int)nunits;
+    if (TILES && ntu > 0 && nunits > 0) {
+        const int64_t sf = start / nb, sl = (end - 1) / nb;
+        P32 += (int)((sl - sf) + (end == (sl + 1) * nb ? 1 : 0)) * ntu;
+    }
+    auto seg_np = [&](int64_t bh) -> int {  // packed units of bh in this CTA's range
+        const int64_t l0 = bh * nb > start ? bh * nb : start, h0 = (bh + 1) * nb < end ? (bh + 1) * nb : end;
+        return (int)(h0 - l0);
+    };
+    auto seg_len = [&](int64_t bh, int np) -> int { return np + ((bh + 1) * nb <= end ? ntu : 0); };
+    // a window tile (tokens 16j..16j+15 of bh): K rows, the V tile, the current token
+    // (K row into its slot, V row apart), the raw q rows -- all bulk copies
+    auto issue_tile = [&](int stg, int64_t bh, int j) {
+        const int t0 = 16 * j, r = a.r;
+        const int64_t b = bh / a.Hkv, kvh = bh % a.Hkv;
+        const bool cur = a.kcur != nullptr && r >= t0 && r < t0 + 16;
+        const int nk = r - t0 < 0 ? 0 : (r - t0 > 16 ? 16 : r - t0);
+        uint8_t *dst = ring + stg * C::STAGE;
+        mbar_arrive_expect_tx(&full[stg], (uint32_t)(nk * 256 + 4096 + (cur ? 512 : 0) + g * 256));
+        const uint8_t *rk = reinterpret_cast<const uint8_t *>(a.ring_k) + (bh * R + t0) * (int64_t)(D * 2);
+        const uint8_t *rv = reinterpret_cast<const uint8_t *>(a.ring_v) + (bh * R + t0) * (int64_t)(D * 2);
+        if (nk > 0) bulk_g2s(dst, rk, (uint32_t)(nk * 256), &full[stg], pol);
+        bulk_g2s(dst + TILE_V_OFF, rv, 4096u, &full[stg], pol);
+        if (cur) {
+            const int64_t cb = (b * a.Hkv + kvh) * (int64_t)(D * 2);
+            bulk_g2s(dst + (r - t0) * 256, reinterpret_cast<const uint8_t *>(a.kcur) + cb, 256u, &full[stg], pol);
+            bulk_g2s(dst + TILE_VCUR_OFF, reinterpret_cast<const uint8_t *>(a.vcur) + cb, 256u, &full[stg], pol);
+        }
+        bulk_g2s(dst + TILE_Q_OFF, reinterpret_cast<const uint8_t *>(a.q) + (b * a.Hq + kvh * g) * (int64_t)(D * 2),
+                 (uint32_t)(g * 256), &full[stg], pol);
+    };
+    // position pos of a walked segment (bh, ps = its first position, np packed units):
+    // pass 0: packed units only (may run ahead of griddepcontrol.wait), 1: tiles only, 2: both
+    auto issue_at = [&](int stg, int64_t bh, int ps, int np, int pos, int pass) {
+        const int off = pos - ps;
+        if (off < np) {
+            if (pass != 1) issue_stage(stg, bh, (int)((bh * nb > start ? bh * nb : start) - bh * nb) + off);
+        } else if (pass != 0) {
+            issue_tile(stg, bh, off - np);
+        }
+    };
 
     // Programmatic dependent launch: the next decode step's CTAs may start as
     // this grid's CTAs retire; each new CTA streams its first NST packed
@@ -922,14 +1088,31 @@ __global__ void __launch_bounds__(NCW_ * 32, 1) decode_attn_kernel(const AttnArg
     griddep_launch_dependents();
     // the ring fill: the first NST units of the range, issued by lane 0 of the last warp
     const bool fill_thread = threadIdx.x == (NCW - 1) * 32;
-    auto fill = [&]() {
-        if (nunits > 0) {
-            int64_t bh = start / nb, uidx = start % nb;
-            for (int64_t p = 0; p < nunits && p < C::NST; ++p) {
-                issue(p, bh, uidx);
-                if (++uidx == nb) {
-                    uidx = 0;
-                    ++bh;
+    auto fill = [&](int pass) {
+        if constexpr (TILES) {
+            if (nunits > 0) {
+                int64_t bh = start / nb;
+                int ps = 0, np = seg_np(bh), len = seg_len(bh, np);
+                for (int p = 0; p < P32 && p < C::NST; ++p) {
+                    while (p >= ps + len) {
+                        ps += len;
+                        ++bh;
+                        np = seg_np(bh);
+                        len = seg_len(bh, np);
+                    }
+                    issue_at(p, bh, ps, np, p, pass);
+                }
+            }
+        } else {
+            (void)pass;
+            if (nunits > 0) {
+                int64_t bh = start / nb, uidx = start % nb;
+                for (int64_t p = 0; p < nunits && p < C::NST; ++p) {
+                    issue(p, bh, uidx);
+                    if (++uidx == nb) {
+                        uidx = 0;
+                        ++bh;
+                    }
                 }
             }
         }
@@ -942,10 +1125,13 @@ __global__ void __launch_bounds__(NCW_ * 32, 1) decode_attn_kernel(const AttnArg
         }
         fence_mbar_init();
         if (kProf) g_t0 = gtime();
-        if (a.pdl_prefetch) fill();
+        if (a.pdl_prefetch) fill(0);  // (packed records: independent of the previous grid)
     }
     griddep_wait();
     if (kProf) g_dep = gtime();
+    if constexpr (TILES) {
+        if (fill_thread && a.pdl_prefetch && ntu > 0) fill(1);  // the tiles read the ring, q, the current token
+    }
     // segments: residual-only mode (nb == 0): CTA c <-> bh c
     const bool active = total > 0 ? nunits > 0 : cta < a.BH;
     const int64_t seg_first = !active ? 0 : (total > 0 ? start / nb : cta);
@@ -955,7 +1141,7 @@ __global__ void __launch_bounds__(NCW_ * 32, 1) decode_attn_kernel(const AttnArg
     const bool gate = !a.pdl_prefetch;
     build_q_tiles<BITS, NCW>(a, qtiles, seg_first, 0, nseg_all < QSEG ? nseg_all : QSEG, warp, lane, gate);
     if (kProf) g_qb = gtime();
-    if (fill_thread && !a.pdl_prefetch) fill();  // after every warp's q loads are in flight
+    if (fill_thread && !a.pdl_prefetch) fill(2);  // after every warp's q loads are in flight
     __syncthreads();  // barrier init + first wave of q tiles visible
     if (!active) return;
     const unsigned long long g_ready = kProf ? gtime() : 0;
@@ -967,7 +1153,7 @@ __global__ void __launch_bounds__(NCW_ * 32, 1) decode_attn_kernel(const AttnArg
     // after it is consumed: p + NST >= nunits (NST > NCW), so it is never refilled;
     // a warp with no unit at all (nunits < NCW) takes stage w, which no unit uses
     const bool smem_last = total > 0 && C::NST > NCW;
-    const int nu32 = (int)nunits;
+    const int nu32 = TILES ? P32 : (int)nunits;  // pipeline positions
     auto last_seg_slot = [&](int w) -> float * {
         if (smem_last) {
             const int pw = w < nu32 ? nu32 - 1 - ((nu32 - 1 - w) % NCW) : w;
@@ -980,6 +1166,17 @@ __global__ void __launch_bounds__(NCW_ * 32, 1) decode_attn_kernel(const AttnArg
     int rtile_base = (int)(nunits % NCW);
     bool seen_tail = false;
     (void)seen_tail;
+    int seg_ps = 0;  // (TILES) first pipeline position of the segment
+    int *wk = reinterpret_cast<int *>(smem + C::WALK_OFF) + warp * 4;  // (TILES) refill walker: bh, ps, np, len
+    if constexpr (TILES) {
+        if (tmode && lane == 0) {
+            const int np0 = seg_np(start / nb);
+            wk[0] = (int)(start / nb);
+            wk[1] = 0;
+            wk[2] = np0;
+            wk[3] = seg_len(start / nb, np0);
+        }
+    }
     for (int64_t bh = seg_first; bh <= seg_last; ++bh) {
         const int k = (int)(bh - seg_first);
         const int b = (int)(bh / a.Hkv), kvh = (int)(bh % a.Hkv);
@@ -1025,7 +1222,7 @@ __global__ void __launch_bounds__(NCW_ * 32, 1) decode_attn_kernel(const AttnArg
         const int ntiles_t = (ntok_t + 15) >> 4;
         int tile_j = -1;     // this warp's tile of this segment
         bool tile_late = false;
-        if (owns_tail) {
+        if (owns_tail && !tmode) {
             const int j = (warp - rtile_base % NCW + NCW) % NCW;
             rtile_base += ntiles_t;
             bool now = true;
@@ -1083,14 +1280,16 @@ __global__ void __launch_bounds__(NCW_ * 32, 1) decode_attn_kernel(const AttnArg
         }
 
         // ---- packed units of this segment: positions p = gidx - start, p % NCW == warp ----
+        const int plen = (int)(hi - lo) + (tmode && owns_tail ? ntu : 0);  // (TILES) positions of bh
         if (total > 0) {
             // positions are CTA-local (32-bit); stage and round advance incrementally
-            const int p0 = (int)(lo - start);
+            const int p0 = TILES ? seg_ps : (int)(lo - start);
             const int u_seg0 = (int)(lo - bh * nb);  // unit index within bh of position p0
             const int first = p0 + ((warp - p0 % NCW) + NCW) % NCW;
-            const int pend = (int)(hi - start);
+            const int pend = p0 + (int)(hi - lo);
             int stg = first % C::NST, round = first / C::NST;
-            for (int p = first; p < pend; p += NCW) {
+            int p = first;
+            for (; p < pend; p += NCW) {
                 const long long ts0 = (kProf && a.prof) ? clk() : 0;
                 // every lane polls the same word (a broadcast): no divergent region
                 while (ld_volatile_shared_u32(consumed_s + 4 * stg) < round) {
@@ -1114,7 +1313,26 @@ __global__ void __launch_bounds__(NCW_ * 32, 1) decode_attn_kernel(const AttnArg
                 // issued -- the same consumer-release ordering TMA pipelines rely on.
                 __syncwarp();
                 if (lane == 0) {
-                    if (p + C::NST < nu32) {
+                    if (TILES && p + C::NST < nu32) {
+                        // (TILES) position p + NST: a packed unit of bh, or beyond bh the walker
+                        const int tp = p + C::NST;
+                        if (tp < pend) {
+                            issue_stage(stg, bh, u_seg0 + (tp - p0));
+                        } else {
+                            int wbh = wk[0], wps = wk[1], wnp = wk[2], wlen = wk[3];
+                            while (tp >= wps + wlen) {
+                                wps += wlen;
+                                ++wbh;
+                                wnp = seg_np(wbh);
+                                wlen = seg_len(wbh, wnp);
+                            }
+                            wk[0] = wbh;
+                            wk[1] = wps;
+                            wk[2] = wnp;
+                            wk[3] = wlen;
+                            issue_at(stg, wbh, wps, wnp, tp, 2);
+                        }
+                    } else if (p + C::NST < nu32) {
                         int64_t bh2 = bh;
                         int u2 = u_seg0 + (p - p0) + C::NST;  // unit index within bh (32-bit)
                         while (u2 >= nb32) {
@@ -1133,7 +1351,56 @@ __global__ void __launch_bounds__(NCW_ * 32, 1) decode_attn_kernel(const AttnArg
                     ++round;
                 }
             }
+            if constexpr (TILES && BITS != 0) {
+                // ---- (TILES) the segment's window tiles: positions pend + j, streamed like
+                //      the records, computed from shared memory, merged into the partial ----
+                for (; p < p0 + plen; p += NCW) {
+                    while (ld_volatile_shared_u32(consumed_s + 4 * stg) < round) {
+                    }
+                    mbar_wait_s(full_s + 8 * stg, (uint32_t)(round & 1));
+                    const uint8_t *sb = ring + stg * C::STAGE;
+                    const int t0 = 16 * (p - pend), r = a.r;
+                    ResPartial rp;
+                    tile_compute_smem(sb, t0, r, r + (a.kcur ? 1 : 0), g, lane, c0, &rp);
+                    merge_tile<BITS>(rp, st, lane);
+                    if (a.write_ring && a.kcur && r >= t0 && r < t0 + 16) {  // append the current token
+                        uint16_t *rkw = reinterpret_cast<uint16_t *>(a.ring_k) + (bh * R + r) * D;
+                        uint16_t *rvw = reinterpret_cast<uint16_t *>(a.ring_v) + bh * R * D;
+                        reinterpret_cast<uint2 *>(rkw)[lane] = reinterpret_cast<const uint2 *>(sb + (r - t0) * 256)[lane];
+                        const uint2 vv = reinterpret_cast<const uint2 *>(sb + TILE_VCUR_OFF)[lane];
+                        rvw[vring_index(4 * lane + 0, r)] = (uint16_t)(vv.x & 0xffffu);
+                        rvw[vring_index(4 * lane + 1, r)] = (uint16_t)(vv.x >> 16);
+                        rvw[vring_index(4 * lane + 2, r)] = (uint16_t)(vv.y & 0xffffu);
+                        rvw[vring_index(4 * lane + 3, r)] = (uint16_t)(vv.y >> 16);
+                    }
+                    __syncwarp();
+                    if (lane == 0) {
+                        const int tp = p + C::NST;
+                        if (tp < nu32) {
+                            int wbh = wk[0], wps = wk[1], wnp = wk[2], wlen = wk[3];
+                            while (tp >= wps + wlen) {
+                                wps += wlen;
+                                ++wbh;
+                                wnp = seg_np(wbh);
+                                wlen = seg_len(wbh, wnp);
+                            }
+                            wk[0] = wbh;
+                            wk[1] = wps;
+                            wk[2] = wnp;
+                            wk[3] = wlen;
+                            issue_at(stg, wbh, wps, wnp, tp, 2);
+                        }
+                        st_volatile_shared_u32(consumed_s + 4 * stg, round + 1);
+                    }
+                    stg += NCW;
+                    if (stg >= C::NST) {
+                        stg -= C::NST;
+                        ++round;
+                    }
+                }
+            }
         }
+        if constexpr (TILES) seg_ps += plen;
 
         const long long te0 = (kProf && a.prof) ? clk() : 0;
         // ---- warp partial -> slot (unnormalized O[h][c], m[h], l[h]).  For the CTA's
@@ -1196,7 +1463,7 @@ __global__ void __launch_bounds__(NCW_ * 32, 1) decode_attn_kernel(const AttnArg
         if (kProf && a.prof) tmr[7] += clk() - te0;
     }
 
-    if (DEFER && !OSK_SKIP_TILES) {  // tiles of the tail segments after the first, after the packed units
+    if (DEFER && !TILES && !OSK_SKIP_TILES) {  // tiles of the tail segments after the first, after the packed units
         const int ntok = a.r + (a.kcur ? 1 : 0);
         const int ntiles = (ntok + 15) >> 4;
         int rbase = (int)(nunits % NCW);
@@ -1443,11 +1710,12 @@ __global__ void lse_merge_kernel(const float *outs, const float *lses, int64_t p
     }
 }
 
-template <int BITS, int NCW, bool DEFER>
+template <int BITS, int NCW, bool DEFER, bool TILES = false>
 cudaError_t launch_d(const AttnArgs &a, cudaStream_t st) {
-    using C = AttnCfg<BITS, NCW>;
+    using C = AttnCfg<BITS, NCW, TILES>;
     static std::atomic<uint64_t> attr_done{0};
-    if (cudaError_t e = ensure_smem_attr(decode_attn_kernel<BITS, NCW, DEFER>, C::SMEM, attr_done); e != cudaSuccess)
+    if (cudaError_t e = ensure_smem_attr(decode_attn_kernel<BITS, NCW, DEFER, TILES>, C::SMEM, attr_done);
+        e != cudaSuccess)
         return e;
     // programmatic stream serialization: may overlap the previous kernel's tail
     // (the kernel orders its dependent accesses with griddepcontrol.wait)
@@ -1461,7 +1729,7 @@ cudaError_t launch_d(const AttnArgs &a, cudaStream_t st) {
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    return cudaLaunchKernelEx(&cfg, decode_attn_kernel<BITS, NCW, DEFER>, a);
+    return cudaLaunchKernelEx(&cfg, decode_attn_kernel<BITS, NCW, DEFER, TILES>, a);
 }
 
 // DEFER pays off when CTAs span several (b, kv head) segments (each with its own
@@ -1470,6 +1738,8 @@ template <int BITS, int NCW>
 cudaError_t launch_t(const AttnArgs &a, cudaStream_t st) {
     static const long force = env_knob("OSCAR_DEFER", -1);  // OSCAR_DEFER=0|1 overrides the choice (experiments)
     const bool defer = force >= 0 ? force == 1 : (a.nb > 0 && (int64_t)a.BH > 2 * (int64_t)a.ncta);
+    if constexpr (BITS != 0 && NCW == 12)
+        if (a.tile_units && !defer) return launch_d<BITS, NCW, false, true>(a, st);
     return defer ? launch_d<BITS, NCW, true>(a, st) : launch_d<BITS, NCW, false>(a, st);
 }
 

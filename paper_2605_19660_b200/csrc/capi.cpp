@@ -548,6 +548,16 @@ struct oscar_kv_handle {
             a.maxseg = 1;  // residual-only mode: one segment per CTA (ncta = BH <= scratch slots)
         }
         a.poll_merge = (poll_knob != 0 && a.ncta <= num_sms) ? 1 : 0;
+        {
+            // small launches (<= 2 records per warp): the window's tiles ride the ring as
+            // pipeline units (the TILES kernel); bulk copies need 16-byte aligned sources.
+            // OSCAR_TILE_UNITS=0: never, 2: for every launch (A/B)
+            static const long tu = env_knob("OSCAR_TILE_UNITS", 1);
+            auto al16 = [](const void *p) { return p == nullptr || ((uintptr_t)p & 15) == 0; };
+            const bool small = a.nb > 0 && a.nb * BH <= (int64_t)24 * a.ncta;
+            a.tile_units = (tu != 0 && (dbits == 2 || dbits == 4) && !cfg.rotate_v && form != 2 && a.nb > 0 &&
+                            (small || tu == 2) && al16(a.q) && al16(a.kcur) && al16(a.vcur)) ? 1 : 0;
+        }
         return a;
     }
 

@@ -141,6 +141,9 @@ struct AttnArgs {
     void *ring_k, *ring_v;    // K [bh][R][D], V [bh][D][R]
     int r;             // residual rows in ring
     int write_ring;    // store kcur/vcur at ring slot r
+    int tile_units;    // small launches: the residual window's 16-token tiles are pipeline units of
+                       // the tail owner, bulk-copied into the shared-memory ring like the records
+                       // (K rows, the tile-major V tile, the current token, the raw q rows)
     int ring_f16;      // rings hold fp16 images (fp64-form caches: the exact rows are in the
                        // residual shadow; fp16 keeps the window's rounding 8x below bf16's)
     int rotates;       // rotate q for the packed part

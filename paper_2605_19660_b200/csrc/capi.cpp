@@ -186,6 +186,7 @@ struct oscar_kv_handle {
     // form (fp32 partials) into the poll form (flag-in-word partials, zero = not
     // written): the partial words are cleared once before the first launch of a plan
     bool partials_dirty = false;
+    bool sync_entry = false;  // inside oscar_kv_decode_step_host (one synchronous step per call)
     void launch_attn(const AttnArgs &a, cudaStream_t s) {
         if (partials_dirty) {
             CK(cudaMemsetAsync(part_o, 0, sizeof(uint64_t) * (size_t)(BH * maxp_alloc * 8 * D), s));
@@ -549,14 +550,20 @@ struct oscar_kv_handle {
         }
         a.poll_merge = (poll_knob != 0 && a.ncta <= num_sms) ? 1 : 0;
         {
-            // small launches (<= 2 records per warp): the window's tiles ride the ring as
-            // pipeline units (the TILES kernel); bulk copies need 16-byte aligned sources.
+            // the window's tiles ride the ring as pipeline units (the TILES kernel) where that
+            // measured faster (profiles/r02/ab_tiles_*): small launches (<= 2 records per
+            // warp), launches of 1.5-2 (b, kv head) segments per CTA (C3 B=64), and the
+            // synchronous host-buffer entry (a cold launch: the tiles' own loads would
+            // queue behind the ring fill).  Bulk copies need 16-byte aligned sources.
             // OSCAR_TILE_UNITS=0: never, 2: for every launch (A/B)
             static const long tu = env_knob("OSCAR_TILE_UNITS", 1);
             auto al16 = [](const void *p) { return p == nullptr || ((uintptr_t)p & 15) == 0; };
             const bool small = a.nb > 0 && a.nb * BH <= (int64_t)24 * a.ncta;
+            const bool segs = 2 * BH >= (int64_t)3 * a.ncta;  // >= 1.5 segments per CTA (DEFER above 2)
             a.tile_units = (tu != 0 && (dbits == 2 || dbits == 4) && !cfg.rotate_v && form != 2 && a.nb > 0 &&
-                            (small || tu == 2) && al16(a.q) && al16(a.kcur) && al16(a.vcur)) ? 1 : 0;
+                            (small || segs || sync_entry || tu == 2) && al16(a.q) && al16(a.kcur) && al16(a.vcur))
+                               ? 1
+                               : 0;
         }
         return a;
     }
@@ -1729,7 +1736,14 @@ int oscar_kv_decode_step_host(oscar_kv_handle *h, const void *q_host, const void
         static const long zc_out = env_knob("OSCAR_HOST_OUT", 1);  // 0: device buffer + one D2H copy (A/B)
         float *zo = zc_out && ((uintptr_t)out_host & 15) == 0 ? (float *)mapped(out_host) : nullptr;  // float4 rows
         float *zl = lse_host ? (float *)mapped(lse_host) : nullptr;
-        h->decode_step(dq, dk, dv, zo ? zo : dout, lse_host ? (zl ? zl : dlse) : nullptr, s);
+        h->sync_entry = true;
+        try {
+            h->decode_step(dq, dk, dv, zo ? zo : dout, lse_host ? (zl ? zl : dlse) : nullptr, s);
+        } catch (...) {
+            h->sync_entry = false;
+            throw;
+        }
+        h->sync_entry = false;
         if (!zo) CK(cudaMemcpyAsync(out_host, dout, ob, cudaMemcpyDeviceToHost, s));
         if (lse_host && !zl) CK(cudaMemcpyAsync(lse_host, dlse, lb, cudaMemcpyDeviceToHost, s));
         CK(cudaStreamSynchronize(s));

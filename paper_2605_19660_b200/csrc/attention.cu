@@ -1739,7 +1739,7 @@ cudaError_t launch_t(const AttnArgs &a, cudaStream_t st) {
     static const long force = env_knob("OSCAR_DEFER", -1);  // OSCAR_DEFER=0|1 overrides the choice (experiments)
     const bool defer = force >= 0 ? force == 1 : (a.nb > 0 && (int64_t)a.BH > 2 * (int64_t)a.ncta);
     if constexpr (BITS != 0 && NCW == 12)
-        if (a.tile_units && !defer) return launch_d<BITS, NCW, false, true>(a, st);
+        if (a.tile_units) return launch_d<BITS, NCW, false, true>(a, st);  // (supersedes DEFER)
     return defer ? launch_d<BITS, NCW, true>(a, st) : launch_d<BITS, NCW, false>(a, st);
 }
 

@@ -552,16 +552,19 @@ struct oscar_kv_handle {
         {
             // the window's tiles ride the ring as pipeline units (the TILES kernel) where that
             // measured faster (profiles/r02/ab_tiles_*): small launches (<= 2 records per
-            // warp), launches of 1.5-2 (b, kv head) segments per CTA (C3 B=64), and the
-            // synchronous host-buffer entry (a cold launch: the tiles' own loads would
-            // queue behind the ring fill).  Bulk copies need 16-byte aligned sources.
+            // warp), launches of 1.5-4 (b, kv head) segments per CTA (C3 B=64 -1.4 %, the C3
+            // 2-rank shard -4.8 %; at C3 B=256's 7 it is 3 % slower), and the synchronous
+            // host-buffer entry (a cold launch: the tiles' own loads would queue behind the
+            // ring fill) up to 4 segments per CTA.  Bulk copies need 16-byte aligned sources.
             // OSCAR_TILE_UNITS=0: never, 2: for every launch (A/B)
             static const long tu = env_knob("OSCAR_TILE_UNITS", 1);
             auto al16 = [](const void *p) { return p == nullptr || ((uintptr_t)p & 15) == 0; };
             const bool small = a.nb > 0 && a.nb * BH <= (int64_t)24 * a.ncta;
-            const bool segs = 2 * BH >= (int64_t)3 * a.ncta;  // >= 1.5 segments per CTA (DEFER above 2)
+            const bool le4 = BH <= (int64_t)4 * a.ncta;
+            const bool segs = 2 * BH >= (int64_t)3 * a.ncta && le4;
             a.tile_units = (tu != 0 && (dbits == 2 || dbits == 4) && !cfg.rotate_v && form != 2 && a.nb > 0 &&
-                            (small || segs || sync_entry || tu == 2) && al16(a.q) && al16(a.kcur) && al16(a.vcur))
+                            (small || segs || (sync_entry && le4) || tu == 2) && al16(a.q) && al16(a.kcur) &&
+                            al16(a.vcur))
                                ? 1
                                : 0;
         }

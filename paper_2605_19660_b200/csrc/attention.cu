@@ -44,6 +44,10 @@ namespace {
 #define OSK_PROF 0
 #endif
 constexpr bool kProf = OSK_PROF != 0;
+// partials per batch of the ticket-form final merge (one L2 round trip each)
+#ifndef OSK_TICKET_FB
+#define OSK_TICKET_FB 32
+#endif
 
 constexpr int MERGE_FLOATS = 8 * D + 16 + D;  // per-warp partial: O[8][128], m[8], l[8] + 128 scratch
 constexpr float LOG2E = 1.4426950408889634f;
@@ -1616,7 +1620,7 @@ __global__ void __launch_bounds__(NCW_ * 32, 1) decode_attn_kernel(const AttnArg
             // never read as flag-in-word ones
             float M = -CUDART_INF_F, Lw = 0.f;  // Lw: this lane's share of the denominator
             float x[4] = {0.f, 0.f, 0.f, 0.f};
-            constexpr int FB = 32;
+            constexpr int FB = OSK_TICKET_FB;
             for (int s0 = 0; s0 < expected; s0 += FB) {
                 const bool mine = s0 + lane < expected;
                 const float *pm =
@@ -1755,7 +1759,8 @@ int attention_grid(int bits, int num_sms, int64_t nb, int BH) {
     if (units == 0) return BH;
     // small launches: ~2/3 of the warps stream packed units, the rest take the
     // residual-window tiles concurrently
-    const int64_t per = (ncw_choice(bits) * 2) / 3;
+    static const long per_env = env_knob("OSCAR_CTA_UNITS", 0);  // experiments: packed units per CTA
+    const int64_t per = per_env > 0 ? per_env : (ncw_choice(bits) * 2) / 3;
     const int64_t want = (units + per - 1) / per;
     return (int)(want < num_sms ? want : num_sms);
 }

@@ -32,10 +32,29 @@ namespace {
 
 constexpr int QT = 128;  // threads per CTA
 constexpr int KU_ROW = 4 * 33;  // doubles per token row of the K_u tile (4 quarters of 32, padded to 33)
-// byte stride of a token row in the shared code tiles: 132 makes the permuted-word
-// gathers of the pack loop (and the V code writes) at most 2-way bank conflicted
-// (128 was 4-way for K, 8-way for V) while three CTAs still fit per SM
-constexpr int CODE_STRIDE = D + 4;
+// shared code tiles hold one code per nibble (codes <= 15), two per byte, so that
+// four prefill CTAs fit per SM (53.75 KB each, 16 warps: the kernel is latency-bound):
+//   K: [token pair][channel] bytes, row stride KC_STRIDE (the low nibble is the even token)
+//   V: [token][channel pair] bytes, row stride VC_STRIDE (the low nibble is the even channel),
+//      16-byte chunks XOR-swizzled by (token >> 1) & 3 (vc_swz): the pack loop's gathers
+//      (4 token pairs 128 B apart per warp) hit distinct banks
+constexpr int KC_STRIDE = D + 4;
+constexpr int VC_STRIDE = D / 2;
+__device__ __forceinline__ int vc_swz(int t) { return ((t >> 1) & 3) << 4; }
+
+// a thread's 32 codes of one group as nibbles of two 64-bit registers (any write order)
+struct Nib32 {
+    uint64_t lo = 0, hi = 0;
+    __device__ __forceinline__ void put(int i, int code) {
+        const int sh = 4 * (i & 15);
+        const uint64_t m = ~(0xFull << sh), v = (uint64_t)(uint32_t)code << sh;
+        if (i < 16) lo = (lo & m) | v;
+        else hi = (hi & m) | v;
+    }
+    __device__ __forceinline__ uint32_t byte(int k) const {  // nibbles 2k, 2k+1
+        return (uint32_t)((k < 8 ? lo >> (8 * k) : hi >> (8 * (k - 8))) & 0xFF);
+    }
+};
 
 // 32 bf16 -> fp64 (exact); bit 15 / 31 of `bad` flags non-finite inputs
 __device__ __forceinline__ void load32(const __nv_bfloat16 *p, double (&x)[32], uint32_t &bad) {
@@ -100,11 +119,18 @@ __device__ __forceinline__ double fast_rsqrt_ref(double x) {
     return dmul(y, dsub(1.5, t));
 }
 
+#ifndef OSK_QC_ROLL
+#define OSK_QC_ROLL 0
+#endif
 // sequential chain over the quad: acc_{c+1} = acc_c (+) f(x_c), c = 0..127
 template <typename F>
 __device__ __forceinline__ double quad_chain(const double (&x)[32], int q, int lane, F f) {
     double acc = 0.0;
+#if OSK_QC_ROLL
+#pragma unroll 1
+#else
 #pragma unroll
+#endif
     for (int step = 0; step < 4; ++step) {
         if (q == step) {
 #pragma unroll
@@ -141,15 +167,15 @@ __device__ __forceinline__ GroupQ group_params_f32(const double (&y)[32], int bi
 // 128-thread quarters of the CTA (GPAR = 1: prefill, throughput; GPAR = 4:
 // the single-block flush, latency).
 template <int BITS, int GPAR>
-__global__ void __launch_bounds__(QT * GPAR) quantize_kernel(const QuantizeArgs a) {
+__global__ void __launch_bounds__(QT * GPAR, GPAR == 1 ? 4 : 1) quantize_kernel(const QuantizeArgs a) {
     using Blk = Block<BITS>;
     extern __shared__ __align__(16) uint8_t smem[];
     double *ku = reinterpret_cast<double *>(smem) + (threadIdx.x / QT) * 32 * KU_ROW;  // [GPAR][32][4][33]
-    uint8_t *ck = smem + GPAR * 32 * KU_ROW * 8;                  // [128][128] K codes
-    uint8_t *cv = ck + R * CODE_STRIDE;                           // [128][128] V codes
+    uint8_t *ck = smem + GPAR * 32 * KU_ROW * 8;                  // [64][KC_STRIDE] K code nibbles
+    uint8_t *cv = ck + (R / 2) * KC_STRIDE;                       // [128][64] V code nibbles
     // params + norms staged in record order: K tail [a][b][norms] (K_PART - KA_OFF
     // bytes), then V tail [a][b] (BYTES - VA_OFF bytes)
-    uint8_t *prm = cv + R * CODE_STRIDE;
+    uint8_t *prm = cv + R * VC_STRIDE;
     __half *ka = reinterpret_cast<__half *>(prm);
     __half *kb = ka + D * NGRP;
     float *nrm = reinterpret_cast<float *>(kb + D * NGRP);
@@ -249,8 +275,11 @@ __global__ void __launch_bounds__(QT * GPAR) quantize_kernel(const QuantizeArgs 
             const GroupQ p = tc.rotate_v ? group_params([&](int i) { return y[i]; }, BITS)
                                          : group_params_f32(y, BITS);
 #pragma unroll
-            quantize_group([&](int i) { return y[i]; }, p, BITS,
-                           [&](int i, int code) { cv[t * CODE_STRIDE + q * 32 + i] = (uint8_t)code; });
+            Nib32 nv;
+            quantize_group([&](int i) { return y[i]; }, p, BITS, [&](int i, int code) { nv.put(i, code); });
+            // channels q*32 .. q*32+31 of token t: 16 contiguous bytes, one 128-bit store
+            *reinterpret_cast<uint4 *>(cv + t * VC_STRIDE + ((q * 16) ^ vc_swz(t))) =
+                make_uint4((uint32_t)nv.lo, (uint32_t)(nv.lo >> 32), (uint32_t)nv.hi, (uint32_t)(nv.hi >> 32));
             __half ha, hb;
             affine16(p, ha, hb);
             flag_status(a.status, p, ha, hb);
@@ -267,8 +296,10 @@ __global__ void __launch_bounds__(QT * GPAR) quantize_kernel(const QuantizeArgs 
             const int c = tid;  // channel
             const int cc = (c >> 5) * 33 + (c & 31);
             const GroupQ p = group_params([&](int i) { return ku[i * KU_ROW + cc]; }, BITS);
-            quantize_group([&](int i) { return ku[i * KU_ROW + cc]; }, p, BITS,
-                           [&](int i, int code) { ck[(gi * G + i) * CODE_STRIDE + c] = (uint8_t)code; });
+            Nib32 nk;
+            quantize_group([&](int i) { return ku[i * KU_ROW + cc]; }, p, BITS, [&](int i, int code) { nk.put(i, code); });
+#pragma unroll
+            for (int k = 0; k < 16; ++k) ck[(gi * (G / 2) + k) * KC_STRIDE + c] = (uint8_t)nk.byte(k);
             // keys use the same affine form as values, x = a*code + b with
             // b = -delta*zp (a constant group is a = 0, b = lo: its codes are 0,
             // quant.cpp:37-42, 65-68); the attention kernel folds b into one
@@ -303,12 +334,15 @@ __global__ void __launch_bounds__(QT * GPAR) quantize_kernel(const QuantizeArgs 
                 int tk, ckn, tv, cvn;
                 k_word_coords(BITS, w, 0, hi, tk, ckn);
                 v_word_coords(BITS, w, 0, hi, tv, cvn);
-                const uint8_t *pk = ck + tk * CODE_STRIDE + ckn;
-                const uint8_t *pv = cv + tv * CODE_STRIDE + cvn;
+                // field f: K token tk + 16f (same nibble parity), V channel cvn + 16f
+                const uint8_t *pk = ck + (tk >> 1) * KC_STRIDE + ckn;
+                const uint8_t *pv = cv + tv * VC_STRIDE;
+                const int bv = cvn >> 1, sv = vc_swz(tv);
+                const int shk = (tk & 1) * 4, shv = (cvn & 1) * 4;
 #pragma unroll
                 for (int f = 0; f < TPW; ++f) {
-                    wk[e] |= (uint32_t)pk[16 * f * CODE_STRIDE] << (hi * 16 + f * BITS);
-                    wv[e] |= (uint32_t)pv[16 * f] << (hi * 16 + f * BITS);
+                    wk[e] |= (((uint32_t)pk[8 * f * KC_STRIDE] >> shk) & 0xFu) << (hi * 16 + f * BITS);
+                    wv[e] |= (((uint32_t)pv[(bv + 8 * f) ^ sv] >> shv) & 0xFu) << (hi * 16 + f * BITS);
                 }
             }
         }
@@ -394,7 +428,7 @@ __global__ void ring_copy_kernel(const RingCopyArgs a) {
 
 template <int BITS, int GPAR>
 cudaError_t launch_q(const QuantizeArgs &a, dim3 grid, cudaStream_t st) {
-    const int smem = GPAR * 32 * KU_ROW * 8 + 2 * R * CODE_STRIDE + (Block<BITS>::K_PART - Block<BITS>::KA_OFF) +
+    const int smem = GPAR * 32 * KU_ROW * 8 + (R / 2) * KC_STRIDE + R * VC_STRIDE + (Block<BITS>::K_PART - Block<BITS>::KA_OFF) +
                      (Block<BITS>::BYTES - Block<BITS>::VA_OFF);
     static std::atomic<uint64_t> attr_done{0};
     if (cudaError_t e = ensure_smem_attr(quantize_kernel<BITS, GPAR>, smem, attr_done); e != cudaSuccess) return e;

@@ -21,11 +21,13 @@ struct GroupQ {
     double lo, hi, delta;
     long long zp;
 };
-template <typename Get>
+// UNR: unroll factor of the element loops (32: register-array getters; a smaller one
+// keeps the code of shared-memory getters compact)
+template <int UNR = 32, typename Get>
 __device__ __forceinline__ GroupQ group_params(Get get, int bits) {
     GroupQ p;
     double lo = get(0), hi = lo;
-#pragma unroll
+#pragma unroll(UNR)
     for (int i = 0; i < 32; ++i) {
         const double x = get(i);
         lo = (x < lo) ? x : lo;  // std::min(lo, x)
@@ -49,7 +51,7 @@ __device__ __forceinline__ GroupQ group_params(Get get, int bits) {
 // half-integer (where the two could round apart; 2 ulp < 1e-9 while
 // |x/delta| < 2^20, checked once per group) is redone with the exact IEEE
 // division afterwards.  The codes are bit-identical to the reference's.
-template <typename Get, typename Put>
+template <int UNR = 32, typename Get, typename Put>
 __device__ __forceinline__ void quantize_group(Get get, const GroupQ &p, int bits, Put put) {
     const int mx = (1 << bits) - 1;
     if (p.delta == 0.0) {
@@ -62,7 +64,7 @@ __device__ __forceinline__ void quantize_group(Get get, const GroupQ &p, int bit
     // codes saturate, so a zero point beyond +-2^30 acts like +-2^30
     const int zp = p.zp > (1ll << 30) ? (1 << 30) : (p.zp < -(1ll << 30) ? -(1 << 30) : (int)p.zp);
     unsigned tie = 0;
-#pragma unroll
+#pragma unroll(UNR)
     for (int i = 0; i < 32; ++i) {
         const double y = dmul(get(i), inv);
         const double fl = floor(y);

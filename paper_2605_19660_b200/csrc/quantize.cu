@@ -120,7 +120,10 @@ __device__ __forceinline__ double fast_rsqrt_ref(double x) {
 }
 
 #ifndef OSK_QC_ROLL
-#define OSK_QC_ROLL 0
+#define OSK_QC_ROLL 1  // the quad chain's step loop rolled: smaller code, prefill -3 % (ab_quant_occupancy)
+#endif
+#ifndef OSK_KROLL
+#define OSK_KROLL 32  // unroll factor of the K-side (shared-memory) group loops
 #endif
 // sequential chain over the quad: acc_{c+1} = acc_c (+) f(x_c), c = 0..127
 template <typename F>
@@ -295,9 +298,10 @@ __global__ void __launch_bounds__(QT * GPAR, GPAR == 1 ? 4 : 1) quantize_kernel(
         {
             const int c = tid;  // channel
             const int cc = (c >> 5) * 33 + (c & 31);
-            const GroupQ p = group_params([&](int i) { return ku[i * KU_ROW + cc]; }, BITS);
+            const GroupQ p = group_params<OSK_KROLL>([&](int i) { return ku[i * KU_ROW + cc]; }, BITS);
             Nib32 nk;
-            quantize_group([&](int i) { return ku[i * KU_ROW + cc]; }, p, BITS, [&](int i, int code) { nk.put(i, code); });
+            quantize_group<OSK_KROLL>([&](int i) { return ku[i * KU_ROW + cc]; }, p, BITS,
+                                      [&](int i, int code) { nk.put(i, code); });
 #pragma unroll
             for (int k = 0; k < 16; ++k) ck[(gi * (G / 2) + k) * KC_STRIDE + c] = (uint8_t)nk.byte(k);
             // keys use the same affine form as values, x = a*code + b with
